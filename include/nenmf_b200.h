@@ -1,0 +1,177 @@
+/*
+ * nenmf_b200.h -- C ABI of libnenmf_b200.so, the sm_100a (B200) hot path of
+ * compressed NeNMF (arXiv 1812.04315).
+ *
+ * The reference (/root/reference/pkg/src/nenmf) is pure Python/NumPy and has
+ * no FFI; its hot path sits behind the public Python API.  Each entry point
+ * below replaces the NumPy/OpenBLAS/LAPACK work of one reference function and
+ * is what a ctypes binding of that function calls:
+ *
+ *   nenmf_solve_nnls        nnls.py:119-227       solve_nnls (whole inner solve)
+ *   nenmf_spectral_norm_sq  matrix.py:131-174     spectral_norm_sq (+ power iteration)
+ *   nenmf_gradient          nnls.py:72-86         gradient
+ *   nenmf_pg_norm_sq        nnls.py:89-107        projected_gradient_norm
+ *   nenmf_rsi               compression.py:120-141 subspace_iteration_pair
+ *   nenmf_compress          compression.py:179-188 compress_problem
+ *   nenmf_abt               factorize.py:110,113  F @ R, L @ G (skinny, long K)
+ *   nenmf_residual_sumsq    factorize.py:139, tracing.py:45-57  ||X - G F||^2
+ *   nenmf_sumsq             matrix.py:177-179     frobenius_norm^2
+ *   nenmf_dual_pass         compression.py:134-139 X @ A and X.T @ B in one pass
+ *   nenmf_orthonormalize    compression.py:88-106 _orthonormal_columns (TSQR)
+ *
+ * Conventions
+ *  - All array pointers are DEVICE pointers, row-major, allocated by the
+ *    caller.  Nothing is allocated or freed inside the library.
+ *  - "skinny" matrices are stored short-dimension-major: a tall n x k panel
+ *    P is passed as Pt (k x n, row-major), i.e. P in column-major order.
+ *  - dtype: NENMF_F64 (parity mode) or NENMF_F32; every array of one call has
+ *    that element type; scalar results are always double.
+ *  - Every call is asynchronous on `stream` (a cudaStream_t, NULL = legacy
+ *    default) and returns a launch status.  Data-dependent failures (zero
+ *    matrix, non-finite iterates, sketch collapse) are written by the kernels
+ *    into a caller-provided device nenmf_device_status and surface when the
+ *    caller reads it back, exactly where the reference raises.
+ *  - Workspace: each op reports its scratch size via *_workspace_bytes;
+ *    pass at least that many bytes (256-byte aligned) in `ws`.
+ *  - No global mutable state; calls on different streams/threads are safe.
+ */
+#ifndef NENMF_B200_H
+#define NENMF_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define NENMF_ABI_VERSION 1
+
+typedef enum { NENMF_F64 = 0, NENMF_F32 = 1 } nenmf_dtype;
+
+/* maps 1:1 onto errors.py classes (see paper_1812_04315_b200/errors.py) */
+typedef enum {
+  NENMF_OK = 0,
+  NENMF_ERR_DIM = 1,                 /* DimensionError          errors.py:10 */
+  NENMF_ERR_ZERO_MATRIX = 2,         /* ZeroMatrixError         errors.py:14 */
+  NENMF_ERR_NUMERICAL_FAILURE = 3,   /* NumericalFailureError   errors.py:30 */
+  NENMF_ERR_NUMERICAL_COLLAPSE = 4,  /* NumericalCollapseError  errors.py:43 */
+  NENMF_ERR_VALUE = 5,               /* ValueError                            */
+  NENMF_ERR_CUDA = 6,
+  NENMF_ERR_WORKSPACE = 7,
+  NENMF_ERR_UNSUPPORTED = 8
+} nenmf_status_code;
+
+/* Written by the kernels (device memory, 64 bytes).  Zero it before use. */
+typedef struct {
+  int32_t code;          /* nenmf_status_code of the first failure, 0 if none */
+  int32_t iteration;     /* inner iteration of a NUMERICAL_FAILURE            */
+  int32_t inner_iters;   /* inner iterations executed by the last solve       */
+  int32_t returned_best; /* 1: best iterate returned, 0: start returned       */
+  double lipschitz;      /* L used by the last solve                           */
+  double best_partial;   /* Gram-form objective of the returned iterate       */
+  double pg_ref;         /* projected-gradient norm at the start point        */
+  double resid[2];       /* 1/2||A best - B||^2, 1/2||A start - B||^2         */
+  double pad;
+} nenmf_device_status;
+
+int nenmf_abi_version(void);
+const char* nenmf_status_string(int code);
+/* number of SMs of the current device (0 if no device) */
+int nenmf_device_sm_count(void);
+
+/* ---- inner solver (nnls.py:119-227) -------------------------------------
+ * Solves min_{F>=0} 1/2||B - A F||^2 from F0.  A (r x p) is passed as
+ * At (p x r).  B is (r x c): row-major with leading dimension ldb when
+ * trans_b == 0, or the transpose of a row-major (c x r) matrix with leading
+ * dimension ldb when trans_b == 1 (this is how vanilla NeNMF's G-half reads
+ * X^T without materialising it, factorize.py:92).  F0 and F_out are (p x c)
+ * and must not alias.  power_vectors: device array of power_count
+ * normalised start vectors of length min(r, p), the reference's seeded
+ * stream in draw order (matrix.py:24,138-149): vector 0 starts the power
+ * iteration, the next one is taken whenever ||W v|| == 0 (past power_count
+ * the re-draw is the zero vector); power_max_iters / power_tol are the
+ * reference's max_iters (100) and tol (1e-9).
+ * Writes status->{code, iteration, inner_iters, returned_best, lipschitz}. */
+size_t nenmf_solve_nnls_workspace_bytes(int dtype, int64_t r, int64_t p, int64_t c);
+int nenmf_solve_nnls(int dtype, const void* At, int64_t r, int64_t p,
+                     const void* B, int64_t c, int64_t ldb, int trans_b,
+                     const void* F0, void* F_out,
+                     int max_iter, double grad_tol, double lipschitz_safety,
+                     const double* power_vectors, int power_count, int power_max_iters,
+                     double power_tol, nenmf_device_status* status, void* ws, size_t ws_bytes,
+                     void* stream);
+
+/* sigma_max(A)^2 by power iteration on the smaller Gram (matrix.py:158-174).
+ * A (r x p) passed as At (p x r).  Result (double) -> *out (device). */
+size_t nenmf_spectral_norm_sq_workspace_bytes(int dtype, int64_t r, int64_t p);
+int nenmf_spectral_norm_sq(int dtype, const void* At, int64_t r, int64_t p,
+                           const double* power_vectors, int power_count, int max_iters, double tol,
+                           double* out, nenmf_device_status* status,
+                           void* ws, size_t ws_bytes, void* stream);
+
+/* grad = A^T (A F - B) in Gram form (nnls.py:72-86); same operand forms as
+ * nenmf_solve_nnls.  grad is (p x c). */
+size_t nenmf_gradient_workspace_bytes(int dtype, int64_t r, int64_t p, int64_t c);
+int nenmf_gradient(int dtype, const void* At, int64_t r, int64_t p,
+                   const void* B, int64_t c, int64_t ldb, int trans_b,
+                   const void* F, void* grad, void* ws, size_t ws_bytes, void* stream);
+
+/* sum over entries of (F > 0 ? g : min(g, 0))^2 -> *out (nnls.py:89-107) */
+size_t nenmf_reduce_workspace_bytes(int64_t count);
+int nenmf_pg_norm_sq(int dtype, const void* F, const void* g, int64_t count,
+                     double* out, void* ws, size_t ws_bytes, void* stream);
+/* sum of squares of `count` contiguous entries -> *out (matrix.py:177-179) */
+int nenmf_sumsq(int dtype, const void* M, int64_t count, double* out,
+                void* ws, size_t ws_bytes, void* stream);
+
+/* ||X - G F||_F^2 -> *out, X (n x m, ld ldx), G passed as Gt (p x n),
+ * F (p x m) (factorize.py:139; tracing.py:45-57) */
+size_t nenmf_residual_sumsq_workspace_bytes(int dtype, int64_t n, int64_t m, int64_t p);
+int nenmf_residual_sumsq(int dtype, const void* X, int64_t n, int64_t m, int64_t ldx,
+                         const void* Gt, const void* F, int64_t p, double* out,
+                         void* ws, size_t ws_bytes, void* stream);
+
+/* C (p x q) = A (p x K) B (q x K)^T, long K (factorize.py:110,113). */
+size_t nenmf_abt_workspace_bytes(int dtype, int64_t p, int64_t q, int64_t K);
+int nenmf_abt(int dtype, const void* A, int64_t p, const void* B, int64_t q, int64_t K,
+              void* C, void* ws, size_t ws_bytes, void* stream);
+
+/* ---- randomized subspace iteration (compression.py:120-188) ------------- */
+
+/* One streaming pass over X (n x m, ld ldx) computing, when the operand is
+ * non-NULL, Yt = At X^T (k x n; At is k x m) and Zt = Bt X (k x m; Bt is
+ * k x n), i.e. X @ A and X.T @ B of the reference (compression.py:134-139)
+ * stored transposed.  Deterministic (fixed-order reduction). */
+size_t nenmf_dual_pass_workspace_bytes(int dtype, int64_t n, int64_t m, int64_t k);
+int nenmf_dual_pass(int dtype, const void* X, int64_t n, int64_t m, int64_t ldx,
+                    const void* At, const void* Bt, int64_t k, void* Yt, void* Zt,
+                    void* ws, size_t ws_bytes, void* stream);
+
+/* In-place orthonormal basis of a tall rows x k panel given as Pt (k x rows):
+ * reduced Householder QR (TSQR), rank deficiency tolerated, collapse (non-
+ * finite input or all-zero diag R) -> status NUMERICAL_COLLAPSE
+ * (compression.py:88-106). */
+size_t nenmf_orthonormalize_workspace_bytes(int64_t rows, int64_t k);
+int nenmf_orthonormalize(int dtype, void* Pt, int64_t rows, int64_t k,
+                         nenmf_device_status* status, void* ws, size_t ws_bytes,
+                         void* stream);
+
+/* Algorithm 2: L (nu x n) and Rt (nu x m, i.e. R transposed) from the
+ * reference's Gaussian draws: omega_l_t = Omega_L^T (nu x m), omega_r
+ * (nu x n) (compression.py:130-141). */
+size_t nenmf_rsi_workspace_bytes(int dtype, int64_t n, int64_t m, int64_t nu);
+int nenmf_rsi(int dtype, const void* X, int64_t n, int64_t m, int64_t ldx,
+              const void* omega_l_t, const void* omega_r, int64_t nu, int q,
+              void* L, void* Rt, nenmf_device_status* status,
+              void* ws, size_t ws_bytes, void* stream);
+
+/* X_L = L X (nu x m) and X_R^T = (X R)^T (nu x n) (compression.py:179-188) */
+int nenmf_compress(int dtype, const void* X, int64_t n, int64_t m, int64_t ldx,
+                   const void* L, const void* Rt, int64_t nu, void* XL, void* XRt,
+                   void* ws, size_t ws_bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NENMF_B200_H */

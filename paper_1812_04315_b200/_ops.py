@@ -1,0 +1,156 @@
+"""Device-level operations: thin, asynchronous wrappers of the C ABI.
+
+All tensors are CUDA tensors of one dtype (float64 for "fp64", float32 for
+"fp32").  Skinny operands follow the library's short-major convention (a tall
+n x k panel is held as its k x n transpose).  Nothing here synchronises unless
+it says so; failures land in device status words.
+"""
+
+from __future__ import annotations
+
+from . import _lib
+
+POWER_TOL = 1e-9        # matrix.py:158 default tol used by solve_nnls (nnls.py:159)
+POWER_MAX_ITERS = 100   # matrix.py:158 default max_iters
+
+
+def _dt(t) -> str:
+    torch = _lib.torch_mod()
+    if t.dtype == torch.float64:
+        return "fp64"
+    if t.dtype == torch.float32:
+        return "fp32"
+    raise TypeError(f"unsupported tensor dtype {t.dtype}")
+
+
+def solve(At, B, F0, Fout, *, trans_b: bool, max_iter: int, grad_tol: float, lipschitz_safety: float,
+          status, status_index: int = 0) -> None:
+    """nenmf_solve_nnls: At (p x r), B (r x c) or, with trans_b, the (c x r)
+    matrix whose transpose is B; F0/Fout (p x c)."""
+    lib, _ = _lib.require_device()
+    dt = _dt(At)
+    p, r = At.shape
+    c = F0.shape[1]
+    ldb = B.shape[1]
+    if trans_b:
+        assert B.shape == (c, r)
+    else:
+        assert B.shape == (r, c)
+    k = min(r, p)
+    pv = _lib.power_vectors(k)
+    code = _lib.code_of(dt)
+    nbytes = lib.nenmf_solve_nnls_workspace_bytes(code, r, p, c)
+    ws = _lib.workspace(nbytes)
+    rc = lib.nenmf_solve_nnls(code, At.data_ptr(), r, p, B.data_ptr(), c, ldb, 1 if trans_b else 0,
+                              F0.data_ptr(), Fout.data_ptr(), int(max_iter), float(grad_tol),
+                              float(lipschitz_safety), pv.data_ptr(), pv.shape[0], POWER_MAX_ITERS,
+                              POWER_TOL, _lib.status_ptr(status, status_index), ws.data_ptr(), ws.numel(),
+                              _lib.stream_handle())
+    _lib.check(rc, "solve_nnls")
+
+
+def spectral_norm_sq(At, tol: float, max_iters: int, out, status) -> None:
+    lib, _ = _lib.require_device()
+    dt = _dt(At)
+    p, r = At.shape
+    pv = _lib.power_vectors(min(r, p))
+    code = _lib.code_of(dt)
+    ws = _lib.workspace(lib.nenmf_spectral_norm_sq_workspace_bytes(code, r, p))
+    rc = lib.nenmf_spectral_norm_sq(code, At.data_ptr(), r, p, pv.data_ptr(), pv.shape[0], int(max_iters),
+                                    float(tol), out.data_ptr(), _lib.status_ptr(status), ws.data_ptr(),
+                                    ws.numel(), _lib.stream_handle())
+    _lib.check(rc, "spectral_norm_sq")
+
+
+def gradient(At, B, F, out, *, trans_b: bool = False) -> None:
+    lib, _ = _lib.require_device()
+    code = _lib.code_of(_dt(At))
+    p, r = At.shape
+    c = F.shape[1]
+    ws = _lib.workspace(lib.nenmf_gradient_workspace_bytes(code, r, p, c))
+    rc = lib.nenmf_gradient(code, At.data_ptr(), r, p, B.data_ptr(), c, B.shape[1], 1 if trans_b else 0,
+                            F.data_ptr(), out.data_ptr(), ws.data_ptr(), ws.numel(), _lib.stream_handle())
+    _lib.check(rc, "gradient")
+
+
+def sumsq(M, out, g=None) -> None:
+    """out[0] = sum M^2, or sum PG(M, g)^2 when g is given."""
+    lib, _ = _lib.require_device()
+    code = _lib.code_of(_dt(M))
+    n = M.numel()
+    ws = _lib.workspace(lib.nenmf_reduce_workspace_bytes(n))
+    if g is None:
+        rc = lib.nenmf_sumsq(code, M.data_ptr(), n, out.data_ptr(), ws.data_ptr(), ws.numel(),
+                             _lib.stream_handle())
+    else:
+        rc = lib.nenmf_pg_norm_sq(code, M.data_ptr(), g.data_ptr(), n, out.data_ptr(), ws.data_ptr(),
+                                  ws.numel(), _lib.stream_handle())
+    _lib.check(rc, "sumsq")
+
+
+def residual_sumsq(X, Gt, F, out) -> None:
+    """out[0] = ||X - Gt^T F||_F^2."""
+    lib, _ = _lib.require_device()
+    code = _lib.code_of(_dt(X))
+    n, m = X.shape
+    p = Gt.shape[0]
+    ws = _lib.workspace(lib.nenmf_residual_sumsq_workspace_bytes(code, n, m, p))
+    rc = lib.nenmf_residual_sumsq(code, X.data_ptr(), n, m, X.stride(0), Gt.data_ptr(), F.data_ptr(), p,
+                                  out.data_ptr(), ws.data_ptr(), ws.numel(), _lib.stream_handle())
+    _lib.check(rc, "residual_sumsq")
+
+
+def abt(A, B, out) -> None:
+    """out (p x q) = A (p x K) B (q x K)^T."""
+    lib, _ = _lib.require_device()
+    code = _lib.code_of(_dt(A))
+    p, K = A.shape
+    q = B.shape[0]
+    ws = _lib.workspace(lib.nenmf_abt_workspace_bytes(code, p, q, K))
+    rc = lib.nenmf_abt(code, A.data_ptr(), p, B.data_ptr(), q, K, out.data_ptr(), ws.data_ptr(), ws.numel(),
+                       _lib.stream_handle())
+    _lib.check(rc, "abt")
+
+
+def dual_pass(X, At, Bt, Yt, Zt) -> None:
+    lib, _ = _lib.require_device()
+    code = _lib.code_of(_dt(X))
+    n, m = X.shape
+    k = (At if At is not None else Bt).shape[0]
+    ws = _lib.workspace(lib.nenmf_dual_pass_workspace_bytes(code, n, m, k))
+    rc = lib.nenmf_dual_pass(code, X.data_ptr(), n, m, X.stride(0), _lib.ptr(At), _lib.ptr(Bt), k,
+                             _lib.ptr(Yt), _lib.ptr(Zt), ws.data_ptr(), ws.numel(), _lib.stream_handle())
+    _lib.check(rc, "dual_pass")
+
+
+def orthonormalize(Pt, status) -> None:
+    lib, _ = _lib.require_device()
+    code = _lib.code_of(_dt(Pt))
+    k, rows = Pt.shape
+    ws = _lib.workspace(lib.nenmf_orthonormalize_workspace_bytes(rows, k))
+    rc = lib.nenmf_orthonormalize(code, Pt.data_ptr(), rows, k, _lib.status_ptr(status), ws.data_ptr(),
+                                  ws.numel(), _lib.stream_handle())
+    _lib.check(rc, "orthonormalize")
+
+
+def rsi(X, omega_l_t, omega_r, q: int, L, Rt, status) -> None:
+    lib, _ = _lib.require_device()
+    code = _lib.code_of(_dt(X))
+    n, m = X.shape
+    nu = omega_r.shape[0]
+    ws = _lib.workspace(lib.nenmf_rsi_workspace_bytes(code, n, m, nu))
+    rc = lib.nenmf_rsi(code, X.data_ptr(), n, m, X.stride(0), omega_l_t.data_ptr(), omega_r.data_ptr(), nu,
+                       int(q), L.data_ptr(), Rt.data_ptr(), _lib.status_ptr(status), ws.data_ptr(), ws.numel(),
+                       _lib.stream_handle())
+    _lib.check(rc, "subspace_iteration_pair")
+
+
+def compress(X, L, Rt, XL, XRt) -> None:
+    lib, _ = _lib.require_device()
+    code = _lib.code_of(_dt(X))
+    n, m = X.shape
+    nu = L.shape[0]
+    ws = _lib.workspace(lib.nenmf_rsi_workspace_bytes(code, n, m, nu))
+    rc = lib.nenmf_compress(code, X.data_ptr(), n, m, X.stride(0), L.data_ptr(), Rt.data_ptr(), nu,
+                            XL.data_ptr(), XRt.data_ptr(), ws.data_ptr(), ws.numel(), _lib.stream_handle())
+    _lib.check(rc, "compress_problem")

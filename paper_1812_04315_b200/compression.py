@@ -1,0 +1,170 @@
+"""Sketch operators and data compression (reference ``compression.py``).
+
+``subspace_iteration_pair`` (Alg. 2, ``compression.py:120-141``) and
+``compress_problem`` (``:179-188``) run on the GPU: the Gaussian draws are
+made on the host with the reference's exact NumPy stream, then every pass
+over X and every QR executes in ``libnenmf_b200`` (fused X-passes that serve
+the L-chain and the R-chain from one read of X; TSQR in shared memory).
+``gaussian_sketch_pair`` is host RNG only, as in the reference.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib, _ops
+from .errors import DimensionError, ZeroMatrixError, raise_for_status
+from .matrix import DenseMatrix, as_matrix, check_seed
+
+GAUSSIAN = "gaussian"
+POWER_ITERATION = "power_iteration"
+SUBSPACE_ITERATION = "subspace_iteration"
+SCHEMES = (GAUSSIAN, POWER_ITERATION, SUBSPACE_ITERATION)
+
+
+@dataclass(frozen=True, eq=False)
+class SketchPair:
+    """L (nu x n) left-compresses, R (m x nu) right-compresses
+    (compression.py:42-55).  ``device`` (extension) optionally caches the
+    device copies (L, R^T) keyed by dtype so factorization can skip re-upload."""
+
+    L: DenseMatrix
+    R: DenseMatrix
+    nu: int
+    scheme: str
+    q: int
+    seed: int
+    device: dict = field(default_factory=dict, repr=False, compare=False)
+
+
+@dataclass(frozen=True, eq=False)
+class CompressedProblem:
+    """X_L = L X (nu x m) and X_R = X R (n x nu) (compression.py:58-63)."""
+
+    X_L: DenseMatrix
+    X_R: DenseMatrix
+
+
+def _check_sketch_dims(n: int, m: int, nu: int) -> None:
+    if nu < 1:
+        raise DimensionError(f"target rank must be >= 1, got {nu}")
+    if n < 1 or m < 1:
+        raise DimensionError(f"data dimensions must be positive, got {n}x{m}")
+
+
+def gaussian_sketch_pair(n: int, m: int, nu: int, seed: int) -> SketchPair:
+    """L = Omega_L / sqrt(nu), R = Omega_R / sqrt(nu), L drawn first
+    (compression.py:73-85).  Host RNG only."""
+    _check_sketch_dims(n, m, nu)
+    gen = np.random.default_rng(check_seed(seed))
+    scale = 1.0 / np.sqrt(nu)
+    L = gen.standard_normal((nu, n)) * scale
+    R = gen.standard_normal((m, nu)) * scale
+    return SketchPair(L=L, R=R, nu=nu, scheme=GAUSSIAN, q=0, seed=seed)
+
+
+def _check_iteration_inputs(n: int, m: int, nu: int, q: int, nonzero: bool) -> None:
+    """compression.py:109-117, same order."""
+    _check_sketch_dims(n, m, nu)
+    if nu > min(n, m):
+        raise DimensionError(f"target rank {nu} exceeds min(n, m) = {min(n, m)}")
+    if q < 1:
+        raise ValueError(f"iteration count must be >= 1, got {q}")
+    if not nonzero:
+        raise ZeroMatrixError("cannot sketch the zero matrix")
+
+
+def sketch_draws(n: int, m: int, nu: int, seed: int):
+    """The reference's Gaussian start blocks, Omega_L (m x nu) then Omega_R
+    (nu x n), from one PCG64 stream (compression.py:130-132)."""
+    gen = np.random.default_rng(check_seed(seed))
+    omega_l = gen.standard_normal((m, nu))
+    omega_r = gen.standard_normal((nu, n))
+    return omega_l, omega_r
+
+
+def rsi_device(Xd, nu: int, q: int, seed: int):
+    """Device RSI on a resident X (CUDA tensor).  Returns (L, Rt, status)
+    tensors without synchronising; Rt is R transposed (nu x m)."""
+    _, torch = _lib.require_device()
+    n, m = Xd.shape
+    omega_l, omega_r = sketch_draws(n, m, nu, seed)
+    dtype = "fp64" if Xd.dtype == torch.float64 else "fp32"
+    om_lt = _lib.to_device(np.ascontiguousarray(omega_l.T), dtype)
+    om_r = _lib.to_device(omega_r, dtype)
+    L = torch.empty((nu, n), dtype=Xd.dtype, device="cuda")
+    Rt = torch.empty((nu, m), dtype=Xd.dtype, device="cuda")
+    status = _lib.new_status()
+    _ops.rsi(Xd, om_lt, om_r, q, L, Rt, status)
+    return L, Rt, status
+
+
+def _is_device_tensor(x) -> bool:
+    return hasattr(x, "is_cuda") and bool(getattr(x, "is_cuda"))
+
+
+def subspace_iteration_pair(X, nu: int, q: int, seed: int, *, dtype: str = "fp64") -> SketchPair:
+    """Randomized subspace iteration with a QR after every product
+    (compression.py:120-141), on the GPU.  Returns NumPy L = Q_col^T and
+    R = Q_row like the reference; the device copies are cached on the pair."""
+    if _is_device_tensor(X):
+        Xd = X
+        dtype = "fp64" if str(X.dtype).endswith("float64") else "fp32"
+        n, m = X.shape
+        nonzero = bool((X != 0).any().item())
+    else:
+        Xh = as_matrix(X, "X")
+        n, m = Xh.shape
+        nonzero = bool(Xh.any())
+        Xd = None
+    _check_iteration_inputs(n, m, nu, q, nonzero)
+    _lib.require_device()
+    if Xd is None:
+        Xd = _lib.to_device(Xh, dtype)
+    L, Rt, status = rsi_device(Xd, nu, q, seed)
+    st = _lib.read_status(status)[0]
+    if st["code"] != 0:
+        raise_for_status(int(st["code"]), int(st["iteration"]), "subspace iteration")
+    pair = SketchPair(L=_lib.to_host(L), R=np.ascontiguousarray(_lib.to_host(Rt).T), nu=nu,
+                      scheme=SUBSPACE_ITERATION, q=q, seed=seed)
+    pair.device[dtype] = (L, Rt)
+    return pair
+
+
+def sketch_on_device(sketch: SketchPair, dtype: str):
+    """(L, R^T) of a sketch as CUDA tensors of ``dtype`` (cached)."""
+    hit = sketch.device.get(dtype)
+    if hit is not None:
+        return hit
+    L = _lib.to_device(np.ascontiguousarray(sketch.L), dtype)
+    Rt = _lib.to_device(np.ascontiguousarray(np.asarray(sketch.R, dtype=np.float64).T), dtype)
+    sketch.device[dtype] = (L, Rt)
+    return L, Rt
+
+
+def compress_device(Xd, L, Rt):
+    """(X_L, X_R^T) on the device from one fused pass over X."""
+    torch = _lib.torch_mod()
+    nu = L.shape[0]
+    n, m = Xd.shape
+    XL = torch.empty((nu, m), dtype=Xd.dtype, device="cuda")
+    XRt = torch.empty((nu, n), dtype=Xd.dtype, device="cuda")
+    _ops.compress(Xd, L, Rt, XL, XRt)
+    return XL, XRt
+
+
+def compress_problem(X, sketch: SketchPair, *, dtype: str = "fp64") -> CompressedProblem:
+    """X_L = L X and X_R = X R (compression.py:179-188), one pass on the GPU."""
+    X = as_matrix(X, "X")
+    n, m = X.shape
+    if np.shape(sketch.L) != (sketch.nu, n) or np.shape(sketch.R) != (m, sketch.nu):
+        raise DimensionError(
+            f"sketch shapes L {np.shape(sketch.L)}, R {np.shape(sketch.R)} do not match "
+            f"data {n}x{m} at target rank {sketch.nu}")
+    _lib.require_device()
+    Xd = _lib.to_device(X, dtype)
+    L, Rt = sketch_on_device(sketch, dtype)
+    XL, XRt = compress_device(Xd, L, Rt)
+    return CompressedProblem(X_L=_lib.to_host(XL), X_R=np.ascontiguousarray(_lib.to_host(XRt).T))

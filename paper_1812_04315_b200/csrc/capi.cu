@@ -1,0 +1,228 @@
+// extern "C" boundary of libnenmf_b200 (declared in include/nenmf_b200.h).
+// Plain pointers and sizes only; dtype-dispatches into the templated kernels.
+#include "common.cuh"
+#include "nnls.cuh"
+#include "rsi.cuh"
+#include "skinny.cuh"
+
+using namespace nenmf;
+
+namespace {
+inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+template <typename T>
+inline const T* C(const void* p) { return static_cast<const T*>(p); }
+template <typename T>
+inline T* M(void* p) { return static_cast<T*>(p); }
+// a live (launching) arena even when the caller passes no scratch: carving
+// then fails with NENMF_ERR_WORKSPACE instead of silently dry-running
+inline Arena live(void* ws, size_t bytes) {
+  return ws != nullptr ? Arena(ws, bytes) : Arena(reinterpret_cast<void*>(256), 0);
+}
+}  // namespace
+
+extern "C" {
+
+int nenmf_abi_version(void) { return NENMF_ABI_VERSION; }
+
+const char* nenmf_status_string(int code) {
+  switch (code) {
+    case NENMF_OK: return "ok";
+    case NENMF_ERR_DIM: return "dimension error";
+    case NENMF_ERR_ZERO_MATRIX: return "zero matrix";
+    case NENMF_ERR_NUMERICAL_FAILURE: return "numerical failure (non-finite iterate)";
+    case NENMF_ERR_NUMERICAL_COLLAPSE: return "numerical collapse (sketch iterate)";
+    case NENMF_ERR_VALUE: return "invalid value";
+    case NENMF_ERR_CUDA: return "CUDA error";
+    case NENMF_ERR_WORKSPACE: return "workspace too small";
+    case NENMF_ERR_UNSUPPORTED: return "unsupported shape";
+    default: return "unknown status";
+  }
+}
+
+int nenmf_device_sm_count(void) { return sm_count(); }
+
+// ------------------------------------------------------------ solver ----
+size_t nenmf_solve_nnls_workspace_bytes(int dtype, int64_t r, int64_t p, int64_t c) {
+  Arena a(nullptr, 0);
+  NENMF_DISPATCH(dtype, [&] {
+    return solve_nnls<scalar_t>(a, nullptr, r, p, nullptr, c, c, false, nullptr, nullptr, 1, 1e-4, 1.0, nullptr, 1,
+                                100, 1e-9, nullptr, nullptr);
+  });
+  // the transposed-B variant carves the same scratch
+  return a.used + 256;
+}
+
+int nenmf_solve_nnls(int dtype, const void* At, int64_t r, int64_t p, const void* B, int64_t c, int64_t ldb,
+                     int trans_b, const void* F0, void* F_out, int max_iter, double grad_tol,
+                     double lipschitz_safety, const double* power_vectors, int power_count, int power_max_iters,
+                     double power_tol, nenmf_device_status* status, void* ws, size_t ws_bytes, void* stream) {
+  if (ws == nullptr || status == nullptr) return NENMF_ERR_VALUE;
+  Arena a(ws, ws_bytes);
+  return NENMF_DISPATCH(dtype, [&] {
+    return solve_nnls<scalar_t>(a, C<scalar_t>(At), r, p, C<scalar_t>(B), c, ldb, trans_b != 0, C<scalar_t>(F0),
+                                M<scalar_t>(F_out), max_iter, grad_tol, lipschitz_safety, power_vectors,
+                                power_count, power_max_iters, power_tol, status, S(stream));
+  });
+}
+
+size_t nenmf_spectral_norm_sq_workspace_bytes(int dtype, int64_t r, int64_t p) {
+  Arena a(nullptr, 0);
+  NENMF_DISPATCH(dtype, [&] {
+    return spectral_norm_sq<scalar_t>(a, nullptr, r, p, nullptr, 1, 100, 1e-9, nullptr, nullptr, nullptr);
+  });
+  return a.used + 256;
+}
+
+int nenmf_spectral_norm_sq(int dtype, const void* At, int64_t r, int64_t p, const double* power_vectors,
+                           int power_count, int max_iters, double tol, double* out, nenmf_device_status* status, void* ws,
+                           size_t ws_bytes, void* stream) {
+  if (ws == nullptr) return NENMF_ERR_VALUE;
+  Arena a(ws, ws_bytes);
+  return NENMF_DISPATCH(dtype, [&] {
+    return spectral_norm_sq<scalar_t>(a, C<scalar_t>(At), r, p, power_vectors, power_count, max_iters, tol, out,
+                                      status, S(stream));
+  });
+}
+
+size_t nenmf_gradient_workspace_bytes(int dtype, int64_t r, int64_t p, int64_t c) {
+  Arena a(nullptr, 0);
+  NENMF_DISPATCH(dtype, [&] {
+    return gradient<scalar_t>(a, nullptr, r, p, nullptr, c, c, false, nullptr, nullptr, nullptr);
+  });
+  return a.used + 256;
+}
+
+int nenmf_gradient(int dtype, const void* At, int64_t r, int64_t p, const void* B, int64_t c, int64_t ldb,
+                   int trans_b, const void* F, void* grad, void* ws, size_t ws_bytes, void* stream) {
+  if (ws == nullptr) return NENMF_ERR_VALUE;
+  Arena a(ws, ws_bytes);
+  return NENMF_DISPATCH(dtype, [&] {
+    return gradient<scalar_t>(a, C<scalar_t>(At), r, p, C<scalar_t>(B), c, ldb, trans_b != 0, C<scalar_t>(F),
+                              M<scalar_t>(grad), S(stream));
+  });
+}
+
+// -------------------------------------------------------- reductions ----
+size_t nenmf_reduce_workspace_bytes(int64_t count) {
+  Arena a(nullptr, 0);
+  sumsq<double>(a, nullptr, nullptr, count, nullptr, nullptr);
+  return a.used + 256;
+}
+
+int nenmf_pg_norm_sq(int dtype, const void* F, const void* g, int64_t count, double* out, void* ws,
+                     size_t ws_bytes, void* stream) {
+  if (g == nullptr || ws == nullptr) return NENMF_ERR_VALUE;
+  Arena a(ws, ws_bytes);
+  return NENMF_DISPATCH(dtype, [&] {
+    return sumsq<scalar_t>(a, C<scalar_t>(F), C<scalar_t>(g), count, out, S(stream));
+  });
+}
+
+int nenmf_sumsq(int dtype, const void* Mx, int64_t count, double* out, void* ws, size_t ws_bytes, void* stream) {
+  if (ws == nullptr) return NENMF_ERR_VALUE;
+  Arena a(ws, ws_bytes);
+  return NENMF_DISPATCH(dtype, [&] { return sumsq<scalar_t>(a, C<scalar_t>(Mx), nullptr, count, out, S(stream)); });
+}
+
+size_t nenmf_residual_sumsq_workspace_bytes(int dtype, int64_t n, int64_t m, int64_t p) {
+  Arena a(nullptr, 0);
+  NENMF_DISPATCH(dtype, [&] {
+    return resid<scalar_t>(a, nullptr, p, n, nullptr, m, m, false, nullptr, nullptr, nullptr, nullptr, nullptr);
+  });
+  return a.used + 256 + 2 * sizeof(double) + 256;
+}
+
+int nenmf_residual_sumsq(int dtype, const void* X, int64_t n, int64_t m, int64_t ldx, const void* Gt,
+                         const void* F, int64_t p, double* out, void* ws, size_t ws_bytes, void* stream) {
+  if (ws == nullptr) return NENMF_ERR_VALUE;
+  Arena a(ws, ws_bytes);
+  double* out2 = a.take<double>(2);
+  if (!a.ok) return NENMF_ERR_WORKSPACE;
+  int rc = NENMF_DISPATCH(dtype, [&] {
+    // rows of X are the "r" dimension: R[i][j] = sum_a Gt[a][i] F[a][j] - X[i][j]
+    return resid<scalar_t>(a, C<scalar_t>(Gt), p, n, C<scalar_t>(X), m, ldx, false, C<scalar_t>(F), nullptr, out2,
+                           nullptr, S(stream));
+  });
+  if (rc != NENMF_OK) return rc;
+  NENMF_CUDA_TRY(cudaMemcpyAsync(out, out2, sizeof(double), cudaMemcpyDeviceToDevice, S(stream)));
+  return NENMF_OK;
+}
+
+size_t nenmf_abt_workspace_bytes(int dtype, int64_t p, int64_t q, int64_t K) {
+  Arena a(nullptr, 0);
+  NENMF_DISPATCH(dtype, [&] { return abt<scalar_t>(a, nullptr, p, nullptr, q, K, nullptr, nullptr); });
+  return a.used + 256;
+}
+
+int nenmf_abt(int dtype, const void* A, int64_t p, const void* B, int64_t q, int64_t K, void* Cm, void* ws,
+              size_t ws_bytes, void* stream) {
+  Arena a = live(ws, ws_bytes);
+  return NENMF_DISPATCH(dtype, [&] {
+    return abt<scalar_t>(a, C<scalar_t>(A), p, C<scalar_t>(B), q, K, M<scalar_t>(Cm), S(stream));
+  });
+}
+
+// --------------------------------------------------------------- RSI ----
+size_t nenmf_dual_pass_workspace_bytes(int dtype, int64_t n, int64_t m, int64_t k) {
+  Arena a(nullptr, 0);
+  NENMF_DISPATCH(dtype, [&] {
+    const scalar_t* sent = reinterpret_cast<const scalar_t*>(alignof(scalar_t));
+    return dual_pass<scalar_t>(a, sent, n, m, m, sent, sent, k, nullptr, nullptr, nullptr);
+  });
+  return a.used + 256;
+}
+
+int nenmf_dual_pass(int dtype, const void* X, int64_t n, int64_t m, int64_t ldx, const void* At, const void* Bt,
+                    int64_t k, void* Yt, void* Zt, void* ws, size_t ws_bytes, void* stream) {
+  Arena a = live(ws, ws_bytes);
+  return NENMF_DISPATCH(dtype, [&] {
+    return dual_pass<scalar_t>(a, C<scalar_t>(X), n, m, ldx, C<scalar_t>(At), C<scalar_t>(Bt), k, M<scalar_t>(Yt),
+                               M<scalar_t>(Zt), S(stream));
+  });
+}
+
+size_t nenmf_orthonormalize_workspace_bytes(int64_t rows, int64_t k) {
+  Arena a(nullptr, 0);
+  orthonormalize<double>(a, nullptr, rows, k, nullptr, nullptr);
+  return a.used + 256;
+}
+
+int nenmf_orthonormalize(int dtype, void* Pt, int64_t rows, int64_t k, nenmf_device_status* status, void* ws,
+                         size_t ws_bytes, void* stream) {
+  if (ws == nullptr) return NENMF_ERR_VALUE;
+  Arena a(ws, ws_bytes);
+  return NENMF_DISPATCH(dtype, [&] { return orthonormalize<scalar_t>(a, M<scalar_t>(Pt), rows, k, status, S(stream)); });
+}
+
+size_t nenmf_rsi_workspace_bytes(int dtype, int64_t n, int64_t m, int64_t nu) {
+  Arena a(nullptr, 0);
+  NENMF_DISPATCH(dtype, [&] {
+    return rsi<scalar_t>(a, nullptr, n, m, m, nullptr, nullptr, nu, 1, nullptr, nullptr, nullptr, nullptr);
+  });
+  // compress reuses the same scratch shape as one pass
+  size_t c = nenmf_dual_pass_workspace_bytes(dtype, n, m, nu);
+  return (a.used > c ? a.used : c) + 256;
+}
+
+int nenmf_rsi(int dtype, const void* X, int64_t n, int64_t m, int64_t ldx, const void* omega_l_t,
+              const void* omega_r, int64_t nu, int q, void* L, void* Rt, nenmf_device_status* status, void* ws,
+              size_t ws_bytes, void* stream) {
+  if (ws == nullptr) return NENMF_ERR_VALUE;
+  Arena a(ws, ws_bytes);
+  return NENMF_DISPATCH(dtype, [&] {
+    return rsi<scalar_t>(a, C<scalar_t>(X), n, m, ldx, C<scalar_t>(omega_l_t), C<scalar_t>(omega_r), nu, q,
+                         M<scalar_t>(L), M<scalar_t>(Rt), status, S(stream));
+  });
+}
+
+int nenmf_compress(int dtype, const void* X, int64_t n, int64_t m, int64_t ldx, const void* L, const void* Rt,
+                   int64_t nu, void* XL, void* XRt, void* ws, size_t ws_bytes, void* stream) {
+  if (ws == nullptr) return NENMF_ERR_VALUE;
+  Arena a(ws, ws_bytes);
+  return NENMF_DISPATCH(dtype, [&] {
+    return compress<scalar_t>(a, C<scalar_t>(X), n, m, ldx, C<scalar_t>(L), C<scalar_t>(Rt), nu, M<scalar_t>(XL),
+                              M<scalar_t>(XRt), S(stream));
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,408 @@
+// Skinny products and fixed-order reductions (CUDA cores, sm_100a).
+//
+//   abt      C = A B^T, long K            F @ R, L @ G, Gram A^T A (factorize.py:110,113; nnls.py:157)
+//   ab       V = At B (B or B^T view)     A.T @ B                   (nnls.py:158)
+//   resid    sum (At^T F - B)^2, 1-2 F's  _true_objective, emit     (nnls.py:115-116,225; factorize.py:139)
+//   sumsq    sum M^2                      frobenius_norm            (matrix.py:177-179)
+//   pg_sumsq sum PG(F,g)^2                projected_gradient_norm   (nnls.py:89-107)
+//   wfv      W F - V                      gradient (Gram form)      (nnls.py:72-86)
+//
+// Every reduction is deterministic: K is cut into chunks whose size depends
+// only on the shape, each output is one sequential FMA chain per chunk, and
+// chunk partials are added in chunk order.  Two calls with the same shapes
+// therefore perform bit-identical arithmetic whatever the memory layout of B
+// -- which is what makes identity-sketch compressed NeNMF reproduce vanilla
+// NeNMF exactly (reference test_factorize.py:161-176).
+#include "skinny.cuh"
+
+namespace nenmf {
+
+// ----------------------------------------------------------------- abt ----
+constexpr int ABT_KT = 32;
+constexpr int64_t ABT_KCHUNK = 4096;
+constexpr int ABT_THREADS = 256;
+constexpr int ABT_MAXO = 32;  // outputs per thread: p*q <= 8192
+
+template <typename T>
+__global__ void __launch_bounds__(ABT_THREADS)
+k_abt(const T* __restrict__ A, int p, const T* __restrict__ B, int q, int64_t K,
+      int64_t kchunk, double* __restrict__ part, T* __restrict__ C) {
+  extern __shared__ double smem_d[];
+  double* As = smem_d;                       // [p][KT+1]
+  double* Bs = smem_d + p * (ABT_KT + 1);    // [q][KT+1]
+  const int tid = threadIdx.x;
+  const int64_t k0 = blockIdx.x * kchunk;
+  const int64_t k1 = min(K, k0 + kchunk);
+  const int npq = p * q;
+  double acc[ABT_MAXO];
+#pragma unroll
+  for (int s = 0; s < ABT_MAXO; ++s) acc[s] = 0.0;
+
+  for (int64_t kt = k0; kt < k1; kt += ABT_KT) {
+    const int nk = (int)imin(ABT_KT, k1 - kt);
+    for (int idx = tid; idx < p * ABT_KT; idx += blockDim.x) {
+      int a = idx / ABT_KT, kk = idx % ABT_KT;
+      As[a * (ABT_KT + 1) + kk] = kk < nk ? (double)A[(int64_t)a * K + kt + kk] : 0.0;
+    }
+    for (int idx = tid; idx < q * ABT_KT; idx += blockDim.x) {
+      int b = idx / ABT_KT, kk = idx % ABT_KT;
+      Bs[b * (ABT_KT + 1) + kk] = kk < nk ? (double)B[(int64_t)b * K + kt + kk] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int s = 0; s < ABT_MAXO; ++s) {
+      int o = tid + s * ABT_THREADS;
+      if (o < npq) {
+        const double* ar = As + (o / q) * (ABT_KT + 1);
+        const double* br = Bs + (o % q) * (ABT_KT + 1);
+        double a = acc[s];
+        for (int kk = 0; kk < nk; ++kk) a = fma(ar[kk], br[kk], a);
+        acc[s] = a;
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int s = 0; s < ABT_MAXO; ++s) {
+    int o = tid + s * ABT_THREADS;
+    if (o < npq) {
+      if (C != nullptr) C[o] = (T)acc[s];
+      else part[(int64_t)blockIdx.x * npq + o] = acc[s];
+    }
+  }
+}
+
+template <typename T>
+__global__ void k_abt_reduce(const double* __restrict__ part, int nchunk, int npq, T* __restrict__ C) {
+  int o = blockIdx.x * blockDim.x + threadIdx.x;
+  if (o >= npq) return;
+  double s = part[o];
+  for (int c = 1; c < nchunk; ++c) s += part[(int64_t)c * npq + o];
+  C[o] = (T)s;
+}
+
+template <typename T>
+int abt(Arena& ws, const T* A, int64_t p, const T* B, int64_t q, int64_t K, T* C, cudaStream_t st) {
+  if (p < 1 || q < 1 || K < 1) return NENMF_ERR_DIM;
+  if (p * q > ABT_THREADS * ABT_MAXO || p > 512 || q > 512) return NENMF_ERR_UNSUPPORTED;
+  const int64_t nchunk = cdiv(K, ABT_KCHUNK);
+  double* part = nchunk > 1 ? ws.take<double>((size_t)nchunk * p * q) : nullptr;
+  if (ws.base == nullptr) return NENMF_OK;
+  if (!ws.ok) return NENMF_ERR_WORKSPACE;
+  size_t smem = (size_t)(p + q) * (ABT_KT + 1) * sizeof(double);
+  NENMF_CUDA_TRY(cudaFuncSetAttribute(k_abt<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k_abt<T><<<(unsigned)nchunk, ABT_THREADS, smem, st>>>(A, (int)p, B, (int)q, K, ABT_KCHUNK, part,
+                                                       nchunk > 1 ? nullptr : C);
+  NENMF_LAUNCH_CHECK();
+  if (nchunk > 1) {
+    int npq = (int)(p * q);
+    k_abt_reduce<T><<<(unsigned)cdiv(npq, 256), 256, 0, st>>>(part, (int)nchunk, npq, C);
+    NENMF_LAUNCH_CHECK();
+  }
+  return NENMF_OK;
+}
+
+// ------------------------------------------------------------------ ab ----
+constexpr int AB_CB = 64;        // output columns per CTA
+constexpr int AB_RT = 32;        // K rows per smem tile
+constexpr int64_t AB_RCHUNK = 1024;
+constexpr int AB_THREADS = 256;  // 64 columns x 4 row groups of p
+constexpr int AB_MAXA = 16;      // p <= 64
+
+template <typename T, bool TRANS>
+__device__ __forceinline__ void load_b_tile(T* Bs, const T* __restrict__ B, int64_t ldb, int64_t r,
+                                            int64_t c, int64_t t0, int nt, int64_t j0) {
+  // Bs[tt][jj] = B(t0+tt, j0+jj); B(t, j) = TRANS ? Bsrc[j*ldb + t] : Bsrc[t*ldb + j]
+  if (!TRANS) {
+    for (int idx = threadIdx.x; idx < AB_RT * AB_CB; idx += blockDim.x) {
+      int tt = idx / AB_CB, jj = idx % AB_CB;
+      int64_t j = j0 + jj;
+      Bs[tt * (AB_CB + 1) + jj] = (tt < nt && j < c) ? B[(t0 + tt) * ldb + j] : T(0);
+    }
+  } else {
+    for (int idx = threadIdx.x; idx < AB_RT * AB_CB; idx += blockDim.x) {
+      int jj = idx / AB_RT, tt = idx % AB_RT;
+      int64_t j = j0 + jj;
+      Bs[tt * (AB_CB + 1) + jj] = (tt < nt && j < c) ? B[j * ldb + t0 + tt] : T(0);
+    }
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ void load_at_tile(T* Ats, const T* __restrict__ At, int p, int64_t r,
+                                             int64_t t0, int nt) {
+  for (int idx = threadIdx.x; idx < p * AB_RT; idx += blockDim.x) {
+    int a = idx / AB_RT, tt = idx % AB_RT;
+    Ats[a * (AB_RT + 1) + tt] = tt < nt ? At[(int64_t)a * r + t0 + tt] : T(0);
+  }
+}
+
+template <typename T, bool TRANS>
+__global__ void __launch_bounds__(AB_THREADS)
+k_ab(const T* __restrict__ At, int p, int64_t r, const T* __restrict__ B, int64_t c, int64_t ldb,
+     int64_t rchunk, T* __restrict__ part, T* __restrict__ V) {
+  extern __shared__ double smem_d[];
+  T* Bs = reinterpret_cast<T*>(smem_d);            // [RT][CB+1]
+  T* Ats = Bs + AB_RT * (AB_CB + 1);               // [p][RT+1]
+  const int jj = threadIdx.x % AB_CB, g = threadIdx.x / AB_CB;
+  const int64_t j0 = (int64_t)blockIdx.x * AB_CB;
+  const int64_t tc0 = (int64_t)blockIdx.y * rchunk, tc1 = min(r, tc0 + rchunk);
+  T acc[AB_MAXA];
+#pragma unroll
+  for (int s = 0; s < AB_MAXA; ++s) acc[s] = T(0);
+  for (int64_t t0 = tc0; t0 < tc1; t0 += AB_RT) {
+    const int nt = (int)imin(AB_RT, tc1 - t0);
+    load_b_tile<T, TRANS>(Bs, B, ldb, r, c, t0, nt, j0);
+    load_at_tile<T>(Ats, At, p, r, t0, nt);
+    __syncthreads();
+    for (int tt = 0; tt < nt; ++tt) {
+      const T b = Bs[tt * (AB_CB + 1) + jj];
+#pragma unroll
+      for (int s = 0; s < AB_MAXA; ++s) {
+        int a = g + 4 * s;
+        if (a < p) acc[s] = fma_acc(Ats[a * (AB_RT + 1) + tt], b, acc[s]);
+      }
+    }
+    __syncthreads();
+  }
+  const int64_t j = j0 + jj;
+  if (j >= c) return;
+#pragma unroll
+  for (int s = 0; s < AB_MAXA; ++s) {
+    int a = g + 4 * s;
+    if (a < p) {
+      if (V != nullptr) V[(int64_t)a * c + j] = acc[s];
+      else part[((int64_t)blockIdx.y * p + a) * c + j] = acc[s];
+    }
+  }
+}
+
+template <typename T>
+__global__ void k_chunk_reduce(const T* __restrict__ part, int nchunk, int64_t count, T* __restrict__ out) {
+  int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (o >= count) return;
+  T s = part[o];
+  for (int c = 1; c < nchunk; ++c) s += part[(int64_t)c * count + o];
+  out[o] = s;
+}
+
+template <typename T>
+int ab(Arena& ws, const T* At, int64_t p, int64_t r, const T* B, int64_t c, int64_t ldb, bool trans,
+       T* V, cudaStream_t st) {
+  if (p < 1 || r < 1 || c < 1) return NENMF_ERR_DIM;
+  if (p > 4 * AB_MAXA) return NENMF_ERR_UNSUPPORTED;
+  const int64_t nchunk = cdiv(r, AB_RCHUNK);
+  T* part = nchunk > 1 ? ws.take<T>((size_t)nchunk * p * c) : nullptr;
+  if (ws.base == nullptr) return NENMF_OK;
+  if (!ws.ok) return NENMF_ERR_WORKSPACE;
+  size_t smem = ((size_t)AB_RT * (AB_CB + 1) + (size_t)p * (AB_RT + 1)) * sizeof(T);
+  dim3 grid((unsigned)cdiv(c, AB_CB), (unsigned)nchunk);
+  T* direct = nchunk > 1 ? nullptr : V;
+  if (trans) {
+    NENMF_CUDA_TRY(cudaFuncSetAttribute(k_ab<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_ab<T, true><<<grid, AB_THREADS, smem, st>>>(At, (int)p, r, B, c, ldb, AB_RCHUNK, part, direct);
+  } else {
+    NENMF_CUDA_TRY(cudaFuncSetAttribute(k_ab<T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_ab<T, false><<<grid, AB_THREADS, smem, st>>>(At, (int)p, r, B, c, ldb, AB_RCHUNK, part, direct);
+  }
+  NENMF_LAUNCH_CHECK();
+  if (nchunk > 1) {
+    int64_t cnt = p * c;
+    k_chunk_reduce<T><<<(unsigned)cdiv(cnt, 256), 256, 0, st>>>(part, (int)nchunk, cnt, V);
+    NENMF_LAUNCH_CHECK();
+  }
+  return NENMF_OK;
+}
+
+// --------------------------------------------------------------- resid ----
+constexpr int RS_THREADS = 256;  // 64 columns x 4 row groups
+
+template <typename T, bool TRANS>
+__global__ void __launch_bounds__(RS_THREADS)
+k_resid(const T* __restrict__ At, int p, int64_t r, const T* __restrict__ B, int64_t c, int64_t ldb,
+        const T* __restrict__ F1, const T* __restrict__ F2, int64_t rchunk,
+        double* __restrict__ part, const int* __restrict__ gate) {
+  if (gate != nullptr && *gate == 0) return;
+  extern __shared__ double smem_d[];
+  __shared__ double red[33];
+  const int nc = F2 != nullptr ? 2 : 1;
+  T* Bs = reinterpret_cast<T*>(smem_d);          // [RT][CB+1]
+  T* Ats = Bs + AB_RT * (AB_CB + 1);             // [p][RT+1]
+  T* Fs = Ats + p * (AB_RT + 1);                 // [nc][p][CB]
+  const int jj = threadIdx.x % AB_CB, g = threadIdx.x / AB_CB;
+  const int64_t j0 = (int64_t)blockIdx.x * AB_CB;
+  const int64_t tc0 = (int64_t)blockIdx.y * rchunk, tc1 = min(r, tc0 + rchunk);
+  for (int idx = threadIdx.x; idx < nc * p * AB_CB; idx += blockDim.x) {
+    int cand = idx / (p * AB_CB), rem = idx % (p * AB_CB), a = rem / AB_CB, j2 = rem % AB_CB;
+    const T* F = cand == 0 ? F1 : F2;
+    int64_t j = j0 + j2;
+    Fs[idx] = j < c ? F[(int64_t)a * c + j] : T(0);
+  }
+  double acc0 = 0.0, acc1 = 0.0;
+  const bool live = (j0 + jj) < c;
+  for (int64_t t0 = tc0; t0 < tc1; t0 += AB_RT) {
+    const int nt = (int)imin(AB_RT, tc1 - t0);
+    load_b_tile<T, TRANS>(Bs, B, ldb, r, c, t0, nt, j0);
+    load_at_tile<T>(Ats, At, p, r, t0, nt);
+    __syncthreads();
+    if (live) {
+      for (int tt = g; tt < nt; tt += 4) {
+        const T b = Bs[tt * (AB_CB + 1) + jj];
+        T s0 = T(0), s1 = T(0);
+        for (int a = 0; a < p; ++a) {
+          const T w = Ats[a * (AB_RT + 1) + tt];
+          s0 = fma_acc(w, Fs[a * AB_CB + jj], s0);
+          if (nc == 2) s1 = fma_acc(w, Fs[(p + a) * AB_CB + jj], s1);
+        }
+        double d0 = (double)(s0 - b);
+        acc0 += d0 * d0;
+        if (nc == 2) {
+          double d1 = (double)(s1 - b);
+          acc1 += d1 * d1;
+        }
+      }
+    }
+    __syncthreads();
+  }
+  const int64_t bid = (int64_t)blockIdx.y * gridDim.x + blockIdx.x;
+  double s0 = block_sum(acc0, red);
+  double s1 = block_sum(acc1, red);
+  if (threadIdx.x == 0) {
+    part[bid * 2 + 0] = s0;
+    part[bid * 2 + 1] = s1;
+  }
+}
+
+// fixed-order sum of `n` pairs -> out[0..1]; optional gate
+__global__ void k_pair_final(const double* __restrict__ part, int64_t n, double* __restrict__ out,
+                             const int* __restrict__ gate) {
+  if (gate != nullptr && *gate == 0) return;
+  __shared__ double red[33];
+  double a = 0.0, b = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    a += part[2 * i];
+    b += part[2 * i + 1];
+  }
+  a = block_sum(a, red);
+  b = block_sum(b, red);
+  if (threadIdx.x == 0) {
+    out[0] = a;
+    out[1] = b;
+  }
+}
+
+template <typename T>
+int resid(Arena& ws, const T* At, int64_t p, int64_t r, const T* B, int64_t c, int64_t ldb, bool trans,
+          const T* F1, const T* F2, double* out2, const int* gate, cudaStream_t st) {
+  if (p < 1 || r < 1 || c < 1) return NENMF_ERR_DIM;
+  if (p > 64) return NENMF_ERR_UNSUPPORTED;
+  const int64_t nchunk = cdiv(r, AB_RCHUNK);
+  dim3 grid((unsigned)cdiv(c, AB_CB), (unsigned)nchunk);
+  double* part = ws.take<double>((size_t)grid.x * grid.y * 2);
+  if (ws.base == nullptr) return NENMF_OK;
+  if (!ws.ok) return NENMF_ERR_WORKSPACE;
+  const int nc = F2 != nullptr ? 2 : 1;
+  size_t smem = ((size_t)AB_RT * (AB_CB + 1) + (size_t)p * (AB_RT + 1) + (size_t)nc * p * AB_CB) * sizeof(T);
+  if (trans) {
+    NENMF_CUDA_TRY(cudaFuncSetAttribute(k_resid<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_resid<T, true><<<grid, RS_THREADS, smem, st>>>(At, (int)p, r, B, c, ldb, F1, F2, AB_RCHUNK, part, gate);
+  } else {
+    NENMF_CUDA_TRY(cudaFuncSetAttribute(k_resid<T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_resid<T, false><<<grid, RS_THREADS, smem, st>>>(At, (int)p, r, B, c, ldb, F1, F2, AB_RCHUNK, part, gate);
+  }
+  NENMF_LAUNCH_CHECK();
+  k_pair_final<<<1, 256, 0, st>>>(part, (int64_t)grid.x * grid.y, out2, gate);
+  NENMF_LAUNCH_CHECK();
+  return NENMF_OK;
+}
+
+// ---------------------------------------------------- sumsq / pg_sumsq ----
+constexpr int RED_THREADS = 256;
+
+inline unsigned red_grid(int64_t count) {
+  return (unsigned)imax(1, imin(cdiv(count, RED_THREADS * 8), 1184));
+}
+
+template <typename T, bool PG>
+__global__ void __launch_bounds__(RED_THREADS)
+k_sumsq(const T* __restrict__ M, const T* __restrict__ g, int64_t count, double* __restrict__ part) {
+  __shared__ double red[33];
+  double acc = 0.0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += stride) {
+    double v;
+    if (PG) {
+      T gv = g[i];
+      v = (double)(M[i] > T(0) ? gv : min0_nan(gv));
+    } else {
+      v = (double)M[i];
+    }
+    acc += v * v;
+  }
+  double s = block_sum(acc, red);
+  if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+
+__global__ void k_final_sum(const double* __restrict__ part, int64_t n, double* __restrict__ out) {
+  __shared__ double red[33];
+  double a = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) a += part[i];
+  a = block_sum(a, red);
+  if (threadIdx.x == 0) *out = a;
+}
+
+template <typename T>
+int sumsq(Arena& ws, const T* M, const T* g, int64_t count, double* out, cudaStream_t st) {
+  if (count < 1) return NENMF_ERR_DIM;
+  unsigned grid = red_grid(count);
+  double* part = ws.take<double>(grid);
+  if (ws.base == nullptr) return NENMF_OK;
+  if (!ws.ok) return NENMF_ERR_WORKSPACE;
+  if (g != nullptr) k_sumsq<T, true><<<grid, RED_THREADS, 0, st>>>(M, g, count, part);
+  else k_sumsq<T, false><<<grid, RED_THREADS, 0, st>>>(M, g, count, part);
+  NENMF_LAUNCH_CHECK();
+  k_final_sum<<<1, 256, 0, st>>>(part, grid, out);
+  NENMF_LAUNCH_CHECK();
+  return NENMF_OK;
+}
+
+// ------------------------------------------------------------------ wfv ----
+template <typename T>
+__global__ void k_wfv(const T* __restrict__ W, int p, const T* __restrict__ F, int64_t c,
+                      const T* __restrict__ V, T* __restrict__ G) {
+  extern __shared__ double smem_d[];
+  T* Ws = reinterpret_cast<T*>(smem_d);
+  for (int i = threadIdx.x; i < p * p; i += blockDim.x) Ws[i] = W[i];
+  __syncthreads();
+  int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= c) return;
+  for (int i = 0; i < p; ++i) {
+    T acc = T(0);
+    for (int l = 0; l < p; ++l) acc = fma_acc(Ws[i * p + l], F[(int64_t)l * c + j], acc);
+    G[(int64_t)i * c + j] = op_sub(acc, V[(int64_t)i * c + j]);
+  }
+}
+
+template <typename T>
+int wf_minus_v(const T* W, int64_t p, const T* F, int64_t c, const T* V, T* G, cudaStream_t st) {
+  size_t smem = (size_t)p * p * sizeof(T);
+  if (smem > 200 * 1024) return NENMF_ERR_UNSUPPORTED;
+  NENMF_CUDA_TRY(cudaFuncSetAttribute(k_wfv<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k_wfv<T><<<(unsigned)cdiv(c, 128), 128, smem, st>>>(W, (int)p, F, c, V, G);
+  NENMF_LAUNCH_CHECK();
+  return NENMF_OK;
+}
+
+// explicit instantiations
+#define NENMF_INST_SKINNY(T)                                                                              \
+  template int abt<T>(Arena&, const T*, int64_t, const T*, int64_t, int64_t, T*, cudaStream_t);           \
+  template int ab<T>(Arena&, const T*, int64_t, int64_t, const T*, int64_t, int64_t, bool, T*,            \
+                     cudaStream_t);                                                                       \
+  template int resid<T>(Arena&, const T*, int64_t, int64_t, const T*, int64_t, int64_t, bool, const T*,   \
+                        const T*, double*, const int*, cudaStream_t);                                     \
+  template int sumsq<T>(Arena&, const T*, const T*, int64_t, double*, cudaStream_t);                      \
+  template int wf_minus_v<T>(const T*, int64_t, const T*, int64_t, const T*, T*, cudaStream_t);
+NENMF_INST_SKINNY(double)
+NENMF_INST_SKINNY(float)
+
+}  // namespace nenmf

@@ -1,0 +1,267 @@
+"""Outer alternating loops of vanilla and compressed NeNMF (reference
+``factorize.py``), driving the GPU kernels.
+
+The loop keeps the reference's control flow, stopping rules, trace cadence,
+clock protocol and exceptions (``factorize.py:116-183``).  All arithmetic runs
+on the device: X, the sketch, X_L / X_R^T and both factors stay resident in
+HBM for the whole run; each half-step is one ``nenmf_solve_nnls`` call (plus
+one skinny product for the compressed A-operand); ``emit`` evaluates the full
+||X - G F||_F on the GPU with the clock paused.  The host synchronises only
+where the reference's semantics need a value: ``emit``, time-budget checks
+and status checks (status words of queued half-steps are drained at those
+points, so a failure still surfaces with its outer and inner indices).
+
+Layout in HBM: X row-major n x m; G held transposed (G^T, p x n) so that both
+half-steps solve the same column-parallel problem; F p x m; L nu x n and R^T
+nu x m; X_L nu x m and X_R^T nu x n.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+from typing import Callable
+
+import numpy as np
+
+from . import _lib, _ops
+from .compression import SketchPair, compress_device, sketch_on_device
+from .errors import DimensionError, NumericalFailureError, ZeroMatrixError, raise_for_status
+from .matrix import DenseMatrix, as_matrix, check_seed, open_uniform
+from .nnls import InnerSolverConfig
+from .tracing import MonotonicClock, SolverClock, TraceRecord
+
+Observer = Callable[[TraceRecord, np.ndarray, np.ndarray], None]
+
+
+@dataclass(frozen=True, eq=False)
+class FactorPair:
+    """Factors G (n x p) and F (p x m), entrywise nonnegative (factorize.py:32-48)."""
+
+    G: DenseMatrix
+    F: DenseMatrix
+    p: int
+
+    def __post_init__(self):
+        if self.G.ndim != 2 or self.F.ndim != 2:
+            raise DimensionError("factors must be 2-D")
+        if self.G.shape[1] != self.p or self.F.shape[0] != self.p:
+            raise DimensionError(
+                f"factor shapes {tuple(self.G.shape)}, {tuple(self.F.shape)} do not match rank {self.p}")
+        if self.G.min() < 0.0 or self.F.min() < 0.0:
+            raise ValueError("factors must be entrywise nonnegative")
+
+
+@dataclass(frozen=True)
+class OuterConfig:
+    """Stopping rules and trace cadence (factorize.py:51-74)."""
+
+    inner: InnerSolverConfig = InnerSolverConfig()
+    time_budget_seconds: float = 15.0
+    max_outer_iterations: int = 0
+    rre_target: float = 0.0
+    trace_every: int = 1
+
+    def __post_init__(self):
+        if self.time_budget_seconds < 0 or self.max_outer_iterations < 0:
+            raise ValueError("stopping limits must be nonnegative")
+        if not (self.time_budget_seconds > 0 or self.max_outer_iterations >= 1):
+            raise ValueError("need a positive time budget or an iteration cap")
+        if self.rre_target < 0:
+            raise ValueError(f"rre_target must be >= 0, got {self.rre_target}")
+        if self.trace_every < 1:
+            raise ValueError(f"trace_every must be >= 1, got {self.trace_every}")
+
+
+def init_factors(n: int, m: int, p: int, seed: int) -> FactorPair:
+    """Seeded open-uniform G then F from one stream (factorize.py:77-86)."""
+    if p < 1:
+        raise DimensionError(f"rank must be >= 1, got {p}")
+    if p > min(n, m):
+        raise DimensionError(f"rank {p} exceeds min(n, m) = {min(n, m)}")
+    gen = np.random.default_rng(check_seed(seed))
+    G = open_uniform(gen, n, p)
+    F = open_uniform(gen, p, m)
+    return FactorPair(G=G, F=F, p=p)
+
+
+_STATUS_CAP = 128  # queued half-steps between status drains
+
+
+class _DeviceLoop:
+    """Device state of one factorization run."""
+
+    def __init__(self, X, init: FactorPair, sketch: SketchPair | None, dtype: str):
+        _, torch = _lib.require_device()
+        self.torch = torch
+        if hasattr(X, "is_cuda") and X.is_cuda:
+            self.X = X if X.is_contiguous() else X.contiguous()
+            dtype = "fp64" if X.dtype == torch.float64 else "fp32"
+        else:
+            self.X = _lib.to_device(as_matrix(X, "X"), dtype)
+        self.dtype = dtype
+        self.n, self.m = self.X.shape
+        self.p = init.p
+        self.sketch = sketch
+        self.scal = torch.zeros(4, dtype=torch.float64, device="cuda")
+        self.status = _lib.new_status(_STATUS_CAP)
+        self.pending: list[tuple[int, str, int]] = []
+
+    def norm_x(self) -> float:
+        _ops.sumsq(self.X, self.scal[0:1])
+        return math.sqrt(self.scal[0].item())
+
+    def prepare(self, init: FactorPair) -> None:
+        torch = self.torch
+        G = init.G
+        self.Gt = (_lib.to_device(G, self.dtype).t().contiguous() if hasattr(G, "is_cuda")
+                   else _lib.to_device(np.ascontiguousarray(np.asarray(G, dtype=np.float64).T), self.dtype))
+        self.F = _lib.to_device(init.F, self.dtype)
+        self.Gt_alt = torch.empty_like(self.Gt)
+        self.F_alt = torch.empty_like(self.F)
+        if self.sketch is not None:
+            L, Rt = sketch_on_device(self.sketch, self.dtype)
+            self.L, self.Rt = L, Rt
+            # the compressed preamble stays on the solver clock (factorize.py:130)
+            self.XL, self.XRt = compress_device(self.X, L, Rt)
+            nu = L.shape[0]
+            self.FR = torch.empty((self.p, nu), dtype=self.X.dtype, device="cuda")
+            self.GLt = torch.empty((self.p, nu), dtype=self.X.dtype, device="cuda")
+
+    def _slot(self, t: int, half: str) -> int:
+        if len(self.pending) >= _STATUS_CAP:
+            self.drain()
+        idx = len(self.pending)
+        self.pending.append((t, half, idx))
+        return idx
+
+    def half_steps(self, t: int, icfg: InnerSolverConfig) -> None:
+        kw = dict(max_iter=icfg.max_iter, grad_tol=icfg.grad_tol, lipschitz_safety=icfg.lipschitz_safety,
+                  status=self.status)
+        if self.sketch is not None:
+            # G-half: A = (F R)^T, B = X_R^T (factorize.py:109-110)
+            _ops.abt(self.F, self.Rt, self.FR)
+            _ops.solve(self.FR, self.XRt, self.Gt, self.Gt_alt, trans_b=False,
+                       status_index=self._slot(t, "G"), **kw)
+            self.Gt, self.Gt_alt = self.Gt_alt, self.Gt
+            # F-half: A = L G, B = X_L (factorize.py:112-113)
+            _ops.abt(self.Gt, self.L, self.GLt)
+            _ops.solve(self.GLt, self.XL, self.F, self.F_alt, trans_b=False,
+                       status_index=self._slot(t, "F"), **kw)
+        else:
+            # G-half: A = F^T, B = X^T read in place (factorize.py:94-95)
+            _ops.solve(self.F, self.X, self.Gt, self.Gt_alt, trans_b=True,
+                       status_index=self._slot(t, "G"), **kw)
+            self.Gt, self.Gt_alt = self.Gt_alt, self.Gt
+            # F-half: A = G, B = X (factorize.py:97-98)
+            _ops.solve(self.Gt, self.X, self.F, self.F_alt, trans_b=False,
+                       status_index=self._slot(t, "F"), **kw)
+        self.F, self.F_alt = self.F_alt, self.F
+
+    def drain(self) -> None:
+        """Synchronise and surface the first failure among queued half-steps."""
+        if not self.pending:
+            return
+        sts = _lib.read_status(self.status)
+        pending, self.pending = self.pending, []
+        self.status.zero_()
+        for t, half, idx in pending:
+            st = sts[idx]
+            code = int(st["code"])
+            if code == 0:
+                continue
+            try:
+                raise_for_status(code, int(st["iteration"]), f"{half} update")
+            except NumericalFailureError as exc:
+                raise NumericalFailureError(
+                    f"outer iteration {t} ({half} update): {exc}",
+                    iteration=exc.iteration, outer_iteration=t) from exc
+
+    def objective(self) -> float:
+        _ops.residual_sumsq(self.X, self.Gt, self.F, self.scal[1:2])
+        return math.sqrt(self.scal[1].item())
+
+    def host_factors(self):
+        return _lib.to_host(self.Gt).T.copy(), _lib.to_host(self.F)
+
+
+def _run_outer(X, init: FactorPair, cfg: OuterConfig, observer, clock, sketch, dtype: str,
+               return_device: bool = False) -> FactorPair:
+    if hasattr(X, "is_cuda") and X.is_cuda:
+        n, m = X.shape
+    else:
+        X = as_matrix(X, "X")
+        n, m = X.shape
+    if tuple(init.G.shape) != (n, init.p) or tuple(init.F.shape) != (init.p, m):
+        raise DimensionError(
+            f"init shapes {tuple(init.G.shape)}, {tuple(init.F.shape)} do not match data {n}x{m}")
+    if sketch is not None and (np.shape(sketch.L) != (sketch.nu, n) or np.shape(sketch.R) != (m, sketch.nu)):
+        raise DimensionError(
+            f"sketch shapes L {np.shape(sketch.L)}, R {np.shape(sketch.R)} do not match "
+            f"data {n}x{m} at target rank {sketch.nu}")
+    run = _DeviceLoop(X, init, sketch, dtype)
+    norm_x = run.norm_x()
+    if norm_x == 0.0:
+        raise ZeroMatrixError("cannot factorize the zero matrix")
+    if clock is None:
+        clock = MonotonicClock()
+    run.prepare(init)
+    stream = run.torch.cuda.current_stream()
+    last_traced = -1
+
+    def emit(t: int) -> float:
+        nonlocal last_traced
+        stream.synchronize()  # charge queued device work to the solver clock
+        run.drain()
+        clock.pause()
+        objective = run.objective()
+        value = objective / norm_x
+        record = TraceRecord(outer_iter=t, solver_elapsed_s=clock.elapsed(),
+                             wall_elapsed_s=clock.wall_elapsed(), rre=value, objective=objective)
+        if observer is not None:
+            G, F = run.host_factors()
+            observer(record, G, F)
+        last_traced = t
+        clock.resume()
+        return value
+
+    current = emit(0)
+    t = 0
+    done = cfg.rre_target > 0 and current <= cfg.rre_target
+    while not done:
+        if cfg.max_outer_iterations > 0 and t >= cfg.max_outer_iterations:
+            break
+        if cfg.time_budget_seconds > 0:
+            stream.synchronize()
+            run.drain()
+            if clock.elapsed() >= cfg.time_budget_seconds:
+                break
+        t += 1
+        run.half_steps(t, cfg.inner)
+        clock.tick()
+        if t % cfg.trace_every == 0:
+            current = emit(t)
+            if cfg.rre_target > 0 and current <= cfg.rre_target:
+                break
+    if last_traced != t:
+        emit(t)
+    run.drain()
+    if return_device:
+        return FactorPair(G=run.Gt.t(), F=run.F, p=init.p)
+    G, F = run.host_factors()
+    return FactorPair(G=G, F=F, p=init.p)
+
+
+def factorize_vanilla(X, init: FactorPair, cfg: OuterConfig = OuterConfig(),
+                      observer: Observer | None = None, clock: SolverClock | None = None, *,
+                      dtype: str = "fp64", return_device: bool = False) -> FactorPair:
+    """Alternating NeNMF on the full data (factorize.py:186-194), on the GPU."""
+    return _run_outer(X, init, cfg, observer, clock, None, dtype, return_device)
+
+
+def factorize_compressed(X, sketch: SketchPair, init: FactorPair, cfg: OuterConfig = OuterConfig(),
+                         observer: Observer | None = None, clock: SolverClock | None = None, *,
+                         dtype: str = "fp64", return_device: bool = False) -> FactorPair:
+    """Alternating NeNMF on the sketch-compressed surrogates (factorize.py:197-213);
+    RRE and objective are still reported against the full X."""
+    return _run_outer(X, init, cfg, observer, clock, sketch, dtype, return_device)
