@@ -79,6 +79,8 @@ int nenmf_abi_version(void);
 const char* nenmf_status_string(int code);
 /* number of SMs of the current device (0 if no device) */
 int nenmf_device_sm_count(void);
+/* kernels this library has launched in this process (diagnostic counter) */
+unsigned long long nenmf_launch_count(void);
 
 /* ---- inner solver (nnls.py:119-227) -------------------------------------
  * Solves min_{F>=0} 1/2||B - A F||^2 from F0.  A (r x p) is passed as

@@ -5,7 +5,14 @@
 #include "rsi.cuh"
 #include "skinny.cuh"
 
+#include <atomic>
+
 using namespace nenmf;
+
+namespace nenmf {
+static std::atomic<unsigned long long> g_launches{0};
+unsigned long long launch_counter_add(unsigned long long n) { return g_launches.fetch_add(n) + n; }
+}  // namespace nenmf
 
 namespace {
 inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
@@ -40,6 +47,8 @@ const char* nenmf_status_string(int code) {
 }
 
 int nenmf_device_sm_count(void) { return sm_count(); }
+
+unsigned long long nenmf_launch_count(void) { return g_launches.load(); }
 
 // ------------------------------------------------------------ solver ----
 size_t nenmf_solve_nnls_workspace_bytes(int dtype, int64_t r, int64_t p, int64_t c) {

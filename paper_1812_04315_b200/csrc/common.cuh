@@ -21,7 +21,14 @@ constexpr int kWarp = 32;
     if (_e != cudaSuccess) return NENMF_ERR_CUDA;              \
   } while (0)
 
-#define NENMF_LAUNCH_CHECK() NENMF_CUDA_TRY(cudaGetLastError())
+// every kernel launch site is followed by NENMF_LAUNCH_CHECK(), which also
+// bumps a diagnostic launch counter (nenmf_launch_count, read by bench.py)
+unsigned long long launch_counter_add(unsigned long long n);
+#define NENMF_LAUNCH_CHECK()            \
+  do {                                  \
+    nenmf::launch_counter_add(1);       \
+    NENMF_CUDA_TRY(cudaGetLastError()); \
+  } while (0)
 
 #define NENMF_TRY(expr)                                        \
   do {                                                         \

@@ -359,6 +359,7 @@ static int launch_nnls(const T* W, const T* V, const T* F0, T* Fbest, T* ring, T
                   (void*)&c, (void*)&cpb, (void*)&Lptr, (void*)&max_iter, (void*)&grad_tol, (void*)&slots,
                   (void*)&st};
   NENMF_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k_nnls<T, PMAX>, dim3(grid), dim3(threads), args, 0, s));
+  launch_counter_add(1);
   return NENMF_OK;
 }
 
