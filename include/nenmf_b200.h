@@ -81,6 +81,9 @@ const char* nenmf_status_string(int code);
 int nenmf_device_sm_count(void);
 /* kernels this library has launched in this process (diagnostic counter) */
 unsigned long long nenmf_launch_count(void);
+/* development aid: per-iteration timeline of the last traced solve
+ * (NENMF_NNLS_TRACE=1 in the environment), 4 x 4096 globaltimer stamps */
+int nenmf_debug_nnls_trace(unsigned long long* host_out, int count);
 
 /* ---- inner solver (nnls.py:119-227) -------------------------------------
  * Solves min_{F>=0} 1/2||B - A F||^2 from F0.  A (r x p) is passed as

@@ -29,6 +29,7 @@ _SIGS = {
     "nenmf_status_string": (C.c_char_p, [_i32]),
     "nenmf_device_sm_count": (_i32, []),
     "nenmf_launch_count": (C.c_ulonglong, []),
+    "nenmf_debug_nnls_trace": (_i32, [_vp, _i32]),
     "nenmf_solve_nnls_workspace_bytes": (_sz, [_i32, _i64, _i64, _i64]),
     "nenmf_solve_nnls": (_i32, [_i32, _vp, _i64, _i64, _vp, _i64, _i64, _i32, _vp, _vp, _i32, _dbl, _dbl,
                                 _vp, _i32, _i32, _dbl, _vp, _vp, _sz, _vp]),

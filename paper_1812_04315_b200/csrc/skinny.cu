@@ -19,7 +19,7 @@ namespace nenmf {
 
 // ----------------------------------------------------------------- abt ----
 constexpr int ABT_KT = 32;
-constexpr int64_t ABT_KCHUNK = 4096;
+constexpr int64_t ABT_KCHUNK = 128;
 constexpr int ABT_THREADS = 256;
 constexpr int ABT_MAXO = 32;  // outputs per thread: p*q <= 8192
 
