@@ -140,10 +140,20 @@ __global__ void k_slab_reduce(const T* __restrict__ part, int nslab, int64_t cou
   out[o] = s;
 }
 
+int dual_pass_tc(Arena& ws, const float* X, int64_t n, int64_t m, int64_t ldx, const float* At, const float* Bt,
+                 int64_t k, float* Yt, float* Zt, cudaStream_t s);
+
 template <typename T>
 int dual_pass(Arena& ws, const T* X, int64_t n, int64_t m, int64_t ldx, const T* At, const T* Bt, int64_t k,
               T* Yt, T* Zt, cudaStream_t s) {
   if (n < 1 || m < 1 || k < 1) return NENMF_ERR_DIM;
+  if constexpr (sizeof(T) == 4) {
+    // FP32 data: tcgen05 BF16x3 pass when the shape fits (dual_tc.cu)
+    int rc = dual_pass_tc(ws, reinterpret_cast<const float*>(X), n, m, ldx, reinterpret_cast<const float*>(At),
+                          reinterpret_cast<const float*>(Bt), k, reinterpret_cast<float*>(Yt),
+                          reinterpret_cast<float*>(Zt), s);
+    if (rc != NENMF_ERR_UNSUPPORTED) return rc;
+  }
   if (k > DU_KMAX) return NENMF_ERR_UNSUPPORTED;
   const int BC = dual_block_cols<T>(k);
   const int64_t gx = cdiv(m, BC), gy = cdiv(n, DU_BR);
