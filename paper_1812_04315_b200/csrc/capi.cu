@@ -9,8 +9,31 @@
 
 using namespace nenmf;
 
+#include <mutex>
+#include <unordered_map>
+
 namespace nenmf {
 static std::atomic<unsigned long long> g_launches{0};
+
+cudaError_t set_smem_attr(const void* fn, size_t bytes) {
+  static std::mutex mu;
+  static std::unordered_map<const void*, size_t> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const void* key = reinterpret_cast<const void*>(reinterpret_cast<uintptr_t>(fn) ^ ((uintptr_t)dev << 56));
+  {
+    std::lock_guard<std::mutex> g(mu);
+    auto it = done.find(key);
+    if (it != done.end() && it->second >= bytes) return cudaSuccess;
+  }
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess) {
+    std::lock_guard<std::mutex> g(mu);
+    size_t& v = done[key];
+    if (v < bytes) v = bytes;
+  }
+  return e;
+}
 unsigned long long launch_counter_add(unsigned long long n) { return g_launches.fetch_add(n) + n; }
 }  // namespace nenmf
 

@@ -64,6 +64,14 @@ inline int sm_count() {
 }
 
 inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per kernel and size
+// (the call is expensive relative to a launch; results are cached)
+cudaError_t set_smem_attr(const void* fn, size_t bytes);
+template <typename K>
+inline cudaError_t set_smem(K* fn, size_t bytes) {
+  return set_smem_attr(reinterpret_cast<const void*>(fn), bytes);
+}
 __host__ __device__ __forceinline__ int64_t imin(int64_t a, int64_t b) { return a < b ? a : b; }
 __host__ __device__ __forceinline__ int64_t imax(int64_t a, int64_t b) { return a > b ? a : b; }
 

@@ -390,11 +390,11 @@ int dual_pass_tc(Arena& ws, const float* X, int64_t n, int64_t m, int64_t ldx, c
   const size_t smem = NSTAGE * stage + 1024;
   const unsigned grid = (unsigned)imin(U.units, sms);
   if (kpad == 32) {
-    NENMF_CUDA_TRY(cudaFuncSetAttribute(k_dual_tc<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    NENMF_CUDA_TRY(set_smem(k_dual_tc<32>, smem));
     k_dual_tc<32><<<grid, NWARPS * 32, smem, s>>>(X, n, m, ldx, A2, lda2, B2, ldb2, (int)k, U, Ypart ? Ypart : Yt,
                                                  Zpart ? Zpart : Zt);
   } else {
-    NENMF_CUDA_TRY(cudaFuncSetAttribute(k_dual_tc<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    NENMF_CUDA_TRY(set_smem(k_dual_tc<16>, smem));
     k_dual_tc<16><<<grid, NWARPS * 32, smem, s>>>(X, n, m, ldx, A2, lda2, B2, ldb2, (int)k, U, Ypart ? Ypart : Yt,
                                                  Zpart ? Zpart : Zt);
   }

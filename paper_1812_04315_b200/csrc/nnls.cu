@@ -130,7 +130,7 @@ static int lipschitz(Arena& ws, const T* At, int64_t r, int64_t p, const T* W, c
     gram = gsmall;
   }
   size_t smem = ((size_t)k * k + 2 * k) * sizeof(double);
-  NENMF_CUDA_TRY(cudaFuncSetAttribute(k_power<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  NENMF_CUDA_TRY(set_smem(k_power<T>, smem));
   k_power<T><<<1, 128, smem, s>>>(gram, (int)k, pvec, pcount, ptol, pmax, safety, Lout, st);
   NENMF_LAUNCH_CHECK();
   return NENMF_OK;

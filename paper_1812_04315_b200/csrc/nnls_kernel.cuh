@@ -597,7 +597,7 @@ static int launch_nnls_t(const NnlsPlan& pl, const T* W, const T* V, const T* F0
                          T* gstate, int p, int64_t c, const double* Lptr, int max_iter, double grad_tol, WinRec* recs,
                          WinRec* results, nenmf_device_status* st, unsigned long long* tracebuf, cudaStream_t s) {
   auto fn = k_nnls<T, TPC, RMAX, SM>;
-  NENMF_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
+  NENMF_CUDA_TRY(set_smem(fn, pl.smem));
   int64_t cpb = pl.cpb;
   int ldS = pl.ldS, ldW = pl.ldW;
   void* args[] = {(void*)&W,    (void*)&V,      (void*)&F0,       (void*)&Fout,     (void*)&snaps, (void*)&salpha,

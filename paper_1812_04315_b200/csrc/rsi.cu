@@ -15,6 +15,8 @@
 // Skinny panels are stored short-major (Pt = P^T, k x rows), so a panel is a
 // column-major tall matrix and every Householder column is contiguous.
 #include "rsi.cuh"
+
+#include <cstdlib>
 #include "skinny.cuh"
 
 namespace nenmf {
@@ -163,7 +165,7 @@ int dual_pass(Arena& ws, const T* X, int64_t n, int64_t m, int64_t ldx, const T*
   if (!ws.ok) return NENMF_ERR_WORKSPACE;
   size_t smem = ((size_t)DU_TR * (DU_TC + 1) + (size_t)k * (DU_TC + 1) + (size_t)k * (DU_TR + 1) +
                  (size_t)k * BC) * sizeof(T);
-  NENMF_CUDA_TRY(cudaFuncSetAttribute(k_dual<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  NENMF_CUDA_TRY(set_smem(k_dual<T>, smem));
   dim3 grid((unsigned)gx, (unsigned)gy);
   k_dual<T><<<grid, DU_THREADS, smem, s>>>(X, n, m, ldx, At, Bt, (int)k, BC, Ypart ? Ypart : Yt, Zpart ? Zpart : Zt);
   NENMF_LAUNCH_CHECK();
@@ -349,7 +351,14 @@ inline int plan_qr(int64_t rows, int64_t k, QrPlan& pl) {
 }
 
 template <typename T>
-int orthonormalize(Arena& ws, T* Pt, int64_t rows, int64_t k, nenmf_device_status* st, cudaStream_t s) {
+int orthonormalize_cholqr(Arena& ws, T* Pt, int64_t rows, int64_t k, nenmf_device_status* st, cudaStream_t s);
+template <typename T>
+int orthonormalize_pair(Arena& ws, T* P0t, int64_t rows0, T* P1t, int64_t rows1, int64_t k,
+                        nenmf_device_status* st, cudaStream_t s);
+
+// Householder TSQR (kept as the reference-faithful alternative: NENMF_QR=tsqr)
+template <typename T>
+int orthonormalize_tsqr(Arena& ws, T* Pt, int64_t rows, int64_t k, nenmf_device_status* st, cudaStream_t s) {
   if (rows < 1 || k < 1 || k > rows) return NENMF_ERR_DIM;
   if (k > 64) return NENMF_ERR_UNSUPPORTED;
   QrPlan pl;
@@ -368,10 +377,10 @@ int orthonormalize(Arena& ws, T* Pt, int64_t rows, int64_t k, nenmf_device_statu
   if (!ws.ok) return NENMF_ERR_WORKSPACE;
   const int hb = qr_block_rows(k);
   size_t smem = (size_t)k * (hb + 1) * sizeof(double);
-  NENMF_CUDA_TRY(cudaFuncSetAttribute(k_qr_block<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  NENMF_CUDA_TRY(cudaFuncSetAttribute(k_qr_block<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  NENMF_CUDA_TRY(cudaFuncSetAttribute(k_qr_apply<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  NENMF_CUDA_TRY(cudaFuncSetAttribute(k_qr_apply<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  NENMF_CUDA_TRY(set_smem(k_qr_block<T>, smem));
+  NENMF_CUDA_TRY(set_smem(k_qr_block<double>, smem));
+  NENMF_CUDA_TRY(set_smem(k_qr_apply<T>, smem));
+  NENMF_CUDA_TRY(set_smem(k_qr_apply<double>, smem));
   // forward: factor every level
   for (int l = 0; l < pl.levels; ++l) {
     const bool top = l == pl.levels - 1;
@@ -400,6 +409,13 @@ int orthonormalize(Arena& ws, T* Pt, int64_t rows, int64_t k, nenmf_device_statu
   return NENMF_OK;
 }
 
+template <typename T>
+int orthonormalize(Arena& ws, T* Pt, int64_t rows, int64_t k, nenmf_device_status* st, cudaStream_t s) {
+  const char* e = getenv("NENMF_QR");
+  if ((e != nullptr && e[0] == 't') || k > 32) return orthonormalize_tsqr<T>(ws, Pt, rows, k, st, s);
+  return orthonormalize_cholqr<T>(ws, Pt, rows, k, st, s);
+}
+
 // ================================================================= RSI ====
 template <typename T>
 int rsi(Arena& ws, const T* X, int64_t n, int64_t m, int64_t ldx, const T* omega_l_t, const T* omega_r, int64_t nu,
@@ -425,6 +441,9 @@ int rsi(Arena& ws, const T* X, int64_t n, int64_t m, int64_t ldx, const T* omega
     Arena c(nullptr, 0);
     orthonormalize<T>(c, L, m, nu, st, s);
     need = max(need, c.used);
+    Arena d(nullptr, 0);
+    orthonormalize_pair<T>(d, L, n, Rt, m, nu, st, s);
+    need = max(need, d.used);
   }
   char* sbase = scratch.take<char>(need);
   if (dry) {
@@ -435,17 +454,24 @@ int rsi(Arena& ws, const T* X, int64_t n, int64_t m, int64_t ldx, const T* omega
   auto fresh = [&]() { return Arena(sbase, need); };
   // start: Y = X Omega_L -> L (as Q_col^T), Z = X^T Omega_R^T -> Rt (compression.py:134-135)
   { Arena a = fresh(); NENMF_TRY(dual_pass<T>(a, X, n, m, ldx, omega_l_t, omega_r, nu, L, Rt, s)); }
-  { Arena a = fresh(); NENMF_TRY(orthonormalize<T>(a, L, n, nu, st, s)); }
-  { Arena a = fresh(); NENMF_TRY(orthonormalize<T>(a, Rt, m, nu, st, s)); }
+  auto qr2 = [&](T* A, int64_t ra, T* B, int64_t rb) -> int {
+    Arena a = fresh();
+    const char* e = getenv("NENMF_QR");
+    if ((e != nullptr && e[0] == 't') || nu > 32) {  // CholeskyQR2 path holds k <= 32
+      NENMF_TRY(orthonormalize<T>(a, A, ra, nu, st, s));
+      Arena b = fresh();
+      return orthonormalize<T>(b, B, rb, nu, st, s);
+    }
+    return orthonormalize_pair<T>(a, A, ra, B, rb, nu, st, s);  // both chains in one launch
+  };
+  NENMF_TRY(qr2(L, n, Rt, m));
   for (int it = 1; it <= q; ++it) {
     // pass a: X^T Q_col (-> tcol, m x nu) and X Q_row (-> trow, n x nu)  (compression.py:138-139)
     { Arena a = fresh(); NENMF_TRY(dual_pass<T>(a, X, n, m, ldx, Rt, L, nu, trow, tcol, s)); }
-    { Arena a = fresh(); NENMF_TRY(orthonormalize<T>(a, tcol, m, nu, st, s)); }
-    { Arena a = fresh(); NENMF_TRY(orthonormalize<T>(a, trow, n, nu, st, s)); }
+    NENMF_TRY(qr2(tcol, m, trow, n));
     // pass b: X Q~_col (-> L) and X^T Q~_row (-> Rt)
     { Arena a = fresh(); NENMF_TRY(dual_pass<T>(a, X, n, m, ldx, tcol, trow, nu, L, Rt, s)); }
-    { Arena a = fresh(); NENMF_TRY(orthonormalize<T>(a, L, n, nu, st, s)); }
-    { Arena a = fresh(); NENMF_TRY(orthonormalize<T>(a, Rt, m, nu, st, s)); }
+    NENMF_TRY(qr2(L, n, Rt, m));
   }
   return NENMF_OK;
 }

@@ -23,10 +23,10 @@ constexpr int64_t ABT_KCHUNK = 128;
 constexpr int ABT_THREADS = 256;
 constexpr int ABT_MAXO = 32;  // outputs per thread: p*q <= 8192
 
-template <typename T>
+template <typename T, typename TO>
 __global__ void __launch_bounds__(ABT_THREADS)
 k_abt(const T* __restrict__ A, int p, const T* __restrict__ B, int q, int64_t K,
-      int64_t kchunk, double* __restrict__ part, T* __restrict__ C) {
+      int64_t kchunk, double* __restrict__ part, TO* __restrict__ C) {
   extern __shared__ double smem_d[];
   double* As = smem_d;                       // [p][KT+1]
   double* Bs = smem_d + p * (ABT_KT + 1);    // [q][KT+1]
@@ -66,23 +66,23 @@ k_abt(const T* __restrict__ A, int p, const T* __restrict__ B, int q, int64_t K,
   for (int s = 0; s < ABT_MAXO; ++s) {
     int o = tid + s * ABT_THREADS;
     if (o < npq) {
-      if (C != nullptr) C[o] = (T)acc[s];
+      if (C != nullptr) C[o] = (TO)acc[s];
       else part[(int64_t)blockIdx.x * npq + o] = acc[s];
     }
   }
 }
 
-template <typename T>
-__global__ void k_abt_reduce(const double* __restrict__ part, int nchunk, int npq, T* __restrict__ C) {
+template <typename TO>
+__global__ void k_abt_reduce(const double* __restrict__ part, int nchunk, int npq, TO* __restrict__ C) {
   int o = blockIdx.x * blockDim.x + threadIdx.x;
   if (o >= npq) return;
   double s = part[o];
   for (int c = 1; c < nchunk; ++c) s += part[(int64_t)c * npq + o];
-  C[o] = (T)s;
+  C[o] = (TO)s;
 }
 
-template <typename T>
-int abt(Arena& ws, const T* A, int64_t p, const T* B, int64_t q, int64_t K, T* C, cudaStream_t st) {
+template <typename T, typename TO>
+int abt_any(Arena& ws, const T* A, int64_t p, const T* B, int64_t q, int64_t K, TO* C, cudaStream_t st) {
   if (p < 1 || q < 1 || K < 1) return NENMF_ERR_DIM;
   if (p * q > ABT_THREADS * ABT_MAXO || p > 512 || q > 512) return NENMF_ERR_UNSUPPORTED;
   const int64_t nchunk = cdiv(K, ABT_KCHUNK);
@@ -90,16 +90,26 @@ int abt(Arena& ws, const T* A, int64_t p, const T* B, int64_t q, int64_t K, T* C
   if (ws.base == nullptr) return NENMF_OK;
   if (!ws.ok) return NENMF_ERR_WORKSPACE;
   size_t smem = (size_t)(p + q) * (ABT_KT + 1) * sizeof(double);
-  NENMF_CUDA_TRY(cudaFuncSetAttribute(k_abt<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  k_abt<T><<<(unsigned)nchunk, ABT_THREADS, smem, st>>>(A, (int)p, B, (int)q, K, ABT_KCHUNK, part,
-                                                       nchunk > 1 ? nullptr : C);
+  NENMF_CUDA_TRY(cudaFuncSetAttribute(k_abt<T, TO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k_abt<T, TO><<<(unsigned)nchunk, ABT_THREADS, smem, st>>>(A, (int)p, B, (int)q, K, ABT_KCHUNK, part,
+                                                           nchunk > 1 ? nullptr : C);
   NENMF_LAUNCH_CHECK();
   if (nchunk > 1) {
     int npq = (int)(p * q);
-    k_abt_reduce<T><<<(unsigned)cdiv(npq, 256), 256, 0, st>>>(part, (int)nchunk, npq, C);
+    k_abt_reduce<TO><<<(unsigned)cdiv(npq, 256), 256, 0, st>>>(part, (int)nchunk, npq, C);
     NENMF_LAUNCH_CHECK();
   }
   return NENMF_OK;
+}
+
+template <typename T>
+int abt(Arena& ws, const T* A, int64_t p, const T* B, int64_t q, int64_t K, T* C, cudaStream_t st) {
+  return abt_any<T, T>(ws, A, p, B, q, K, C, st);
+}
+
+template <typename T>
+int gram_d(Arena& ws, const T* A, int64_t p, int64_t K, double* G, cudaStream_t st) {
+  return abt_any<T, double>(ws, A, p, A, p, K, G, st);
 }
 
 // ------------------------------------------------------------------ ab ----
@@ -387,7 +397,7 @@ template <typename T>
 int wf_minus_v(const T* W, int64_t p, const T* F, int64_t c, const T* V, T* G, cudaStream_t st) {
   size_t smem = (size_t)p * p * sizeof(T);
   if (smem > 200 * 1024) return NENMF_ERR_UNSUPPORTED;
-  NENMF_CUDA_TRY(cudaFuncSetAttribute(k_wfv<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  NENMF_CUDA_TRY(set_smem(k_wfv<T>, smem));
   k_wfv<T><<<(unsigned)cdiv(c, 128), 128, smem, st>>>(W, (int)p, F, c, V, G);
   NENMF_LAUNCH_CHECK();
   return NENMF_OK;
@@ -396,6 +406,7 @@ int wf_minus_v(const T* W, int64_t p, const T* F, int64_t c, const T* V, T* G, c
 // explicit instantiations
 #define NENMF_INST_SKINNY(T)                                                                              \
   template int abt<T>(Arena&, const T*, int64_t, const T*, int64_t, int64_t, T*, cudaStream_t);           \
+  template int gram_d<T>(Arena&, const T*, int64_t, int64_t, double*, cudaStream_t);                      \
   template int ab<T>(Arena&, const T*, int64_t, int64_t, const T*, int64_t, int64_t, bool, T*,            \
                      cudaStream_t);                                                                       \
   template int resid<T>(Arena&, const T*, int64_t, int64_t, const T*, int64_t, int64_t, bool, const T*,   \

@@ -9,6 +9,10 @@ namespace nenmf {
 template <typename T>
 int abt(Arena& ws, const T* A, int64_t p, const T* B, int64_t q, int64_t K, T* C, cudaStream_t st);
 
+// G (p x p, double) = A A^T for A (p x K): Gram of a short-major panel
+template <typename T>
+int gram_d(Arena& ws, const T* A, int64_t p, int64_t K, double* G, cudaStream_t st);
+
 template <typename T>
 int ab(Arena& ws, const T* At, int64_t p, int64_t r, const T* B, int64_t c, int64_t ldb, bool trans,
        T* V, cudaStream_t st);
