@@ -24,7 +24,9 @@
 
 #include <cooperative_groups.h>
 #include <climits>
+#include <cmath>
 #include <cstdlib>
+#include <mutex>
 
 namespace nenmf {
 
@@ -138,6 +140,40 @@ static int lipschitz(Arena& ws, const T* At, int64_t r, int64_t p, const T* W, c
 
 __device__ unsigned long long g_nnls_trace[4][NN_TRACE_LEN];
 
+// Momentum weights w_k = (alpha_k - 1) / alpha_{k+1} depend only on k
+// (nnls.py:68-69, 213): computed once per device on the host with the same
+// IEEE rounding sequence as alpha_next_d and kept in device memory, so the
+// solver loop carries no sqrt/div on its critical path.
+constexpr int NN_WTAB_LEN = 1 << 16;
+__device__ double g_wtab[NN_WTAB_LEN];
+
+static const double* momentum_table(int max_iter) {
+  if (max_iter > NN_WTAB_LEN) return nullptr;
+  static std::mutex mu;
+  static bool ready[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev >= 64) return nullptr;
+  std::lock_guard<std::mutex> lk(mu);
+  if (!ready[dev]) {
+    static double host[NN_WTAB_LEN];
+    volatile double alpha = 1.0;
+    for (int k = 0; k < NN_WTAB_LEN; ++k) {
+      volatile double t = 4.0 * alpha;
+      t = t * alpha;
+      t = t + 1.0;
+      volatile double sq = std::sqrt((double)t);
+      volatile double a1 = (1.0 + sq) / 2.0;
+      host[k] = (alpha - 1.0) / a1;
+      alpha = a1;
+    }
+    if (cudaMemcpyToSymbol(g_wtab, host, sizeof(host)) != cudaSuccess) return nullptr;
+    ready[dev] = true;
+  }
+  void* ptr = nullptr;
+  if (cudaGetSymbolAddress(&ptr, g_wtab) != cudaSuccess) return nullptr;
+  return static_cast<const double*>(ptr);
+}
+
 template <typename T>
 static int launch_nnls(const NnlsPlan& pl, const T* W, const T* V, const T* F0, T* Fout, T* snaps, double* salpha,
                        T* gstate, int p, int64_t c, const double* Lptr, int max_iter, double grad_tol, WinRec* recs,
@@ -165,22 +201,37 @@ int solve_nnls(Arena& ws, const T* At, int64_t r, int64_t p, const T* B, int64_t
   const bool dry = ws.base == nullptr;
   const NnlsPlan pl = plan_nnls<T>(p, c);
   const int64_t pc = p * c;
+  // tensor-core solver: p <= 32 and at most 15 blocks of 8 columns per CTA
+  int sms = sm_count();
+  if (sms <= 0) sms = 148;
+  const int mgrid = (int)imax(1, imin(sms, cdiv(c, 8)));
+  const int64_t mcpb = cdiv(c, mgrid);
+  const bool use_mma = p <= 32 && mcpb <= imin(8 * (NW_MAXW - 1), nnls_mma_max_cols<T>((int)p)) &&
+                       getenv("NENMF_NNLS_SIMT") == nullptr;
+  const int grid_used = use_mma ? mgrid : pl.grid;
   T* W = ws.take<T>((size_t)p * p);
   T* V = ws.take<T>((size_t)pc);
   double* Lbuf = ws.take<double>(4);
   T* snaps = ws.take<T>((size_t)(NW_SNAP + 1) * 4 * pc);
-  double* salpha = ws.take<double>((size_t)pl.grid * NW_MAXW * (NW_SNAP + 1) * 2);
-  T* gstate = pl.smem_state ? nullptr : ws.take<T>((size_t)4 * pc);
-  WinRec* recs = ws.take<WinRec>((size_t)NW_SLOTS * pl.grid + NW_SLOTS);
-  WinRec* results = recs + (size_t)NW_SLOTS * pl.grid;
+  double* salpha = ws.take<double>((size_t)imax(pl.grid, mgrid) * NW_MAXW * (NW_SNAP + 1) * 2);
+  T* gstate = (use_mma || pl.smem_state) ? nullptr : ws.take<T>((size_t)4 * pc);
+  WinRec* recs = ws.take<WinRec>((size_t)NW_SLOTS * grid_used + NW_SLOTS);
+  WinRec* results = recs + (size_t)NW_SLOTS * grid_used;
   if (!dry && !ws.ok) return NENMF_ERR_WORKSPACE;
   NENMF_TRY(abt<T>(ws, At, p, At, p, r, W, s));                       // W = A^T A   (nnls.py:157)
   NENMF_TRY(ab<T>(ws, At, p, r, B, c, ldb, trans, V, s));             // V = A^T B   (nnls.py:158)
   NENMF_TRY(lipschitz<T>(ws, At, r, p, W, pvec, pcount, pmax, ptol, safety, Lbuf, st, s));  // (nnls.py:159)
   if (!dry) {
-    NENMF_CUDA_TRY(cudaMemsetAsync(recs, 0, sizeof(WinRec) * ((size_t)NW_SLOTS * pl.grid + NW_SLOTS), s));
-    NENMF_TRY(launch_nnls<T>(pl, W, V, F0, Fout, snaps, salpha, gstate, (int)p, c, Lbuf, max_iter, grad_tol, recs,
-                             results, st, s));
+    NENMF_CUDA_TRY(cudaMemsetAsync(recs, 0, sizeof(WinRec) * ((size_t)NW_SLOTS * grid_used + NW_SLOTS), s));
+    if (use_mma) {
+      unsigned long long* tracebuf = nullptr;
+      if (getenv("NENMF_NNLS_TRACE") != nullptr) NENMF_CUDA_TRY(cudaGetSymbolAddress((void**)&tracebuf, g_nnls_trace));
+      NENMF_TRY(launch_nnls_mma<T>(W, V, F0, Fout, snaps, salpha, (int)p, c, mgrid, mcpb, Lbuf, max_iter, grad_tol,
+                                   recs, results, st, tracebuf, momentum_table(max_iter), s));
+    } else {
+      NENMF_TRY(launch_nnls<T>(pl, W, V, F0, Fout, snaps, salpha, gstate, (int)p, c, Lbuf, max_iter, grad_tol, recs,
+                               results, st, s));
+    }
   }
   // explicit residuals of best and start, only when an iterate improved (nnls.py:219-227)
   NENMF_TRY(resid<T>(ws, At, p, r, B, c, ldb, trans, Fout, F0, Lbuf + 2, &st->returned_best, s));

@@ -99,6 +99,212 @@ static NnlsPlan plan_nnls(int64_t p, int64_t c) {
 }
 
 
+
+struct SolverShared {
+  volatile int resolved, best_j, halt;
+  volatile int posted[NW_MAXW];
+  int kdone[NW_MAXW], bsw[NW_MAXW];  // per warp: iterations done, window held in the best slot
+  int stop_at, fail_at;
+  double best_part, pg_ref;
+};
+
+__device__ __forceinline__ void solver_shared_init(SolverShared& sh) {
+  if (threadIdx.x < NW_MAXW) {
+    sh.posted[threadIdx.x] = -3;
+    sh.kdone[threadIdx.x] = 0;
+    sh.bsw[threadIdx.x] = -1;
+  }
+  if (threadIdx.x == 0) {
+    sh.resolved = -2;
+    sh.best_j = -1;
+    sh.halt = 0;
+    sh.stop_at = -1;
+    sh.fail_at = -1;
+    sh.best_part = 0.0;
+    sh.pg_ref = 0.0;
+  }
+}
+
+// The resolver warp of a persistent solver CTA (see nnls_kernel.cuh):
+// publishes this CTA's window records, summarizes the windows it owns and
+// applies the reference's per-iteration decisions (nnls.py:177,196-203) in
+// order.  `pp` holds the compute warps' per-iteration sums [PPD][MAXW][3].
+static __device__ void resolver_warp(SolverShared& sh, const double* pp, int ncw, int max_iter, double grad_tol, double L,
+                              WinRec* __restrict__ recs, WinRec* __restrict__ results,
+                              unsigned long long* __restrict__ tracebuf) {
+  const int lane = threadIdx.x & 31;
+  const int G = gridDim.x;
+  const bool trace = tracebuf != nullptr;
+  auto g_nnls_trace = [&](int row) { return tracebuf + (size_t)row * NN_TRACE_LEN; };
+    const int nwin = (max_iter + NW_WIN - 1) / NW_WIN;
+    int pubw = -1;                       // next window to publish (-1: the start point)
+    int sumw = (int)blockIdx.x - 1;      // next owned window to summarize (window -1 -> CTA 0)
+    int resw = -1;                       // next window to resolve
+    int best_j = -1, stop_at = -1, fail_at = -1;
+    double best_part = 0.0, pg_ref = 0.0;
+    bool halt = false;
+    unsigned long long t_prog = gtimer_ns();
+    auto rec_idx = [&](int w) { return (w + 1 + NW_SLOTS) % NW_SLOTS; };
+    auto win_first = [&](int w) { return w < 0 ? -1 : w * NW_WIN; };
+    auto win_last = [&](int w) { return w < 0 ? -1 : min(max_iter - 1, w * NW_WIN + NW_WIN - 1); };
+    while (!halt && resw < nwin) {
+      bool progress = false;
+      // A. publish this CTA's record of window pubw once every compute warp posted it
+      if (pubw < nwin) {
+        const int last = win_last(pubw);
+        const int posted = lane < ncw ? sh.posted[lane] : INT_MAX;
+        if (__all_sync(0xffffffffu, posted >= last)) {
+          __threadfence_block();
+          WinRec* rec = recs + (int64_t)rec_idx(pubw) * G + blockIdx.x;
+          const int j = win_first(pubw) + lane;
+          if (j <= last) {
+            const double* q = pp + (size_t)((j + NW_PPD) % NW_PPD) * NW_MAXW * 3;
+            double v0 = 0.0, v1 = 0.0, v2 = 0.0;
+            for (int w = 0; w < ncw; ++w) {
+              v0 += q[w * 3 + 0];
+              v1 += q[w * 3 + 1];
+              v2 += q[w * 3 + 2];
+            }
+            rec->v[lane][0] = v0;
+            rec->v[lane][1] = v1;
+            rec->v[lane][2] = v2;
+          }
+          __syncwarp();
+          if (lane == 0) {
+            fence_gpu();
+            st_relaxed_u64(&rec->tag, (unsigned long long)(pubw + 2));
+          }
+          __syncwarp();
+          if (trace && blockIdx.x == 0 && lane == 0 && pubw + 1 < NN_TRACE_LEN)
+            g_nnls_trace(1)[pubw + 1] = gtimer_ns();
+          ++pubw;
+          progress = true;
+        }
+      }
+      // B. summarize the owned window sumw (all CTAs' records, CTA order)
+      if (sumw < nwin) {
+        const WinRec* row = recs + (int64_t)rec_idx(sumw) * G;
+        const unsigned long long want = (unsigned long long)(sumw + 2);
+        bool ok = true;
+        for (int b = lane; b < G; b += 32) ok &= ld_relaxed_u64(&row[b].tag) == want;
+        if (__all_sync(0xffffffffu, ok)) {
+          fence_gpu();
+          const int j = win_first(sumw) + lane;
+          double v0 = 0.0, v1 = 0.0, v2 = 0.0;
+          if (j <= win_last(sumw)) {
+            int b = 0;
+            for (; b + 4 <= G; b += 4) {
+              double x[4][3];
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                x[u][0] = __ldcg(&row[b + u].v[lane][0]);
+                x[u][1] = __ldcg(&row[b + u].v[lane][1]);
+                x[u][2] = __ldcg(&row[b + u].v[lane][2]);
+              }
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                v0 += x[u][0];
+                v1 += x[u][1];
+                v2 += x[u][2];
+              }
+            }
+            for (; b < G; ++b) {
+              v0 += __ldcg(&row[b].v[lane][0]);
+              v1 += __ldcg(&row[b].v[lane][1]);
+              v2 += __ldcg(&row[b].v[lane][2]);
+            }
+          }
+          WinRec* res = results + rec_idx(sumw);
+          res->v[lane][0] = v0;
+          res->v[lane][1] = v1;
+          res->v[lane][2] = v2;
+          __syncwarp();
+          if (lane == 0) {
+            fence_gpu();
+            st_relaxed_u64(&res->tag, want);
+          }
+          __syncwarp();
+          sumw += G;
+          progress = true;
+        }
+      }
+      // C. resolve window resw
+      {
+        const WinRec* res = results + rec_idx(resw);
+        const unsigned long long want = (unsigned long long)(resw + 2);
+        const bool ready = ld_relaxed_u64(&res->tag) == want;  // same address in all lanes
+        if (ready) {
+          fence_gpu();
+          const double r0 = __ldcg(&res->v[lane][0]);
+          const double r1 = __ldcg(&res->v[lane][1]);
+          const double r2 = __ldcg(&res->v[lane][2]);
+          const int first = win_first(resw), last = win_last(resw);
+          for (int j = first; j <= last && !halt; ++j) {
+            const int t = j - (resw < 0 ? -1 : first);
+            const double pg = sqrt(__shfl_sync(0xffffffffu, r0, t));
+            const double partial = 0.5 * (__shfl_sync(0xffffffffu, r1, t) - __shfl_sync(0xffffffffu, r2, t));
+            if (j < 0) {
+              pg_ref = pg;
+              best_part = partial;
+              if (!(isfinite(partial) && isfinite(pg) && isfinite(L))) {
+                fail_at = 0;
+                halt = true;
+              }
+            } else if (!(isfinite(pg) && isfinite(partial))) {
+              fail_at = j;
+              halt = true;
+            } else {
+              if (partial < best_part) {  // nnls.py:198-201
+                best_part = partial;
+                best_j = j;
+              }
+              if (pg <= grad_tol * pg_ref) {  // nnls.py:202-203
+                stop_at = j;
+                halt = true;
+              }
+            }
+            if (trace && blockIdx.x == 0 && lane == 0 && j + 1 < NN_TRACE_LEN) g_nnls_trace(2)[j + 1] = gtimer_ns();
+          }
+          if (lane == 0) {
+            sh.best_j = best_j;
+            __threadfence_block();
+            sh.resolved = last;
+            if (halt) sh.halt = 1;
+          }
+          __syncwarp();
+          ++resw;
+          progress = true;
+        }
+      }
+      if (progress) {
+        t_prog = gtimer_ns();
+      } else {
+        __nanosleep(32);
+        if (gtimer_ns() - t_prog > NN_WATCHDOG_NS) {
+          fail_at = -2;
+          halt = true;
+        }
+      }
+    }
+    if (lane == 0) {
+      sh.best_j = best_j;
+      sh.stop_at = stop_at;
+      sh.fail_at = fail_at;
+      sh.best_part = best_part;
+      sh.pg_ref = pg_ref;
+      __threadfence_block();
+      sh.halt = 1;
+    }
+  }
+
+template <typename T>
+int launch_nnls_mma(const T* W, const T* V, const T* F0, T* Fout, T* snaps, double* salpha, int p, int64_t c, int grid,
+                    int64_t cpb, const double* Lptr, int max_iter, double grad_tol, WinRec* recs, WinRec* results,
+                    nenmf_device_status* st, unsigned long long* tracebuf, const double* wtab, cudaStream_t s);
+
+template <typename T>
+int nnls_mma_max_cols(int p);  // columns one CTA of the tensor-core solver can hold
+
 template <typename T, int TPC>
 int launch_nnls_tpc(const NnlsPlan& pl, const T* W, const T* V, const T* F0, T* Fout, T* snaps, double* salpha,
                     T* gstate, int p, int64_t c, const double* Lptr, int max_iter, double grad_tol, WinRec* recs,

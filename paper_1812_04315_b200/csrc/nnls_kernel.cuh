@@ -42,11 +42,7 @@ k_nnls(const T* __restrict__ W, const T* __restrict__ V, const T* __restrict__ F
   T* Ws = reinterpret_cast<T*>(smem_d);                                       // [PM][ldW], zero padded
   double* pp = smem_d + (((size_t)PM * ldW * sizeof(T) + 15) / 16) * 2;        // [PPD][MAXW][3]
   T* Sb = reinterpret_cast<T*>(pp + (size_t)NW_PPD * NW_MAXW * 3);            // [5][p][ldS]
-  __shared__ volatile int s_resolved, s_best_j, s_halt;
-  __shared__ volatile int s_posted[NW_MAXW];
-  __shared__ int s_kdone[NW_MAXW], s_bsw[NW_MAXW];  // per warp: iterations done, window in the best slot
-  __shared__ int s_stop_at, s_fail_at;
-  __shared__ double s_best_part, s_pg_ref;
+  __shared__ SolverShared sh;
 
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int ncw = (blockDim.x >> 5) - 1;
@@ -61,20 +57,7 @@ k_nnls(const T* __restrict__ W, const T* __restrict__ V, const T* __restrict__ F
     const int r = i / ldW, l = i % ldW;
     Ws[i] = (r < p && l < p) ? W[r * p + l] : T(0);
   }
-  if (tid < NW_MAXW) {
-    s_posted[tid] = -3;
-    s_kdone[tid] = 0;
-    s_bsw[tid] = -1;
-  }
-  if (tid == 0) {
-    s_resolved = -2;
-    s_best_j = -1;
-    s_halt = 0;
-    s_stop_at = -1;
-    s_fail_at = -1;
-    s_best_part = 0.0;
-    s_pg_ref = 0.0;
-  }
+  solver_shared_init(sh);
   __syncthreads();
   if (st->code != 0) return;  // an earlier stage failed (uniform)
   const double L = *Lptr;
@@ -214,7 +197,7 @@ k_nnls(const T* __restrict__ W, const T* __restrict__ V, const T* __restrict__ F
     auto post_flag = [&](int j) {
       if (lane == 0) {
         __threadfence_block();
-        s_posted[wid] = j;
+        sh.posted[wid] = j;
       }
     };
 
@@ -283,15 +266,15 @@ k_nnls(const T* __restrict__ W, const T* __restrict__ V, const T* __restrict__ F
         int ok = 1;
         if (lane == 0) {
           const int need = (w - NW_FLIGHT) * NW_WIN - 1;
-          while (s_resolved < need && !s_halt) __nanosleep(64);
-          ok = s_halt ? 0 : 1;
+          while (sh.resolved < need && !sh.halt) __nanosleep(64);
+          ok = sh.halt ? 0 : 1;
         }
         ok = __shfl_sync(0xffffffffu, ok, 0);
         if (!ok) break;
         // snapshot slot w % NW_SNAP; if it still holds the best window, save it first
         const int slot = w % NW_SNAP;
         const int evicted = w - NW_SNAP;
-        const int bj = s_best_j;
+        const int bj = sh.best_j;
         const bool save = evicted >= 0 && bj >= 0 && bj / NW_WIN == evicted;
         for (int base = 0; wfirst + base < ncols; base += cstride) {
           const int cl = cfirst + base;
@@ -316,7 +299,7 @@ k_nnls(const T* __restrict__ W, const T* __restrict__ V, const T* __restrict__ F
           if (save) {
             sa[NW_SNAP * 2 + 0] = sa[slot * 2 + 0];
             sa[NW_SNAP * 2 + 1] = sa[slot * 2 + 1];
-            s_bsw[wid] = evicted;
+            sh.bsw[wid] = evicted;
           }
           sa[slot * 2 + 0] = alpha;
           sa[slot * 2 + 1] = w_prev;
@@ -344,178 +327,19 @@ k_nnls(const T* __restrict__ W, const T* __restrict__ V, const T* __restrict__ F
       const double a1n = alpha_next_d(alpha);
       w_prev = __ddiv_rn(alpha - 1.0, a1n);
       alpha = a1n;
-      if (lane == 0 && s_halt) go = false;
+      if (lane == 0 && sh.halt) go = false;
       go = __shfl_sync(0xffffffffu, go ? 1 : 0, 0) != 0;
     }
-    if (lane == 0) s_kdone[wid] = k;  // warps may stop at different k; each keeps its own columns
+    if (lane == 0) sh.kdone[wid] = k;  // warps may stop at different k; each keeps its own columns
   } else {
-    // ------------------------------------------------------------ resolver
-    const int nwin = (max_iter + NW_WIN - 1) / NW_WIN;
-    int pubw = -1;                       // next window to publish (-1: the start point)
-    int sumw = (int)blockIdx.x - 1;      // next owned window to summarize (window -1 -> CTA 0)
-    int resw = -1;                       // next window to resolve
-    int best_j = -1, stop_at = -1, fail_at = -1;
-    double best_part = 0.0, pg_ref = 0.0;
-    bool halt = false;
-    unsigned long long t_prog = gtimer_ns();
-    auto rec_idx = [&](int w) { return (w + 1 + NW_SLOTS) % NW_SLOTS; };
-    auto win_first = [&](int w) { return w < 0 ? -1 : w * NW_WIN; };
-    auto win_last = [&](int w) { return w < 0 ? -1 : min(max_iter - 1, w * NW_WIN + NW_WIN - 1); };
-    while (!halt && resw < nwin) {
-      bool progress = false;
-      // A. publish this CTA's record of window pubw once every compute warp posted it
-      if (pubw < nwin) {
-        const int last = win_last(pubw);
-        const int posted = lane < ncw ? s_posted[lane] : INT_MAX;
-        if (__all_sync(0xffffffffu, posted >= last)) {
-          __threadfence_block();
-          WinRec* rec = recs + (int64_t)rec_idx(pubw) * G + blockIdx.x;
-          const int j = win_first(pubw) + lane;
-          if (j <= last) {
-            const double* q = pp + (size_t)((j + NW_PPD) % NW_PPD) * NW_MAXW * 3;
-            double v0 = 0.0, v1 = 0.0, v2 = 0.0;
-            for (int w = 0; w < ncw; ++w) {
-              v0 += q[w * 3 + 0];
-              v1 += q[w * 3 + 1];
-              v2 += q[w * 3 + 2];
-            }
-            rec->v[lane][0] = v0;
-            rec->v[lane][1] = v1;
-            rec->v[lane][2] = v2;
-          }
-          __syncwarp();
-          if (lane == 0) {
-            fence_gpu();
-            st_relaxed_u64(&rec->tag, (unsigned long long)(pubw + 2));
-          }
-          __syncwarp();
-          if (trace && blockIdx.x == 0 && lane == 0 && pubw + 1 < NN_TRACE_LEN)
-            g_nnls_trace(1)[pubw + 1] = gtimer_ns();
-          ++pubw;
-          progress = true;
-        }
-      }
-      // B. summarize the owned window sumw (all CTAs' records, CTA order)
-      if (sumw < nwin) {
-        const WinRec* row = recs + (int64_t)rec_idx(sumw) * G;
-        const unsigned long long want = (unsigned long long)(sumw + 2);
-        bool ok = true;
-        for (int b = lane; b < G; b += 32) ok &= ld_relaxed_u64(&row[b].tag) == want;
-        if (__all_sync(0xffffffffu, ok)) {
-          fence_gpu();
-          const int j = win_first(sumw) + lane;
-          double v0 = 0.0, v1 = 0.0, v2 = 0.0;
-          if (j <= win_last(sumw)) {
-            int b = 0;
-            for (; b + 4 <= G; b += 4) {
-              double x[4][3];
-#pragma unroll
-              for (int u = 0; u < 4; ++u) {
-                x[u][0] = __ldcg(&row[b + u].v[lane][0]);
-                x[u][1] = __ldcg(&row[b + u].v[lane][1]);
-                x[u][2] = __ldcg(&row[b + u].v[lane][2]);
-              }
-#pragma unroll
-              for (int u = 0; u < 4; ++u) {
-                v0 += x[u][0];
-                v1 += x[u][1];
-                v2 += x[u][2];
-              }
-            }
-            for (; b < G; ++b) {
-              v0 += __ldcg(&row[b].v[lane][0]);
-              v1 += __ldcg(&row[b].v[lane][1]);
-              v2 += __ldcg(&row[b].v[lane][2]);
-            }
-          }
-          WinRec* res = results + rec_idx(sumw);
-          res->v[lane][0] = v0;
-          res->v[lane][1] = v1;
-          res->v[lane][2] = v2;
-          __syncwarp();
-          if (lane == 0) {
-            fence_gpu();
-            st_relaxed_u64(&res->tag, want);
-          }
-          __syncwarp();
-          sumw += G;
-          progress = true;
-        }
-      }
-      // C. resolve window resw
-      {
-        const WinRec* res = results + rec_idx(resw);
-        const unsigned long long want = (unsigned long long)(resw + 2);
-        const bool ready = ld_relaxed_u64(&res->tag) == want;  // same address in all lanes
-        if (ready) {
-          fence_gpu();
-          const double r0 = __ldcg(&res->v[lane][0]);
-          const double r1 = __ldcg(&res->v[lane][1]);
-          const double r2 = __ldcg(&res->v[lane][2]);
-          const int first = win_first(resw), last = win_last(resw);
-          for (int j = first; j <= last && !halt; ++j) {
-            const int t = j - (resw < 0 ? -1 : first);
-            const double pg = sqrt(__shfl_sync(0xffffffffu, r0, t));
-            const double partial = 0.5 * (__shfl_sync(0xffffffffu, r1, t) - __shfl_sync(0xffffffffu, r2, t));
-            if (j < 0) {
-              pg_ref = pg;
-              best_part = partial;
-              if (!(isfinite(partial) && isfinite(pg) && isfinite(L))) {
-                fail_at = 0;
-                halt = true;
-              }
-            } else if (!(isfinite(pg) && isfinite(partial))) {
-              fail_at = j;
-              halt = true;
-            } else {
-              if (partial < best_part) {  // nnls.py:198-201
-                best_part = partial;
-                best_j = j;
-              }
-              if (pg <= grad_tol * pg_ref) {  // nnls.py:202-203
-                stop_at = j;
-                halt = true;
-              }
-            }
-            if (trace && blockIdx.x == 0 && lane == 0 && j + 1 < NN_TRACE_LEN) g_nnls_trace(2)[j + 1] = gtimer_ns();
-          }
-          if (lane == 0) {
-            s_best_j = best_j;
-            __threadfence_block();
-            s_resolved = last;
-            if (halt) s_halt = 1;
-          }
-          __syncwarp();
-          ++resw;
-          progress = true;
-        }
-      }
-      if (progress) {
-        t_prog = gtimer_ns();
-      } else {
-        __nanosleep(32);
-        if (gtimer_ns() - t_prog > NN_WATCHDOG_NS) {
-          fail_at = -2;
-          halt = true;
-        }
-      }
-    }
-    if (lane == 0) {
-      s_best_j = best_j;
-      s_stop_at = stop_at;
-      s_fail_at = fail_at;
-      s_best_part = best_part;
-      s_pg_ref = pg_ref;
-      __threadfence_block();
-      s_halt = 1;
-    }
+    resolver_warp(sh, pp, ncw, max_iter, grad_tol, L, recs, results, tracebuf);
   }
   __syncthreads();  // compute warps done; decisions final
 
   // ---------------------------------------------------------------- output
-  const int bj = s_best_j;
-  if (!resolver && bj >= 0 && s_fail_at < 0) {
-    const int kd = s_kdone[wid];  // iterations this warp computed: 0 .. kd-1
+  const int bj = sh.best_j;
+  if (!resolver && bj >= 0 && sh.fail_at < 0) {
+    const int kd = sh.kdone[wid];  // iterations this warp computed: 0 .. kd-1
     if (bj == kd - 1 || bj == kd - 2) {
       // still live in a parity buffer
       const int buf = bj & 1;
@@ -531,7 +355,7 @@ k_nnls(const T* __restrict__ W, const T* __restrict__ V, const T* __restrict__ F
     } else {
       // recompute F_bj from the snapshot of its window (same arithmetic)
       const int wb = bj / NW_WIN;
-      const int slot = (s_bsw[wid] == wb && wb + NW_SNAP <= (kd - 1) / NW_WIN) ? NW_SNAP : wb % NW_SNAP;
+      const int slot = (sh.bsw[wid] == wb && wb + NW_SNAP <= (kd - 1) / NW_WIN) ? NW_SNAP : wb % NW_SNAP;
       const int k0 = wb * NW_WIN;
       const double* sa = snap_alpha + ((int64_t)blockIdx.x * NW_MAXW + wid) * (NW_SNAP + 1) * 2;
       double alpha = sa[slot * 2 + 0];
@@ -582,12 +406,12 @@ k_nnls(const T* __restrict__ W, const T* __restrict__ V, const T* __restrict__ F
     }
   }
   if (blockIdx.x == 0 && tid == 0) {
-    if (s_fail_at >= 0) status_fail(st, NENMF_ERR_NUMERICAL_FAILURE, s_fail_at);
-    if (s_fail_at == -2) status_fail(st, NENMF_ERR_CUDA, -2);
-    st->inner_iters = s_stop_at >= 0 ? s_stop_at + 1 : (s_fail_at >= 0 ? s_fail_at : max_iter);
-    st->returned_best = s_best_j >= 0 ? 1 : 0;
-    st->best_partial = s_best_part;
-    st->pg_ref = s_pg_ref;
+    if (sh.fail_at >= 0) status_fail(st, NENMF_ERR_NUMERICAL_FAILURE, sh.fail_at);
+    if (sh.fail_at == -2) status_fail(st, NENMF_ERR_CUDA, -2);
+    st->inner_iters = sh.stop_at >= 0 ? sh.stop_at + 1 : (sh.fail_at >= 0 ? sh.fail_at : max_iter);
+    st->returned_best = sh.best_j >= 0 ? 1 : 0;
+    st->best_partial = sh.best_part;
+    st->pg_ref = sh.pg_ref;
   }
 }
 
