@@ -95,6 +95,13 @@ __device__ __forceinline__ float fma_acc(float a, float b, float c) { return fma
 // np.maximum(x, 0) keeping NaN (numpy propagates NaN; fmax would not)
 template <typename T>
 __device__ __forceinline__ T relu_nan(T x) { return (x >= T(0) || x != x) ? x : T(0); }
+// max(x, 0) propagating NaN in one instruction (the sign of a zero may differ)
+__device__ __forceinline__ float relu_nan_fast(float x) {
+  float r;
+  asm("max.NaN.f32 %0, %1, 0f00000000;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ double relu_nan_fast(double x) { return relu_nan(x); }
 // np.minimum(x, 0) keeping NaN
 template <typename T>
 __device__ __forceinline__ T min0_nan(T x) { return (x <= T(0) || x != x) ? x : T(0); }

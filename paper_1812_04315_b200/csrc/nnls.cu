@@ -204,9 +204,9 @@ int solve_nnls(Arena& ws, const T* At, int64_t r, int64_t p, const T* B, int64_t
   // tensor-core solver: p <= 32 and at most 15 blocks of 8 columns per CTA
   int sms = sm_count();
   if (sms <= 0) sms = 148;
-  const int mgrid = (int)imax(1, imin(sms, cdiv(c, 8)));
+  const int mgrid = (int)imax(1, imin(sms, cdiv(c, nnls_mma_col_block<T>())));
   const int64_t mcpb = cdiv(c, mgrid);
-  const bool use_mma = p <= 32 && mcpb <= imin(8 * (NW_MAXW - 1), nnls_mma_max_cols<T>((int)p)) &&
+  const bool use_mma = p <= 32 && mcpb <= nnls_mma_max_cols<T>((int)p) && max_iter <= NN_WTAB_LEN &&
                        getenv("NENMF_NNLS_SIMT") == nullptr;
   const int grid_used = use_mma ? mgrid : pl.grid;
   T* W = ws.take<T>((size_t)p * p);
@@ -224,10 +224,12 @@ int solve_nnls(Arena& ws, const T* At, int64_t r, int64_t p, const T* B, int64_t
   if (!dry) {
     NENMF_CUDA_TRY(cudaMemsetAsync(recs, 0, sizeof(WinRec) * ((size_t)NW_SLOTS * grid_used + NW_SLOTS), s));
     if (use_mma) {
+      const double* wtab = momentum_table(max_iter);
+      if (wtab == nullptr) return NENMF_ERR_CUDA;
       unsigned long long* tracebuf = nullptr;
       if (getenv("NENMF_NNLS_TRACE") != nullptr) NENMF_CUDA_TRY(cudaGetSymbolAddress((void**)&tracebuf, g_nnls_trace));
       NENMF_TRY(launch_nnls_mma<T>(W, V, F0, Fout, snaps, salpha, (int)p, c, mgrid, mcpb, Lbuf, max_iter, grad_tol,
-                                   recs, results, st, tracebuf, momentum_table(max_iter), s));
+                                   recs, results, st, tracebuf, wtab, s));
     } else {
       NENMF_TRY(launch_nnls<T>(pl, W, V, F0, Fout, snaps, salpha, gstate, (int)p, c, Lbuf, max_iter, grad_tol, recs,
                                results, st, s));

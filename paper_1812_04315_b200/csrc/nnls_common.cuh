@@ -222,6 +222,7 @@ static __device__ void resolver_warp(SolverShared& sh, const double* pp, int ncw
           if (lane == 0) {
             fence_gpu();
             st_relaxed_u64(&res->tag, want);
+            if (trace && sumw + 1 < 1024) g_nnls_trace(3)[3072 + sumw + 1] = gtimer_ns();
           }
           __syncwarp();
           sumw += G;
@@ -304,6 +305,8 @@ int launch_nnls_mma(const T* W, const T* V, const T* F0, T* Fout, T* snaps, doub
 
 template <typename T>
 int nnls_mma_max_cols(int p);  // columns one CTA of the tensor-core solver can hold
+template <typename T>
+int nnls_mma_col_block();      // columns per compute warp of the tensor-core solver
 
 template <typename T, int TPC>
 int launch_nnls_tpc(const NnlsPlan& pl, const T* W, const T* V, const T* F0, T* Fout, T* snaps, double* salpha,
