@@ -280,8 +280,8 @@ def run_ours(args, rank, world, local_rank):
                 "ms_per_step": ms_e2e},
         "gpu_launches": int(launches),
         "clocks": clocks,
-        "roofline": roof["dominant"],
-        "roofline_rsi": roof["rsi"],
+        "roofline": roof["rsi"],
+        "solver": roof["solver"],
         "kernels": roof["table"],
         "cpu_baseline": cpu,
     }
@@ -352,21 +352,27 @@ def kernel_rooflines(w, Xd, dtype):
     ms_solve = ev_time(solve, 5)
     iters = int(_lib.read_status(status)[0]["inner_iters"])
     s = Xd.element_size()
-    # streamed-state model of one inner iteration: read F_{k-1},F_{k-2},g_{k-1},g_{k-2},V; write F_k,g_k
-    solve_bytes = iters * 7 * w.p * w.m * s
     pass_gbs = pass_bytes / (ms_pass * 1e-3) / 1e9
-    solve_gbs = solve_bytes / (ms_solve * 1e-3) / 1e9
-    rsi = {"bound": "hbm", "kernel": "k_dual (RSI X-pass)", "achieved": pass_gbs, "peak": hbm, "unit": "GB/s",
-           "frac": pass_gbs / hbm, "traffic": _traffic("k_dual"), "peak_source": src,
-           "ms_per_launch": ms_pass, "bytes_per_launch": pass_bytes,
-           "rsi_total_ms": ms_rsi, "rsi_effective_gbs": rsi_bytes / (ms_rsi * 1e-3) / 1e9}
-    dom = {"bound": "hbm", "kernel": "k_nnls (persistent inner solver, F-half)", "achieved": solve_gbs,
-           "peak": hbm, "unit": "GB/s", "frac": solve_gbs / hbm, "traffic": _traffic("k_nnls"),
-           "peak_source": src, "ms_per_launch": ms_solve, "inner_iters": iters,
-           "us_per_inner_iter": 1e3 * ms_solve / max(iters, 1),
-           "bytes_model": "7*p*m*s per inner iteration (state streamed); actual state is L2-resident"}
+    rsi = {"bound": "hbm", "kernel": "RSI X-pass (k_dual_tc: one read of X -> X*A and X^T*B)",
+           "achieved": pass_gbs, "peak": hbm, "unit": "GB/s", "frac": pass_gbs / hbm,
+           "traffic": _traffic("k_dual_tc"), "peak_source": src,
+           "algorithmic_bytes_per_launch": pass_bytes, "ms_per_launch": ms_pass,
+           "rsi_total_ms": ms_rsi, "rsi_effective_gbs": rsi_bytes / (ms_rsi * 1e-3) / 1e9,
+           "rsi_bytes_model": "(2q+2)*n*m*s_X (SURVEY 8d)"}
+    # the inner solver is latency-bound (state lives in registers; one
+    # dependent iteration after another), so its figure is time per iteration
+    # next to the floors of SURVEY 8(d): HBM if the state were streamed, and
+    # the tensor-pipe flops of W*F
+    us_it = 1e3 * ms_solve / max(iters, 1)
+    flops_it = 2 * w.p * w.p * w.m
+    stream_bytes_it = 9 * w.p * w.m * s
+    solver = {"bound": "latency", "kernel": "k_nnls_mma (persistent inner solver, F-half at cfg2)",
+              "ms_per_launch": ms_solve, "inner_iters": iters, "us_per_inner_iter": us_it,
+              "flops_per_iter": flops_it, "achieved_tflops": flops_it / (us_it * 1e-6) / 1e12,
+              "hbm_floor_us_if_streamed": stream_bytes_it / (hbm * 1e9) * 1e6,
+              "traffic": _traffic("k_nnls_mma")}
     table = {"dual_pass_ms": ms_pass, "rsi_ms": ms_rsi, "solve_F_half_ms": ms_solve}
-    return {"rsi": rsi, "dominant": dom, "table": table}
+    return {"rsi": rsi, "solver": solver, "table": table}
 
 
 def main():
