@@ -191,59 +191,93 @@ k_dual_tc(const float* __restrict__ X, int64_t n, int64_t m, int64_t ldx, const 
 
   if (wid < NPROD) {
     // ------------------------------------------------------------ producers
+    // Each thread owns 16 float4 of every tile.  The loads run one tile ahead
+    // in a rolling register queue: slot j is refilled with the next tile's
+    // float4 right after it has been split into the current stage, so ~64 KB
+    // per SM stay in flight while the producers convert (HBM latency hidden).
     const int ptid = tid;  // 0 .. 255
+    constexpr int NQ = TILE * 32 / (NPROD * 32);  // 16 float4 per thread per tile
+    int u = blockIdx.x, rt = 0, ct = 0, rt0 = 0, rt1 = 0, ct0 = 0, ct1 = 0, rc_, cb_;
+    bool valid = u < U.units;
+    if (valid) {
+      unit_bounds(U, u, rt0, rt1, ct0, ct1, rc_, cb_);
+      rt = rt0;
+      ct = ct0;
+    }
+    auto advance = [&]() {
+      if (++ct < ct1) return;
+      ct = ct0;
+      if (++rt < rt1) return;
+      u += gridDim.x;
+      valid = u < U.units;
+      if (valid) {
+        unit_bounds(U, u, rt0, rt1, ct0, ct1, rc_, cb_);
+        rt = rt0;
+        ct = ct0;
+      }
+    };
+    auto load = [&](int trt, int tct, int j) -> float4 {
+      const int q = ptid + j * NPROD * 32;
+      const int row = q >> 5, c4 = q & 31;
+      const int64_t gr = (int64_t)trt * TILE + row, gc = (int64_t)tct * TILE + 4 * c4;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (gr < n && gc < m) v = __ldcs(reinterpret_cast<const float4*>(X + gr * ldx + gc));
+      return v;
+    };
+    float4 R[NQ];
+    if (valid) {
+#pragma unroll
+      for (int j = 0; j < NQ; ++j) R[j] = load(rt, ct, j);
+    }
     int t = 0;
-    for (int u = blockIdx.x; u < U.units; u += gridDim.x) {
-      int rt0, rt1, ct0, ct1, rc, cb;
-      unit_bounds(U, u, rt0, rt1, ct0, ct1, rc, cb);
-      for (int rt = rt0; rt < rt1; ++rt)
-        for (int ct = ct0; ct < ct1; ++ct, ++t) {
-          const int s = t % NSTAGE;
-          mbar_wait(&bar_empty[s], ((t / NSTAGE) & 1) ^ 1);
-          uint8_t* st = smem + (size_t)s * STAGE;
-          uint8_t* xhi = st;
-          uint8_t* xlo = st + 2 * SUB_BYTES;
-          uint8_t* a2 = st + 4 * SUB_BYTES;
-          uint8_t* b2 = a2 + 2 * SK_SUB;
-          const int64_t r0 = (int64_t)rt * TILE, c0 = (int64_t)ct * TILE;
-          // X tile: 128 rows x 32 float4; a warp covers one row
-#pragma unroll 4
-          for (int q = ptid; q < TILE * 32; q += NPROD * 32) {
-            const int row = q >> 5, c4 = q & 31;
-            const int64_t gr = r0 + row, gc = c0 + 4 * c4;
-            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (gr < n && gc < m) v = __ldg(reinterpret_cast<const float4*>(X + gr * ldx + gc));
-            const __nv_bfloat162 h01 = __floats2bfloat162_rn(v.x, v.y);
-            const __nv_bfloat162 h23 = __floats2bfloat162_rn(v.z, v.w);
-            const float2 f01 = __bfloat1622float2(h01), f23 = __bfloat1622float2(h23);
-            const __nv_bfloat162 l01 = __floats2bfloat162_rn(v.x - f01.x, v.y - f01.y);
-            const __nv_bfloat162 l23 = __floats2bfloat162_rn(v.z - f23.x, v.w - f23.y);
-            const int sub = c4 >> 4, cc = c4 & 15;
-            const uint32_t off = (uint32_t)sub * SUB_BYTES + (uint32_t)row * 128 +
-                                 ((uint32_t)((cc >> 1) ^ (row & 7)) << 4) + (uint32_t)(cc & 1) * 8;
-            uint2 hv, lv;
-            hv.x = *reinterpret_cast<const uint32_t*>(&h01);
-            hv.y = *reinterpret_cast<const uint32_t*>(&h23);
-            lv.x = *reinterpret_cast<const uint32_t*>(&l01);
-            lv.y = *reinterpret_cast<const uint32_t*>(&l23);
-            *reinterpret_cast<uint2*>(xhi + off) = hv;
-            *reinterpret_cast<uint2*>(xlo + off) = lv;
-          }
-          // skinny tiles: N2 rows x 128 K-elements (bf16) = N2 x 16 chunks of 16 B
-          for (int q = ptid; q < N2 * 16; q += NPROD * 32) {
-            const int row = q >> 4, ch16 = q & 15, sub = ch16 >> 3, ch = ch16 & 7;
-            const uint32_t off = (uint32_t)sub * SK_SUB + (uint32_t)row * 128 + ((uint32_t)(ch ^ (row & 7)) << 4);
-            const int64_t ca = c0 + ch16 * 8;
-            uint4 va = make_uint4(0, 0, 0, 0), vb = make_uint4(0, 0, 0, 0);
-            if (ca < lda2) va = __ldg(reinterpret_cast<const uint4*>(A2 + (int64_t)row * lda2 + ca));
-            const int64_t rb = r0 + ch16 * 8;
-            if (rb < ldb2) vb = __ldg(reinterpret_cast<const uint4*>(B2 + (int64_t)row * ldb2 + rb));
-            *reinterpret_cast<uint4*>(a2 + off) = va;
-            *reinterpret_cast<uint4*>(b2 + off) = vb;
-          }
-          fence_proxy_async();
-          mbar_arrive(&bar_full[s]);
-        }
+    while (valid) {
+      const int crt = rt, cct = ct;
+      advance();  // (rt, ct, valid) now name the next tile
+      const int s = t % NSTAGE;
+      mbar_wait(&bar_empty[s], ((t / NSTAGE) & 1) ^ 1);
+      uint8_t* st = smem + (size_t)s * STAGE;
+      uint8_t* xhi = st;
+      uint8_t* xlo = st + 2 * SUB_BYTES;
+      uint8_t* a2 = st + 4 * SUB_BYTES;
+      uint8_t* b2 = a2 + 2 * SK_SUB;
+      const int64_t r0 = (int64_t)crt * TILE, c0 = (int64_t)cct * TILE;
+#pragma unroll
+      for (int j = 0; j < NQ; ++j) {
+        const float4 v = R[j];
+        if (valid) R[j] = load(rt, ct, j);
+        const int q = ptid + j * NPROD * 32;
+        const int row = q >> 5, c4 = q & 31;
+        const __nv_bfloat162 h01 = __floats2bfloat162_rn(v.x, v.y);
+        const __nv_bfloat162 h23 = __floats2bfloat162_rn(v.z, v.w);
+        const float2 f01 = __bfloat1622float2(h01), f23 = __bfloat1622float2(h23);
+        const __nv_bfloat162 l01 = __floats2bfloat162_rn(v.x - f01.x, v.y - f01.y);
+        const __nv_bfloat162 l23 = __floats2bfloat162_rn(v.z - f23.x, v.w - f23.y);
+        const int sub = c4 >> 4, cc = c4 & 15;
+        const uint32_t off = (uint32_t)sub * SUB_BYTES + (uint32_t)row * 128 +
+                             ((uint32_t)((cc >> 1) ^ (row & 7)) << 4) + (uint32_t)(cc & 1) * 8;
+        uint2 hv, lv;
+        hv.x = *reinterpret_cast<const uint32_t*>(&h01);
+        hv.y = *reinterpret_cast<const uint32_t*>(&h23);
+        lv.x = *reinterpret_cast<const uint32_t*>(&l01);
+        lv.y = *reinterpret_cast<const uint32_t*>(&l23);
+        *reinterpret_cast<uint2*>(xhi + off) = hv;
+        *reinterpret_cast<uint2*>(xlo + off) = lv;
+      }
+      // skinny tiles: N2 rows x 128 K-elements (bf16) = N2 x 16 chunks of 16 B
+      for (int q = ptid; q < N2 * 16; q += NPROD * 32) {
+        const int row = q >> 4, ch16 = q & 15, sub = ch16 >> 3, ch = ch16 & 7;
+        const uint32_t off = (uint32_t)sub * SK_SUB + (uint32_t)row * 128 + ((uint32_t)(ch ^ (row & 7)) << 4);
+        const int64_t ca = c0 + ch16 * 8;
+        uint4 va = make_uint4(0, 0, 0, 0), vb = make_uint4(0, 0, 0, 0);
+        if (ca < lda2) va = __ldg(reinterpret_cast<const uint4*>(A2 + (int64_t)row * lda2 + ca));
+        const int64_t rb = r0 + ch16 * 8;
+        if (rb < ldb2) vb = __ldg(reinterpret_cast<const uint4*>(B2 + (int64_t)row * ldb2 + rb));
+        *reinterpret_cast<uint4*>(a2 + off) = va;
+        *reinterpret_cast<uint4*>(b2 + off) = vb;
+      }
+      fence_proxy_async();
+      mbar_arrive(&bar_full[s]);
+      ++t;
     }
   } else if (wid == MMA_WARP) {
     // ------------------------------------------------------------ MMA issuer
@@ -297,7 +331,21 @@ k_dual_tc(const float* __restrict__ X, int64_t n, int64_t m, int64_t ldx, const 
     const int quad = wid & 3;  // TMEM lanes 32 quad .. 32 quad + 31
     const uint32_t lane_base = (uint32_t)(32 * quad) << 16;
     int row_count = 0, unit_count = 0;
-    float v[2 * KPAD];
+    // hi and lo halves of an accumulator row, 16 columns at a time (keeps the
+    // epilogue at 32 live registers)
+    auto emit = [&](uint32_t ta, float* dst, int64_t ld, int64_t idx, bool live) {
+#pragma unroll
+      for (int h = 0; h < KPAD / 16; ++h) {
+        float vh[16], vl[16];
+        tmem_ld16(ta + 16 * h, vh);
+        tmem_ld16(ta + KPAD + 16 * h, vl);
+        if (live) {
+#pragma unroll
+          for (int a = 0; a < 16; ++a)
+            if (16 * h + a < k) dst[(int64_t)(16 * h + a) * ld + idx] = vh[a] + vl[a];
+        }
+      }
+    };
     for (int u = blockIdx.x; u < U.units; u += gridDim.x, ++unit_count) {
       int rt0, rt1, ct0, ct1, rc, cb;
       unit_bounds(U, u, rt0, rt1, ct0, ct1, rc, cb);
@@ -307,34 +355,16 @@ k_dual_tc(const float* __restrict__ X, int64_t n, int64_t m, int64_t ldx, const 
         const int yb = row_count & 1;
         mbar_wait(&bar_yfull[yb], (row_count >> 1) & 1);
         tc_fence_after();
-        const uint32_t ta = tmem + lane_base + ycol0 + (uint32_t)yb * N2;
-        if (KPAD == 32) {
-          tmem_ld32(ta, v);
-          tmem_ld32(ta + 32, v + 32);
-        } else {
-          tmem_ld16(ta, v);
-          tmem_ld16(ta + 16, v + 16);
-        }
+        const int64_t row = (int64_t)rt * TILE + 32 * quad + lane;
+        emit(tmem + lane_base + ycol0 + (uint32_t)yb * N2, yslab, n, row, row < n);
         tc_fence_before();
         mbar_arrive(&bar_yempty[yb]);
-        const int64_t row = (int64_t)rt * TILE + 32 * quad + lane;
-        if (row < n)
-          for (int a = 0; a < k; ++a) yslab[(int64_t)a * n + row] = v[a] + v[KPAD + a];
       }
       mbar_wait(&bar_zfull, unit_count & 1);
       tc_fence_after();
       for (int ct = ct0; ct < ct1; ++ct) {
-        const uint32_t ta = tmem + lane_base + zcol0 + (uint32_t)(ct - ct0) * N2;
-        if (KPAD == 32) {
-          tmem_ld32(ta, v);
-          tmem_ld32(ta + 32, v + 32);
-        } else {
-          tmem_ld16(ta, v);
-          tmem_ld16(ta + 16, v + 16);
-        }
         const int64_t col = (int64_t)ct * TILE + 32 * quad + lane;
-        if (col < m)
-          for (int a = 0; a < k; ++a) zslab[(int64_t)a * m + col] = v[a] + v[KPAD + a];
+        emit(tmem + lane_base + zcol0 + (uint32_t)(ct - ct0) * N2, zslab, m, col, col < m);
       }
       tc_fence_before();
       mbar_arrive(&bar_zempty);

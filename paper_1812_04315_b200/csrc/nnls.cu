@@ -209,32 +209,76 @@ int solve_nnls(Arena& ws, const T* At, int64_t r, int64_t p, const T* B, int64_t
   const bool use_mma = p <= 32 && mcpb <= nnls_mma_max_cols<T>((int)p) && max_iter <= NN_WTAB_LEN &&
                        getenv("NENMF_NNLS_SIMT") == nullptr;
   const int grid_used = use_mma ? mgrid : pl.grid;
-  T* W = ws.take<T>((size_t)p * p);
-  T* V = ws.take<T>((size_t)pc);
+  // fused prologue/epilogue (W, V, L and the tie-break inside the solver
+  // launch) for the compressed problems' short operands
+  const bool fused = use_mma && r <= NN_FUSE_RMAX && getenv("NENMF_NNLS_UNFUSED") == nullptr;
+  T* W = fused ? nullptr : ws.take<T>((size_t)p * p);
+  T* V = fused ? nullptr : ws.take<T>((size_t)pc);
   double* Lbuf = ws.take<double>(4);
   T* snaps = ws.take<T>((size_t)(NW_SNAP + 1) * 4 * pc);
-  double* salpha = ws.take<double>((size_t)imax(pl.grid, mgrid) * NW_MAXW * (NW_SNAP + 1) * 2);
+  double* salpha = use_mma ? nullptr : ws.take<double>((size_t)pl.grid * NW_MAXW * (NW_SNAP + 1) * 2);
   T* gstate = (use_mma || pl.smem_state) ? nullptr : ws.take<T>((size_t)4 * pc);
-  WinRec* recs = ws.take<WinRec>((size_t)NW_SLOTS * grid_used + NW_SLOTS);
+  double* rpart = fused ? ws.take<double>((size_t)2 * grid_used) : nullptr;
+  // window records + (fused) the grid-barrier counter, zeroed together
+  const size_t rec_bytes = sizeof(WinRec) * ((size_t)NW_SLOTS * grid_used + NW_SLOTS) + 64;
+  unsigned char* recmem = ws.take<unsigned char>(rec_bytes);
+  WinRec* recs = reinterpret_cast<WinRec*>(recmem);
   WinRec* results = recs + (size_t)NW_SLOTS * grid_used;
+  unsigned int* bar = reinterpret_cast<unsigned int*>(results + NW_SLOTS);
   if (!dry && !ws.ok) return NENMF_ERR_WORKSPACE;
-  NENMF_TRY(abt<T>(ws, At, p, At, p, r, W, s));                       // W = A^T A   (nnls.py:157)
-  NENMF_TRY(ab<T>(ws, At, p, r, B, c, ldb, trans, V, s));             // V = A^T B   (nnls.py:158)
-  NENMF_TRY(lipschitz<T>(ws, At, r, p, W, pvec, pcount, pmax, ptol, safety, Lbuf, st, s));  // (nnls.py:159)
+  if (!fused) {
+    NENMF_TRY(abt<T>(ws, At, p, At, p, r, W, s));                       // W = A^T A   (nnls.py:157)
+    NENMF_TRY(ab<T>(ws, At, p, r, B, c, ldb, trans, V, s));             // V = A^T B   (nnls.py:158)
+    NENMF_TRY(lipschitz<T>(ws, At, r, p, W, pvec, pcount, pmax, ptol, safety, Lbuf, st, s));  // (nnls.py:159)
+  }
   if (!dry) {
-    NENMF_CUDA_TRY(cudaMemsetAsync(recs, 0, sizeof(WinRec) * ((size_t)NW_SLOTS * grid_used + NW_SLOTS), s));
+    NENMF_CUDA_TRY(cudaMemsetAsync(recmem, 0, rec_bytes, s));
     if (use_mma) {
       const double* wtab = momentum_table(max_iter);
       if (wtab == nullptr) return NENMF_ERR_CUDA;
-      unsigned long long* tracebuf = nullptr;
-      if (getenv("NENMF_NNLS_TRACE") != nullptr) NENMF_CUDA_TRY(cudaGetSymbolAddress((void**)&tracebuf, g_nnls_trace));
-      NENMF_TRY(launch_nnls_mma<T>(W, V, F0, Fout, snaps, salpha, (int)p, c, mgrid, mcpb, Lbuf, max_iter, grad_tol,
-                                   recs, results, st, tracebuf, wtab, s));
+      MmaArgs<T> a{};
+      a.W = W;
+      a.V = V;
+      a.L = Lbuf;
+      a.At = At;
+      a.B = B;
+      a.r = r;
+      a.ldb = ldb;
+      a.trans = trans ? 1 : 0;
+      a.fused = fused ? 1 : 0;
+      a.pvec = pvec;
+      a.pcount = pcount;
+      a.pmax = pmax;
+      a.ptol = ptol;
+      a.safety = safety;
+      a.F0 = F0;
+      a.Fout = Fout;
+      a.snaps = snaps;
+      a.p = (int)p;
+      a.c = c;
+      a.cpb = mcpb;
+      a.max_iter = max_iter;
+      a.grad_tol = grad_tol;
+      a.recs = recs;
+      a.results = results;
+      a.st = st;
+      a.tracebuf = nullptr;
+      if (getenv("NENMF_NNLS_TRACE") != nullptr) NENMF_CUDA_TRY(cudaGetSymbolAddress((void**)&a.tracebuf, g_nnls_trace));
+      a.wtab = wtab;
+      // NENMF_NNLS_DBG (timing experiments only; results are not valid):
+      // 1 = no resolver, 2 = no snapshots, 4 = no per-iteration sums
+      const char* dbg_env = getenv("NENMF_NNLS_DBG");
+      a.dbg = dbg_env != nullptr ? atoi(dbg_env) : 0;
+      a.rpart = rpart;
+      a.bar = bar;
+      NENMF_TRY(launch_nnls_mma<T>(a, mgrid, s));
+      if (fused) return NENMF_OK;
     } else {
       NENMF_TRY(launch_nnls<T>(pl, W, V, F0, Fout, snaps, salpha, gstate, (int)p, c, Lbuf, max_iter, grad_tol, recs,
                                results, st, s));
     }
   }
+  if (fused) return NENMF_OK;
   // explicit residuals of best and start, only when an iterate improved (nnls.py:219-227)
   NENMF_TRY(resid<T>(ws, At, p, r, B, c, ldb, trans, Fout, F0, Lbuf + 2, &st->returned_best, s));
   if (dry) return NENMF_OK;

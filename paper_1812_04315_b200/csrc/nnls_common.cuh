@@ -298,10 +298,42 @@ static __device__ void resolver_warp(SolverShared& sh, const double* pp, int ncw
     }
   }
 
+// Arguments of the tensor-core solver.  Unfused: W = A^T A, V = A^T B and L
+// are precomputed by separate kernels.  Fused (r <= NN_FUSE_RMAX): every CTA
+// forms W, its own columns of V and L (the reference's power iteration) from
+// At and B itself, and the explicit-residual tie-break plus the final select
+// (nnls.py:219-227) run inside the same launch.
+constexpr int NN_FUSE_RMAX = 64;
 template <typename T>
-int launch_nnls_mma(const T* W, const T* V, const T* F0, T* Fout, T* snaps, double* salpha, int p, int64_t c, int grid,
-                    int64_t cpb, const double* Lptr, int max_iter, double grad_tol, WinRec* recs, WinRec* results,
-                    nenmf_device_status* st, unsigned long long* tracebuf, const double* wtab, cudaStream_t s);
+struct MmaArgs {
+  const T* W;
+  const T* V;
+  double* L;  // unfused: input L; fused: output [L, r_best, r_start]
+  const T* At;
+  const T* B;
+  int64_t r, ldb;
+  int trans, fused;
+  const double* pvec;
+  int pcount, pmax;
+  double ptol, safety;
+  const T* F0;
+  T* Fout;
+  T* snaps;
+  int p;
+  int64_t c, cpb;
+  int max_iter;
+  double grad_tol;
+  WinRec* recs;
+  WinRec* results;
+  nenmf_device_status* st;
+  unsigned long long* tracebuf;
+  const double* wtab;
+  int dbg;
+  double* rpart;      // fused: [grid][2] per-CTA residual partials
+  unsigned int* bar;  // fused: grid barrier counter (zeroed with recs)
+};
+template <typename T>
+int launch_nnls_mma(const MmaArgs<T>& a, int grid, cudaStream_t s);
 
 template <typename T>
 int nnls_mma_max_cols(int p);  // columns one CTA of the tensor-core solver can hold

@@ -61,18 +61,41 @@ __device__ __forceinline__ void mma_f64(double (&c)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
+// smem carve-up of the fused prologue/epilogue (after the pp ring)
+template <typename T>
+struct FusedSmem {
+  static size_t bytes(int p, int64_t r, int ncw) {
+    return ((size_t)p * r + 3) / 4 * 4 * sizeof(T) + 32 * 32 * sizeof(T) + 32 * 32 * sizeof(double) + 64 * sizeof(double) +
+           (size_t)ncw * 32 * MmaShape<T>::CB * sizeof(T) + (size_t)NW_MAXW * 2 * sizeof(double) + 64;
+  }
+};
+
 template <typename T, int NT>
 __global__ void __launch_bounds__(mma_threads<T>(NT), 1)
-k_nnls_mma(const T* __restrict__ W, const T* __restrict__ V, const T* __restrict__ F0, T* __restrict__ Fout,
-           T* __restrict__ snaps, double* __restrict__ snap_alpha, int p, int64_t c, int64_t cpb,
-           const double* __restrict__ Lptr, int max_iter, double grad_tol, WinRec* __restrict__ recs,
-           WinRec* __restrict__ results, nenmf_device_status* st, unsigned long long* __restrict__ tracebuf,
-           const double* __restrict__ wtab, int dbg) {
+k_nnls_mma(const __grid_constant__ MmaArgs<T> A) {
   using S = MmaShape<T>;
   constexpr int NE = S::EPT * NT;  // state elements per thread
+  const T* __restrict__ F0 = A.F0;
+  T* __restrict__ Fout = A.Fout;
+  T* __restrict__ snaps = A.snaps;
+  const int p = A.p, max_iter = A.max_iter, dbg = A.dbg;
+  const int64_t c = A.c, cpb = A.cpb;
+  const double* __restrict__ wtab = A.wtab;
+  unsigned long long* __restrict__ tracebuf = A.tracebuf;
+  nenmf_device_status* st = A.st;
+  const bool fused = A.fused != 0;
+  const int r = (int)A.r;
   extern __shared__ __align__(16) double smem_d[];
   double* pp = smem_d;  // [PPD][MAXW][3]
+  // fused-mode scratch
+  T* At_s = reinterpret_cast<T*>(pp + (size_t)NW_PPD * NW_MAXW * 3);  // [p][r]
+  T* W_s = At_s + ((size_t)p * r + 3) / 4 * 4;                          // [32][32]
+  double* gram = reinterpret_cast<double*>(W_s + 32 * 32);             // [k][k]
+  double* pv = gram + 32 * 32;                                          // [64]
+  T* ftile_all = reinterpret_cast<T*>(pv + 64);                         // [ncw][32][CB]
   __shared__ SolverShared sh;
+  __shared__ double s_L, s_red[NW_MAXW][2];
+  __shared__ int s_start_wins;
 
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int ncw = (blockDim.x >> 5) - 1;
@@ -83,8 +106,6 @@ k_nnls_mma(const T* __restrict__ W, const T* __restrict__ V, const T* __restrict
   solver_shared_init(sh);
   __syncthreads();
   if (st->code != 0) return;
-  const double L = *Lptr;
-  const T rnegL = (T)(-1.0 / L);
 
   // element e of this thread: solver row / CTA-local column
   auto erow = [&](int e) -> int {
@@ -105,9 +126,100 @@ k_nnls_mma(const T* __restrict__ W, const T* __restrict__ V, const T* __restrict
     else return (int64_t)(8 * (e >> 1) + (e & 1)) * c + ebase;
   };
   auto snref = [&](int s, int b, int e) -> T& { return snaps[(int64_t)(s * 4 + b) * pc + eoff(e)]; };
+  // B(t, global column j) of the reference's V = A^T B (B may be a transposed view)
+  auto bval = [&](int t, int64_t j) -> T { return A.trans ? A.B[j * A.ldb + t] : A.B[(int64_t)t * A.ldb + j]; };
+
+  T nv[NE];  // -V in the accumulator layout (compute warps)
+  if (fused) {
+    // ---- prologue: At -> smem, W = A^T A (k_abt order: double, t ascending)
+    for (int i = tid; i < p * r; i += blockDim.x) At_s[i] = A.At[i];
+    __syncthreads();
+    for (int o = tid; o < p * p; o += blockDim.x) {
+      const int a = o / p, b = o % p;
+      double acc = 0.0;
+      for (int t = 0; t < r; ++t) acc = fma((double)At_s[a * r + t], (double)At_s[b * r + t], acc);
+      W_s[a * 32 + b] = (T)acc;
+    }
+    __syncthreads();
+    if (resolver) {
+      // L = lambda_max of the smaller Gram (matrix.py:131-174, as k_power):
+      // one row per lane, fixed-order warp sums -> identical in every CTA
+      const int k = p <= r ? p : r;
+      if (p > r) {  // A A^T (r x r), k_gram_rows order
+        for (int o = lane; o < r * r; o += 32) {
+          const int s2 = o / r, t2 = o % r;
+          double acc = 0.0;
+          for (int a = 0; a < p; ++a) acc = fma((double)At_s[a * r + s2], (double)At_s[a * r + t2], acc);
+          gram[o] = (double)(T)acc;
+        }
+      } else {
+        for (int o = lane; o < k * k; o += 32) gram[o] = (double)W_s[(o / k) * 32 + (o % k)];
+      }
+      double* v = pv;
+      if (lane < k) v[lane] = A.pvec[lane];
+      __syncwarp();
+      int draw = 1;
+      double est = 0.0;
+      bool conv_any = false;
+      for (int it = 0; it < A.pmax; ++it) {
+        double wi = 0.0;
+        if (lane < k)
+          for (int l = 0; l < k; ++l) wi = fma(gram[lane * k + l], v[l], wi);
+        const double nw = sqrt(warp_sum(lane < k ? fma(wi, wi, 0.0) : 0.0));
+        __syncwarp();
+        if (nw == 0.0) {
+          if (lane < k) v[lane] = draw < A.pcount ? A.pvec[(int64_t)draw * k + lane] : 0.0;
+          ++draw;
+          __syncwarp();
+          continue;
+        }
+        const bool conv = fabs(nw - est) <= A.ptol * nw;
+        est = nw;
+        if (lane < k) v[lane] = __ddiv_rn(wi, nw);
+        __syncwarp();
+        if (conv) {
+          conv_any = true;
+          break;
+        }
+      }
+      if (!conv_any) est = est * 1.01;
+      if (lane == 0) {
+        s_L = A.safety * est;
+        if (blockIdx.x == 0) {
+          A.L[0] = s_L;
+          st->lipschitz = s_L;
+        }
+      }
+    } else {
+      // this warp's columns of V = A^T B (k_ab order: T precision, t ascending)
+#pragma unroll
+      for (int e = 0; e < NE; ++e) {
+        T acc = T(0);
+        if (evalid(e)) {
+          const int a = erow(e);
+          const int64_t j = j0 + ecol(e);
+          for (int t = 0; t < r; ++t) acc = fma_acc(At_s[a * r + t], bval(t, j), acc);
+        }
+        nv[e] = -acc;
+      }
+    }
+    __syncthreads();
+    if (s_L == 0.0) {  // zero Gram: ZeroMatrixError (matrix.py:172-173)
+      if (blockIdx.x == 0 && tid == 0) status_fail(st, NENMF_ERR_ZERO_MATRIX, 0);
+      return;
+    }
+  } else {
+    if (tid == 0) s_L = A.L[0];
+    __syncthreads();
+  }
+  const double L = s_L;
+  const T rnegL = (T)(-1.0 / L);
+  const T* __restrict__ W = A.W;
 
   if (!resolver) {
-    auto wval = [&](int i, int l) -> T { return (i < p && l < p) ? W[i * p + l] : T(0); };
+    auto wval = [&](int i, int l) -> T {
+      return (i < p && l < p) ? (fused ? W_s[i * 32 + l] : W[i * p + l]) : T(0);
+    };
     // W^T fragments (B operand), resident for the whole solve; b[kt][nt]
     uint32_t bhi[NT][NT][2], blo[NT][NT][2];
     double bd[2 * NT][NT];
@@ -131,7 +243,7 @@ k_nnls_mma(const T* __restrict__ W, const T* __restrict__ V, const T* __restrict
     // State per element (accumulator layout), with u = F - g / L:
     //   F_k = max(0, Y - grad_Y / L) = max(0, u_{k-1} + w_k (u_{k-1} - u_{k-2}))
     // (Y and grad_Y of nnls.py:189-191,208-213 folded into one affine update)
-    T ua[NE], ub[NE], fa[NE], fb[NE], nv[NE];  // nv = -V
+    T ua[NE], ub[NE], fa[NE], fb[NE];
     // g = W f - V in the accumulator layout (the MMA chain starts from -V)
     auto grad = [&](const T (&fe)[NE], T (&g)[NE]) {
       if constexpr (S::EPT == 4) {
@@ -238,7 +350,7 @@ k_nnls_mma(const T* __restrict__ W, const T* __restrict__ V, const T* __restrict
       const bool ok = evalid(e);
       fa[e] = ok ? F0[eoff(e)] : T(0);
       fb[e] = fa[e];
-      nv[e] = ok ? -V[eoff(e)] : T(0);
+      if (!fused) nv[e] = ok ? -A.V[eoff(e)] : T(0);
     }
     T ps0, ps1;  // sums of the last iteration, posted during the next one
     {
@@ -366,13 +478,13 @@ k_nnls_mma(const T* __restrict__ W, const T* __restrict__ V, const T* __restrict
     // (waits for the resolver's final decision through the block barrier below)
     asm volatile("bar.sync 1, %0;" ::"r"(blockDim.x) : "memory");
     const int bj = sh.best_j;
-    if (bj >= 0 && sh.fail_at < 0 && has_cols) {
+    const bool ok_best = bj >= 0 && sh.fail_at == -1;
+    if (ok_best && has_cols) {
       const int kd = sh.kdone[wid];
-      if (bj == kd - 1 || bj == kd - 2) {
+      if (bj == kd - 2) {
 #pragma unroll
-        for (int e = 0; e < NE; ++e)
-          if (evalid(e)) Fout[eoff(e)] = bj == kd - 1 ? fa[e] : fb[e];
-      } else {
+        for (int e = 0; e < NE; ++e) fa[e] = fb[e];
+      } else if (bj != kd - 1) {
         // recompute from the snapshot at the start of the best iterate's window
         const int wb = bj / NW_WIN;
         const int slot = (sh.bsw[wid] == wb && wb + NW_SNAP <= (kd - 1) / NW_WIN) ? NW_SNAP : wb % NW_SNAP;
@@ -396,45 +508,111 @@ k_nnls_mma(const T* __restrict__ W, const T* __restrict__ V, const T* __restrict
             ub[e] = t;
           }
         }
+      }
+      // fa = the best iterate
 #pragma unroll
-        for (int e = 0; e < NE; ++e)
-          if (evalid(e)) Fout[eoff(e)] = fa[e];
+      for (int e = 0; e < NE; ++e)
+        if (evalid(e)) Fout[eoff(e)] = fa[e];
+    }
+    if (fused && ok_best) {
+      // explicit residuals 1/2||A F - B||^2 of best and start over this warp's
+      // columns (k_resid arithmetic: T products over rows, double squares)
+      double acc[2] = {0.0, 0.0};
+      if (has_cols) {
+        T* ft = ftile_all + (size_t)wid * 32 * S::CB;
+        const int nloc = imin(S::CB, ncols - cblk);
+        for (int cand = 0; cand < 2; ++cand) {
+#pragma unroll
+          for (int e = 0; e < NE; ++e)
+            if (evalid(e)) ft[erow(e) * S::CB + (ecol(e) - cblk)] = cand == 0 ? fa[e] : F0[eoff(e)];
+          __syncwarp();
+          for (int idx = lane; idx < r * S::CB; idx += 32) {
+            const int t = idx / S::CB, jl = idx % S::CB;
+            if (jl < nloc) {
+              T sacc = T(0);
+              for (int a2 = 0; a2 < p; ++a2) sacc = fma_acc(At_s[a2 * r + t], ft[a2 * S::CB + jl], sacc);
+              const double d = (double)(sacc - bval(t, j0 + cblk + jl));
+              acc[cand] += d * d;
+            }
+          }
+          __syncwarp();
+        }
+      }
+      const double r0 = warp_sum(acc[0]), r1 = warp_sum(acc[1]);
+      if (lane == 0) {
+        s_red[wid][0] = r0;
+        s_red[wid][1] = r1;
       }
     }
   } else {
-    if (!(dbg & 1)) resolver_warp(sh, pp, ncw, max_iter, grad_tol, L, recs, results, tracebuf);
+    if (!(dbg & 1)) resolver_warp(sh, pp, ncw, max_iter, A.grad_tol, L, A.recs, A.results, tracebuf);
     asm volatile("bar.sync 1, %0;" ::"r"(blockDim.x) : "memory");
   }
   __syncthreads();
+  const int bj = sh.best_j;
+  const bool ok_best = bj >= 0 && sh.fail_at == -1;
+  int start_wins = 0;
+  if (fused && sh.fail_at == -1) {
+    // tie-break (nnls.py:219-227): fixed-order sums over warps, then over CTAs
+    // after a grid barrier; every CTA reaches the same decision
+    start_wins = 1;
+    if (ok_best) {
+      if (tid == 0) {
+        double a0 = 0.0, a1 = 0.0;
+        for (int w = 0; w < ncw; ++w) {
+          a0 += s_red[w][0];
+          a1 += s_red[w][1];
+        }
+        A.rpart[2 * blockIdx.x] = a0;
+        A.rpart[2 * blockIdx.x + 1] = a1;
+        __threadfence();
+        atomicAdd(A.bar, 1u);
+        while (atomicAdd(A.bar, 0u) < gridDim.x) __nanosleep(64);
+        __threadfence();
+        double b0 = 0.0, b1 = 0.0;
+        for (int g = 0; g < (int)gridDim.x; ++g) {
+          b0 += __ldcg(&A.rpart[2 * g]);
+          b1 += __ldcg(&A.rpart[2 * g + 1]);
+        }
+        const double nb = sqrt(b0), ns = sqrt(b1);
+        const double tb = 0.5 * (nb * nb), ts = 0.5 * (ns * ns);
+        s_start_wins = (tb <= ts) ? 0 : 1;
+        if (blockIdx.x == 0) {
+          st->resid[0] = tb;
+          st->resid[1] = ts;
+          A.L[1] = b0;
+          A.L[2] = b1;
+        }
+      }
+      __syncthreads();
+      start_wins = s_start_wins;
+    }
+    if (start_wins && !resolver && cblk < ncols) {
+#pragma unroll
+      for (int e = 0; e < NE; ++e)
+        if (evalid(e)) Fout[eoff(e)] = F0[eoff(e)];
+    }
+  }
   if (blockIdx.x == 0 && tid == 0) {
     if (sh.fail_at >= 0) status_fail(st, NENMF_ERR_NUMERICAL_FAILURE, sh.fail_at);
     if (sh.fail_at == -2) status_fail(st, NENMF_ERR_CUDA, -2);
     st->inner_iters = sh.stop_at >= 0 ? sh.stop_at + 1 : (sh.fail_at >= 0 ? sh.fail_at : max_iter);
-    st->returned_best = sh.best_j >= 0 ? 1 : 0;
+    st->returned_best = (bj >= 0 && !start_wins) ? 1 : 0;
     st->best_partial = sh.best_part;
     st->pg_ref = sh.pg_ref;
   }
 }
 
 template <typename T, int NT>
-static int launch_nnls_mma_t(const T* W, const T* V, const T* F0, T* Fout, T* snaps, double* salpha, int p, int64_t c,
-                             int grid, int64_t cpb, const double* Lptr, int max_iter, double grad_tol, WinRec* recs,
-                             WinRec* results, nenmf_device_status* st, unsigned long long* tracebuf,
-                             const double* wtab, cudaStream_t s) {
-  const int ncw = (int)cdiv(cpb, MmaShape<T>::CB);
+static int launch_nnls_mma_t(const MmaArgs<T>& a, int grid, cudaStream_t s) {
+  const int ncw = (int)cdiv(a.cpb, MmaShape<T>::CB);
   const int threads = 32 * (ncw + 1);
   if (threads > mma_threads<T>(NT) || ncw >= NW_MAXW) return NENMF_ERR_UNSUPPORTED;
-  const size_t smem = (size_t)NW_PPD * NW_MAXW * 3 * sizeof(double);
-  // NENMF_NNLS_DBG (timing experiments only; results are not valid):
-  // 1 = no resolver, 2 = no snapshots, 4 = no per-iteration sums
-  const char* dbg_env = getenv("NENMF_NNLS_DBG");
-  const int dbg = dbg_env != nullptr ? atoi(dbg_env) : 0;
+  size_t smem = (size_t)NW_PPD * NW_MAXW * 3 * sizeof(double);
+  if (a.fused) smem += FusedSmem<T>::bytes(a.p, a.r, ncw);
   auto fn = k_nnls_mma<T, NT>;
   NENMF_CUDA_TRY(set_smem(fn, smem));
-  void* args[] = {(void*)&W,    (void*)&V,        (void*)&F0,       (void*)&Fout,    (void*)&snaps,
-                  (void*)&salpha, (void*)&p,      (void*)&c,        (void*)&cpb,     (void*)&Lptr,
-                  (void*)&max_iter, (void*)&grad_tol, (void*)&recs, (void*)&results, (void*)&st,
-                  (void*)&tracebuf, (void*)&wtab, (void*)&dbg};
+  void* args[] = {(void*)&a};
   NENMF_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)fn, dim3(grid), dim3(threads), args, smem, s));
   launch_counter_add(1);
   return NENMF_OK;
@@ -451,19 +629,12 @@ static int launch_nnls_mma_t(const T* W, const T* V, const T* F0, T* Fout, T* sn
     return MmaShape<T>::CB * imin(NW_MAXW - 1, mma_threads<T>(nt) / 32 - 1);                          \
   }                                                                                                   \
   template <>                                                                                         \
-  int launch_nnls_mma<T>(const T* W, const T* V, const T* F0, T* Fout, T* snaps, double* salpha, int p, \
-                         int64_t c, int grid, int64_t cpb, const double* Lptr, int max_iter,          \
-                         double grad_tol, WinRec* recs, WinRec* results, nenmf_device_status* st,     \
-                         unsigned long long* tracebuf, const double* wtab, cudaStream_t s) {          \
-    switch ((int)cdiv(p, 8)) {                                                                        \
-      case 1: return launch_nnls_mma_t<T, 1>(W, V, F0, Fout, snaps, salpha, p, c, grid, cpb, Lptr,    \
-                                             max_iter, grad_tol, recs, results, st, tracebuf, wtab, s); \
-      case 2: return launch_nnls_mma_t<T, 2>(W, V, F0, Fout, snaps, salpha, p, c, grid, cpb, Lptr,    \
-                                             max_iter, grad_tol, recs, results, st, tracebuf, wtab, s); \
-      case 3: return launch_nnls_mma_t<T, 3>(W, V, F0, Fout, snaps, salpha, p, c, grid, cpb, Lptr,    \
-                                             max_iter, grad_tol, recs, results, st, tracebuf, wtab, s); \
-      case 4: return launch_nnls_mma_t<T, 4>(W, V, F0, Fout, snaps, salpha, p, c, grid, cpb, Lptr,    \
-                                             max_iter, grad_tol, recs, results, st, tracebuf, wtab, s); \
+  int launch_nnls_mma<T>(const MmaArgs<T>& a, int grid, cudaStream_t s) {                             \
+    switch ((int)cdiv(a.p, 8)) {                                                                      \
+      case 1: return launch_nnls_mma_t<T, 1>(a, grid, s);                                             \
+      case 2: return launch_nnls_mma_t<T, 2>(a, grid, s);                                             \
+      case 3: return launch_nnls_mma_t<T, 3>(a, grid, s);                                             \
+      case 4: return launch_nnls_mma_t<T, 4>(a, grid, s);                                             \
       default: return NENMF_ERR_UNSUPPORTED;                                                          \
     }                                                                                                 \
   }

@@ -1,0 +1,90 @@
+"""The fused solver launch (W = AᵀA, V = AᵀB, λmax and the explicit-residual
+tie-break computed inside the persistent kernel, used when r <= 64) against
+the unfused sequence of separate kernels (NENMF_NNLS_UNFUSED=1) and against
+the CPU oracle.  W, V and L use the same arithmetic in both paths, so the
+iterates agree to rounding of the residual sums (which only feed the
+tie-break)."""
+
+import numpy as np
+import pytest
+
+import nenmf_oracle as orc
+import paper_1812_04315_b200 as nm
+
+pytestmark = pytest.mark.gpu
+
+
+def _case(r, p, c, seed, scale=1.0):
+    rng = np.random.default_rng(seed)
+    A = rng.random((r, p)) * scale
+    B = A @ rng.random((p, c)) + 0.05 * rng.standard_normal((r, c))
+    F0 = rng.random((p, c))
+    return A, B, F0
+
+
+SHAPES = [(5, 3, 1), (30, 20, 37), (30, 20, 1000), (64, 32, 300), (12, 20, 100), (40, 9, 2500)]
+
+
+@pytest.mark.parametrize("dtype,tol", [("fp64", 1e-12), ("fp32", 1e-5)])
+@pytest.mark.parametrize("shape", SHAPES)
+def test_fused_matches_unfused(monkeypatch, dtype, tol, shape):
+    r, p, c = shape
+    A, B, F0 = _case(r, p, c, seed=r * 1000 + p * 10 + c)
+    cfg = nm.InnerSolverConfig(max_iter=200, grad_tol=1e-6)
+    rep_f, rep_u = [], []
+    Ff = nm.solve_nnls(A, B, F0, cfg, dtype=dtype, report=rep_f)
+    monkeypatch.setenv("NENMF_NNLS_UNFUSED", "1")
+    Fu = nm.solve_nnls(A, B, F0, cfg, dtype=dtype, report=rep_u)
+    assert rep_f[0].lipschitz == rep_u[0].lipschitz          # same power iteration
+    assert rep_f[0].inner_iters == rep_u[0].inner_iters
+    assert rep_f[0].returned_best == rep_u[0].returned_best
+    assert np.abs(Ff - Fu).max() <= tol * max(np.abs(Fu).max(), 1.0)
+
+
+@pytest.mark.parametrize("shape", SHAPES)
+def test_fused_vs_oracle_fp64(shape):
+    r, p, c = shape
+    A, B, F0 = _case(r, p, c, seed=7 + r + p + c)
+    cfg = nm.InnerSolverConfig(max_iter=150, grad_tol=1e-5)
+    rep = []
+    F = nm.solve_nnls(A, B, F0, cfg, report=rep)
+    info = orc.SolveInfo()
+    ref = orc.nesterov_nnls(A, B, F0, 150, 1e-5, 1.0, info)
+    assert abs(rep[0].inner_iters - info.iterations) <= 1
+    assert np.abs(F - ref).max() <= 1e-5 * np.abs(ref).max()
+
+
+def test_fused_start_wins_and_no_improvement():
+    """F0 already optimal: no iterate improves, the start point is returned
+    unchanged (nnls.py:219-227 with best never set)."""
+    rng = np.random.default_rng(3)
+    A = rng.random((20, 6))
+    F0 = rng.random((6, 50))
+    B = A @ F0
+    rep = []
+    F = nm.solve_nnls(A, B, F0, nm.InnerSolverConfig(max_iter=30), report=rep)
+    assert np.abs(F - F0).max() <= 1e-12
+    assert rep[0].inner_iters >= 1
+
+
+def test_fused_trans_view_matches(monkeypatch):
+    """vanilla NeNMF with n, m <= 64: its G-half passes B = Xᵀ as a transposed
+    view (r = m), so the fused kernel reads B through the trans path."""
+    rng = np.random.default_rng(11)
+    n, m, p = 48, 60, 7
+    X = rng.random((n, p)) @ rng.random((p, m)) + 0.01 * rng.random((n, m))
+    init = nm.init_factors(n, m, p, seed=5)
+    cfg = nm.OuterConfig(inner=nm.InnerSolverConfig(max_iter=60), time_budget_seconds=0.0,
+                         max_outer_iterations=4)
+    a = nm.factorize_vanilla(X, init, cfg, clock=nm.IterationClock())
+    monkeypatch.setenv("NENMF_NNLS_UNFUSED", "1")
+    b = nm.factorize_vanilla(X, init, cfg, clock=nm.IterationClock())
+    assert np.abs(a.G - b.G).max() <= 1e-12 * np.abs(b.G).max()
+    assert np.abs(a.F - b.F).max() <= 1e-12 * np.abs(b.F).max()
+
+
+def test_fused_zero_matrix_raises():
+    A = np.zeros((10, 4))
+    B = np.ones((10, 30))
+    with pytest.raises(nm.ZeroMatrixError):
+        nm.solve_nnls(A, B, np.ones((4, 30)))
