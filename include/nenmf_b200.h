@@ -107,6 +107,20 @@ int nenmf_solve_nnls(int dtype, const void* At, int64_t r, int64_t p,
                      double power_tol, nenmf_device_status* status, void* ws, size_t ws_bytes,
                      void* stream);
 
+/* nenmf_solve_nnls plus the operand of the next half-step of the outer loop:
+ * next_out (p x next_k) = F_out next_bt^T with next_bt (next_k x c), i.e.
+ * F R (factorize.py:110) after an F-half and L G (factorize.py:113) after a
+ * G-half.  Formed inside the solver launch when it is fused (r <= 64); same
+ * result as a separate nenmf_abt(F_out, next_bt) up to summation order. */
+size_t nenmf_solve_nnls_next_workspace_bytes(int dtype, int64_t r, int64_t p, int64_t c, int64_t next_k);
+int nenmf_solve_nnls_next(int dtype, const void* At, int64_t r, int64_t p,
+                          const void* B, int64_t c, int64_t ldb, int trans_b,
+                          const void* F0, void* F_out,
+                          int max_iter, double grad_tol, double lipschitz_safety,
+                          const double* power_vectors, int power_count, int power_max_iters,
+                          double power_tol, const void* next_bt, int64_t next_k, void* next_out,
+                          nenmf_device_status* status, void* ws, size_t ws_bytes, void* stream);
+
 /* sigma_max(A)^2 by power iteration on the smaller Gram (matrix.py:158-174).
  * A (r x p) passed as At (p x r).  Result (double) -> *out (device). */
 size_t nenmf_spectral_norm_sq_workspace_bytes(int dtype, int64_t r, int64_t p);

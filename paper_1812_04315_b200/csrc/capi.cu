@@ -74,14 +74,40 @@ int nenmf_device_sm_count(void) { return sm_count(); }
 unsigned long long nenmf_launch_count(void) { return g_launches.load(); }
 
 // ------------------------------------------------------------ solver ----
-size_t nenmf_solve_nnls_workspace_bytes(int dtype, int64_t r, int64_t p, int64_t c) {
-  Arena a(nullptr, 0);
-  NENMF_DISPATCH(dtype, [&] {
-    return solve_nnls<scalar_t>(a, nullptr, r, p, nullptr, c, c, false, nullptr, nullptr, 1, 1e-4, 1.0, nullptr, 1,
-                                100, 1e-9, nullptr, nullptr);
-  });
+size_t nenmf_solve_nnls_next_workspace_bytes(int dtype, int64_t r, int64_t p, int64_t c, int64_t nup) {
+  // the larger of the tensor-core and SIMT plans (max_iter decides between them);
   // the transposed-B variant carves the same scratch
-  return a.used + 256;
+  size_t best = 0;
+  for (int mi : {1, (1 << 16) + 1}) {
+    Arena a(nullptr, 0);
+    NENMF_DISPATCH(dtype, [&] {
+      const scalar_t* dummy = nup > 0 ? reinterpret_cast<const scalar_t*>(256) : nullptr;
+      return solve_nnls<scalar_t>(a, nullptr, r, p, nullptr, c, c, false, nullptr, nullptr, mi, 1e-4, 1.0, nullptr,
+                                  1, 100, 1e-9, nullptr, nullptr, dummy, nup, nup > 0 ? const_cast<scalar_t*>(dummy)
+                                                                                     : nullptr);
+    });
+    best = a.used > best ? a.used : best;
+  }
+  return best + 256;
+}
+
+size_t nenmf_solve_nnls_workspace_bytes(int dtype, int64_t r, int64_t p, int64_t c) {
+  return nenmf_solve_nnls_next_workspace_bytes(dtype, r, p, c, 0);
+}
+
+int nenmf_solve_nnls_next(int dtype, const void* At, int64_t r, int64_t p, const void* B, int64_t c, int64_t ldb,
+                          int trans_b, const void* F0, void* F_out, int max_iter, double grad_tol,
+                          double lipschitz_safety, const double* power_vectors, int power_count, int power_max_iters,
+                          double power_tol, const void* next_bt, int64_t next_k, void* next_out,
+                          nenmf_device_status* status, void* ws, size_t ws_bytes, void* stream) {
+  if (ws == nullptr || status == nullptr) return NENMF_ERR_VALUE;
+  Arena a(ws, ws_bytes);
+  return NENMF_DISPATCH(dtype, [&] {
+    return solve_nnls<scalar_t>(a, C<scalar_t>(At), r, p, C<scalar_t>(B), c, ldb, trans_b != 0, C<scalar_t>(F0),
+                                M<scalar_t>(F_out), max_iter, grad_tol, lipschitz_safety, power_vectors,
+                                power_count, power_max_iters, power_tol, status, S(stream), C<scalar_t>(next_bt),
+                                next_k, M<scalar_t>(next_out));
+  });
 }
 
 int nenmf_solve_nnls(int dtype, const void* At, int64_t r, int64_t p, const void* B, int64_t c, int64_t ldb,

@@ -194,8 +194,10 @@ static int launch_nnls(const NnlsPlan& pl, const T* W, const T* V, const T* F0, 
 template <typename T>
 int solve_nnls(Arena& ws, const T* At, int64_t r, int64_t p, const T* B, int64_t c, int64_t ldb, bool trans,
                const T* F0, T* Fout, int max_iter, double grad_tol, double safety, const double* pvec,
-               int pcount, int pmax, double ptol, nenmf_device_status* st, cudaStream_t s) {
+               int pcount, int pmax, double ptol, nenmf_device_status* st, cudaStream_t s, const T* Pt,
+               int64_t nup, T* Pout) {
   if (r < 1 || p < 1 || c < 1) return NENMF_ERR_DIM;
+  if (Pt != nullptr && (nup < 1 || Pout == nullptr)) return NENMF_ERR_VALUE;
   if (p > 64) return NENMF_ERR_UNSUPPORTED;
   if (max_iter < 1 || pcount < 1) return NENMF_ERR_VALUE;
   const bool dry = ws.base == nullptr;
@@ -211,7 +213,17 @@ int solve_nnls(Arena& ws, const T* At, int64_t r, int64_t p, const T* B, int64_t
   const int grid_used = use_mma ? mgrid : pl.grid;
   // fused prologue/epilogue (W, V, L and the tie-break inside the solver
   // launch) for the compressed problems' short operands
-  const bool fused = use_mma && r <= NN_FUSE_RMAX && getenv("NENMF_NNLS_UNFUSED") == nullptr;
+  const int cbm = nnls_mma_col_block<T>();
+  const bool fused = use_mma && r <= NN_FUSE_RMAX && getenv("NENMF_NNLS_UNFUSED") == nullptr &&
+                     (size_t)NW_PPD * NW_MAXW * 3 * sizeof(double) +
+                             fused_smem_bytes(sizeof(T), (int)p, r, (int)cdiv(mcpb, cbm), cbm, mcpb) <=
+                         227 * 1024;
+  // the next product inside the launch when its tiles fit too
+  const bool fused_next = fused && Pt != nullptr &&
+                          (size_t)NW_PPD * NW_MAXW * 3 * sizeof(double) +
+                                  fused_smem_bytes(sizeof(T), (int)p, r, (int)cdiv(mcpb, cbm), cbm, mcpb) +
+                                  (size_t)(p + nup) * mcpb * sizeof(T) <=
+                              227 * 1024;
   T* W = fused ? nullptr : ws.take<T>((size_t)p * p);
   T* V = fused ? nullptr : ws.take<T>((size_t)pc);
   double* Lbuf = ws.take<double>(4);
@@ -219,6 +231,7 @@ int solve_nnls(Arena& ws, const T* At, int64_t r, int64_t p, const T* B, int64_t
   double* salpha = use_mma ? nullptr : ws.take<double>((size_t)pl.grid * NW_MAXW * (NW_SNAP + 1) * 2);
   T* gstate = (use_mma || pl.smem_state) ? nullptr : ws.take<T>((size_t)4 * pc);
   double* rpart = fused ? ws.take<double>((size_t)2 * grid_used) : nullptr;
+  double* npart = fused_next ? ws.take<double>((size_t)grid_used * p * nup) : nullptr;
   // window records + (fused) the grid-barrier counter, zeroed together
   const size_t rec_bytes = sizeof(WinRec) * ((size_t)NW_SLOTS * grid_used + NW_SLOTS) + 64;
   unsigned char* recmem = ws.take<unsigned char>(rec_bytes);
@@ -271,21 +284,30 @@ int solve_nnls(Arena& ws, const T* At, int64_t r, int64_t p, const T* B, int64_t
       a.dbg = dbg_env != nullptr ? atoi(dbg_env) : 0;
       a.rpart = rpart;
       a.bar = bar;
+      a.Pt = fused_next ? Pt : nullptr;
+      a.nup = fused_next ? nup : 0;
+      a.Pout = fused_next ? Pout : nullptr;
+      a.npart = npart;
       NENMF_TRY(launch_nnls_mma<T>(a, mgrid, s));
-      if (fused) return NENMF_OK;
+      if (fused) {
+        if (Pt != nullptr && !fused_next) NENMF_TRY(abt<T>(ws, Fout, p, Pt, nup, c, Pout, s));
+        return NENMF_OK;
+      }
     } else {
       NENMF_TRY(launch_nnls<T>(pl, W, V, F0, Fout, snaps, salpha, gstate, (int)p, c, Lbuf, max_iter, grad_tol, recs,
                                results, st, s));
     }
   }
-  if (fused) return NENMF_OK;
+  if (fused) return (Pt != nullptr && !fused_next) ? abt<T>(ws, Fout, p, Pt, nup, c, Pout, s) : NENMF_OK;
   // explicit residuals of best and start, only when an iterate improved (nnls.py:219-227)
   NENMF_TRY(resid<T>(ws, At, p, r, B, c, ldb, trans, Fout, F0, Lbuf + 2, &st->returned_best, s));
-  if (dry) return NENMF_OK;
-  k_decide<<<1, 1, 0, s>>>(Lbuf + 2, st);
-  NENMF_LAUNCH_CHECK();
-  k_select<T><<<(unsigned)imin(cdiv(pc, 256), 1184), 256, 0, s>>>(F0, Fout, pc, st);
-  NENMF_LAUNCH_CHECK();
+  if (!dry) {
+    k_decide<<<1, 1, 0, s>>>(Lbuf + 2, st);
+    NENMF_LAUNCH_CHECK();
+    k_select<T><<<(unsigned)imin(cdiv(pc, 256), 1184), 256, 0, s>>>(F0, Fout, pc, st);
+    NENMF_LAUNCH_CHECK();
+  }
+  if (Pt != nullptr) NENMF_TRY(abt<T>(ws, Fout, p, Pt, nup, c, Pout, s));
   return NENMF_OK;
 }
 
@@ -324,7 +346,7 @@ namespace nenmf {
 #define NENMF_INST_NNLS(T)                                                                                    \
   template int solve_nnls<T>(Arena&, const T*, int64_t, int64_t, const T*, int64_t, int64_t, bool, const T*,  \
                              T*, int, double, double, const double*, int, int, double, nenmf_device_status*,   \
-                             cudaStream_t);                                                                  \
+                             cudaStream_t, const T*, int64_t, T*);                                           \
   template int spectral_norm_sq<T>(Arena&, const T*, int64_t, int64_t, const double*, int, int, double, double*, \
                                    nenmf_device_status*, cudaStream_t);                                      \
   template int gradient<T>(Arena&, const T*, int64_t, int64_t, const T*, int64_t, int64_t, bool, const T*,    \

@@ -6,10 +6,14 @@ namespace nenmf {
 
 // Whole solve_nnls (nnls.py:119-227).  F_out receives the returned iterate;
 // F0 and F_out must not alias.  The caller zeroes *st before the first use.
+// Optional next product (Pt != nullptr): Pout (p x nup) = F_out Pt^T with Pt
+// (nup x c) -- the operand of the next half-step (F R or L G,
+// factorize.py:110,113), formed inside the solver launch when it is fused.
 template <typename T>
 int solve_nnls(Arena& ws, const T* At, int64_t r, int64_t p, const T* B, int64_t c, int64_t ldb, bool trans,
                const T* F0, T* Fout, int max_iter, double grad_tol, double safety, const double* pvec,
-               int pcount, int pmax, double ptol, nenmf_device_status* st, cudaStream_t s);
+               int pcount, int pmax, double ptol, nenmf_device_status* st, cudaStream_t s,
+               const T* Pt = nullptr, int64_t nup = 0, T* Pout = nullptr);
 
 template <typename T>
 int spectral_norm_sq(Arena& ws, const T* At, int64_t r, int64_t p, const double* pvec, int pcount, int pmax,

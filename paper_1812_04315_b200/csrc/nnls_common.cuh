@@ -48,6 +48,11 @@ __device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long
 __device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long v) {
   asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
+__device__ __forceinline__ unsigned int ld_acquire_u32(const unsigned int* p) {
+  unsigned int v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 __device__ __forceinline__ void fence_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 
 // ------------------------------------------------------------------- plan
@@ -137,8 +142,10 @@ static __device__ void resolver_warp(SolverShared& sh, const double* pp, int ncw
   const bool trace = tracebuf != nullptr;
   auto g_nnls_trace = [&](int row) { return tracebuf + (size_t)row * NN_TRACE_LEN; };
     const int nwin = (max_iter + NW_WIN - 1) / NW_WIN;
+    const int nq = (nwin + 1) * NW_WIN;  // pairs of windows -1 .. nwin-1
     int pubw = -1;                       // next window to publish (-1: the start point)
-    int sumw = (int)blockIdx.x - 1;      // next owned window to summarize (window -1 -> CTA 0)
+    int sumq = (int)blockIdx.x;          // next owned (window, iteration) pair to summarize
+    int ready_w = -2;                    // window whose records were all seen published
     int resw = -1;                       // next window to resolve
     int best_j = -1, stop_at = -1, fail_at = -1;
     double best_part = 0.0, pg_ref = 0.0;
@@ -181,59 +188,55 @@ static __device__ void resolver_warp(SolverShared& sh, const double* pp, int ncw
           progress = true;
         }
       }
-      // B. summarize the owned window sumw (all CTAs' records, CTA order)
-      if (sumw < nwin) {
-        const WinRec* row = recs + (int64_t)rec_idx(sumw) * G;
-        const unsigned long long want = (unsigned long long)(sumw + 2);
-        bool ok = true;
-        for (int b = lane; b < G; b += 32) ok &= ld_relaxed_u64(&row[b].tag) == want;
-        if (__all_sync(0xffffffffu, ok)) {
+      // B. summarize the owned (window, iteration) pairs: pair q = 32 (w + 1) + j
+      //    is summed over all CTAs' records by CTA q mod G (lane-strided over
+      //    CTAs, fixed butterfly: deterministic) and counted into results[w].
+      if (sumq < nq) {
+        const int w = sumq / NW_WIN - 1, j = sumq % NW_WIN;
+        const WinRec* row = recs + (int64_t)rec_idx(w) * G;
+        const unsigned long long want = (unsigned long long)(w + 2);
+        bool ok = w == ready_w;
+        if (!ok) {
+          ok = true;
+          for (int b = lane; b < G; b += 32) ok &= ld_relaxed_u64(&row[b].tag) == want;
+          ok = __all_sync(0xffffffffu, ok);
+          if (ok) ready_w = w;
+        }
+        if (ok) {
           fence_gpu();
-          const int j = win_first(sumw) + lane;
           double v0 = 0.0, v1 = 0.0, v2 = 0.0;
-          if (j <= win_last(sumw)) {
-            int b = 0;
-            for (; b + 4 <= G; b += 4) {
-              double x[4][3];
-#pragma unroll
-              for (int u = 0; u < 4; ++u) {
-                x[u][0] = __ldcg(&row[b + u].v[lane][0]);
-                x[u][1] = __ldcg(&row[b + u].v[lane][1]);
-                x[u][2] = __ldcg(&row[b + u].v[lane][2]);
-              }
-#pragma unroll
-              for (int u = 0; u < 4; ++u) {
-                v0 += x[u][0];
-                v1 += x[u][1];
-                v2 += x[u][2];
-              }
+          const int it = w < 0 ? (j == 0 ? -1 : INT_MAX) : w * NW_WIN + j;
+          if (it <= win_last(w)) {
+            for (int b = lane; b < G; b += 32) {
+              v0 += __ldcg(&row[b].v[j][0]);
+              v1 += __ldcg(&row[b].v[j][1]);
+              v2 += __ldcg(&row[b].v[j][2]);
             }
-            for (; b < G; ++b) {
-              v0 += __ldcg(&row[b].v[lane][0]);
-              v1 += __ldcg(&row[b].v[lane][1]);
-              v2 += __ldcg(&row[b].v[lane][2]);
-            }
+            v0 = warp_sum(v0);
+            v1 = warp_sum(v1);
+            v2 = warp_sum(v2);
           }
-          WinRec* res = results + rec_idx(sumw);
-          res->v[lane][0] = v0;
-          res->v[lane][1] = v1;
-          res->v[lane][2] = v2;
-          __syncwarp();
           if (lane == 0) {
-            fence_gpu();
-            st_relaxed_u64(&res->tag, want);
-            if (trace && sumw + 1 < 1024) g_nnls_trace(3)[3072 + sumw + 1] = gtimer_ns();
+            WinRec* res = results + rec_idx(w);
+            res->v[j][0] = v0;
+            res->v[j][1] = v1;
+            res->v[j][2] = v2;
+            __threadfence();
+            atomicAdd(&res->tag, 1ull);
+            if (trace && w + 1 < 1024 && j == 0) g_nnls_trace(3)[3072 + w + 1] = gtimer_ns();
           }
           __syncwarp();
-          sumw += G;
+          sumq += G;
           progress = true;
         }
       }
       // C. resolve window resw
       {
         const WinRec* res = results + rec_idx(resw);
-        const unsigned long long want = (unsigned long long)(resw + 2);
-        const bool ready = ld_relaxed_u64(&res->tag) == want;  // same address in all lanes
+        // results of a ring slot count 32 per use: window resw is the
+        // ((resw + 1) / NW_SLOTS)-th use of its slot
+        const unsigned long long want = (unsigned long long)NW_WIN * ((resw + 1) / NW_SLOTS + 1);
+        const bool ready = ld_relaxed_u64(&res->tag) >= want;  // same address in all lanes
         if (ready) {
           fence_gpu();
           const double r0 = __ldcg(&res->v[lane][0]);
@@ -304,6 +307,13 @@ static __device__ void resolver_warp(SolverShared& sh, const double* pp, int ncw
 // At and B itself, and the explicit-residual tie-break plus the final select
 // (nnls.py:219-227) run inside the same launch.
 constexpr int NN_FUSE_RMAX = 64;
+// extra dynamic smem of the fused mode (after the [PPD][MAXW][3] sum ring):
+// At [p][r] | W [32][32] | gram [32][32] double | pv [64] double |
+// ftile [ncw][2][32][cb] | Bs [r][cpb]
+inline size_t fused_smem_bytes(size_t ts, int p, int64_t r, int ncw, int cb, int64_t cpb) {
+  return ((size_t)p * r + 3) / 4 * 4 * ts + 32 * 32 * ts + 32 * 32 * sizeof(double) + 64 * sizeof(double) +
+         (size_t)ncw * 2 * 32 * cb * ts + (size_t)r * cpb * ts + 64;
+}
 template <typename T>
 struct MmaArgs {
   const T* W;
@@ -330,7 +340,11 @@ struct MmaArgs {
   const double* wtab;
   int dbg;
   double* rpart;      // fused: [grid][2] per-CTA residual partials
-  unsigned int* bar;  // fused: grid barrier counter (zeroed with recs)
+  unsigned int* bar;  // fused: grid barrier counters [2] (zeroed with recs)
+  const T* Pt;        // fused next product Pout (p x nup) = F_out Pt^T, Pt (nup x c)
+  int64_t nup;
+  T* Pout;
+  double* npart;      // [grid][p][nup] per-CTA partials
 };
 template <typename T>
 int launch_nnls_mma(const MmaArgs<T>& a, int grid, cudaStream_t s);

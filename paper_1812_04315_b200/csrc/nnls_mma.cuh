@@ -62,14 +62,6 @@ __device__ __forceinline__ void mma_f64(double (&c)[2], double a, double b) {
 }
 
 // smem carve-up of the fused prologue/epilogue (after the pp ring)
-template <typename T>
-struct FusedSmem {
-  static size_t bytes(int p, int64_t r, int ncw) {
-    return ((size_t)p * r + 3) / 4 * 4 * sizeof(T) + 32 * 32 * sizeof(T) + 32 * 32 * sizeof(double) + 64 * sizeof(double) +
-           (size_t)ncw * 32 * MmaShape<T>::CB * sizeof(T) + (size_t)NW_MAXW * 2 * sizeof(double) + 64;
-  }
-};
-
 template <typename T, int NT>
 __global__ void __launch_bounds__(mma_threads<T>(NT), 1)
 k_nnls_mma(const __grid_constant__ MmaArgs<T> A) {
@@ -93,6 +85,7 @@ k_nnls_mma(const __grid_constant__ MmaArgs<T> A) {
   double* gram = reinterpret_cast<double*>(W_s + 32 * 32);             // [k][k]
   double* pv = gram + 32 * 32;                                          // [64]
   T* ftile_all = reinterpret_cast<T*>(pv + 64);                         // [ncw][32][CB]
+  T* Bs = ftile_all + (size_t)((blockDim.x >> 5) - 1) * 2 * 32 * S::CB;  // [r][cpb]: B of this CTA's columns
   __shared__ SolverShared sh;
   __shared__ double s_L, s_red[NW_MAXW][2];
   __shared__ int s_start_wins;
@@ -105,6 +98,7 @@ k_nnls_mma(const __grid_constant__ MmaArgs<T> A) {
   const int gq = lane >> 2, tq = lane & 3;
   solver_shared_init(sh);
   __syncthreads();
+  if (tracebuf != nullptr && blockIdx.x == 0 && tid == 0) tracebuf[NN_TRACE_LEN + 60 + 0] = gtimer_ns();
   if (st->code != 0) return;
 
   // element e of this thread: solver row / CTA-local column
@@ -127,7 +121,8 @@ k_nnls_mma(const __grid_constant__ MmaArgs<T> A) {
   };
   auto snref = [&](int s, int b, int e) -> T& { return snaps[(int64_t)(s * 4 + b) * pc + eoff(e)]; };
   // B(t, global column j) of the reference's V = A^T B (B may be a transposed view)
-  auto bval = [&](int t, int64_t j) -> T { return A.trans ? A.B[j * A.ldb + t] : A.B[(int64_t)t * A.ldb + j]; };
+  // B(t, CTA-local column jl) of the reference's V = A^T B, staged in smem
+  auto bval = [&](int t, int jl) -> T { return Bs[(size_t)t * cpb + jl]; };
 
   T nv[NE];  // -V in the accumulator layout (compute warps)
   if (fused) {
@@ -183,6 +178,7 @@ k_nnls_mma(const __grid_constant__ MmaArgs<T> A) {
         }
       }
       if (!conv_any) est = est * 1.01;
+      if (tracebuf != nullptr && blockIdx.x == 0 && lane == 0) tracebuf[NN_TRACE_LEN + 60 + 11] = gtimer_ns();
       if (lane == 0) {
         s_L = A.safety * est;
         if (blockIdx.x == 0) {
@@ -191,14 +187,23 @@ k_nnls_mma(const __grid_constant__ MmaArgs<T> A) {
         }
       }
     } else {
+      // B columns of this CTA -> smem (compute warps, overlapping the power
+      // iteration; coalesced along B's contiguous dimension)
+      if (A.trans) {
+        for (int jl = wid; jl < ncols; jl += ncw)
+          for (int t = lane; t < r; t += 32) Bs[(size_t)t * cpb + jl] = A.B[(j0 + jl) * A.ldb + t];
+      } else {
+        for (int t = wid; t < r; t += ncw)
+          for (int jl = lane; jl < ncols; jl += 32) Bs[(size_t)t * cpb + jl] = A.B[(int64_t)t * A.ldb + j0 + jl];
+      }
+      asm volatile("bar.sync 2, %0;" ::"r"(ncw * 32) : "memory");
       // this warp's columns of V = A^T B (k_ab order: T precision, t ascending)
 #pragma unroll
       for (int e = 0; e < NE; ++e) {
         T acc = T(0);
         if (evalid(e)) {
-          const int a = erow(e);
-          const int64_t j = j0 + ecol(e);
-          for (int t = 0; t < r; ++t) acc = fma_acc(At_s[a * r + t], bval(t, j), acc);
+          const int a = erow(e), jl = ecol(e);
+          for (int t = 0; t < r; ++t) acc = fma_acc(At_s[a * r + t], bval(t, jl), acc);
         }
         nv[e] = -acc;
       }
@@ -213,6 +218,7 @@ k_nnls_mma(const __grid_constant__ MmaArgs<T> A) {
     __syncthreads();
   }
   const double L = s_L;
+  if (tracebuf != nullptr && blockIdx.x == 0 && tid == 0) tracebuf[NN_TRACE_LEN + 60 + 3] = gtimer_ns();
   const T rnegL = (T)(-1.0 / L);
   const T* __restrict__ W = A.W;
 
@@ -477,10 +483,13 @@ k_nnls_mma(const __grid_constant__ MmaArgs<T> A) {
     // -------------------------------------------------------------- output
     // (waits for the resolver's final decision through the block barrier below)
     asm volatile("bar.sync 1, %0;" ::"r"(blockDim.x) : "memory");
+  if (tracebuf != nullptr && blockIdx.x == 0 && tid == 0) tracebuf[NN_TRACE_LEN + 60 + 6] = gtimer_ns();
     const int bj = sh.best_j;
     const bool ok_best = bj >= 0 && sh.fail_at == -1;
+    if (tracebuf != nullptr && blockIdx.x == 0 && tid == 0) tracebuf[NN_TRACE_LEN + 60 + 12] = gtimer_ns();
     if (ok_best && has_cols) {
       const int kd = sh.kdone[wid];
+      if (tracebuf != nullptr && blockIdx.x == 0 && tid == 0) tracebuf[NN_TRACE_LEN + 60 + 13] = gtimer_ns();
       if (bj == kd - 2) {
 #pragma unroll
         for (int e = 0; e < NE; ++e) fa[e] = fb[e];
@@ -495,8 +504,9 @@ k_nnls_mma(const __grid_constant__ MmaArgs<T> A) {
           ua[e] = ok ? sp[eoff(e)] : T(0);
           ub[e] = ok ? sp[pc + eoff(e)] : T(0);
         }
+        const T wrec = wload(wb * NW_WIN);  // w of iterations wb*32 .. wb*32+31
         for (int kk = wb * NW_WIN; kk <= bj; ++kk) {
-          const T w = kk == 0 ? T(0) : (T)wtab[kk - 1];
+          const T w = __shfl_sync(0xffffffffu, wrec, kk % NW_WIN);
           extrapolate(ua, ub, w, fa);
           T g[NE], d0, d1;
           grad(fa, g);
@@ -509,6 +519,11 @@ k_nnls_mma(const __grid_constant__ MmaArgs<T> A) {
           }
         }
       }
+      if (tracebuf != nullptr && blockIdx.x == 0 && tid == 0) {
+        tracebuf[NN_TRACE_LEN + 60 + 4] = gtimer_ns();
+        tracebuf[NN_TRACE_LEN + 80] = bj;
+        tracebuf[NN_TRACE_LEN + 81] = kd;
+      }
       // fa = the best iterate
 #pragma unroll
       for (int e = 0; e < NE; ++e)
@@ -516,29 +531,48 @@ k_nnls_mma(const __grid_constant__ MmaArgs<T> A) {
     }
     if (fused && ok_best) {
       // explicit residuals 1/2||A F - B||^2 of best and start over this warp's
-      // columns (k_resid arithmetic: T products over rows, double squares)
+      // columns (k_resid arithmetic: T products summed over rows in order,
+      // double squares); each lane owns one column and a stride of rows t
       double acc[2] = {0.0, 0.0};
       if (has_cols) {
-        T* ft = ftile_all + (size_t)wid * 32 * S::CB;
+        T* ft = ftile_all + (size_t)wid * 2 * 32 * S::CB;  // [2][32][CB]
         const int nloc = imin(S::CB, ncols - cblk);
-        for (int cand = 0; cand < 2; ++cand) {
 #pragma unroll
-          for (int e = 0; e < NE; ++e)
-            if (evalid(e)) ft[erow(e) * S::CB + (ecol(e) - cblk)] = cand == 0 ? fa[e] : F0[eoff(e)];
-          __syncwarp();
-          for (int idx = lane; idx < r * S::CB; idx += 32) {
-            const int t = idx / S::CB, jl = idx % S::CB;
-            if (jl < nloc) {
-              T sacc = T(0);
-              for (int a2 = 0; a2 < p; ++a2) sacc = fma_acc(At_s[a2 * r + t], ft[a2 * S::CB + jl], sacc);
-              const double d = (double)(sacc - bval(t, j0 + cblk + jl));
-              acc[cand] += d * d;
-            }
+        for (int e = 0; e < NE; ++e)
+          if (evalid(e)) {
+            const int o = erow(e) * S::CB + (ecol(e) - cblk);
+            ft[o] = fa[e];
+            ft[32 * S::CB + o] = F0[eoff(e)];
           }
-          __syncwarp();
+        __syncwarp();
+        const int jl = lane % S::CB;
+        constexpr int TSTEP = 32 / S::CB;
+        if (jl < nloc) {
+          T f0[8 * NT], f1[8 * NT];  // p <= 8 NT
+#pragma unroll
+          for (int a2 = 0; a2 < 8 * NT; ++a2) {
+            f0[a2] = a2 < p ? ft[a2 * S::CB + jl] : T(0);
+            f1[a2] = a2 < p ? ft[32 * S::CB + a2 * S::CB + jl] : T(0);
+          }
+          for (int t = lane / S::CB; t < r; t += TSTEP) {
+            T s0 = T(0), s1 = T(0);
+#pragma unroll
+            for (int a2 = 0; a2 < 8 * NT; ++a2)
+              if (a2 < p) {
+                const T w = At_s[a2 * r + t];
+                s0 = fma_acc(w, f0[a2], s0);
+                s1 = fma_acc(w, f1[a2], s1);
+              }
+            const T b = bval(t, cblk + jl);
+            const double d0 = (double)(s0 - b), d1 = (double)(s1 - b);
+            acc[0] += d0 * d0;
+            acc[1] += d1 * d1;
+          }
         }
+        __syncwarp();
       }
       const double r0 = warp_sum(acc[0]), r1 = warp_sum(acc[1]);
+  if (tracebuf != nullptr && blockIdx.x == 0 && tid == 0) tracebuf[NN_TRACE_LEN + 60 + 7] = gtimer_ns();
       if (lane == 0) {
         s_red[wid][0] = r0;
         s_red[wid][1] = r1;
@@ -546,12 +580,14 @@ k_nnls_mma(const __grid_constant__ MmaArgs<T> A) {
     }
   } else {
     if (!(dbg & 1)) resolver_warp(sh, pp, ncw, max_iter, A.grad_tol, L, A.recs, A.results, tracebuf);
+    if (tracebuf != nullptr && blockIdx.x == 0 && lane == 0) tracebuf[NN_TRACE_LEN + 60 + 14] = gtimer_ns();
     asm volatile("bar.sync 1, %0;" ::"r"(blockDim.x) : "memory");
   }
   __syncthreads();
   const int bj = sh.best_j;
   const bool ok_best = bj >= 0 && sh.fail_at == -1;
   int start_wins = 0;
+  if (tracebuf != nullptr && blockIdx.x == 0 && tid == 0) tracebuf[NN_TRACE_LEN + 60 + 8] = gtimer_ns();
   if (fused && sh.fail_at == -1) {
     // tie-break (nnls.py:219-227): fixed-order sums over warps, then over CTAs
     // after a grid barrier; every CTA reaches the same decision
@@ -567,21 +603,29 @@ k_nnls_mma(const __grid_constant__ MmaArgs<T> A) {
         A.rpart[2 * blockIdx.x + 1] = a1;
         __threadfence();
         atomicAdd(A.bar, 1u);
-        while (atomicAdd(A.bar, 0u) < gridDim.x) __nanosleep(64);
-        __threadfence();
+        while (ld_acquire_u32(A.bar) < gridDim.x) __nanosleep(32);
+      }
+      if (wid == 0) {
+        __syncwarp();
+        // CTA partials summed lane-strided then by a fixed butterfly: the same
+        // order (and value) in every CTA
         double b0 = 0.0, b1 = 0.0;
-        for (int g = 0; g < (int)gridDim.x; ++g) {
+        for (int g = lane; g < (int)gridDim.x; g += 32) {
           b0 += __ldcg(&A.rpart[2 * g]);
           b1 += __ldcg(&A.rpart[2 * g + 1]);
         }
-        const double nb = sqrt(b0), ns = sqrt(b1);
-        const double tb = 0.5 * (nb * nb), ts = 0.5 * (ns * ns);
-        s_start_wins = (tb <= ts) ? 0 : 1;
-        if (blockIdx.x == 0) {
-          st->resid[0] = tb;
-          st->resid[1] = ts;
-          A.L[1] = b0;
-          A.L[2] = b1;
+        b0 = warp_sum(b0);
+        b1 = warp_sum(b1);
+        if (lane == 0) {
+          const double nb = sqrt(b0), ns = sqrt(b1);
+          const double tb = 0.5 * (nb * nb), ts = 0.5 * (ns * ns);
+          s_start_wins = (tb <= ts) ? 0 : 1;
+          if (blockIdx.x == 0) {
+            st->resid[0] = tb;
+            st->resid[1] = ts;
+            A.L[1] = b0;
+            A.L[2] = b1;
+          }
         }
       }
       __syncthreads();
@@ -593,6 +637,50 @@ k_nnls_mma(const __grid_constant__ MmaArgs<T> A) {
         if (evalid(e)) Fout[eoff(e)] = F0[eoff(e)];
     }
   }
+  if (fused && A.Pt != nullptr && sh.fail_at == -1) {
+    // ---- next product Pout = F_out Pt^T (factorize.py:110,113): per-CTA
+    // partials over its columns, a grid barrier, then each CTA reduces a
+    // slice of the p x nup outputs in fixed CTA order
+    const int nup = (int)A.nup, no = p * nup;
+    T* Fs = Bs + (size_t)r * cpb;  // [p][cpb]
+    T* Ps = Fs + (size_t)p * cpb;  // [nup][cpb]
+    const bool use_best = ok_best && !start_wins;
+    for (int i = tid; i < p * ncols; i += blockDim.x) {
+      const int a2 = i / ncols, jl = i % ncols;
+      Fs[(size_t)a2 * cpb + jl] =
+          use_best ? ftile_all[(size_t)(jl / S::CB) * 2 * 32 * S::CB + a2 * S::CB + jl % S::CB]
+                   : F0[(int64_t)a2 * c + j0 + jl];
+    }
+    for (int i = tid; i < nup * ncols; i += blockDim.x) {
+      const int b = i / ncols, jl = i % ncols;
+      Ps[(size_t)b * cpb + jl] = A.Pt[(int64_t)b * c + j0 + jl];
+    }
+    __syncthreads();
+    for (int o = tid; o < no; o += blockDim.x) {
+      const int a2 = o / nup, b = o % nup;
+      double acc2 = 0.0;
+      for (int jl = 0; jl < ncols; ++jl)
+        acc2 = fma((double)Fs[(size_t)a2 * cpb + jl], (double)Ps[(size_t)b * cpb + jl], acc2);
+      A.npart[(size_t)blockIdx.x * no + o] = acc2;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence();
+      atomicAdd(A.bar + 1, 1u);
+      while (ld_acquire_u32(A.bar + 1) < gridDim.x) __nanosleep(32);
+    }
+    __syncthreads();
+    const int per = (no + (int)gridDim.x - 1) / (int)gridDim.x;
+    const int o0 = (int)blockIdx.x * per, o1 = min(no, o0 + per);
+    const int nwarps = blockDim.x >> 5;
+    for (int o = o0 + wid; o < o1; o += nwarps) {
+      double sacc = 0.0;
+      for (int g = lane; g < (int)gridDim.x; g += 32) sacc += __ldcg(&A.npart[(size_t)g * no + o]);
+      sacc = warp_sum(sacc);
+      if (lane == 0) A.Pout[o] = (T)sacc;
+    }
+  }
+  if (tracebuf != nullptr && blockIdx.x == 0 && tid == 0) tracebuf[NN_TRACE_LEN + 60 + 10] = gtimer_ns();
   if (blockIdx.x == 0 && tid == 0) {
     if (sh.fail_at >= 0) status_fail(st, NENMF_ERR_NUMERICAL_FAILURE, sh.fail_at);
     if (sh.fail_at == -2) status_fail(st, NENMF_ERR_CUDA, -2);
@@ -609,7 +697,9 @@ static int launch_nnls_mma_t(const MmaArgs<T>& a, int grid, cudaStream_t s) {
   const int threads = 32 * (ncw + 1);
   if (threads > mma_threads<T>(NT) || ncw >= NW_MAXW) return NENMF_ERR_UNSUPPORTED;
   size_t smem = (size_t)NW_PPD * NW_MAXW * 3 * sizeof(double);
-  if (a.fused) smem += FusedSmem<T>::bytes(a.p, a.r, ncw);
+  if (a.fused) smem += fused_smem_bytes(sizeof(T), a.p, a.r, ncw, MmaShape<T>::CB, a.cpb);
+  if (a.fused && a.Pt != nullptr) smem += (size_t)(a.p + a.nup) * a.cpb * sizeof(T);
+  if (smem > 227 * 1024) return NENMF_ERR_UNSUPPORTED;
   auto fn = k_nnls_mma<T, NT>;
   NENMF_CUDA_TRY(set_smem(fn, smem));
   void* args[] = {(void*)&a};

@@ -126,6 +126,7 @@ class _DeviceLoop:
             self.XL, self.XRt = compress_device(self.X, L, Rt)
             nu = L.shape[0]
             self.FR = torch.empty((self.p, nu), dtype=self.X.dtype, device="cuda")
+            self.fr_ready = False
             self.GLt = torch.empty((self.p, nu), dtype=self.X.dtype, device="cuda")
 
     def _slot(self, t: int, half: str) -> int:
@@ -139,15 +140,19 @@ class _DeviceLoop:
         kw = dict(max_iter=icfg.max_iter, grad_tol=icfg.grad_tol, lipschitz_safety=icfg.lipschitz_safety,
                   status=self.status)
         if self.sketch is not None:
-            # G-half: A = (F R)^T, B = X_R^T (factorize.py:109-110)
-            _ops.abt(self.F, self.Rt, self.FR)
+            # G-half: A = (F R)^T, B = X_R^T (factorize.py:109-110); F R comes
+            # from the previous F-half's launch (or once, before the first)
+            if not self.fr_ready:
+                _ops.abt(self.F, self.Rt, self.FR)
+            # ... and L G for the F-half is formed by this G-half's launch
             _ops.solve(self.FR, self.XRt, self.Gt, self.Gt_alt, trans_b=False,
-                       status_index=self._slot(t, "G"), **kw)
+                       status_index=self._slot(t, "G"), next_bt=self.L, next_out=self.GLt, **kw)
             self.Gt, self.Gt_alt = self.Gt_alt, self.Gt
-            # F-half: A = L G, B = X_L (factorize.py:112-113)
-            _ops.abt(self.Gt, self.L, self.GLt)
+            # F-half: A = L G, B = X_L (factorize.py:112-113); it also forms the
+            # next G-half's F R
             _ops.solve(self.GLt, self.XL, self.F, self.F_alt, trans_b=False,
-                       status_index=self._slot(t, "F"), **kw)
+                       status_index=self._slot(t, "F"), next_bt=self.Rt, next_out=self.FR, **kw)
+            self.fr_ready = True
         else:
             # G-half: A = F^T, B = X^T read in place (factorize.py:94-95)
             _ops.solve(self.F, self.X, self.Gt, self.Gt_alt, trans_b=True,

@@ -88,3 +88,35 @@ def test_fused_zero_matrix_raises():
     B = np.ones((10, 30))
     with pytest.raises(nm.ZeroMatrixError):
         nm.solve_nnls(A, B, np.ones((4, 30)))
+
+
+@pytest.mark.parametrize("unfused", [False, True])
+@pytest.mark.parametrize("dtype,tol", [("fp64", 1e-12), ("fp32", 1e-5)])
+@pytest.mark.parametrize("shape", [(30, 20, 10000, 30), (12, 5, 333, 7), (40, 32, 2000, 64)])
+def test_next_product(monkeypatch, unfused, dtype, tol, shape):
+    """nenmf_solve_nnls_next: next_out = F_out next_btᵀ formed by the solver
+    launch (fused) or by a separate product (fallback) -- factorize.py:110,113."""
+    import torch
+    from paper_1812_04315_b200 import _lib, _ops
+    if unfused:
+        monkeypatch.setenv("NENMF_NNLS_UNFUSED", "1")
+    r, p, c, k = shape
+    A, B, F0 = _case(r, p, c, seed=c + k)
+    P = np.random.default_rng(k).standard_normal((k, c))
+    tdt = torch.float64 if dtype == "fp64" else torch.float32
+    dev = lambda a: torch.as_tensor(np.ascontiguousarray(a), dtype=tdt, device="cuda")
+    At, Bd, F0d, Pd = dev(A.T), dev(B), dev(F0), dev(P)
+    Fo = torch.empty_like(F0d)
+    out = torch.empty((p, k), dtype=tdt, device="cuda")
+    st = _lib.new_status()
+    _ops.solve(At, Bd, F0d, Fo, trans_b=False, max_iter=60, grad_tol=1e-6, lipschitz_safety=1.0, status=st,
+               next_bt=Pd, next_out=out)
+    F = Fo.double().cpu().numpy()
+    ref = F @ P.astype(np.float64 if dtype == "fp64" else np.float32).astype(np.float64).T
+    got = out.double().cpu().numpy()
+    assert np.abs(got - ref).max() <= tol * np.abs(ref).max()
+    # the solve itself is unchanged by the extra product
+    Fo2 = torch.empty_like(F0d)
+    _ops.solve(At, Bd, F0d, Fo2, trans_b=False, max_iter=60, grad_tol=1e-6, lipschitz_safety=1.0,
+               status=_lib.new_status())
+    assert torch.equal(Fo, Fo2)
