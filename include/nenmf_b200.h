@@ -190,6 +190,31 @@ int nenmf_compress(int dtype, const void* X, int64_t n, int64_t m, int64_t ldx,
                    const void* L, const void* Rt, int64_t nu, void* XL, void* XRt,
                    void* ws, size_t ws_bytes, void* stream);
 
+/* ---- prepared X (FP32 tensor-core passes) -------------------------------
+ * The FP32 passes read X in a "prepared" tile-major form: every 128 x 128
+ * tile as bf16 hi/lo planes in the tensor-core shared-memory layout, the
+ * same 4 bytes per element as X.  nenmf_rsi/nenmf_compress prepare X
+ * internally on every call; the *_prepared variants take a copy made once
+ * by nenmf_prepare_x (Xp may be NULL: then they behave like the plain call),
+ * so one preparation serves the sketch and the compression of the same X
+ * (compression.py:120-141 followed by :179-188).  nenmf_prepared_x_bytes
+ * returns 0 when the dtype/shape has no prepared form (FP64, k > 32). */
+size_t nenmf_prepared_x_bytes(int dtype, int64_t n, int64_t m, int64_t k);
+int nenmf_prepare_x(int dtype, const void* X, int64_t n, int64_t m, int64_t ldx, int64_t k,
+                    void* Xp, void* stream);
+size_t nenmf_dual_pass_prepared_workspace_bytes(int dtype, int64_t n, int64_t m, int64_t k);
+int nenmf_dual_pass_prepared(int dtype, const void* Xp, int64_t n, int64_t m,
+                             const void* At, const void* Bt, int64_t k, void* Yt, void* Zt,
+                             void* ws, size_t ws_bytes, void* stream);
+size_t nenmf_rsi_prepared_workspace_bytes(int dtype, int64_t n, int64_t m, int64_t nu);
+int nenmf_rsi_prepared(int dtype, const void* X, const void* Xp, int64_t n, int64_t m,
+                       int64_t ldx, const void* omega_l_t, const void* omega_r, int64_t nu,
+                       int q, void* L, void* Rt, nenmf_device_status* status,
+                       void* ws, size_t ws_bytes, void* stream);
+int nenmf_compress_prepared(int dtype, const void* X, const void* Xp, int64_t n, int64_t m,
+                            int64_t ldx, const void* L, const void* Rt, int64_t nu,
+                            void* XL, void* XRt, void* ws, size_t ws_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -54,6 +54,14 @@ _SIGS = {
     "nenmf_rsi_workspace_bytes": (_sz, [_i32, _i64, _i64, _i64]),
     "nenmf_rsi": (_i32, [_i32, _vp, _i64, _i64, _i64, _vp, _vp, _i64, _i32, _vp, _vp, _vp, _vp, _sz, _vp]),
     "nenmf_compress": (_i32, [_i32, _vp, _i64, _i64, _i64, _vp, _vp, _i64, _vp, _vp, _vp, _sz, _vp]),
+    "nenmf_prepared_x_bytes": (_sz, [_i32, _i64, _i64, _i64]),
+    "nenmf_prepare_x": (_i32, [_i32, _vp, _i64, _i64, _i64, _i64, _vp, _vp]),
+    "nenmf_dual_pass_prepared_workspace_bytes": (_sz, [_i32, _i64, _i64, _i64]),
+    "nenmf_dual_pass_prepared": (_i32, [_i32, _vp, _i64, _i64, _vp, _vp, _i64, _vp, _vp, _vp, _sz, _vp]),
+    "nenmf_rsi_prepared_workspace_bytes": (_sz, [_i32, _i64, _i64, _i64]),
+    "nenmf_rsi_prepared": (_i32, [_i32, _vp, _vp, _i64, _i64, _i64, _vp, _vp, _i64, _i32, _vp, _vp, _vp, _vp, _sz,
+                                  _vp]),
+    "nenmf_compress_prepared": (_i32, [_i32, _vp, _vp, _i64, _i64, _i64, _vp, _vp, _i64, _vp, _vp, _vp, _sz, _vp]),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -146,24 +146,61 @@ def orthonormalize(Pt, status) -> None:
     _lib.check(rc, "orthonormalize")
 
 
-def rsi(X, omega_l_t, omega_r, q: int, L, Rt, status) -> None:
+def prepare_x(X, k: int):
+    """Tile-major bf16 hi/lo copy of an FP32 X for the tensor-core passes
+    (nenmf_prepare_x), or None when the dtype/shape has no prepared form."""
+    lib, torch = _lib.require_device()
+    code = _lib.code_of(_dt(X))
+    n, m = X.shape
+    nbytes = lib.nenmf_prepared_x_bytes(code, n, m, int(k))
+    if nbytes == 0:
+        return None
+    Xp = torch.empty(nbytes, dtype=torch.uint8, device=X.device)
+    rc = lib.nenmf_prepare_x(code, X.data_ptr(), n, m, X.stride(0), int(k), Xp.data_ptr(), _lib.stream_handle())
+    _lib.check(rc, "prepare_x")
+    return Xp
+
+
+def dual_pass_prepared(Xp, n: int, m: int, At, Bt, Yt, Zt) -> None:
+    lib, _ = _lib.require_device()
+    code = _lib.code_of(_dt(At))
+    k = At.shape[0]
+    ws = _lib.workspace(lib.nenmf_dual_pass_prepared_workspace_bytes(code, n, m, k))
+    rc = lib.nenmf_dual_pass_prepared(code, Xp.data_ptr(), n, m, At.data_ptr(), Bt.data_ptr(), k, Yt.data_ptr(),
+                                      Zt.data_ptr(), ws.data_ptr(), ws.numel(), _lib.stream_handle())
+    _lib.check(rc, "dual_pass_prepared")
+
+
+def rsi(X, omega_l_t, omega_r, q: int, L, Rt, status, Xp=None) -> None:
     lib, _ = _lib.require_device()
     code = _lib.code_of(_dt(X))
     n, m = X.shape
     nu = omega_r.shape[0]
-    ws = _lib.workspace(lib.nenmf_rsi_workspace_bytes(code, n, m, nu))
-    rc = lib.nenmf_rsi(code, X.data_ptr(), n, m, X.stride(0), omega_l_t.data_ptr(), omega_r.data_ptr(), nu,
-                       int(q), L.data_ptr(), Rt.data_ptr(), _lib.status_ptr(status), ws.data_ptr(), ws.numel(),
-                       _lib.stream_handle())
+    if Xp is not None:
+        ws = _lib.workspace(lib.nenmf_rsi_prepared_workspace_bytes(code, n, m, nu))
+        rc = lib.nenmf_rsi_prepared(code, X.data_ptr(), Xp.data_ptr(), n, m, X.stride(0), omega_l_t.data_ptr(),
+                                    omega_r.data_ptr(), nu, int(q), L.data_ptr(), Rt.data_ptr(),
+                                    _lib.status_ptr(status), ws.data_ptr(), ws.numel(), _lib.stream_handle())
+    else:
+        ws = _lib.workspace(lib.nenmf_rsi_workspace_bytes(code, n, m, nu))
+        rc = lib.nenmf_rsi(code, X.data_ptr(), n, m, X.stride(0), omega_l_t.data_ptr(), omega_r.data_ptr(), nu,
+                           int(q), L.data_ptr(), Rt.data_ptr(), _lib.status_ptr(status), ws.data_ptr(), ws.numel(),
+                           _lib.stream_handle())
     _lib.check(rc, "subspace_iteration_pair")
 
 
-def compress(X, L, Rt, XL, XRt) -> None:
+def compress(X, L, Rt, XL, XRt, Xp=None) -> None:
     lib, _ = _lib.require_device()
     code = _lib.code_of(_dt(X))
     n, m = X.shape
     nu = L.shape[0]
-    ws = _lib.workspace(lib.nenmf_rsi_workspace_bytes(code, n, m, nu))
-    rc = lib.nenmf_compress(code, X.data_ptr(), n, m, X.stride(0), L.data_ptr(), Rt.data_ptr(), nu,
-                            XL.data_ptr(), XRt.data_ptr(), ws.data_ptr(), ws.numel(), _lib.stream_handle())
+    if Xp is not None:
+        ws = _lib.workspace(lib.nenmf_dual_pass_prepared_workspace_bytes(code, n, m, nu))
+        rc = lib.nenmf_compress_prepared(code, X.data_ptr(), Xp.data_ptr(), n, m, X.stride(0), L.data_ptr(),
+                                         Rt.data_ptr(), nu, XL.data_ptr(), XRt.data_ptr(), ws.data_ptr(), ws.numel(),
+                                         _lib.stream_handle())
+    else:
+        ws = _lib.workspace(lib.nenmf_rsi_workspace_bytes(code, n, m, nu))
+        rc = lib.nenmf_compress(code, X.data_ptr(), n, m, X.stride(0), L.data_ptr(), Rt.data_ptr(), nu,
+                                XL.data_ptr(), XRt.data_ptr(), ws.data_ptr(), ws.numel(), _lib.stream_handle())
     _lib.check(rc, "compress_problem")

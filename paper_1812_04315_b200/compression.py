@@ -85,9 +85,11 @@ def sketch_draws(n: int, m: int, nu: int, seed: int):
     return omega_l, omega_r
 
 
-def rsi_device(Xd, nu: int, q: int, seed: int):
+def rsi_device(Xd, nu: int, q: int, seed: int, prepared=None):
     """Device RSI on a resident X (CUDA tensor).  Returns (L, Rt, status)
-    tensors without synchronising; Rt is R transposed (nu x m)."""
+    tensors without synchronising; Rt is R transposed (nu x m).  ``prepared``
+    is an optional ``_ops.prepare_x`` copy of Xd (made once, reused by the
+    compression pass)."""
     _, torch = _lib.require_device()
     n, m = Xd.shape
     omega_l, omega_r = sketch_draws(n, m, nu, seed)
@@ -97,8 +99,21 @@ def rsi_device(Xd, nu: int, q: int, seed: int):
     L = torch.empty((nu, n), dtype=Xd.dtype, device="cuda")
     Rt = torch.empty((nu, m), dtype=Xd.dtype, device="cuda")
     status = _lib.new_status()
-    _ops.rsi(Xd, om_lt, om_r, q, L, Rt, status)
+    _ops.rsi(Xd, om_lt, om_r, q, L, Rt, status, Xp=prepared)
     return L, Rt, status
+
+
+def _x_key(Xd):
+    return (Xd.data_ptr(), tuple(Xd.shape), tuple(Xd.stride()), Xd.dtype, Xd._version)
+
+
+def prepared_for(sketch: "SketchPair", Xd):
+    """The prepared copy of Xd cached on ``sketch`` by subspace_iteration_pair
+    when it was computed from this very tensor (same storage, unmodified)."""
+    hit = sketch.device.get("prepared")
+    if hit is not None and hit[0] == _x_key(Xd):
+        return hit[1]
+    return None
 
 
 def _is_device_tensor(x) -> bool:
@@ -121,15 +136,21 @@ def subspace_iteration_pair(X, nu: int, q: int, seed: int, *, dtype: str = "fp64
         Xd = None
     _check_iteration_inputs(n, m, nu, q, nonzero)
     _lib.require_device()
+    on_device = Xd is not None
     if Xd is None:
         Xd = _lib.to_device(Xh, dtype)
-    L, Rt, status = rsi_device(Xd, nu, q, seed)
+    # a device-resident X is prepared once here and the copy is kept on the
+    # pair, so factorize_compressed's compression pass reuses it
+    Xp = _ops.prepare_x(Xd, nu) if on_device else None
+    L, Rt, status = rsi_device(Xd, nu, q, seed, prepared=Xp)
     st = _lib.read_status(status)[0]
     if st["code"] != 0:
         raise_for_status(int(st["code"]), int(st["iteration"]), "subspace iteration")
     pair = SketchPair(L=_lib.to_host(L), R=np.ascontiguousarray(_lib.to_host(Rt).T), nu=nu,
                       scheme=SUBSPACE_ITERATION, q=q, seed=seed)
     pair.device[dtype] = (L, Rt)
+    if Xp is not None:
+        pair.device["prepared"] = (_x_key(Xd), Xp)
     return pair
 
 
@@ -144,14 +165,14 @@ def sketch_on_device(sketch: SketchPair, dtype: str):
     return L, Rt
 
 
-def compress_device(Xd, L, Rt):
+def compress_device(Xd, L, Rt, prepared=None):
     """(X_L, X_R^T) on the device from one fused pass over X."""
     torch = _lib.torch_mod()
     nu = L.shape[0]
     n, m = Xd.shape
     XL = torch.empty((nu, m), dtype=Xd.dtype, device="cuda")
     XRt = torch.empty((nu, n), dtype=Xd.dtype, device="cuda")
-    _ops.compress(Xd, L, Rt, XL, XRt)
+    _ops.compress(Xd, L, Rt, XL, XRt, Xp=prepared)
     return XL, XRt
 
 

@@ -283,4 +283,66 @@ int nenmf_compress(int dtype, const void* X, int64_t n, int64_t m, int64_t ldx, 
   });
 }
 
+// ------------------------------------------------------ prepared X (FP32) --
+size_t nenmf_prepared_x_bytes(int dtype, int64_t n, int64_t m, int64_t k) {
+  if (dtype != NENMF_F32 || !tc_pass_eligible(n, m, k)) return 0;
+  return tc_presplit_bytes(n, m);
+}
+
+int nenmf_prepare_x(int dtype, const void* X, int64_t n, int64_t m, int64_t ldx, int64_t k, void* Xp,
+                    void* stream) {
+  if (nenmf_prepared_x_bytes(dtype, n, m, k) == 0) return NENMF_ERR_UNSUPPORTED;
+  if (X == nullptr || Xp == nullptr || ldx < m) return NENMF_ERR_VALUE;
+  return tc_presplit(static_cast<const float*>(X), n, m, ldx, static_cast<uint8_t*>(Xp), S(stream));
+}
+
+size_t nenmf_dual_pass_prepared_workspace_bytes(int dtype, int64_t n, int64_t m, int64_t k) {
+  if (nenmf_prepared_x_bytes(dtype, n, m, k) == 0) return 0;
+  Arena a(nullptr, 0);
+  const float* sent = reinterpret_cast<const float*>(16);
+  dual_pass_tc_pre(a, reinterpret_cast<const uint8_t*>(16), n, m, sent, sent, k, nullptr, nullptr, nullptr);
+  return a.used + 256;
+}
+
+int nenmf_dual_pass_prepared(int dtype, const void* Xp, int64_t n, int64_t m, const void* At, const void* Bt,
+                             int64_t k, void* Yt, void* Zt, void* ws, size_t ws_bytes, void* stream) {
+  if (nenmf_prepared_x_bytes(dtype, n, m, k) == 0) return NENMF_ERR_UNSUPPORTED;
+  if (ws == nullptr || Xp == nullptr) return NENMF_ERR_VALUE;
+  Arena a(ws, ws_bytes);
+  return dual_pass_tc_pre(a, static_cast<const uint8_t*>(Xp), n, m, static_cast<const float*>(At),
+                          static_cast<const float*>(Bt), k, static_cast<float*>(Yt), static_cast<float*>(Zt),
+                          S(stream));
+}
+
+size_t nenmf_rsi_prepared_workspace_bytes(int dtype, int64_t n, int64_t m, int64_t nu) {
+  if (nenmf_prepared_x_bytes(dtype, n, m, nu) == 0) return nenmf_rsi_workspace_bytes(dtype, n, m, nu);
+  Arena a(nullptr, 0);
+  rsi<float>(a, nullptr, n, m, m, nullptr, nullptr, nu, 1, nullptr, nullptr, nullptr, nullptr,
+             reinterpret_cast<const uint8_t*>(16));
+  size_t c = nenmf_dual_pass_prepared_workspace_bytes(dtype, n, m, nu);
+  return (a.used > c ? a.used : c) + 256;
+}
+
+int nenmf_rsi_prepared(int dtype, const void* X, const void* Xp, int64_t n, int64_t m, int64_t ldx,
+                       const void* omega_l_t, const void* omega_r, int64_t nu, int q, void* L, void* Rt,
+                       nenmf_device_status* status, void* ws, size_t ws_bytes, void* stream) {
+  if (ws == nullptr) return NENMF_ERR_VALUE;
+  Arena a(ws, ws_bytes);
+  return NENMF_DISPATCH(dtype, [&] {
+    return rsi<scalar_t>(a, C<scalar_t>(X), n, m, ldx, C<scalar_t>(omega_l_t), C<scalar_t>(omega_r), nu, q,
+                         M<scalar_t>(L), M<scalar_t>(Rt), status, S(stream), static_cast<const uint8_t*>(Xp));
+  });
+}
+
+int nenmf_compress_prepared(int dtype, const void* X, const void* Xp, int64_t n, int64_t m, int64_t ldx,
+                            const void* L, const void* Rt, int64_t nu, void* XL, void* XRt, void* ws,
+                            size_t ws_bytes, void* stream) {
+  if (ws == nullptr) return NENMF_ERR_VALUE;
+  Arena a(ws, ws_bytes);
+  return NENMF_DISPATCH(dtype, [&] {
+    return compress<scalar_t>(a, C<scalar_t>(X), n, m, ldx, C<scalar_t>(L), C<scalar_t>(Rt), nu, M<scalar_t>(XL),
+                              M<scalar_t>(XRt), S(stream), static_cast<const uint8_t*>(Xp));
+  });
+}
+
 }  // extern "C"

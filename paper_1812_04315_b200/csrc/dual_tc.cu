@@ -2,37 +2,53 @@
 // from ONE read of X (compression.py:134-139,188), BF16x3 split precision.
 //
 // Every fp32 element x is split into bf16 hi = rn(x) and lo = rn(x - hi);
-// the skinny operands likewise.  Each 128 x 128 tile of X is staged in shared
-// memory as hi and lo bf16 tiles in the canonical 128-byte-swizzled layout,
-// and the SAME bytes feed both products:
+// the skinny operands likewise, and x a ~= x_hi a_hi + x_hi a_lo + x_lo a_hi
+// (relative error ~1e-5, fp32-class).
+//
+// X is split ONCE per sketch (k_presplit_x) into "tile-major" form: every
+// 128 x 128 tile is one contiguous 64 KB block [hi | lo] already in the
+// canonical 128-byte-swizzled K-major shared-memory layout, so a pass is a
+// plain stream of 1-D bulk copies (cp.async.bulk, mbarrier complete_tx) into
+// shared memory: no producer threads, no register staging.  The pre-split
+// copy holds exactly 4 bytes per element, the same bytes as fp32 X, and every
+// one of the 2q+2 passes of the sketch (and the compression pass) reads it.
+//
+// The SAME shared-memory bytes feed both products:
 //   Y (rows of X as M, columns as K)  : A = X tile, K-major descriptor
 //   Z (columns of X as M, rows as K)  : A = X tile, MN-major descriptor
-// Per K-chunk two MMAs per product: [x_hi] x [a_hi | a_lo] (N = 2 kpad) and
-// [x_lo] x [a_hi] (N = kpad) into the same TMEM accumulator, so
-// x a ~= x_hi a_hi + x_hi a_lo + x_lo a_hi (relative error ~1e-5, fp32-class).
+// Per 16-wide K-chunk three MMAs with N = kpad into one TMEM accumulator:
+// x_hi a_hi, x_hi a_lo, x_lo a_hi.
 //
 // Work: units of (row chunk) x (column block of CT tiles).  Z accumulators of
 // the column block live in TMEM for the whole unit; Y accumulators (double
 // buffered) for one tile row.  Partial sums per unit are written to global
-// slabs and reduced in fixed order (deterministic).
+// slabs and reduced in fixed order (deterministic).  The unit grid is chosen
+// on the host to balance tiles per CTA against slab traffic.
 //
-// Roles (13 warps): 0-7 producers (global fp32 -> split -> swizzled smem),
-// 8 MMA issuer + TMEM owner, 9-12 epilogue (TMEM -> registers -> global).
+// Roles (6 warps): 0 bulk-copy producer (one elected thread), 1 MMA issuer +
+// TMEM owner, 2-5 epilogue (TMEM -> registers -> global; lane quadrant = warp % 4).
 #include "rsi.cuh"
 
 #include <cuda_bf16.h>
+
+#include <cstdlib>
+#include <map>
+#include <mutex>
+#include <tuple>
+#include <vector>
 
 namespace nenmf {
 
 namespace tc {
 
 constexpr int TILE = 128;
-constexpr int NPROD = 8;          // producer warps
-constexpr int MMA_WARP = 8;
-constexpr int EPI_WARP0 = 9;      // epilogue warps 9..12 (TMEM lane quadrant = warp % 4)
-constexpr int NWARPS = 13;
+constexpr int PROD_WARP = 0;
+constexpr int MMA_WARP = 1;
+constexpr int EPI_WARP0 = 2;      // epilogue warps 2..5 (TMEM lane quadrant = warp % 4)
+constexpr int NWARPS = 6;
 constexpr int NSTAGE = 2;
-constexpr int SUB_BYTES = TILE * 128;  // one 128-row x 64-col bf16 sub-tile
+constexpr int SUB_BYTES = TILE * 128;       // one 128-row x 64-col bf16 sub-tile
+constexpr int XTILE_BYTES = 4 * SUB_BYTES;  // [hi sub0 | hi sub1 | lo sub0 | lo sub1] = 64 KB
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -113,6 +129,28 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+// 1-D bulk copy global -> shared, completion counted on the mbarrier
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+
 struct Units {
   int n_rt, n_ct;       // tiles along rows / columns of X
   int n_cb, n_rc;       // column blocks, row chunks
@@ -129,34 +167,87 @@ __device__ __forceinline__ void unit_bounds(const Units& U, int u, int& rt0, int
   ct1 = (int)((int64_t)(cb + 1) * U.n_ct / U.n_cb);
 }
 
-// [hi rows 0..k) | zero | lo rows kpad..kpad+k) | zero], each row ld2 (multiple of 8) bf16
-__global__ void k_split_bf16(const float* __restrict__ S, int k, int64_t len, int kpad, int64_t ld2,
-                             __nv_bfloat16* __restrict__ out) {
-  const int64_t total = (int64_t)2 * kpad * ld2;
+// X (n x m fp32, leading dimension ldx) -> tile-major pre-split bf16 hi/lo.
+// One thread per (tile, row, 8-column chunk): reads 32 B, writes 16 B of hi
+// and 16 B of lo at the swizzled position; padding outside X is zero.
+__global__ void k_presplit_x(const float* __restrict__ X, int64_t n, int64_t m, int64_t ldx, int n_ct, int64_t total,
+                             uint8_t* __restrict__ Xs) {
+  const bool vec = ((m | ldx) & 3) == 0 && (reinterpret_cast<uintptr_t>(X) & 15) == 0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t row = i / ld2, col = i % ld2;
-    const int a = (int)(row % kpad);
-    const bool lo = row >= kpad;
-    float v = 0.f;
-    if (a < k && col < len) {
-      const float x = S[(int64_t)a * len + col];
-      const __nv_bfloat16 h = __float2bfloat16_rn(x);
-      v = lo ? (x - __bfloat162float(h)) : x;
+    const int c8 = (int)(i & 15);
+    const int r = (int)((i >> 4) & 127);
+    const int64_t tile = i >> 11;
+    const int64_t rt = tile / n_ct, ct = tile % n_ct;
+    const int64_t gr = rt * TILE + r, gc = ct * TILE + 8 * c8;
+    float v[8];
+    if (gr < n && vec && gc + 8 <= m) {
+      const float4 a = __ldcs(reinterpret_cast<const float4*>(X + gr * ldx + gc));
+      const float4 b = __ldcs(reinterpret_cast<const float4*>(X + gr * ldx + gc + 4));
+      v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] = (gr < n && gc + j < m) ? X[gr * ldx + gc + j] : 0.f;
     }
-    out[i] = __float2bfloat16_rn(v);
+    uint32_t hw[4], lw[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * j], v[2 * j + 1]);
+      const float2 f = __bfloat1622float2(h);
+      const __nv_bfloat162 l = __floats2bfloat162_rn(v[2 * j] - f.x, v[2 * j + 1] - f.y);
+      hw[j] = *reinterpret_cast<const uint32_t*>(&h);
+      lw[j] = *reinterpret_cast<const uint32_t*>(&l);
+    }
+    const int sub = c8 >> 3, ch = c8 & 7;
+    const int64_t off = tile * XTILE_BYTES + sub * SUB_BYTES + r * 128 + ((ch ^ (r & 7)) << 4);
+    *reinterpret_cast<uint4*>(Xs + off) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+    *reinterpret_cast<uint4*>(Xs + off + 2 * SUB_BYTES) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+  }
+}
+
+// Skinny operand S (k x len fp32 row-major) -> per 128-wide K tile:
+// [sub0 | sub1], each sub = 2 kpad rows (hi rows 0..kpad, lo rows kpad..2kpad)
+// x 128 B, swizzled; rows >= k and columns >= len are zero.
+__global__ void k_split_skinny(const float* __restrict__ S, int k, int64_t len, int kpad, int64_t total,
+                               uint8_t* __restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int ch = (int)(i & 7);
+    const int64_t rest = i >> 3;
+    const int row = (int)(rest % (2 * kpad));
+    const int64_t ts = rest / (2 * kpad);  // tile * 2 + sub
+    const int sub = (int)(ts & 1);
+    const int64_t tile = ts >> 1;
+    const int a = row % kpad;
+    const bool lo = row >= kpad;
+    const int64_t c0 = tile * TILE + sub * 64 + ch * 8;
+    uint32_t w[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      float x0 = 0.f, x1 = 0.f;
+      if (a < k) {
+        if (c0 + 2 * j < len) x0 = S[(int64_t)a * len + c0 + 2 * j];
+        if (c0 + 2 * j + 1 < len) x1 = S[(int64_t)a * len + c0 + 2 * j + 1];
+      }
+      if (lo) {
+        x0 -= __bfloat162float(__float2bfloat16_rn(x0));
+        x1 -= __bfloat162float(__float2bfloat16_rn(x1));
+      }
+      const __nv_bfloat162 h = __floats2bfloat162_rn(x0, x1);
+      w[j] = *reinterpret_cast<const uint32_t*>(&h);
+    }
+    const int64_t off = ts * (int64_t)(2 * kpad) * 128 + row * 128 + ((ch ^ (row & 7)) << 4);
+    *reinterpret_cast<uint4*>(out + off) = make_uint4(w[0], w[1], w[2], w[3]);
   }
 }
 
 template <int KPAD>
 __global__ void __launch_bounds__(NWARPS * 32, 1)
-k_dual_tc(const float* __restrict__ X, int64_t n, int64_t m, int64_t ldx, const __nv_bfloat16* __restrict__ A2,
-          int64_t lda2, const __nv_bfloat16* __restrict__ B2, int64_t ldb2, int k, Units U,
-          float* __restrict__ Ypart, float* __restrict__ Zpart) {
-  constexpr int N2 = 2 * KPAD;                 // [hi | lo] columns
-  constexpr int SK_SUB = N2 * 128;             // skinny sub-tile bytes (N2 rows x 128 B)
-  constexpr int STAGE = 4 * SUB_BYTES + 4 * SK_SUB;  // Xhi(2 sub) Xlo(2 sub) A2(2 sub) B2(2 sub)
-  constexpr uint32_t ID_Y2 = idesc_bf16(N2, false), ID_Y1 = idesc_bf16(KPAD, false);
-  constexpr uint32_t ID_Z2 = idesc_bf16(N2, true), ID_Z1 = idesc_bf16(KPAD, true);
+k_dual_bulk(const uint8_t* __restrict__ Xs, int64_t n, int64_t m, const uint8_t* __restrict__ A2,
+            const uint8_t* __restrict__ B2, int k, Units U, float* __restrict__ Ypart, float* __restrict__ Zpart) {
+  constexpr int SK_SUB = 2 * KPAD * 128;             // skinny sub-tile bytes (hi + lo rows x 128 B)
+  constexpr int SK_TILE = 2 * SK_SUB;                // one 128-wide K tile of a skinny operand
+  constexpr int STAGE = XTILE_BYTES + 2 * SK_TILE;   // X tile | A tile | B tile
+  constexpr uint32_t ID_Y = idesc_bf16(KPAD, false), ID_Z = idesc_bf16(KPAD, true);
+  constexpr uint32_t LO_OFF = KPAD * 128;            // lo rows of a skinny sub-tile
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
   __shared__ __align__(8) uint64_t bar_full[NSTAGE], bar_empty[NSTAGE], bar_yfull[2], bar_yempty[2], bar_zfull,
@@ -166,7 +257,7 @@ k_dual_tc(const float* __restrict__ X, int64_t n, int64_t m, int64_t ldx, const 
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   if (tid == 0) {
     for (int s = 0; s < NSTAGE; ++s) {
-      mbar_init(&bar_full[s], NPROD * 32);
+      mbar_init(&bar_full[s], 1);
       mbar_init(&bar_empty[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
@@ -186,98 +277,28 @@ k_dual_tc(const float* __restrict__ X, int64_t n, int64_t m, int64_t ldx, const 
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = tmem_base_sh;
-  // TMEM columns: Y buffers [0, 2 N2), Z accumulators [2 N2, 2 N2 + CT N2)
-  const uint32_t ycol0 = 0, zcol0 = 2 * N2;
+  // TMEM columns: Y buffers [0, 2 KPAD), Z accumulators [2 KPAD, 2 KPAD + CT KPAD)
+  const uint32_t ycol0 = 0, zcol0 = 2 * KPAD;
 
-  if (wid < NPROD) {
-    // ------------------------------------------------------------ producers
-    // Each thread owns 16 float4 of every tile.  The loads run one tile ahead
-    // in a rolling register queue: slot j is refilled with the next tile's
-    // float4 right after it has been split into the current stage, so ~64 KB
-    // per SM stay in flight while the producers convert (HBM latency hidden).
-    const int ptid = tid;  // 0 .. 255
-    constexpr int NQ = TILE * 32 / (NPROD * 32);  // 16 float4 per thread per tile
-    int u = blockIdx.x, rt = 0, ct = 0, rt0 = 0, rt1 = 0, ct0 = 0, ct1 = 0, rc_, cb_;
-    bool valid = u < U.units;
-    if (valid) {
-      unit_bounds(U, u, rt0, rt1, ct0, ct1, rc_, cb_);
-      rt = rt0;
-      ct = ct0;
-    }
-    auto advance = [&]() {
-      if (++ct < ct1) return;
-      ct = ct0;
-      if (++rt < rt1) return;
-      u += gridDim.x;
-      valid = u < U.units;
-      if (valid) {
-        unit_bounds(U, u, rt0, rt1, ct0, ct1, rc_, cb_);
-        rt = rt0;
-        ct = ct0;
+  if (wid == PROD_WARP) {
+    // ------------------------------------------------------------ producer
+    if (lane == 0) {
+      const uint64_t pol_x = policy_evict_first(), pol_s = policy_evict_last();
+      int t = 0;
+      for (int u = blockIdx.x; u < U.units; u += gridDim.x) {
+        int rt0, rt1, ct0, ct1, rc, cb;
+        unit_bounds(U, u, rt0, rt1, ct0, ct1, rc, cb);
+        for (int rt = rt0; rt < rt1; ++rt)
+          for (int ct = ct0; ct < ct1; ++ct, ++t) {
+            const int s = t % NSTAGE;
+            mbar_wait(&bar_empty[s], ((t / NSTAGE) & 1) ^ 1);
+            uint8_t* st = smem + (size_t)s * STAGE;
+            mbar_expect_tx(&bar_full[s], (uint32_t)STAGE);
+            bulk_g2s(st, Xs + ((int64_t)rt * U.n_ct + ct) * XTILE_BYTES, XTILE_BYTES, &bar_full[s], pol_x);
+            bulk_g2s(st + XTILE_BYTES, A2 + (int64_t)ct * SK_TILE, SK_TILE, &bar_full[s], pol_s);
+            bulk_g2s(st + XTILE_BYTES + SK_TILE, B2 + (int64_t)rt * SK_TILE, SK_TILE, &bar_full[s], pol_s);
+          }
       }
-    };
-    auto load = [&](int trt, int tct, int j) -> float4 {
-      const int q = ptid + j * NPROD * 32;
-      const int row = q >> 5, c4 = q & 31;
-      const int64_t gr = (int64_t)trt * TILE + row, gc = (int64_t)tct * TILE + 4 * c4;
-      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (gr < n && gc < m) v = __ldcs(reinterpret_cast<const float4*>(X + gr * ldx + gc));
-      return v;
-    };
-    float4 R[NQ];
-    if (valid) {
-#pragma unroll
-      for (int j = 0; j < NQ; ++j) R[j] = load(rt, ct, j);
-    }
-    int t = 0;
-    while (valid) {
-      const int crt = rt, cct = ct;
-      advance();  // (rt, ct, valid) now name the next tile
-      const int s = t % NSTAGE;
-      mbar_wait(&bar_empty[s], ((t / NSTAGE) & 1) ^ 1);
-      uint8_t* st = smem + (size_t)s * STAGE;
-      uint8_t* xhi = st;
-      uint8_t* xlo = st + 2 * SUB_BYTES;
-      uint8_t* a2 = st + 4 * SUB_BYTES;
-      uint8_t* b2 = a2 + 2 * SK_SUB;
-      const int64_t r0 = (int64_t)crt * TILE, c0 = (int64_t)cct * TILE;
-#pragma unroll
-      for (int j = 0; j < NQ; ++j) {
-        const float4 v = R[j];
-        if (valid) R[j] = load(rt, ct, j);
-        const int q = ptid + j * NPROD * 32;
-        const int row = q >> 5, c4 = q & 31;
-        const __nv_bfloat162 h01 = __floats2bfloat162_rn(v.x, v.y);
-        const __nv_bfloat162 h23 = __floats2bfloat162_rn(v.z, v.w);
-        const float2 f01 = __bfloat1622float2(h01), f23 = __bfloat1622float2(h23);
-        const __nv_bfloat162 l01 = __floats2bfloat162_rn(v.x - f01.x, v.y - f01.y);
-        const __nv_bfloat162 l23 = __floats2bfloat162_rn(v.z - f23.x, v.w - f23.y);
-        const int sub = c4 >> 4, cc = c4 & 15;
-        const uint32_t off = (uint32_t)sub * SUB_BYTES + (uint32_t)row * 128 +
-                             ((uint32_t)((cc >> 1) ^ (row & 7)) << 4) + (uint32_t)(cc & 1) * 8;
-        uint2 hv, lv;
-        hv.x = *reinterpret_cast<const uint32_t*>(&h01);
-        hv.y = *reinterpret_cast<const uint32_t*>(&h23);
-        lv.x = *reinterpret_cast<const uint32_t*>(&l01);
-        lv.y = *reinterpret_cast<const uint32_t*>(&l23);
-        *reinterpret_cast<uint2*>(xhi + off) = hv;
-        *reinterpret_cast<uint2*>(xlo + off) = lv;
-      }
-      // skinny tiles: N2 rows x 128 K-elements (bf16) = N2 x 16 chunks of 16 B
-      for (int q = ptid; q < N2 * 16; q += NPROD * 32) {
-        const int row = q >> 4, ch16 = q & 15, sub = ch16 >> 3, ch = ch16 & 7;
-        const uint32_t off = (uint32_t)sub * SK_SUB + (uint32_t)row * 128 + ((uint32_t)(ch ^ (row & 7)) << 4);
-        const int64_t ca = c0 + ch16 * 8;
-        uint4 va = make_uint4(0, 0, 0, 0), vb = make_uint4(0, 0, 0, 0);
-        if (ca < lda2) va = __ldg(reinterpret_cast<const uint4*>(A2 + (int64_t)row * lda2 + ca));
-        const int64_t rb = r0 + ch16 * 8;
-        if (rb < ldb2) vb = __ldg(reinterpret_cast<const uint4*>(B2 + (int64_t)row * ldb2 + rb));
-        *reinterpret_cast<uint4*>(a2 + off) = va;
-        *reinterpret_cast<uint4*>(b2 + off) = vb;
-      }
-      fence_proxy_async();
-      mbar_arrive(&bar_full[s]);
-      ++t;
     }
   } else if (wid == MMA_WARP) {
     // ------------------------------------------------------------ MMA issuer
@@ -296,27 +317,32 @@ k_dual_tc(const float* __restrict__ X, int64_t n, int64_t m, int64_t ldx, const 
           tc_fence_after();
           if (lane == 0) {
             const uint32_t st = smem_u32(smem + (size_t)s * STAGE);
-            const uint32_t xhi = st, xlo = st + 2 * SUB_BYTES, a2 = st + 4 * SUB_BYTES, b2 = a2 + 2 * SK_SUB;
-            const uint32_t dy = tmem + ycol0 + (uint32_t)yb * N2;
-            const uint32_t dz = tmem + zcol0 + (uint32_t)(ct - ct0) * N2;
+            const uint32_t xhi = st, xlo = st + 2 * SUB_BYTES, a2 = st + XTILE_BYTES, b2 = a2 + SK_TILE;
+            const uint32_t dy = tmem + ycol0 + (uint32_t)yb * KPAD;
+            const uint32_t dz = tmem + zcol0 + (uint32_t)(ct - ct0) * KPAD;
             // Y: K = 128 columns of X = 2 sub-tiles x 4 chunks of 16
 #pragma unroll
             for (int kk = 0; kk < 8; ++kk) {
               const uint32_t sub = kk >> 2, koff = (kk & 3) * 32;
               const uint64_t ah = sdesc(xhi + sub * SUB_BYTES + koff, 16, 1024);
               const uint64_t al = sdesc(xlo + sub * SUB_BYTES + koff, 16, 1024);
-              const uint64_t bb = sdesc(a2 + sub * SK_SUB + koff, 16, 1024);
-              umma(dy, ah, bb, ID_Y2, (ct > ct0 || kk > 0) ? 1u : 0u);
-              umma(dy, al, bb, ID_Y1, 1u);
+              const uint64_t bh = sdesc(a2 + sub * SK_SUB + koff, 16, 1024);
+              const uint64_t bl = sdesc(a2 + sub * SK_SUB + LO_OFF + koff, 16, 1024);
+              umma(dy, ah, bh, ID_Y, (ct > ct0 || kk > 0) ? 1u : 0u);
+              umma(dy, ah, bl, ID_Y, 1u);
+              umma(dy, al, bh, ID_Y, 1u);
             }
             // Z: K = 128 rows of X = 8 chunks of 16 rows; A is MN-major (LBO = next 64 columns)
 #pragma unroll
             for (int kk = 0; kk < 8; ++kk) {
               const uint64_t ah = sdesc(xhi + kk * 2048, SUB_BYTES, 1024);
               const uint64_t al = sdesc(xlo + kk * 2048, SUB_BYTES, 1024);
-              const uint64_t bb = sdesc(b2 + (kk >> 2) * SK_SUB + (kk & 3) * 32, 16, 1024);
-              umma(dz, ah, bb, ID_Z2, (rt > rt0 || kk > 0) ? 1u : 0u);
-              umma(dz, al, bb, ID_Z1, 1u);
+              const uint32_t bsub = b2 + (kk >> 2) * SK_SUB + (kk & 3) * 32;
+              const uint64_t bh = sdesc(bsub, 16, 1024);
+              const uint64_t bl = sdesc(bsub + LO_OFF, 16, 1024);
+              umma(dz, ah, bh, ID_Z, (rt > rt0 || kk > 0) ? 1u : 0u);
+              umma(dz, ah, bl, ID_Z, 1u);
+              umma(dz, al, bh, ID_Z, 1u);
             }
             umma_commit(&bar_empty[s]);
             if (ct == ct1 - 1) umma_commit(&bar_yfull[yb]);
@@ -331,18 +357,15 @@ k_dual_tc(const float* __restrict__ X, int64_t n, int64_t m, int64_t ldx, const 
     const int quad = wid & 3;  // TMEM lanes 32 quad .. 32 quad + 31
     const uint32_t lane_base = (uint32_t)(32 * quad) << 16;
     int row_count = 0, unit_count = 0;
-    // hi and lo halves of an accumulator row, 16 columns at a time (keeps the
-    // epilogue at 32 live registers)
     auto emit = [&](uint32_t ta, float* dst, int64_t ld, int64_t idx, bool live) {
 #pragma unroll
       for (int h = 0; h < KPAD / 16; ++h) {
-        float vh[16], vl[16];
-        tmem_ld16(ta + 16 * h, vh);
-        tmem_ld16(ta + KPAD + 16 * h, vl);
+        float v[16];
+        tmem_ld16(ta + 16 * h, v);
         if (live) {
 #pragma unroll
           for (int a = 0; a < 16; ++a)
-            if (16 * h + a < k) dst[(int64_t)(16 * h + a) * ld + idx] = vh[a] + vl[a];
+            if (16 * h + a < k) dst[(int64_t)(16 * h + a) * ld + idx] = v[a];
         }
       }
     };
@@ -356,7 +379,7 @@ k_dual_tc(const float* __restrict__ X, int64_t n, int64_t m, int64_t ldx, const 
         mbar_wait(&bar_yfull[yb], (row_count >> 1) & 1);
         tc_fence_after();
         const int64_t row = (int64_t)rt * TILE + 32 * quad + lane;
-        emit(tmem + lane_base + ycol0 + (uint32_t)yb * N2, yslab, n, row, row < n);
+        emit(tmem + lane_base + ycol0 + (uint32_t)yb * KPAD, yslab, n, row, row < n);
         tc_fence_before();
         mbar_arrive(&bar_yempty[yb]);
       }
@@ -364,7 +387,7 @@ k_dual_tc(const float* __restrict__ X, int64_t n, int64_t m, int64_t ldx, const 
       tc_fence_after();
       for (int ct = ct0; ct < ct1; ++ct) {
         const int64_t col = (int64_t)ct * TILE + 32 * quad + lane;
-        emit(tmem + lane_base + zcol0 + (uint32_t)(ct - ct0) * N2, zslab, m, col, col < m);
+        emit(tmem + lane_base + zcol0 + (uint32_t)(ct - ct0) * KPAD, zslab, m, col, col < m);
       }
       tc_fence_before();
       mbar_arrive(&bar_zempty);
@@ -385,48 +408,109 @@ __global__ void k_slabs(const float* __restrict__ part, int nslab, int64_t count
   out[o] = s;
 }
 
+// Unit grid: balance tiles per CTA (units are dealt round-robin to the
+// persistent CTAs) against the slab traffic of the partial sums.
+inline Units choose_units(int64_t n, int64_t m, int64_t k, int ctmax, int sms) {
+  static std::mutex mu;
+  static std::map<std::tuple<int64_t, int64_t, int64_t, int, int>, Units> cache;
+  const auto key = std::make_tuple(n, m, k, ctmax, sms);
+  {
+    std::lock_guard<std::mutex> g(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+  }
+  Units best{};
+  best.n_rt = (int)cdiv(n, TILE);
+  best.n_ct = (int)cdiv(m, TILE);
+  double best_cost = 1e300;
+  std::vector<double> load;
+  for (int n_cb = (int)cdiv(best.n_ct, ctmax); n_cb <= best.n_ct; ++n_cb) {
+    for (int n_rc = 1; n_rc <= best.n_rt; ++n_rc) {
+      const int units = n_cb * n_rc;
+      if (units > 4 * sms) break;
+      const int G = units < sms ? units : sms;
+      load.assign(G, 0.0);
+      for (int u = 0; u < units; ++u) {
+        const int rc = u / n_cb, cb = u % n_cb;
+        const int64_t rows = (int64_t)(rc + 1) * best.n_rt / n_rc - (int64_t)rc * best.n_rt / n_rc;
+        const int64_t cols = (int64_t)(cb + 1) * best.n_ct / n_cb - (int64_t)cb * best.n_ct / n_cb;
+        load[u % G] += (double)(rows * cols) + 0.5;  // + per-unit Z drain
+      }
+      double mx = 0;
+      for (double v : load) mx = v > mx ? v : mx;
+      // slab bytes (written + read back, mostly L2-resident) per CTA, in tiles of X
+      const double slab = (double)((n_cb > 1 ? n_cb * n : 0) + (n_rc > 1 ? n_rc * m : 0)) * k * 4.0 * 2.0;
+      const double cost = mx + 0.35 * slab / G / XTILE_BYTES;
+      if (cost < best_cost) {
+        best_cost = cost;
+        best.n_cb = n_cb;
+        best.n_rc = n_rc;
+        best.units = units;
+      }
+    }
+  }
+  std::lock_guard<std::mutex> g(mu);
+  cache[key] = best;
+  return best;
+}
+
 }  // namespace tc
 
-// Returns NENMF_ERR_UNSUPPORTED when the shape is outside the fast path
-// (the caller then uses the CUDA-core pass).  Needs both operands.
-int dual_pass_tc(Arena& ws, const float* X, int64_t n, int64_t m, int64_t ldx, const float* At, const float* Bt,
-                 int64_t k, float* Yt, float* Zt, cudaStream_t s) {
+bool tc_pass_eligible(int64_t n, int64_t m, int64_t k) {
+  if (k < 1 || k > 32 || n < tc::TILE || m < tc::TILE) return false;
+  return getenv("NENMF_NO_TC") == nullptr;
+}
+
+size_t tc_presplit_bytes(int64_t n, int64_t m) {
+  return (size_t)cdiv(n, tc::TILE) * (size_t)cdiv(m, tc::TILE) * tc::XTILE_BYTES;
+}
+
+int tc_presplit(const float* X, int64_t n, int64_t m, int64_t ldx, uint8_t* Xs, cudaStream_t s) {
   using namespace tc;
-  if (At == nullptr || Bt == nullptr || k < 1 || k > 32) return NENMF_ERR_UNSUPPORTED;
-  if (m % 4 != 0 || ldx % 4 != 0 || n < TILE || m < TILE) return NENMF_ERR_UNSUPPORTED;
-  if (getenv("NENMF_NO_TC") != nullptr) return NENMF_ERR_UNSUPPORTED;
-  const int kpad = k <= 16 ? 16 : 32;
-  const int ctmax = (512 - 4 * kpad) / (2 * kpad);
+  const int n_ct = (int)cdiv(m, TILE);
+  const int64_t total = cdiv(n, TILE) * n_ct * (int64_t)TILE * 16;
   int sms = sm_count();
   if (sms <= 0) sms = 148;
-  Units U;
-  U.n_rt = (int)cdiv(n, TILE);
-  U.n_ct = (int)cdiv(m, TILE);
-  U.n_cb = (int)cdiv(U.n_ct, ctmax);
-  U.n_rc = (int)imax(1, imin(U.n_rt, sms / imax(1, U.n_cb)));
-  U.units = U.n_cb * U.n_rc;
-  const int64_t lda2 = cdiv(m, 8) * 8, ldb2 = cdiv(n, 8) * 8;
-  __nv_bfloat16* A2 = ws.take<__nv_bfloat16>((size_t)2 * kpad * lda2);
-  __nv_bfloat16* B2 = ws.take<__nv_bfloat16>((size_t)2 * kpad * ldb2);
+  k_presplit_x<<<(unsigned)imin(cdiv(total, 256), (int64_t)sms * 8), 256, 0, s>>>(X, n, m, ldx, n_ct, total, Xs);
+  NENMF_LAUNCH_CHECK();
+  return NENMF_OK;
+}
+
+// One pass over a pre-split X (tc_presplit): Yt = At X^T (k x n), Zt = Bt X (k x m).
+int dual_pass_tc_pre(Arena& ws, const uint8_t* Xs, int64_t n, int64_t m, const float* At, const float* Bt,
+                     int64_t k, float* Yt, float* Zt, cudaStream_t s) {
+  using namespace tc;
+  if (At == nullptr || Bt == nullptr || !tc_pass_eligible(n, m, k)) return NENMF_ERR_UNSUPPORTED;
+  const int kpad = k <= 16 ? 16 : 32;
+  const int ctmax = (512 - 2 * kpad) / kpad;
+  int sms = sm_count();
+  if (sms <= 0) sms = 148;
+  const Units U = choose_units(n, m, k, ctmax, sms);
+  const int64_t sk_tile = (int64_t)2 * 2 * kpad * 128;
+  uint8_t* A2 = ws.take<uint8_t>((size_t)U.n_ct * sk_tile);
+  uint8_t* B2 = ws.take<uint8_t>((size_t)U.n_rt * sk_tile);
   float* Ypart = U.n_cb > 1 ? ws.take<float>((size_t)U.n_cb * k * n) : nullptr;
   float* Zpart = U.n_rc > 1 ? ws.take<float>((size_t)U.n_rc * k * m) : nullptr;
   if (ws.base == nullptr) return NENMF_OK;
   if (!ws.ok) return NENMF_ERR_WORKSPACE;
-  k_split_bf16<<<(unsigned)imin(1184, cdiv(2 * kpad * lda2, 256)), 256, 0, s>>>(At, (int)k, m, kpad, lda2, A2);
-  NENMF_LAUNCH_CHECK();
-  k_split_bf16<<<(unsigned)imin(1184, cdiv(2 * kpad * ldb2, 256)), 256, 0, s>>>(Bt, (int)k, n, kpad, ldb2, B2);
-  NENMF_LAUNCH_CHECK();
-  const size_t stage = 4 * SUB_BYTES + 4 * (size_t)(2 * kpad) * 128;
+  {
+    const int64_t ta = (int64_t)U.n_ct * 2 * 2 * kpad * 8, tb = (int64_t)U.n_rt * 2 * 2 * kpad * 8;
+    k_split_skinny<<<(unsigned)imin(cdiv(ta, 256), 1184), 256, 0, s>>>(At, (int)k, m, kpad, ta, A2);
+    NENMF_LAUNCH_CHECK();
+    k_split_skinny<<<(unsigned)imin(cdiv(tb, 256), 1184), 256, 0, s>>>(Bt, (int)k, n, kpad, tb, B2);
+    NENMF_LAUNCH_CHECK();
+  }
+  const size_t stage = XTILE_BYTES + 2 * (size_t)sk_tile;
   const size_t smem = NSTAGE * stage + 1024;
   const unsigned grid = (unsigned)imin(U.units, sms);
+  float* Yo = Ypart ? Ypart : Yt;
+  float* Zo = Zpart ? Zpart : Zt;
   if (kpad == 32) {
-    NENMF_CUDA_TRY(set_smem(k_dual_tc<32>, smem));
-    k_dual_tc<32><<<grid, NWARPS * 32, smem, s>>>(X, n, m, ldx, A2, lda2, B2, ldb2, (int)k, U, Ypart ? Ypart : Yt,
-                                                 Zpart ? Zpart : Zt);
+    NENMF_CUDA_TRY(set_smem(k_dual_bulk<32>, smem));
+    k_dual_bulk<32><<<grid, NWARPS * 32, smem, s>>>(Xs, n, m, A2, B2, (int)k, U, Yo, Zo);
   } else {
-    NENMF_CUDA_TRY(set_smem(k_dual_tc<16>, smem));
-    k_dual_tc<16><<<grid, NWARPS * 32, smem, s>>>(X, n, m, ldx, A2, lda2, B2, ldb2, (int)k, U, Ypart ? Ypart : Yt,
-                                                 Zpart ? Zpart : Zt);
+    NENMF_CUDA_TRY(set_smem(k_dual_bulk<16>, smem));
+    k_dual_bulk<16><<<grid, NWARPS * 32, smem, s>>>(Xs, n, m, A2, B2, (int)k, U, Yo, Zo);
   }
   NENMF_LAUNCH_CHECK();
   if (Ypart) {
@@ -437,6 +521,21 @@ int dual_pass_tc(Arena& ws, const float* X, int64_t n, int64_t m, int64_t ldx, c
     k_slabs<<<(unsigned)cdiv(k * m, 256), 256, 0, s>>>(Zpart, U.n_rc, k * m, Zt);
     NENMF_LAUNCH_CHECK();
   }
+  return NENMF_OK;
+}
+
+// Stand-alone pass over fp32 X: pre-split into the workspace, then one pass.
+// Returns NENMF_ERR_UNSUPPORTED when the shape is outside the fast path (the
+// caller then uses the CUDA-core pass).  Needs both operands.
+int dual_pass_tc(Arena& ws, const float* X, int64_t n, int64_t m, int64_t ldx, const float* At, const float* Bt,
+                 int64_t k, float* Yt, float* Zt, cudaStream_t s) {
+  if (At == nullptr || Bt == nullptr || !tc_pass_eligible(n, m, k)) return NENMF_ERR_UNSUPPORTED;
+  uint8_t* Xs = ws.take<uint8_t>(tc_presplit_bytes(n, m));
+  Arena rest = ws;
+  if (ws.base != nullptr && !ws.ok) return NENMF_ERR_WORKSPACE;
+  if (ws.base != nullptr) NENMF_TRY(tc_presplit(X, n, m, ldx, Xs, s));
+  NENMF_TRY(dual_pass_tc_pre(rest, Xs, n, m, At, Bt, k, Yt, Zt, s));
+  ws = rest;
   return NENMF_OK;
 }
 

@@ -419,13 +419,29 @@ int orthonormalize(Arena& ws, T* Pt, int64_t rows, int64_t k, nenmf_device_statu
 // ================================================================= RSI ====
 template <typename T>
 int rsi(Arena& ws, const T* X, int64_t n, int64_t m, int64_t ldx, const T* omega_l_t, const T* omega_r, int64_t nu,
-        int q, T* L, T* Rt, nenmf_device_status* st, cudaStream_t s) {
+        int q, T* L, T* Rt, nenmf_device_status* st, cudaStream_t s, const uint8_t* Xpre) {
   if (nu < 1 || nu > min(n, m)) return NENMF_ERR_DIM;
   if (q < 1) return NENMF_ERR_VALUE;
   const bool dry = ws.base == nullptr;
+  // FP32: X is split once into the tile-major bf16 hi/lo form every
+  // tensor-core pass of the sketch streams (dual_tc.cu)
+  bool pre = false;
+  if constexpr (sizeof(T) == 4) pre = tc_pass_eligible(n, m, nu);
+  // (a caller-prepared copy, nenmf_prepare_x, is used as is)
+  const bool own = pre && Xpre == nullptr;
+  uint8_t* Xs = own ? ws.take<uint8_t>(tc_presplit_bytes(n, m)) : const_cast<uint8_t*>(Xpre);
   T* tcol = ws.take<T>((size_t)nu * m);  // Q~ of the L-chain (m x nu panel)
   T* trow = ws.take<T>((size_t)nu * n);  // Q~ of the R-chain (n x nu panel)
   if (!dry && !ws.ok) return NENMF_ERR_WORKSPACE;
+  auto pass = [&](Arena& a, const T* At, const T* Bt, T* Yt, T* Zt) -> int {
+    if constexpr (sizeof(T) == 4) {
+      if (pre)
+        return dual_pass_tc_pre(a, dry ? reinterpret_cast<const uint8_t*>(16) : Xs, n, m,
+                                reinterpret_cast<const float*>(At), reinterpret_cast<const float*>(Bt), nu,
+                                reinterpret_cast<float*>(Yt), reinterpret_cast<float*>(Zt), s);
+    }
+    return dual_pass<T>(a, X, n, m, ldx, At, Bt, nu, Yt, Zt, s);
+  };
   // scratch of the passes and QRs is reused stage after stage
   Arena scratch = ws;
   size_t need = 0;
@@ -433,7 +449,12 @@ int rsi(Arena& ws, const T* X, int64_t n, int64_t m, int64_t ldx, const T* omega
     // sizing dry runs: non-null sentinels so both pass outputs are counted
     const T* sent = reinterpret_cast<const T*>(alignof(T));
     Arena a(nullptr, 0);
-    dual_pass<T>(a, sent, n, m, ldx, sent, sent, nu, nullptr, nullptr, s);
+    if (pre) {
+      dual_pass_tc_pre(a, reinterpret_cast<const uint8_t*>(16), n, m, reinterpret_cast<const float*>(sent),
+                       reinterpret_cast<const float*>(sent), nu, nullptr, nullptr, s);
+    } else {
+      dual_pass<T>(a, sent, n, m, ldx, sent, sent, nu, nullptr, nullptr, s);
+    }
     need = max(need, a.used);
     Arena b(nullptr, 0);
     orthonormalize<T>(b, L, n, nu, st, s);
@@ -452,8 +473,11 @@ int rsi(Arena& ws, const T* X, int64_t n, int64_t m, int64_t ldx, const T* omega
   }
   if (!scratch.ok) return NENMF_ERR_WORKSPACE;
   auto fresh = [&]() { return Arena(sbase, need); };
+  if constexpr (sizeof(T) == 4) {
+    if (own) NENMF_TRY(tc_presplit(reinterpret_cast<const float*>(X), n, m, ldx, Xs, s));
+  }
   // start: Y = X Omega_L -> L (as Q_col^T), Z = X^T Omega_R^T -> Rt (compression.py:134-135)
-  { Arena a = fresh(); NENMF_TRY(dual_pass<T>(a, X, n, m, ldx, omega_l_t, omega_r, nu, L, Rt, s)); }
+  { Arena a = fresh(); NENMF_TRY(pass(a, omega_l_t, omega_r, L, Rt)); }
   auto qr2 = [&](T* A, int64_t ra, T* B, int64_t rb) -> int {
     Arena a = fresh();
     const char* e = getenv("NENMF_QR");
@@ -467,10 +491,10 @@ int rsi(Arena& ws, const T* X, int64_t n, int64_t m, int64_t ldx, const T* omega
   NENMF_TRY(qr2(L, n, Rt, m));
   for (int it = 1; it <= q; ++it) {
     // pass a: X^T Q_col (-> tcol, m x nu) and X Q_row (-> trow, n x nu)  (compression.py:138-139)
-    { Arena a = fresh(); NENMF_TRY(dual_pass<T>(a, X, n, m, ldx, Rt, L, nu, trow, tcol, s)); }
+    { Arena a = fresh(); NENMF_TRY(pass(a, Rt, L, trow, tcol)); }
     NENMF_TRY(qr2(tcol, m, trow, n));
     // pass b: X Q~_col (-> L) and X^T Q~_row (-> Rt)
-    { Arena a = fresh(); NENMF_TRY(dual_pass<T>(a, X, n, m, ldx, tcol, trow, nu, L, Rt, s)); }
+    { Arena a = fresh(); NENMF_TRY(pass(a, tcol, trow, L, Rt)); }
     NENMF_TRY(qr2(L, n, Rt, m));
   }
   return NENMF_OK;
@@ -478,8 +502,13 @@ int rsi(Arena& ws, const T* X, int64_t n, int64_t m, int64_t ldx, const T* omega
 
 template <typename T>
 int compress(Arena& ws, const T* X, int64_t n, int64_t m, int64_t ldx, const T* L, const T* Rt, int64_t nu, T* XL,
-             T* XRt, cudaStream_t s) {
+             T* XRt, cudaStream_t s, const uint8_t* Xpre) {
   // X_R^T = Rt X^T (Y side with At = Rt); X_L = L X (Z side with Bt = L)
+  if constexpr (sizeof(T) == 4) {
+    if (Xpre != nullptr && tc_pass_eligible(n, m, nu))
+      return dual_pass_tc_pre(ws, Xpre, n, m, reinterpret_cast<const float*>(Rt), reinterpret_cast<const float*>(L),
+                              nu, reinterpret_cast<float*>(XRt), reinterpret_cast<float*>(XL), s);
+  }
   return dual_pass<T>(ws, X, n, m, ldx, Rt, L, nu, XRt, XL, s);
 }
 
@@ -488,9 +517,9 @@ int compress(Arena& ws, const T* X, int64_t n, int64_t m, int64_t ldx, const T* 
                             T*, cudaStream_t);                                                              \
   template int orthonormalize<T>(Arena&, T*, int64_t, int64_t, nenmf_device_status*, cudaStream_t);         \
   template int rsi<T>(Arena&, const T*, int64_t, int64_t, int64_t, const T*, const T*, int64_t, int, T*, T*, \
-                      nenmf_device_status*, cudaStream_t);                                                  \
+                      nenmf_device_status*, cudaStream_t, const uint8_t*);                                  \
   template int compress<T>(Arena&, const T*, int64_t, int64_t, int64_t, const T*, const T*, int64_t, T*, T*, \
-                           cudaStream_t);
+                           cudaStream_t, const uint8_t*);
 NENMF_INST_RSI(double)
 NENMF_INST_RSI(float)
 

@@ -13,10 +13,17 @@ int orthonormalize(Arena& ws, T* Pt, int64_t rows, int64_t k, nenmf_device_statu
 
 template <typename T>
 int rsi(Arena& ws, const T* X, int64_t n, int64_t m, int64_t ldx, const T* omega_l_t, const T* omega_r, int64_t nu,
-        int q, T* L, T* Rt, nenmf_device_status* st, cudaStream_t s);
+        int q, T* L, T* Rt, nenmf_device_status* st, cudaStream_t s, const uint8_t* Xpre = nullptr);
 
 template <typename T>
 int compress(Arena& ws, const T* X, int64_t n, int64_t m, int64_t ldx, const T* L, const T* Rt, int64_t nu, T* XL,
-             T* XRt, cudaStream_t s);
+             T* XRt, cudaStream_t s, const uint8_t* Xpre = nullptr);
+
+// FP32 tensor-core pass over a pre-split X (dual_tc.cu)
+bool tc_pass_eligible(int64_t n, int64_t m, int64_t k);
+size_t tc_presplit_bytes(int64_t n, int64_t m);
+int tc_presplit(const float* X, int64_t n, int64_t m, int64_t ldx, uint8_t* Xs, cudaStream_t s);
+int dual_pass_tc_pre(Arena& ws, const uint8_t* Xs, int64_t n, int64_t m, const float* At, const float* Bt,
+                     int64_t k, float* Yt, float* Zt, cudaStream_t s);
 
 }  // namespace nenmf

@@ -25,7 +25,7 @@ from typing import Callable
 import numpy as np
 
 from . import _lib, _ops
-from .compression import SketchPair, compress_device, sketch_on_device
+from .compression import SketchPair, compress_device, prepared_for, sketch_on_device
 from .errors import DimensionError, NumericalFailureError, ZeroMatrixError, raise_for_status
 from .matrix import DenseMatrix, as_matrix, check_seed, open_uniform
 from .nnls import InnerSolverConfig
@@ -123,7 +123,7 @@ class _DeviceLoop:
             L, Rt = sketch_on_device(self.sketch, self.dtype)
             self.L, self.Rt = L, Rt
             # the compressed preamble stays on the solver clock (factorize.py:130)
-            self.XL, self.XRt = compress_device(self.X, L, Rt)
+            self.XL, self.XRt = compress_device(self.X, L, Rt, prepared=prepared_for(self.sketch, self.X))
             nu = L.shape[0]
             self.FR = torch.empty((self.p, nu), dtype=self.X.dtype, device="cuda")
             self.fr_ready = False
