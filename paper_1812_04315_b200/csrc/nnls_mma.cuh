@@ -19,8 +19,10 @@ namespace nenmf {
 // accumulator fragment of n-tile t IS the A fragment of k-tile t, so an
 // iteration never leaves registers: elementwise update on the accumulator
 // layout -> A fragments -> MMAs -> next accumulator.
-//   FP32: m16n8k8 TF32, 16 columns per warp, 3xTF32 split (two chains:
-//         lo*hi + hi*lo, then hi*hi), W^T hi/lo fragments resident
+//   FP32: 16 columns per warp, split precision: hi*hi on m16n8k8 TF32 and
+//         the two correction terms lo*hi + hi*lo as ONE m16n8k16 BF16 MMA per
+//         k-tile (K = [F_lo | F_hi] against [W_hi ; W_lo]); 18 instead of 27
+//         MMAs per iteration at p <= 24, W^T fragments resident
 //   FP64: m8n8k4 F64, 8 columns per warp, exact products
 template <typename T>
 struct MmaShape;
@@ -54,6 +56,18 @@ __device__ __forceinline__ void mma_tf32(float (&c)[4], const uint32_t (&a)[4], 
       "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
       : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ void mma_bf16(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+// two fp32 -> packed bf16x2 (round to nearest), first value in the low half
+__device__ __forceinline__ uint32_t pack_bf16(float lo_idx, float hi_idx) {
+  uint32_t r;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi_idx), "f"(lo_idx));
+  return r;
 }
 __device__ __forceinline__ void mma_f64(double (&c)[2], double a, double b) {
   asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
@@ -226,20 +240,26 @@ k_nnls_mma(const __grid_constant__ MmaArgs<T> A) {
     auto wval = [&](int i, int l) -> T {
       return (i < p && l < p) ? (fused ? W_s[i * 32 + l] : W[i * p + l]) : T(0);
     };
-    // W^T fragments (B operand), resident for the whole solve; b[kt][nt]
-    uint32_t bhi[NT][NT][2], blo[NT][NT][2];
+    // W^T fragments (B operand), resident for the whole solve; b[kt][nt]:
+    // bhi = TF32 hi (m16n8k8), bco = BF16 [W_hi ; W_lo] of the correction MMA
+    uint32_t bhi[NT][NT][2], bco[NT][NT][2];
     double bd[2 * NT][NT];
     if constexpr (S::EPT == 4) {
 #pragma unroll
       for (int kt = 0; kt < NT; ++kt)
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt)
+        for (int nt = 0; nt < NT; ++nt) {
+          float wh[2], wl[2];
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             const float w = (float)wval(8 * nt + gq, 8 * kt + 2 * tq + h);
             bhi[kt][nt][h] = tf32_hi(w);
-            blo[kt][nt][h] = tf32_lo(w, bhi[kt][nt][h]);
+            wh[h] = __uint_as_float(bhi[kt][nt][h]);
+            wl[h] = w - wh[h];
           }
+          bco[kt][nt][0] = pack_bf16(wh[0], wh[1]);  // K 2tq, 2tq+1   <-> F_lo rows
+          bco[kt][nt][1] = pack_bf16(wl[0], wl[1]);  // K 2tq+8, 2tq+9 <-> F_hi rows
+        }
     } else {
 #pragma unroll
       for (int kk = 0; kk < 2 * NT; ++kk)
@@ -253,15 +273,23 @@ k_nnls_mma(const __grid_constant__ MmaArgs<T> A) {
     // g = W f - V in the accumulator layout (the MMA chain starts from -V)
     auto grad = [&](const T (&fe)[NE], T (&g)[NE]) {
       if constexpr (S::EPT == 4) {
-        uint32_t ahi[NT][4], alo[NT][4];
+        // accumulator element (col, row): c0 (gq, 2tq), c1 (gq, 2tq+1), c2 (gq+8, 2tq), c3 (gq+8, 2tq+1)
+        uint32_t ahi[NT][4], aco[NT][4];
 #pragma unroll
         for (int t = 0; t < NT; ++t) {
-          const float v4[4] = {(float)fe[4 * t + 0], (float)fe[4 * t + 2], (float)fe[4 * t + 1], (float)fe[4 * t + 3]};
-#pragma unroll
-          for (int r = 0; r < 4; ++r) {
-            ahi[t][r] = tf32_hi(v4[r]);
-            alo[t][r] = tf32_lo(v4[r], ahi[t][r]);
-          }
+          const float c0 = (float)fe[4 * t + 0], c1 = (float)fe[4 * t + 1], c2 = (float)fe[4 * t + 2],
+                      c3 = (float)fe[4 * t + 3];
+          const uint32_t h0 = tf32_hi(c0), h1 = tf32_hi(c1), h2 = tf32_hi(c2), h3 = tf32_hi(c3);
+          ahi[t][0] = h0;  // (gq,   K slot tq   -> row 2tq)
+          ahi[t][1] = h2;  // (gq+8, K slot tq)
+          ahi[t][2] = h1;  // (gq,   K slot tq+4 -> row 2tq+1)
+          ahi[t][3] = h3;
+          const float f0 = __uint_as_float(h0), f1 = __uint_as_float(h1), f2 = __uint_as_float(h2),
+                      f3 = __uint_as_float(h3);
+          aco[t][0] = pack_bf16(c0 - f0, c1 - f1);  // (gq,   K 2tq, 2tq+1): F_lo
+          aco[t][1] = pack_bf16(c2 - f2, c3 - f3);  // (gq+8, K 2tq, 2tq+1)
+          aco[t][2] = pack_bf16(f0, f1);            // (gq,   K 2tq+8, 2tq+9): F_hi
+          aco[t][3] = pack_bf16(f2, f3);
         }
         // n-tiles innermost: consecutive MMAs are independent, so the NT
         // accumulation chains overlap in the tensor pipe
@@ -271,12 +299,9 @@ k_nnls_mma(const __grid_constant__ MmaArgs<T> A) {
 #pragma unroll
           for (int r = 0; r < 4; ++r) cc[nt][r] = (float)nv[4 * nt + r];
 #pragma unroll
-        for (int kt = 0; kt < NT; ++kt) {  // 3xTF32, small terms first
+        for (int kt = 0; kt < NT; ++kt)  // correction terms F_lo W_hi + F_hi W_lo first (small)
 #pragma unroll
-          for (int nt = 0; nt < NT; ++nt) mma_tf32(cc[nt], alo[kt], bhi[kt][nt][0], bhi[kt][nt][1]);
-#pragma unroll
-          for (int nt = 0; nt < NT; ++nt) mma_tf32(cc[nt], ahi[kt], blo[kt][nt][0], blo[kt][nt][1]);
-        }
+          for (int nt = 0; nt < NT; ++nt) mma_bf16(cc[nt], aco[kt], bco[kt][nt][0], bco[kt][nt][1]);
 #pragma unroll
         for (int kt = 0; kt < NT; ++kt)
 #pragma unroll
@@ -335,19 +360,49 @@ k_nnls_mma(const __grid_constant__ MmaArgs<T> A) {
     };
     // F -> g -> (u, sums); u overwrites uo
     auto finish = [&](const T (&fe)[NE], const T (&g)[NE], T (&uo)[NE], T& s0, T& s1) {
-      s0 = s1 = T(0);
+      if constexpr (sizeof(T) == 4) {
+        // packed fp32x2 arithmetic (FFMA2/FADD2 on sm_100): elements 2i, 2i+1
+        // are two solver rows of one column
+        float2 a0 = make_float2(0.f, 0.f), a1 = make_float2(0.f, 0.f);
+        const float2 rl = make_float2(rnegL, rnegL);
 #pragma unroll
-      for (int e = 0; e < NE; ++e) {
-        uo[e] = fma_acc(g[e], rnegL, fe[e]);
-        const T pgv = fe[e] > T(0) ? g[e] : min0_nan(g[e]);
-        s0 = fma_acc(pgv, pgv, s0);
-        s1 = fma_acc(fe[e], g[e] + nv[e], s1);
+        for (int e = 0; e < NE; e += 2) {
+          const float2 f2 = make_float2(fe[e], fe[e + 1]), g2 = make_float2(g[e], g[e + 1]);
+          const float2 u2 = __ffma2_rn(g2, rl, f2);
+          uo[e] = u2.x;
+          uo[e + 1] = u2.y;
+          const float2 pg2 = make_float2(fe[e] > 0.f ? g[e] : min0_nan(g[e]), fe[e + 1] > 0.f ? g[e + 1] : min0_nan(g[e + 1]));
+          a0 = __ffma2_rn(pg2, pg2, a0);
+          a1 = __ffma2_rn(f2, __fadd2_rn(g2, make_float2(nv[e], nv[e + 1])), a1);
+        }
+        s0 = a0.x + a0.y;
+        s1 = a1.x + a1.y;
+      } else {
+        s0 = s1 = T(0);
+#pragma unroll
+        for (int e = 0; e < NE; ++e) {
+          uo[e] = fma_acc(g[e], rnegL, fe[e]);
+          const T pgv = fe[e] > T(0) ? g[e] : min0_nan(g[e]);
+          s0 = fma_acc(pgv, pgv, s0);
+          s1 = fma_acc(fe[e], g[e] + nv[e], s1);
+        }
       }
     };
     // F_k from (u_{k-1}, u_{k-2}) into fo
     auto extrapolate = [&](const T (&u1)[NE], const T (&u2)[NE], T w, T (&fo)[NE]) {
+      if constexpr (sizeof(T) == 4) {
+        const float2 w2 = make_float2(w, w), m1 = make_float2(-1.f, -1.f);
 #pragma unroll
-      for (int e = 0; e < NE; ++e) fo[e] = relu_nan_fast(fma_acc(u1[e] - u2[e], w, u1[e]));
+        for (int e = 0; e < NE; e += 2) {
+          const float2 a = make_float2(u1[e], u1[e + 1]), b = make_float2(u2[e], u2[e + 1]);
+          const float2 y = __ffma2_rn(__ffma2_rn(b, m1, a), w2, a);  // u1 + w (u1 - u2)
+          fo[e] = relu_nan_fast(y.x);
+          fo[e + 1] = relu_nan_fast(y.y);
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < NE; ++e) fo[e] = relu_nan_fast(fma_acc(u1[e] - u2[e], w, u1[e]));
+      }
     };
 
     // start point (nnls.py:163-178); columns/rows outside the problem stay 0
