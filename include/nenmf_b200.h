@@ -17,7 +17,8 @@
  *   nenmf_residual_sumsq    factorize.py:139, tracing.py:45-57  ||X - G F||^2
  *   nenmf_sumsq             matrix.py:177-179     frobenius_norm^2
  *   nenmf_dual_pass         compression.py:134-139 X @ A and X.T @ B in one pass
- *   nenmf_orthonormalize    compression.py:88-106 _orthonormal_columns (TSQR)
+ *   nenmf_orthonormalize    compression.py:88-106 _orthonormal_columns (CholeskyQR2;
+ *                           Householder TSQR for k > 32)
  *
  * Conventions
  *  - All array pointers are DEVICE pointers, row-major, allocated by the
@@ -189,6 +190,28 @@ int nenmf_rsi(int dtype, const void* X, int64_t n, int64_t m, int64_t ldx,
 int nenmf_compress(int dtype, const void* X, int64_t n, int64_t m, int64_t ldx,
                    const void* L, const void* Rt, int64_t nu, void* XL, void* XRt,
                    void* ws, size_t ws_bytes, void* stream);
+
+/* ---- stages of the orthonormalisation, for row-sharded panels ----------
+ * nenmf_orthonormalize is CholeskyQR2 (rank-revealing first pass).  When a
+ * tall panel is split by rows across ranks, the caller runs its stages with
+ * an all-reduce of the k x k Gram matrix in between:
+ *   nenmf_panel_gram    G = P^T P of the local rows (fp64, fixed order)
+ *   (all-reduce G over ranks)
+ *   nenmf_panel_factor  (pivoted) Cholesky of G -> R (k x k), meta (1 + k
+ *                       ints: rank, pivot order); identical on every rank
+ *   nenmf_panel_trsm    local rows: Pout = Pin Pi R^-1; columns past the rank
+ *                       get fixed pseudo-random values keyed by the GLOBAL row
+ *                       index row0 + i (so shards reproduce the 1-GPU panel);
+ *                       full_rank_only skips the solve when rank < k
+ * Pass 1: pivot = 1 on P (-> Q1); pass 2: pivot = 0 on Q1 (-> Q). */
+size_t nenmf_panel_gram_workspace_bytes(int dtype, int64_t rows, int64_t k);
+int nenmf_panel_gram(int dtype, const void* Pt, int64_t rows, int64_t k, double* G,
+                     void* ws, size_t ws_bytes, void* stream);
+int nenmf_panel_factor(const double* G, int64_t k, int pivot, double* R, int* meta,
+                       nenmf_device_status* status, void* stream);
+int nenmf_panel_trsm(int dtype, const void* Pin_t, int64_t rows, int64_t k, const double* R,
+                     const int* meta, void* Pout_t, int64_t row0, int full_rank_only,
+                     void* stream);
 
 /* ---- prepared X (FP32 tensor-core passes) -------------------------------
  * The FP32 passes read X in a "prepared" tile-major form: every 128 x 128

@@ -283,6 +283,34 @@ int nenmf_compress(int dtype, const void* X, int64_t n, int64_t m, int64_t ldx, 
   });
 }
 
+// ------------------------------------------- row-sharded panel QR stages --
+size_t nenmf_panel_gram_workspace_bytes(int dtype, int64_t rows, int64_t k) {
+  Arena a(nullptr, 0);
+  NENMF_DISPATCH(dtype, [&] { return panel_gram<scalar_t>(a, nullptr, rows, k, nullptr, nullptr); });
+  return a.used + 256;
+}
+
+int nenmf_panel_gram(int dtype, const void* Pt, int64_t rows, int64_t k, double* G, void* ws, size_t ws_bytes,
+                     void* stream) {
+  if (ws == nullptr || G == nullptr) return NENMF_ERR_VALUE;
+  Arena a(ws, ws_bytes);
+  return NENMF_DISPATCH(dtype, [&] { return panel_gram<scalar_t>(a, C<scalar_t>(Pt), rows, k, G, S(stream)); });
+}
+
+int nenmf_panel_factor(const double* G, int64_t k, int pivot, double* R, int* meta, nenmf_device_status* status,
+                       void* stream) {
+  if (G == nullptr || R == nullptr || meta == nullptr) return NENMF_ERR_VALUE;
+  return panel_factor(G, k, pivot ? 1 : 0, R, meta, status, S(stream));
+}
+
+int nenmf_panel_trsm(int dtype, const void* Pin_t, int64_t rows, int64_t k, const double* R, const int* meta,
+                     void* Pout_t, int64_t row0, int full_rank_only, void* stream) {
+  return NENMF_DISPATCH(dtype, [&] {
+    return panel_trsm<scalar_t>(C<scalar_t>(Pin_t), rows, k, R, meta, M<scalar_t>(Pout_t), row0,
+                                full_rank_only ? 1 : 0, S(stream));
+  });
+}
+
 // ------------------------------------------------------ prepared X (FP32) --
 size_t nenmf_prepared_x_bytes(int dtype, int64_t n, int64_t m, int64_t k) {
   if (dtype != NENMF_F32 || !tc_pass_eligible(n, m, k)) return 0;

@@ -1,15 +1,15 @@
 // Orthonormal basis of a tall panel (the role of np.linalg.qr in
 // compression.py:88-106) by rank-revealing CholeskyQR2, all on the device.
 //
-//   G1 = P^T P (fp64, fixed-order split-K)                   gram_d
-//   pivoted Cholesky of G1 -> rank r, P Pi = Q1 R11          k_factor     (1 CTA)
-//   Q1 = P Pi R11^{-1} (row-parallel triangular solves);      k_trsm_apply
+//   G1 = P^T P (fp64, fixed-order split-K)                   k_gram_part  (all SMs)
+//   pivoted Cholesky of G1 -> rank r, P Pi = Q1 R11          k_gram_factor (1 CTA)
+//   Q1 = P Pi R11^{-1} (row-parallel triangular solves);      k_trsm
 //        columns r..k-1 replaced by fixed pseudo-random
 //        vectors (the reference's trailing Householder columns of a
 //        rank-deficient panel are rounding noise; any orthonormal completion
 //        spans the same determined subspace)
-//   G2 = Q1^T Q1, Cholesky R2 (no pivoting)                  k_factor     (1 CTA)
-//   Q  = Q1 R2^{-1}                                          k_trsm_apply
+//   G2 = Q1^T Q1, Cholesky R2 (no pivoting)                  k_gram_factor (1 CTA)
+//   Q  = Q1 R2^{-1}                                          k_trsm
 //
 // Cost: four streaming passes over the panel plus two one-CTA k x k
 // factorisations, instead of a k-step Householder sweep.  The compressed
@@ -22,100 +22,113 @@
 #include "rsi.cuh"
 #include "skinny.cuh"
 
-#include <cooperative_groups.h>
 
 namespace nenmf {
 
 constexpr int QC_KMAX = 32;  // the register-row factorisation holds k <= 32
 
-// (Pivoted) Cholesky of a k x k Gram matrix, right-looking, by ONE warp:
-// lane a keeps row a of the Schur complement in registers (k <= 32), the
-// pivot row is exchanged with shuffles; no block barriers.  Rows of R are
-// produced in pivot order with columns in the original index space:
-// P[:, perm] = Q R11 (R11[j][l] = R[j*k + perm[l]]).  Without pivoting perm is
-// the identity.  Pivots <= rel_tol * max(diag) end it (rank).  S (k*k) holds
-// the Gram matrix; R (k*k) is shared scratch.  Only warp 0 works.
-__device__ void block_factor(double* S, double* R, int k, int pivot, double rel_tol, double* __restrict__ Rout,
-                             int* __restrict__ meta, nenmf_device_status* st) {
+// (Pivoted) Cholesky of a k x k Gram matrix (k <= 32), right-looking, by the
+// whole CTA: the Schur complement stays in shared memory S; per step the
+// pivot is chosen by warp 0 (largest remaining diagonal, compared on its
+// leading 32 bits, lowest index among equals: deterministic), the pivot
+// column of R is formed by k threads and the rank-1 update of the remaining
+// block by all threads.  Rows of R are produced in pivot order with columns in
+// the original index space: P[:, perm] = Q R11 (R11[j][l] = R[j*k + perm[l]]).
+// Without pivoting perm is the identity.  A pivot <= rel_tol * max(diag) ends
+// it (rank).  R (k*k) is shared scratch.
+__device__ void block_factor(double* S_in, double* /*R scratch (unused)*/, int k, int pivot, double rel_tol,
+                             double* __restrict__ Rout, int* __restrict__ meta, nenmf_device_status* st) {
+  // row stride 32 inside: element (a, b) at a * 32 + b, no integer division
+  __shared__ double S[QC_KMAX * QC_KMAX];
+  __shared__ double Rc[QC_KMAX];  // the current column of R (remaining rows)
   __shared__ int perm[QC_KMAX];
-  if (threadIdx.x < 32) {
-    const int lane = threadIdx.x;
-    const unsigned FULL = 0xffffffffu;
-    double row[32];
-#pragma unroll
-    for (int b = 0; b < 32; ++b) row[b] = (lane < k && b < k) ? S[lane * k + b] : 0.0;
-    bool rem = lane < k;
-    bool bad = false;
-#pragma unroll
-    for (int b = 0; b < 32; ++b) bad |= !isfinite(row[b]);
-    bad = __any_sync(FULL, bad);
-    double diag = 0.0;
-#pragma unroll
-    for (int b = 0; b < 32; ++b)
-      if (b == lane) diag = row[b];
-    double mx = rem ? diag : 0.0;
+  __shared__ int rem[QC_KMAX];
+  __shared__ int s_piv, s_stop, s_bad;
+  __shared__ double s_rjj, s_inv, s_tau;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nwarp = blockDim.x >> 5;
+  const unsigned FULL = 0xffffffffu;
+  const int kk = k * k;
+  if (tid == 0) s_bad = 0;
+  __syncthreads();
+  for (int a = wid; a < QC_KMAX; a += nwarp) {
+    const double v = (a < k && lane < k) ? S_in[a * k + lane] : 0.0;
+    S[a * 32 + lane] = v;
+    if (!isfinite(v)) s_bad = 1;
+  }
+  for (int e = tid; e < kk; e += blockDim.x) Rout[e] = 0.0;
+  if (tid < QC_KMAX) rem[tid] = tid < k ? 1 : 0;
+  __syncthreads();
+  if (tid < 32) {
+    double mx = lane < k ? S[lane * 33] : 0.0;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(FULL, mx, o));
-    for (int e = lane; e < k * k; e += 32) R[e] = 0.0;
-    int rank = k;
-    if (bad || !(mx > 0.0)) {
-      rank = 0;
-      if (lane == 0) status_fail(st, NENMF_ERR_NUMERICAL_COLLAPSE, -1);
-    } else {
-      const double tau = rel_tol * mx;
-      for (int j = 0; j < k; ++j) {
-        int best;
-        double bv;
-        if (pivot) {
-          bv = rem ? diag : -1.0;
-          best = rem ? lane : -1;
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) {
-            const double ov = __shfl_xor_sync(FULL, bv, o);
-            const int oi = __shfl_xor_sync(FULL, best, o);
-            if (ov > bv || (ov == bv && oi >= 0 && (best < 0 || oi < best))) {
-              bv = ov;
-              best = oi;
-            }
-          }
-        } else {
-          best = j;
-          bv = __shfl_sync(FULL, diag, j);
-        }
-        if (!(bv > tau)) {
-          rank = j;
-          break;
-        }
-        const int pj = best;
-        if (lane == pj) rem = false;
-        if (lane == 0) perm[j] = pj;
-        const double rjj = sqrt(bv), inv = 1.0 / rjj;
-        // R[j][a] = S[a][pj] / rjj for remaining rows a (column pj of my row)
-        double sap = 0.0;
-#pragma unroll
-        for (int b = 0; b < 32; ++b)
-          if (b == pj) sap = row[b];
-        const double ra = rem ? sap * inv : (lane == pj ? rjj : 0.0);
-        if (lane < k) R[j * k + lane] = ra;
-        const double rself = rem ? ra : 0.0;
-        // Schur update of my row: row[b] -= R[j][a] R[j][b]
-#pragma unroll
-        for (int b = 0; b < 32; ++b) {
-          const double rb = __shfl_sync(FULL, rem ? ra : 0.0, b);
-          row[b] = fma(-rself, rb, row[b]);
-        }
-#pragma unroll
-        for (int b = 0; b < 32; ++b)
-          if (b == lane) diag = row[b];
-      }
-    }
-    __syncwarp();
-    for (int e = lane; e < k * k; e += 32) Rout[e] = R[e];
-    for (int i = lane; i < k; i += 32) meta[1 + i] = i < rank ? perm[i] : -1;
     if (lane == 0) {
-      meta[0] = rank;
-      if (!pivot && rank < k) status_fail(st, NENMF_ERR_NUMERICAL_COLLAPSE, -1);
+      if (!(mx > 0.0)) s_bad = 1;
+      s_tau = rel_tol * mx;
     }
+  }
+  __syncthreads();
+  int rank = k;
+  if (s_bad) {
+    rank = 0;
+    if (tid == 0) status_fail(st, NENMF_ERR_NUMERICAL_COLLAPSE, -1);
+  } else {
+    for (int j = 0; j < k; ++j) {
+      if (tid < 32) {
+        const bool live = lane < k && rem[lane];
+        const double d = live ? S[lane * 33] : -1.0;
+        int pj;
+        if (pivot) {
+          // positive doubles order like their bit patterns: compare the top 32 bits
+          const unsigned key = d > 0.0 ? (unsigned)(__double_as_longlong(d) >> 32) : 0u;
+          const unsigned best = __reduce_max_sync(FULL, key);
+          const unsigned cand = __ballot_sync(FULL, live && key == best);
+          pj = cand ? __ffs(cand) - 1 : j;
+        } else {
+          pj = j;
+        }
+        const double bv = __shfl_sync(FULL, d, pj);
+        const bool stop = !(bv > s_tau);
+        double rjj = 0.0, inv = 0.0;
+        if (!stop) {
+          rjj = sqrt(bv);
+          inv = 1.0 / rjj;
+        }
+        // R[j][a] = S[a][pj] / rjj for the remaining rows, rjj at the pivot
+        const bool other = live && lane != pj;
+        const double ra = other ? S[lane * 32 + pj] * inv : (lane == pj ? rjj : 0.0);
+        if (!stop) {
+          Rc[lane] = other ? ra : 0.0;
+          if (lane < k) Rout[j * k + lane] = ra;
+        }
+        if (lane == 0) {
+          s_stop = stop;
+          s_piv = pj;
+          perm[j] = pj;
+        }
+        if (lane == pj) rem[lane] = 0;
+      }
+      __syncthreads();
+      if (s_stop) {
+        rank = j;
+        break;
+      }
+      // rank-1 update of the remaining block (Rc is 0 outside it)
+      {
+        const double rb = Rc[lane];
+        for (int a = wid; a < k; a += nwarp) {
+          const double ra = Rc[a];
+          if (ra != 0.0 && rb != 0.0) S[a * 32 + lane] = fma(-ra, rb, S[a * 32 + lane]);
+        }
+      }
+      __syncthreads();
+    }
+  }
+  __syncthreads();
+  for (int i = tid; i < k; i += blockDim.x) meta[1 + i] = i < rank ? perm[i] : -1;
+  if (tid == 0) {
+    meta[0] = rank;
+    if (!pivot && rank < k) status_fail(st, NENMF_ERR_NUMERICAL_COLLAPSE, -1);
   }
   __syncthreads();
 }
@@ -133,7 +146,7 @@ __device__ __forceinline__ double hash_uniform(uint64_t a, uint64_t b) {
 template <typename T, int KM>
 __device__ __forceinline__ void trsm_row(const T* __restrict__ in_t, int64_t rows, int k, const double* Rs,
                                          const int* perm, const double* rdiag_inv, int r, int64_t i,
-                                         T* __restrict__ out_t) {
+                                         T* __restrict__ out_t, int64_t row0 = 0) {
   double q[KM];
   // all loads first (independent), then the dependent substitution
 #pragma unroll
@@ -151,187 +164,310 @@ __device__ __forceinline__ void trsm_row(const T* __restrict__ in_t, int64_t row
   }
 #pragma unroll
   for (int l = 0; l < KM; ++l)
-    if (l < k) out_t[(int64_t)l * rows + i] = (T)(l < r ? q[l] : hash_uniform((uint64_t)i, (uint64_t)l));
+    if (l < k) out_t[(int64_t)l * rows + i] = (T)(l < r ? q[l] : hash_uniform((uint64_t)(i + row0), (uint64_t)l));
 }
 
-// Gram partial sum_{i in [r0, r1)} p_i p_i^T of a short-major panel -> out (k*k)
-template <typename T>
-__device__ void block_gram(const T* __restrict__ Pt, int64_t rows, int k, int64_t r0, int64_t r1, double* tile,
-                           double* __restrict__ out) {
-  constexpr int RS = 128;
-  const int kk = k * k;
-  double acc[QC_KMAX * QC_KMAX / 256];
-#pragma unroll
-  for (int t = 0; t < QC_KMAX * QC_KMAX / 256; ++t) acc[t] = 0.0;
-  for (int64_t base = r0; base < r1; base += RS) {
-    const int nr = (int)imin(RS, r1 - base);
-    __syncthreads();
-    for (int idx = threadIdx.x; idx < k * RS; idx += blockDim.x) {
-      const int a = idx / RS, rr = idx - a * RS;
-      tile[a * (RS + 1) + rr] = rr < nr ? (double)Pt[(int64_t)a * rows + base + rr] : 0.0;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int t = 0; t < QC_KMAX * QC_KMAX / 256; ++t) {
-      const int e = threadIdx.x + 256 * t;
-      if (e < kk) {
-        const int a = e / k, b = e - a * k;
-        const double* pa = tile + a * (RS + 1);
-        const double* pb = tile + b * (RS + 1);
-        double s = acc[t];
-        for (int rr = 0; rr < nr; ++rr) s = fma(pa[rr], pb[rr], s);
-        acc[t] = s;
-      }
-    }
-  }
-#pragma unroll
-  for (int t = 0; t < QC_KMAX * QC_KMAX / 256; ++t) {
-    const int e = threadIdx.x + 256 * t;
-    if (e < kk) out[e] = acc[t];
-  }
-}
-
-template <typename T>
-struct QrPanel {
-  T* Pt;
-  int64_t rows;
-  nenmf_device_status* st;
-  double* part;  // [ncta][k*k]
-  double* R;     // k*k
-  int* meta;     // 1 + k
-  T* Q1;         // k * rows
-  int cta0, ncta;
+// ---------------------------------------------------------------------------
+// Decomposed CholeskyQR2: every stage is its own launch so that the Gram
+// matrices can be all-reduced between ranks when the panel is row-sharded
+// (SURVEY 8(e)); on one GPU the same sequence runs back to back.
+//   k_gram_part   Gram partials of row blocks, all SMs      (fixed CTA split)
+//   k_gram_factor fixed-order reduction of the partials (+ optional extra
+//                 all-reduced input) and the one-warp (pivoted) Cholesky
+//   k_trsm        row-parallel triangular solves (+ random completion)
+// Up to two panels per launch (the L- and R-chains of RSI).
+struct PanelSet {
+  const void* in[2];   // short-major panels k x rows[i]
+  void* out[2];
+  int64_t rows[2];
+  int64_t row0[2];     // global index of the first row (random completion hash)
+  int cta0[2], ncta[2];
+  double* part[2];     // [ncta][k*k]
+  double* G[2];        // reduced Gram (k*k); input of the factor when `gin`
+  double* R[2];        // k*k
+  int* meta[2];        // 1 + k: rank, perm
+  int npan;
 };
 
-// Rank-revealing CholeskyQR2 of one or two panels in ONE cooperative launch:
-// Gram partials | leader: reduce + pivoted Cholesky | triangular solves +
-// Gram partials of Q1 | leader: reduce + Cholesky | triangular solves.
-__device__ unsigned long long g_qr_trace[16];
-__device__ __forceinline__ void qr_stamp(int i) {
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    g_qr_trace[i] = t;
+// Gram partials on the FP64 tensor pipe: G = P^T P with DMMA m8n8k4, the
+// row block of the CTA split over its 8 warps in 4-row steps.  The A fragment
+// (8 columns x 4 rows) and the B fragment of the same column block hold the
+// same values, so one fp32->fp64 load per column block feeds both; only the
+// upper-triangle tiles are formed and mirrored (G is exactly symmetric).
+// Warp partials are summed in warp order (deterministic).
+__device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+      : "+d"(d[0]), "+d"(d[1])
+      : "d"(a), "d"(b));
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_gram_part(PanelSet P, int k) {
+  extern __shared__ double qsm[];  // [8 warps][32][32]
+  const int pi = (P.npan > 1 && (int)blockIdx.x >= P.cta0[1]) ? 1 : 0;
+  const int local = (int)blockIdx.x - P.cta0[pi];
+  const int64_t rows = P.rows[pi];
+  const int64_t r0 = (int64_t)local * rows / P.ncta[pi], r1 = (int64_t)(local + 1) * rows / P.ncta[pi];
+  const T* __restrict__ Pt = reinterpret_cast<const T*>(P.in[pi]);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, gq = lane >> 2, tq = lane & 3;
+  const int nb = (k + 7) >> 3;  // 8-column blocks
+  double acc[10][2];
+#pragma unroll
+  for (int t = 0; t < 10; ++t) acc[t][0] = acc[t][1] = 0.0;
+  auto load = [&](int64_t r, double (&f)[4]) {
+    const int64_t row = r + tq;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int col = 8 * b + gq;
+      f[b] = (b < nb && col < k && row < r1) ? (double)__ldg(&Pt[(int64_t)col * rows + row]) : 0.0;
+    }
+  };
+  double fn[4];
+  load(r0 + 4 * wid, fn);  // software pipelined: the next step's loads are in flight during the DMMAs
+  for (int64_t r = r0 + 4 * wid; r < r1; r += 32) {
+    double f[4];
+#pragma unroll
+    for (int b = 0; b < 4; ++b) f[b] = fn[b];
+    if (r + 32 < r1) load(r + 32, fn);
+    int t = 0;
+#pragma unroll
+    for (int ma = 0; ma < 4; ++ma)
+#pragma unroll
+      for (int na = ma; na < 4; ++na, ++t)
+        if (na < nb) dmma(acc[t], f[ma], f[na]);
+  }
+  double* W = qsm + (size_t)wid * 1024;
+  {
+    int t = 0;
+#pragma unroll
+    for (int ma = 0; ma < 4; ++ma)
+#pragma unroll
+      for (int na = ma; na < 4; ++na, ++t) {
+        if (na >= nb) continue;
+        const int i = 8 * ma + gq, j = 8 * na + 2 * tq;
+        W[i * 32 + j] = acc[t][0];
+        W[i * 32 + j + 1] = acc[t][1];
+        W[j * 32 + i] = acc[t][0];
+        W[(j + 1) * 32 + i] = acc[t][1];
+      }
+  }
+  __syncthreads();
+  double* out = P.part[pi] + (int64_t)local * k * k;
+  for (int e = threadIdx.x; e < k * k; e += blockDim.x) {
+    const int a = e / k, b = e - a * k;
+    double v = 0.0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) v += qsm[(size_t)w * 1024 + a * 32 + b];
+    out[e] = v;
   }
 }
 
-// grid-wide barrier over co-resident CTAs (cooperative launch): monotone
-// counter, barrier number `gen` completes at gen * gridDim.x arrivals
-__device__ __forceinline__ void grid_barrier(unsigned* ctr, unsigned gen) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    atomicAdd(ctr, 1u);
-    const unsigned target = gen * gridDim.x;
-    while (true) {
-      unsigned v;
-      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
-      if (v >= target) break;
-      __nanosleep(20);
+// one CTA per panel: G = sum of partials in CTA order (then written to P.G),
+// or G read from P.G when the partials were reduced elsewhere (gin);
+// factorisation into P.R / P.meta
+__global__ void __launch_bounds__(256) k_gram_factor(PanelSet P, int k, int pivot, double tol, int gin,
+                                                     nenmf_device_status* st) {
+  extern __shared__ double qsm[];
+  double* S = qsm;
+  double* Rw = S + k * k;
+  const int pi = blockIdx.x;
+  const int kk = k * k;
+  if (st != nullptr && st->code != 0) {
+    if (threadIdx.x == 0) P.meta[pi][0] = 0;
+    return;
+  }
+  if (gin) {
+    for (int e = threadIdx.x; e < kk; e += blockDim.x) S[e] = P.G[pi][e];
+  } else {
+    const double* part = P.part[pi];
+    const int nc = P.ncta[pi];
+    // 8 independent loads in flight per thread; fixed order (deterministic)
+    for (int e = threadIdx.x; e < kk; e += blockDim.x) {
+      double sv[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) sv[u] = 0.0;
+      int c = 0;
+      for (; c + 8 <= nc; c += 8) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = __ldcg(part + (int64_t)(c + u) * kk + e);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) sv[u] += v[u];
+      }
+      for (; c < nc; ++c) sv[0] += __ldcg(part + (int64_t)c * kk + e);
+      S[e] = ((sv[0] + sv[1]) + (sv[2] + sv[3])) + ((sv[4] + sv[5]) + (sv[6] + sv[7]));
+      if (P.G[pi] != nullptr) P.G[pi][e] = S[e];
     }
   }
   __syncthreads();
+  if (pivot < 0) return;
+  block_factor(S, Rw, k, pivot, tol, P.R[pi], P.meta[pi], st);
 }
 
 template <typename T, int KM>
-__global__ void __launch_bounds__(256) k_qr2(QrPanel<T> P0, QrPanel<T> P1, int npanels, int k, unsigned* bar) {
-  extern __shared__ double qsm[];
-  double* S = qsm;                    // k*k
-  double* R = S + k * k;              // k*k
-  double* tile = R + k * k;           // k * 129
+__global__ void __launch_bounds__(256) k_trsm(PanelSet P, int k, int full_only) {
+  __shared__ double R[QC_KMAX * QC_KMAX];
   __shared__ int perm[QC_KMAX];
   __shared__ double rdinv[QC_KMAX];
-  const bool second = npanels > 1 && (int)blockIdx.x >= P1.cta0;
-  const QrPanel<T>& P = second ? P1 : P0;
-  const int local = (int)blockIdx.x - P.cta0;
-  const int64_t r0 = (int64_t)local * P.rows / P.ncta, r1 = (int64_t)(local + 1) * P.rows / P.ncta;
+  const int pi = (P.npan > 1 && (int)blockIdx.x >= P.cta0[1]) ? 1 : 0;
+  const int local = (int)blockIdx.x - P.cta0[pi];
+  const int r = P.meta[pi][0];
+  if (r <= 0 || (full_only && r < k)) return;
   const int kk = k * k;
+  for (int e = threadIdx.x; e < kk; e += blockDim.x) R[e] = P.R[pi][e];
+  for (int i = threadIdx.x; i < k; i += blockDim.x) perm[i] = P.meta[pi][1 + i];
+  __syncthreads();
+  for (int i = threadIdx.x; i < r; i += blockDim.x) rdinv[i] = 1.0 / R[i * k + perm[i]];
+  __syncthreads();
+  const int64_t rows = P.rows[pi];
+  const int64_t r0 = (int64_t)local * rows / P.ncta[pi], r1 = (int64_t)(local + 1) * rows / P.ncta[pi];
+  const T* in_t = reinterpret_cast<const T*>(P.in[pi]);
+  T* out_t = reinterpret_cast<T*>(P.out[pi]);
+  for (int64_t i = r0 + threadIdx.x; i < r1; i += blockDim.x)
+    trsm_row<T, KM>(in_t, rows, k, R, perm, rdinv, r, i, out_t, P.row0[pi]);
+}
 
-  auto reduce_factor = [&](int pivot, double tol) {
-    if (local == 0) {
-      for (int e = threadIdx.x; e < kk; e += blockDim.x) {
-        double s = 0.0;
-        for (int c = 0; c < P.ncta; ++c) s += P.part[(int64_t)c * kk + e];
-        S[e] = s;
-      }
-      __syncthreads();
-      block_factor(S, R, k, pivot, tol, P.R, P.meta, P.st);
-    }
-  };
-  auto solve_rows = [&](const T* in_t, T* out_t) {
-    for (int e = threadIdx.x; e < kk; e += blockDim.x) R[e] = P.R[e];
-    for (int i = threadIdx.x; i < k; i += blockDim.x) perm[i] = P.meta[1 + i];
-    __syncthreads();
-    const int r = P.meta[0];
-    for (int i = threadIdx.x; i < r; i += blockDim.x) rdinv[i] = 1.0 / R[i * k + perm[i]];
-    __syncthreads();
-    for (int64_t i = r0 + threadIdx.x; i < r1; i += blockDim.x)
-      trsm_row<T, KM>(in_t, P.rows, k, R, perm, rdinv, r, i, out_t);
-    __syncthreads();
-  };
+inline size_t gram_smem(int) { return (size_t)8 * 1024 * sizeof(double); }
+inline size_t factor_smem(int k) { return (size_t)2 * k * k * sizeof(double); }
 
-  qr_stamp(0);
-  block_gram<T>(P.Pt, P.rows, k, r0, r1, tile, P.part + (int64_t)local * kk);  // G1 partials
-  qr_stamp(1);
-  grid_barrier(bar, 1);
-  qr_stamp(2);
-  reduce_factor(1, 1e-14);  // rank-revealing pass
-  qr_stamp(3);
-  grid_barrier(bar, 2);
-  qr_stamp(4);
-  const bool ok = P.meta[0] > 0;
-  if (ok) {
-    solve_rows(P.Pt, P.Q1);
-    qr_stamp(5);
-    __threadfence_block();
-    block_gram<T>(P.Q1, P.rows, k, r0, r1, tile, P.part + (int64_t)local * kk);  // G2 partials
+// CTAs per panel: the whole GPU shared by the panels, >= 256 rows per CTA
+// (the one-CTA factor kernel reduces the per-CTA Gram partials)
+inline void split_ctas(PanelSet& P) {
+  int sms = sm_count();
+  if (sms <= 0) sms = 148;
+  int64_t tot = 0;
+  for (int i = 0; i < P.npan; ++i) tot += P.rows[i];
+  int c0 = 0;
+  for (int i = 0; i < P.npan; ++i) {
+    const int64_t want = imax(1, imin(cdiv(P.rows[i], 256), (int64_t)sms * P.rows[i] / imax(tot, 1)));
+    P.ncta[i] = (int)imax(1, want);
+    P.cta0[i] = c0;
+    c0 += P.ncta[i];
   }
-  qr_stamp(6);
-  grid_barrier(bar, 3);
-  qr_stamp(7);
-  if (ok) reduce_factor(0, 1e-300);  // CholeskyQR2 second pass
-  qr_stamp(8);
-  grid_barrier(bar, 4);
-  qr_stamp(9);
-  if (ok && P.meta[0] == k) solve_rows(P.Q1, P.Pt);
-  qr_stamp(10);
+}
+
+template <typename T>
+int launch_gram_part(PanelSet& P, int k, cudaStream_t s) {
+  const size_t smem = gram_smem(k);
+  NENMF_CUDA_TRY(set_smem(k_gram_part<T>, smem));
+  k_gram_part<T><<<P.cta0[P.npan - 1] + P.ncta[P.npan - 1], 256, smem, s>>>(P, k);
+  NENMF_LAUNCH_CHECK();
+  return NENMF_OK;
+}
+
+int launch_gram_factor(PanelSet& P, int k, int pivot, double tol, int gin, nenmf_device_status* st,
+                       cudaStream_t s) {
+  k_gram_factor<<<P.npan, 256, factor_smem(k), s>>>(P, k, pivot, tol, gin, st);
+  NENMF_LAUNCH_CHECK();
+  return NENMF_OK;
+}
+
+template <typename T>
+int launch_trsm(PanelSet& P, int k, int full_only, cudaStream_t s) {
+  k_trsm<T, QC_KMAX><<<P.cta0[P.npan - 1] + P.ncta[P.npan - 1], 256, 0, s>>>(P, k, full_only);
+  NENMF_LAUNCH_CHECK();
+  return NENMF_OK;
 }
 
 template <typename T>
 int orthonormalize_pair(Arena& ws, T* P0t, int64_t rows0, T* P1t, int64_t rows1, int64_t k,
                         nenmf_device_status* st, cudaStream_t s) {
   if (k < 1 || k > QC_KMAX || rows0 < k || (P1t != nullptr && rows1 < k)) return k > QC_KMAX ? NENMF_ERR_UNSUPPORTED : NENMF_ERR_DIM;
-  const int npan = P1t != nullptr ? 2 : 1;
-  auto ctas = [](int64_t rows) { return (int)imax(1, imin(32, cdiv(rows, 64))); };
-  QrPanel<T> Q[2];
-  const int64_t rowsv[2] = {rows0, rows1};
+  PanelSet P{};
+  P.npan = P1t != nullptr ? 2 : 1;
   T* ptv[2] = {P0t, P1t};
-  int cta0 = 0;
-  for (int i = 0; i < npan; ++i) {
-    Q[i].Pt = ptv[i];
-    Q[i].rows = rowsv[i];
-    Q[i].st = st;
-    Q[i].ncta = ctas(rowsv[i]);
-    Q[i].cta0 = cta0;
-    cta0 += Q[i].ncta;
-    Q[i].part = ws.take<double>((size_t)Q[i].ncta * k * k);
-    Q[i].R = ws.take<double>((size_t)k * k);
-    Q[i].meta = ws.take<int>((size_t)k + 4);
-    Q[i].Q1 = ws.take<T>((size_t)k * rowsv[i]);
+  const int64_t rowsv[2] = {rows0, rows1};
+  T* q1[2] = {nullptr, nullptr};
+  for (int i = 0; i < P.npan; ++i) {
+    P.rows[i] = rowsv[i];
+    P.row0[i] = 0;
   }
-  if (npan == 1) Q[1] = Q[0];
-  unsigned* bar = ws.take<unsigned>(64);
+  split_ctas(P);
+  for (int i = 0; i < P.npan; ++i) {
+    P.part[i] = ws.take<double>((size_t)P.ncta[i] * k * k);
+    P.R[i] = ws.take<double>((size_t)k * k);
+    P.meta[i] = ws.take<int>((size_t)k + 4);
+    q1[i] = ws.take<T>((size_t)k * rowsv[i]);
+    P.G[i] = nullptr;
+  }
   if (ws.base == nullptr) return NENMF_OK;
   if (!ws.ok) return NENMF_ERR_WORKSPACE;
-  NENMF_CUDA_TRY(cudaMemsetAsync(bar, 0, sizeof(unsigned), s));
-  const size_t smem = ((size_t)2 * k * k + (size_t)k * 129) * sizeof(double);
-  int kint = (int)k;
-  void* args[] = {(void*)&Q[0], (void*)&Q[1], (void*)&npan, (void*)&kint, (void*)&bar};
-  NENMF_CUDA_TRY(set_smem(k_qr2<T, 32>, smem));
-  NENMF_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k_qr2<T, 32>, dim3(cta0), dim3(256), args, smem, s));
-  launch_counter_add(1);
+  const int kint = (int)k;
+  // pass 1: rank-revealing pivoted Cholesky of P^T P, Q1 = P Pi R11^-1 (+ completion)
+  for (int i = 0; i < P.npan; ++i) {
+    P.in[i] = ptv[i];
+    P.out[i] = q1[i];
+  }
+  NENMF_TRY(launch_gram_part<T>(P, kint, s));
+  NENMF_TRY(launch_gram_factor(P, kint, 1, 1e-14, 0, st, s));
+  NENMF_TRY(launch_trsm<T>(P, kint, 0, s));
+  // pass 2: Cholesky of Q1^T Q1 (no pivoting), Q = Q1 R2^-1 back into the panel
+  for (int i = 0; i < P.npan; ++i) {
+    P.in[i] = q1[i];
+    P.out[i] = ptv[i];
+  }
+  NENMF_TRY(launch_gram_part<T>(P, kint, s));
+  NENMF_TRY(launch_gram_factor(P, kint, 0, 1e-300, 0, st, s));
+  NENMF_TRY(launch_trsm<T>(P, kint, 1, s));
   return NENMF_OK;
 }
+
+// ---- sharded building blocks (C ABI: nenmf_panel_*) ----------------------
+template <typename T>
+int panel_gram(Arena& ws, const T* Pt, int64_t rows, int64_t k, double* G, cudaStream_t s) {
+  if (k < 1 || k > QC_KMAX || rows < 1) return k > QC_KMAX ? NENMF_ERR_UNSUPPORTED : NENMF_ERR_DIM;
+  PanelSet P{};
+  P.npan = 1;
+  P.rows[0] = rows;
+  split_ctas(P);
+  P.part[0] = ws.take<double>((size_t)P.ncta[0] * k * k);
+  P.R[0] = ws.take<double>((size_t)k * k);
+  P.meta[0] = ws.take<int>((size_t)k + 4);
+  if (ws.base == nullptr) return NENMF_OK;
+  if (!ws.ok) return NENMF_ERR_WORKSPACE;
+  P.in[0] = Pt;
+  P.G[0] = G;
+  NENMF_TRY(launch_gram_part<T>(P, (int)k, s));
+  // reduce only (the factorisation runs after the cross-rank all-reduce):
+  // k_gram_factor with pivot = -1 stops after writing G
+  k_gram_factor<<<1, 256, factor_smem((int)k), s>>>(P, (int)k, -1, 0.0, 0, nullptr);
+  NENMF_LAUNCH_CHECK();
+  return NENMF_OK;
+}
+
+int panel_factor(const double* G, int64_t k, int pivot, double* R, int* meta, nenmf_device_status* st,
+                 cudaStream_t s) {
+  if (k < 1 || k > QC_KMAX) return k > QC_KMAX ? NENMF_ERR_UNSUPPORTED : NENMF_ERR_DIM;
+  PanelSet P{};
+  P.npan = 1;
+  P.G[0] = const_cast<double*>(G);
+  P.R[0] = R;
+  P.meta[0] = meta;
+  return launch_gram_factor(P, (int)k, pivot, pivot ? 1e-14 : 1e-300, 1, st, s);
+}
+
+template <typename T>
+int panel_trsm(const T* Pin_t, int64_t rows, int64_t k, const double* R, const int* meta, T* Pout_t, int64_t row0,
+               int full_only, cudaStream_t s) {
+  if (k < 1 || k > QC_KMAX || rows < 1) return k > QC_KMAX ? NENMF_ERR_UNSUPPORTED : NENMF_ERR_DIM;
+  PanelSet P{};
+  P.npan = 1;
+  P.rows[0] = rows;
+  P.row0[0] = row0;
+  split_ctas(P);
+  P.in[0] = Pin_t;
+  P.out[0] = Pout_t;
+  P.R[0] = const_cast<double*>(R);
+  P.meta[0] = const_cast<int*>(meta);
+  return launch_trsm<T>(P, (int)k, full_only, s);
+}
+
+template int panel_gram<double>(Arena&, const double*, int64_t, int64_t, double*, cudaStream_t);
+template int panel_gram<float>(Arena&, const float*, int64_t, int64_t, double*, cudaStream_t);
+template int panel_trsm<double>(const double*, int64_t, int64_t, const double*, const int*, double*, int64_t, int,
+                                cudaStream_t);
+template int panel_trsm<float>(const float*, int64_t, int64_t, const double*, const int*, float*, int64_t, int,
+                               cudaStream_t);
 
 template <typename T>
 int orthonormalize_cholqr(Arena& ws, T* Pt, int64_t rows, int64_t k, nenmf_device_status* st, cudaStream_t s) {
@@ -348,6 +484,4 @@ template int orthonormalize_cholqr<float>(Arena&, float*, int64_t, int64_t, nenm
 
 }  // namespace nenmf
 
-extern "C" int nenmf_debug_qr_trace(unsigned long long* host_out) {
-  return cudaMemcpyFromSymbol(host_out, nenmf::g_qr_trace, sizeof(unsigned long long) * 16) == cudaSuccess ? 0 : 6;
-}
+

@@ -19,6 +19,15 @@ template <typename T>
 int compress(Arena& ws, const T* X, int64_t n, int64_t m, int64_t ldx, const T* L, const T* Rt, int64_t nu, T* XL,
              T* XRt, cudaStream_t s, const uint8_t* Xpre = nullptr);
 
+// decomposed CholeskyQR2 stages (qr.cu) for row-sharded panels
+template <typename T>
+int panel_gram(Arena& ws, const T* Pt, int64_t rows, int64_t k, double* G, cudaStream_t s);
+int panel_factor(const double* G, int64_t k, int pivot, double* R, int* meta, nenmf_device_status* st,
+                 cudaStream_t s);
+template <typename T>
+int panel_trsm(const T* Pin_t, int64_t rows, int64_t k, const double* R, const int* meta, T* Pout_t, int64_t row0,
+               int full_only, cudaStream_t s);
+
 // FP32 tensor-core pass over a pre-split X (dual_tc.cu)
 bool tc_pass_eligible(int64_t n, int64_t m, int64_t k);
 size_t tc_presplit_bytes(int64_t n, int64_t m);
