@@ -204,3 +204,32 @@ def compress(X, L, Rt, XL, XRt, Xp=None) -> None:
         rc = lib.nenmf_compress(code, X.data_ptr(), n, m, X.stride(0), L.data_ptr(), Rt.data_ptr(), nu,
                                 XL.data_ptr(), XRt.data_ptr(), ws.data_ptr(), ws.numel(), _lib.stream_handle())
     _lib.check(rc, "compress_problem")
+
+
+# ------------------------------------------- CholeskyQR2 stages (row shards)
+def panel_gram(Pt, G) -> None:
+    """G (k x k, float64) = P^T P of the local rows of a short-major panel."""
+    lib, _ = _lib.require_device()
+    code = _lib.code_of(_dt(Pt))
+    k, rows = Pt.shape
+    ws = _lib.workspace(lib.nenmf_panel_gram_workspace_bytes(code, rows, k))
+    rc = lib.nenmf_panel_gram(code, Pt.data_ptr(), rows, k, G.data_ptr(), ws.data_ptr(), ws.numel(),
+                              _lib.stream_handle())
+    _lib.check(rc, "panel_gram")
+
+
+def panel_factor(G, pivot: bool, R, meta, status) -> None:
+    lib, _ = _lib.require_device()
+    k = G.shape[0]
+    rc = lib.nenmf_panel_factor(G.data_ptr(), k, 1 if pivot else 0, R.data_ptr(), meta.data_ptr(),
+                                _lib.status_ptr(status), _lib.stream_handle())
+    _lib.check(rc, "panel_factor")
+
+
+def panel_trsm(Pin, R, meta, Pout, row0: int, full_rank_only: bool) -> None:
+    lib, _ = _lib.require_device()
+    code = _lib.code_of(_dt(Pin))
+    k, rows = Pin.shape
+    rc = lib.nenmf_panel_trsm(code, Pin.data_ptr(), rows, k, R.data_ptr(), meta.data_ptr(), Pout.data_ptr(),
+                              int(row0), 1 if full_rank_only else 0, _lib.stream_handle())
+    _lib.check(rc, "panel_trsm")

@@ -190,9 +190,60 @@ class _DeviceLoop:
         return _lib.to_host(self.Gt).T.copy(), _lib.to_host(self.F)
 
 
+class _ShardedDeviceLoop(_DeviceLoop):
+    """Device state of a row-sharded run (sharded.py): this rank holds rows
+    [row0, row0 + n_r) of X; the compressed operands are replicated, so the
+    half-steps are the 1-GPU ones and every rank computes the same G and F.
+    ||X|| and the objective are all-reduced over the shards."""
+
+    def __init__(self, X_local, n: int, row0: int, init: FactorPair, L, Rt, XL, XRt, comm):
+        _, torch = _lib.require_device()
+        self.torch = torch
+        self.X = X_local if X_local.is_contiguous() else X_local.contiguous()
+        self.dtype = "fp64" if X_local.dtype == torch.float64 else "fp32"
+        self.n, self.m = int(n), int(X_local.shape[1])
+        self.row0, self.n_r = int(row0), int(X_local.shape[0])
+        self.p = init.p
+        self.sketch = "sharded"  # compressed half-steps
+        self.scal = torch.zeros(4, dtype=torch.float64, device="cuda")
+        self.status = _lib.new_status(_STATUS_CAP)
+        self.pending = []
+        self.comm = comm
+        self._ops_in = (L, Rt, XL, XRt)
+
+    def norm_x(self) -> float:
+        self.scal[0:1].zero_()
+        _ops.sumsq(self.X, self.scal[0:1])
+        self.comm.all_reduce(self.scal[0:1])
+        return math.sqrt(self.scal[0].item())
+
+    def prepare(self, init: FactorPair) -> None:
+        torch = self.torch
+        G = init.G
+        self.Gt = (_lib.to_device(G, self.dtype).t().contiguous() if hasattr(G, "is_cuda")
+                   else _lib.to_device(np.ascontiguousarray(np.asarray(G, dtype=np.float64).T), self.dtype))
+        self.F = _lib.to_device(init.F, self.dtype)
+        self.Gt_alt = torch.empty_like(self.Gt)
+        self.F_alt = torch.empty_like(self.F)
+        self.L, self.Rt, self.XL, self.XRt = self._ops_in
+        nu = self.L.shape[0]
+        self.FR = torch.empty((self.p, nu), dtype=self.X.dtype, device="cuda")
+        self.fr_ready = False
+        self.GLt = torch.empty((self.p, nu), dtype=self.X.dtype, device="cuda")
+
+    def objective(self) -> float:
+        Gl = self.Gt[:, self.row0:self.row0 + self.n_r].contiguous()
+        self.scal[1:2].zero_()
+        _ops.residual_sumsq(self.X, Gl, self.F, self.scal[1:2])
+        self.comm.all_reduce(self.scal[1:2])
+        return math.sqrt(self.scal[1].item())
+
+
 def _run_outer(X, init: FactorPair, cfg: OuterConfig, observer, clock, sketch, dtype: str,
-               return_device: bool = False) -> FactorPair:
-    if hasattr(X, "is_cuda") and X.is_cuda:
+               return_device: bool = False, run: _DeviceLoop | None = None) -> FactorPair:
+    if run is not None:
+        n, m = run.n, run.m
+    elif hasattr(X, "is_cuda") and X.is_cuda:
         n, m = X.shape
     else:
         X = as_matrix(X, "X")
@@ -204,7 +255,8 @@ def _run_outer(X, init: FactorPair, cfg: OuterConfig, observer, clock, sketch, d
         raise DimensionError(
             f"sketch shapes L {np.shape(sketch.L)}, R {np.shape(sketch.R)} do not match "
             f"data {n}x{m} at target rank {sketch.nu}")
-    run = _DeviceLoop(X, init, sketch, dtype)
+    if run is None:
+        run = _DeviceLoop(X, init, sketch, dtype)
     norm_x = run.norm_x()
     if norm_x == 0.0:
         raise ZeroMatrixError("cannot factorize the zero matrix")

@@ -1,0 +1,241 @@
+"""Row-sharded compressed NeNMF across GPUs.
+
+One process per GPU (``torchrun``), X split into row blocks: rank r holds
+rows [row0_r, row0_r + n_r) of X (``row_block``).  The exchange steps, all
+through ``torch.distributed`` (NCCL over NVLink on GPUs), carry only the small
+sketch-sized partials named by the north star:
+
+* RSI pass (compression.py:134-139): Y = X_r A is local (this rank's rows of
+  the n-panel); Z = sum_r X_r^T B_r is ONE all-reduce of the nu x m partial
+  per pass (2q + 2 per sketch).
+* n-panel orthonormalisation: CholeskyQR2 whose two nu x nu Gram matrices are
+  all-reduced (fp64); the factorisation is replicated and identical on every
+  rank; random completion columns are keyed by the global row index, so the
+  shards reproduce the 1-GPU panel.
+* m-panel orthonormalisation: replicated (identical input, deterministic
+  kernel -> bit-identical on every rank).
+* compression (compression.py:179-188): X_L = sum_r L_r X_r, one nu x m
+  all-reduce; X_R stays row-local.
+* factorization (factorize.py:197-213): X_R^T and L are all-gathered once
+  (nu x n each) and the outer loop then runs replicated (every rank holds the
+  same G and F; no per-step traffic); the reported RRE uses the sharded
+  ||X_r - G_r F||^2 and ||X_r||^2, one all-reduced scalar each.
+
+The local arithmetic goes through an ops backend: ``DeviceOps`` (the C-ABI
+kernels; the product path) by default.  The CPU tests substitute a NumPy
+backend to check this exchange logic with ``gloo`` at world size 2.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib, _ops
+from .compression import SketchPair, SUBSPACE_ITERATION, _check_iteration_inputs, sketch_draws
+from .errors import DimensionError, raise_for_status
+
+
+def row_block(n: int, world: int, rank: int) -> tuple[int, int]:
+    """(row0, rows) of rank ``rank`` in a balanced split of n rows."""
+    r0 = rank * n // world
+    r1 = (rank + 1) * n // world
+    return r0, r1 - r0
+
+
+class Comm:
+    """The collectives of the sharded path over a torch.distributed group."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.size = dist.get_world_size(group)
+
+    def all_reduce(self, t):
+        if self.size > 1:
+            self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM, group=self.group)
+        return t
+
+    def all_gather_cols(self, local, n: int):
+        """(k x n_r) blocks in rank order -> (k x n); ragged blocks are padded."""
+        torch = _lib.torch_mod()
+        if self.size == 1:
+            return local
+        counts = [row_block(n, self.size, r)[1] for r in range(self.size)]
+        w = max(counts)
+        k = local.shape[0]
+        pad = torch.zeros((k, w), dtype=local.dtype, device=local.device)
+        pad[:, : local.shape[1]] = local
+        parts = [torch.empty_like(pad) for _ in range(self.size)]
+        self.dist.all_gather(parts, pad, group=self.group)
+        return torch.cat([p[:, :c] for p, c in zip(parts, counts)], dim=1).contiguous()
+
+
+class DeviceOps:
+    """Local arithmetic of a shard on its GPU (libnenmf_b200 kernels)."""
+
+    def __init__(self):
+        _, self.torch = _lib.require_device()
+
+    def tensor(self, a, like):
+        return _lib.to_device(np.ascontiguousarray(a), "fp64" if like.dtype == self.torch.float64 else "fp32")
+
+    def empty(self, shape, like, dtype=None):
+        return self.torch.empty(shape, dtype=dtype or like.dtype, device=like.device)
+
+    def prepare(self, X, k):
+        return _ops.prepare_x(X, k)
+
+    def dual_pass(self, X, Xp, At, Bt):
+        """(At X^T, Bt X): this shard's rows of X A and its partial of X^T B."""
+        n, m = X.shape
+        k = At.shape[0]
+        Yt = self.empty((k, n), X)
+        Zt = self.empty((k, m), X)
+        if Xp is not None:
+            _ops.dual_pass_prepared(Xp, n, m, At, Bt, Yt, Zt)
+        else:
+            _ops.dual_pass(X, At, Bt, Yt, Zt)
+        return Yt, Zt
+
+    def gram(self, Pt):
+        k = Pt.shape[0]
+        G = self.torch.empty((k, k), dtype=self.torch.float64, device=Pt.device)
+        _ops.panel_gram(Pt, G)
+        return G
+
+    def factor(self, G, pivot, status):
+        k = G.shape[0]
+        R = self.torch.empty((k, k), dtype=self.torch.float64, device=G.device)
+        meta = self.torch.empty(k + 4, dtype=self.torch.int32, device=G.device)
+        _ops.panel_factor(G, pivot, R, meta, status)
+        return R, meta
+
+    def trsm(self, Pin, R, meta, Pout, row0, full_rank_only):
+        _ops.panel_trsm(Pin, R, meta, Pout, row0, full_rank_only)
+
+    def qr(self, Pt, status):
+        _ops.orthonormalize(Pt, status)
+
+    def new_status(self):
+        return _lib.new_status()
+
+    def check_status(self, status, what):
+        st = _lib.read_status(status)[0]
+        if st["code"] != 0:
+            raise_for_status(int(st["code"]), int(st["iteration"]), what)
+
+    def sumsq(self, X):
+        out = self.torch.zeros(1, dtype=self.torch.float64, device=X.device)
+        _ops.sumsq(X, out)
+        return out
+
+    def residual_sumsq(self, X, Gt, F):
+        out = self.torch.zeros(1, dtype=self.torch.float64, device=X.device)
+        _ops.residual_sumsq(X, Gt, F, out)
+        return out
+
+
+def _qr_rows(ops, comm: Comm, Pt, row0: int, status):
+    """CholeskyQR2 of a row-sharded panel (this rank's columns Pt, k x n_r),
+    in place: two Gram all-reduces, replicated factorisations."""
+    Q1 = ops.empty(Pt.shape, Pt)
+    G = comm.all_reduce(ops.gram(Pt))
+    R, meta = ops.factor(G, True, status)
+    ops.trsm(Pt, R, meta, Q1, row0, False)
+    G2 = comm.all_reduce(ops.gram(Q1))
+    R2, meta2 = ops.factor(G2, False, status)
+    ops.trsm(Q1, R2, meta2, Pt, row0, True)
+    return Pt
+
+
+@dataclass
+class ShardedSketch:
+    """This rank's part of a sketch: L_r (nu x n_r, its columns of L) and the
+    replicated R^T (nu x m)."""
+
+    L_local: object
+    Rt: object
+    n: int
+    row0: int
+    nu: int
+    q: int
+    seed: int
+    prepared: object = None  # the prepared copy of X_r (FP32), reused by compress
+
+
+def subspace_iteration_pair_sharded(X_local, n: int, nu: int, q: int, seed: int, *, comm: Comm | None = None,
+                                    ops=None) -> ShardedSketch:
+    """Algorithm 2 (compression.py:120-141) on a row-sharded X: the same
+    sequence of products and orthonormalisations as the 1-GPU
+    ``subspace_iteration_pair``, with the exchanges listed in the module doc."""
+    comm = comm or Comm()
+    ops = ops or DeviceOps()
+    n_r, m = X_local.shape
+    row0, expect = row_block(n, comm.size, comm.rank)
+    if expect != n_r:
+        raise DimensionError(f"rank {comm.rank} holds {n_r} rows, row_block gives {expect}")
+    nz = ops.sumsq(X_local)
+    comm.all_reduce(nz)
+    _check_iteration_inputs(n, m, nu, q, bool(float(nz[0]) > 0.0))
+    omega_l, omega_r = sketch_draws(n, m, nu, seed)          # every rank draws the full stream
+    Olt = ops.tensor(omega_l.T, X_local)                      # Omega_L^T (nu x m), replicated
+    Orl = ops.tensor(omega_r[:, row0:row0 + n_r], X_local)   # this rank's columns of Omega_R
+    Xp = ops.prepare(X_local, nu)
+    status = ops.new_status()
+    # start: L = (X Omega_L)^T (local columns), R^T = Omega_R X (all-reduced)
+    L, Rt = ops.dual_pass(X_local, Xp, Olt, Orl)
+    comm.all_reduce(Rt)
+    _qr_rows(ops, comm, L, row0, status)
+    ops.qr(Rt, status)
+    for _ in range(q):
+        trow, tcol = ops.dual_pass(X_local, Xp, Rt, L)   # X Q_row (local), X^T Q_col (partial)
+        comm.all_reduce(tcol)
+        ops.qr(tcol, status)
+        _qr_rows(ops, comm, trow, row0, status)
+        L, Rt = ops.dual_pass(X_local, Xp, tcol, trow)
+        comm.all_reduce(Rt)
+        _qr_rows(ops, comm, L, row0, status)
+        ops.qr(Rt, status)
+    ops.check_status(status, "subspace iteration")
+    return ShardedSketch(L_local=L, Rt=Rt, n=n, row0=row0, nu=nu, q=q, seed=seed, prepared=Xp)
+
+
+def compress_problem_sharded(X_local, sketch: ShardedSketch, *, comm: Comm | None = None, ops=None):
+    """(X_L (nu x m, all-reduced), X_R^T local columns (nu x n_r))."""
+    comm = comm or Comm()
+    ops = ops or DeviceOps()
+    XRt, XL = ops.dual_pass(X_local, sketch.prepared, sketch.Rt, sketch.L_local)
+    comm.all_reduce(XL)
+    return XL, XRt
+
+
+def gather_sketch(sketch: ShardedSketch, *, comm: Comm | None = None) -> SketchPair:
+    """The full SketchPair (host NumPy, like the 1-GPU API) from the shards."""
+    comm = comm or Comm()
+    L = comm.all_gather_cols(sketch.L_local, sketch.n)
+    pair = SketchPair(L=_lib.to_host(L), R=np.ascontiguousarray(_lib.to_host(sketch.Rt).T), nu=sketch.nu,
+                      scheme=SUBSPACE_ITERATION, q=sketch.q, seed=sketch.seed)
+    return pair
+
+
+def factorize_compressed_sharded(X_local, n: int, sketch: ShardedSketch, init, cfg=None, observer=None, clock=None,
+                                 *, comm: Comm | None = None, return_device: bool = False):
+    """Compressed NeNMF (factorize.py:197-213) on a row-sharded X: sharded
+    compression, one all-gather of X_R^T and of L, then the replicated outer
+    loop of ``factorize_compressed``; RRE from all-reduced shard residuals.
+    ``init`` holds the FULL initial factors (the same on every rank)."""
+    from .factorize import OuterConfig, _run_outer, _ShardedDeviceLoop
+
+    comm = comm or Comm()
+    cfg = cfg or OuterConfig()
+    XL, XRt_local = compress_problem_sharded(X_local, sketch, comm=comm)
+    XRt = comm.all_gather_cols(XRt_local, n)
+    L = comm.all_gather_cols(sketch.L_local, n)
+    run = _ShardedDeviceLoop(X_local, n, sketch.row0, init, L, sketch.Rt, XL, XRt, comm)
+    return _run_outer(X_local, init, cfg, observer, clock, None, run.dtype, return_device, run=run)
