@@ -191,6 +191,25 @@ int nenmf_compress(int dtype, const void* X, int64_t n, int64_t m, int64_t ldx,
                    const void* L, const void* Rt, int64_t nu, void* XL, void* XRt,
                    void* ws, size_t ws_bytes, void* stream);
 
+/* ---- the reference's Gaussian sketch draws, on the device ----------------
+ * Omega_L (m x nu) then Omega_R (nu x n) from ONE numpy.random.default_rng
+ * (seed).standard_normal stream (compression.py:130-132), bit-identical to
+ * NumPy: PCG64 state/increment as 128-bit halves (numpy PCG64(seed).state),
+ * `tables` = NumPy's ziggurat tables fi[256], wi[256] (double), ki[256]
+ * (uint64) in device memory.  Writes omega_l_t = Omega_L^T (nu x m) and
+ * omega_r (nu x n) in `dtype`; *ok (device int) = 1 on success, 0 if the
+ * chunked walk could not be stitched (the caller redraws on the host).
+ * tails (device, 1 + 2 * nenmf_sketch_tail_capacity entries): [count] then
+ * (draw index, u53 << 1 | negative) of every draw from the ziggurat tail;
+ * the caller rewrites those values as +-(r + (-log1p(-u53 2^-53)) / r) with
+ * the C library's log1p (CUDA's log1p may differ from it by one ulp). */
+size_t nenmf_sketch_draws_workspace_bytes(int64_t n, int64_t m, int64_t nu);
+int64_t nenmf_sketch_tail_capacity(int64_t n, int64_t m, int64_t nu);
+int nenmf_sketch_draws(int dtype, const void* tables, uint64_t state_lo, uint64_t state_hi,
+                       uint64_t inc_lo, uint64_t inc_hi, int64_t n, int64_t m, int64_t nu,
+                       void* omega_l_t, void* omega_r, int* ok, unsigned long long* tails,
+                       void* ws, size_t ws_bytes, void* stream);
+
 /* ---- stages of the orthonormalisation, for row-sharded panels ----------
  * nenmf_orthonormalize is CholeskyQR2 (rank-revealing first pass).  When a
  * tall panel is split by rows across ranks, the caller runs its stages with

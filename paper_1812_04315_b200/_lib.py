@@ -54,6 +54,10 @@ _SIGS = {
     "nenmf_rsi_workspace_bytes": (_sz, [_i32, _i64, _i64, _i64]),
     "nenmf_rsi": (_i32, [_i32, _vp, _i64, _i64, _i64, _vp, _vp, _i64, _i32, _vp, _vp, _vp, _vp, _sz, _vp]),
     "nenmf_compress": (_i32, [_i32, _vp, _i64, _i64, _i64, _vp, _vp, _i64, _vp, _vp, _vp, _sz, _vp]),
+    "nenmf_sketch_draws_workspace_bytes": (_sz, [_i64, _i64, _i64]),
+    "nenmf_sketch_tail_capacity": (_i64, [_i64, _i64, _i64]),
+    "nenmf_sketch_draws": (_i32, [_i32, _vp, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, _i64, _i64, _i64,
+                                  _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
     "nenmf_panel_gram_workspace_bytes": (_sz, [_i32, _i64, _i64]),
     "nenmf_panel_gram": (_i32, [_i32, _vp, _i64, _i64, _vp, _vp, _sz, _vp]),
     "nenmf_panel_factor": (_i32, [_vp, _i64, _i32, _vp, _vp, _vp, _vp]),

@@ -10,6 +10,7 @@ the L-chain and the R-chain from one read of X; TSQR in shared memory).
 
 from __future__ import annotations
 
+import math
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -85,20 +86,117 @@ def sketch_draws(n: int, m: int, nu: int, seed: int):
     return omega_l, omega_r
 
 
-def rsi_device(Xd, nu: int, q: int, seed: int, prepared=None):
+_ZIG_TABLES: dict = {}
+# ziggurat tail constants of NumPy's random_standard_normal
+_ZIG_R = 3.6541528853610087963519472518
+_ZIG_INV_R = 0.27366123732975827203338247596
+
+
+def _numpy_ziggurat_tables():
+    """NumPy's standard_normal ziggurat tables (fi, wi: double[256]; ki:
+    uint64[256]) read from the installed NumPy build (the reference's RNG
+    dependency), or None if they cannot be located and checked."""
+    if "host" in _ZIG_TABLES:
+        return _ZIG_TABLES["host"]
+    import os
+    import struct
+
+    import numpy.random
+
+    tabs = None
+    try:
+        d = os.path.dirname(numpy.random.__file__)
+        for name in sorted(os.listdir(d)):
+            if not (name.startswith("_generator") and name.endswith(".so")):
+                continue
+            blob = open(os.path.join(d, name), "rb").read()
+            i = blob.find(struct.pack("<d", 8.68362706080130616677e-16))  # wi[0]
+            if i < 2048:
+                continue
+            fi = np.frombuffer(blob[i - 2048:i], dtype="<f8")
+            wi = np.frombuffer(blob[i:i + 2048], dtype="<f8")
+            ki = np.frombuffer(blob[i + 2048:i + 4096], dtype="<u8")
+            if fi[0] == 1.0 and 0.97 < fi[1] < 0.98 and ki[0] == 0x000EF33D8025EF6A and ki[1] == 0 \
+                    and np.all(np.diff(fi) < 0):
+                tabs = np.concatenate([fi.view(np.uint64), wi.view(np.uint64), ki]).copy()
+                break
+    except OSError:
+        tabs = None
+    _ZIG_TABLES["host"] = tabs
+    return tabs
+
+
+def sketch_draws_device(n: int, m: int, nu: int, seed: int, dtype: str):
+    """The draws of ``sketch_draws`` generated on the device (nenmf_sketch_draws,
+    bit-identical to NumPy): (Omega_L^T (nu x m), Omega_R (nu x n), ok flag),
+    or None when NumPy's ziggurat tables are not available."""
+    lib, torch = _lib.require_device()
+    tabs = _numpy_ziggurat_tables()
+    if tabs is None:
+        return None
+    dev = torch.cuda.current_device()
+    dt = _ZIG_TABLES.get(dev)
+    if dt is None:
+        dt = _ZIG_TABLES[dev] = torch.from_numpy(tabs.view(np.int64).copy()).to("cuda")
+    st = np.random.PCG64(check_seed(seed)).state["state"]
+    s, inc = int(st["state"]), int(st["inc"])
+    M64 = (1 << 64) - 1
+    tdt = _lib.torch_dtype(dtype)
+    olt = torch.empty((nu, m), dtype=tdt, device="cuda")
+    orr = torch.empty((nu, n), dtype=tdt, device="cuda")
+    ok = torch.zeros(1, dtype=torch.int32, device="cuda")
+    cap = int(lib.nenmf_sketch_tail_capacity(n, m, nu))
+    tails = torch.empty(1 + 2 * cap, dtype=torch.int64, device="cuda")
+    ws = _lib.workspace(lib.nenmf_sketch_draws_workspace_bytes(n, m, nu))
+    rc = lib.nenmf_sketch_draws(_lib.code_of(dtype), dt.data_ptr(), s & M64, s >> 64, inc & M64, inc >> 64, n, m,
+                                nu, olt.data_ptr(), orr.data_ptr(), ok.data_ptr(), tails.data_ptr(), ws.data_ptr(),
+                                ws.numel(), _lib.stream_handle())
+    _lib.check(rc, "sketch_draws")
+    # the tail draws with the C library's log1p (compression.py:131-132 -> NumPy's
+    # random_standard_normal): a few hundred values, rewritten in place
+    cnt = int(tails[0].item())
+    if 0 < cnt <= cap:
+        rec = tails[1:1 + 2 * cnt].cpu().numpy().view(np.uint64).reshape(cnt, 2)
+        idx = rec[:, 0].astype(np.int64)
+        u = (rec[:, 1] >> np.uint64(1)).astype(np.float64) * (1.0 / 9007199254740992.0)
+        neg = (rec[:, 1] & np.uint64(1)).astype(bool)
+        xx = np.array([-_ZIG_INV_R * math.log1p(-v) for v in u])
+        val = np.where(neg, -(_ZIG_R + xx), _ZIG_R + xx)
+        nl = m * nu
+        isl = idx < nl
+        tv = torch.from_numpy(val).to(device="cuda", dtype=tdt)
+        if isl.any():
+            il = torch.from_numpy(idx[isl]).cuda()
+            olt.view(-1).index_put_(((il % nu) * m + il // nu,), tv[torch.from_numpy(isl).cuda()])
+        if (~isl).any():
+            ir = torch.from_numpy(idx[~isl] - nl).cuda()
+            orr.view(-1).index_put_((ir,), tv[torch.from_numpy(~isl).cuda()])
+    return olt, orr, ok
+
+
+def rsi_device(Xd, nu: int, q: int, seed: int, prepared=None, draws=None):
     """Device RSI on a resident X (CUDA tensor).  Returns (L, Rt, status)
-    tensors without synchronising; Rt is R transposed (nu x m).  ``prepared``
-    is an optional ``_ops.prepare_x`` copy of Xd (made once, reused by the
-    compression pass)."""
+    tensors; Rt is R transposed (nu x m).  ``prepared`` is an optional
+    ``_ops.prepare_x`` copy of Xd (made once, reused by the compression pass).
+    The Gaussian draws are made on the device (bit-identical to NumPy's
+    stream); in the never-observed case that the device stream cannot be
+    stitched, they are redrawn on the host and the sketch recomputed."""
     _, torch = _lib.require_device()
     n, m = Xd.shape
-    omega_l, omega_r = sketch_draws(n, m, nu, seed)
     dtype = "fp64" if Xd.dtype == torch.float64 else "fp32"
-    om_lt = _lib.to_device(np.ascontiguousarray(omega_l.T), dtype)
-    om_r = _lib.to_device(omega_r, dtype)
+    dev = draws if draws is not None else sketch_draws_device(n, m, nu, seed, dtype)
     L = torch.empty((nu, n), dtype=Xd.dtype, device="cuda")
     Rt = torch.empty((nu, m), dtype=Xd.dtype, device="cuda")
     status = _lib.new_status()
+    if dev is not None:
+        om_lt, om_r, ok = dev
+        _ops.rsi(Xd, om_lt, om_r, q, L, Rt, status, Xp=prepared)
+        if bool(ok.item()):
+            return L, Rt, status
+    omega_l, omega_r = sketch_draws(n, m, nu, seed)
+    om_lt = _lib.to_device(np.ascontiguousarray(omega_l.T), dtype)
+    om_r = _lib.to_device(omega_r, dtype)
+    status.zero_()
     _ops.rsi(Xd, om_lt, om_r, q, L, Rt, status, Xp=prepared)
     return L, Rt, status
 

@@ -34,7 +34,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _lib, _ops
-from .compression import SketchPair, SUBSPACE_ITERATION, _check_iteration_inputs, sketch_draws
+from .compression import SketchPair, SUBSPACE_ITERATION, _check_iteration_inputs, sketch_draws, sketch_draws_device
 from .errors import DimensionError, raise_for_status
 
 
@@ -90,6 +90,17 @@ class DeviceOps:
 
     def prepare(self, X, k):
         return _ops.prepare_x(X, k)
+
+    def draws(self, n, m, nu, seed, like):
+        dtype = "fp64" if like.dtype == self.torch.float64 else "fp32"
+        dev = sketch_draws_device(n, m, nu, seed, dtype)
+        if dev is not None:
+            return dev
+        omega_l, omega_r = sketch_draws(n, m, nu, seed)
+        return self.tensor(omega_l.T, like), self.tensor(omega_r, like), None
+
+    def draws_ok(self, ok):
+        return ok is None or bool(ok.item())
 
     def dual_pass(self, X, Xp, At, Bt):
         """(At X^T, Bt X): this shard's rows of X A and its partial of X^T B."""
@@ -154,6 +165,31 @@ def _qr_rows(ops, comm: Comm, Pt, row0: int, status):
     return Pt
 
 
+def _rsi_loop(X_local, q, comm, ops, row0, Olt, Orl, Xp):
+    status = ops.new_status()
+    # start: L = (X Omega_L)^T (local columns), R^T = Omega_R X (all-reduced)
+    L, Rt = ops.dual_pass(X_local, Xp, Olt, Orl)
+    comm.all_reduce(Rt)
+    _qr_rows(ops, comm, L, row0, status)
+    ops.qr(Rt, status)
+    for _ in range(q):
+        trow, tcol = ops.dual_pass(X_local, Xp, Rt, L)   # X Q_row (local), X^T Q_col (partial)
+        comm.all_reduce(tcol)
+        ops.qr(tcol, status)
+        _qr_rows(ops, comm, trow, row0, status)
+        L, Rt = ops.dual_pass(X_local, Xp, tcol, trow)
+        comm.all_reduce(Rt)
+        _qr_rows(ops, comm, L, row0, status)
+        ops.qr(Rt, status)
+    return L, Rt, status
+
+
+def _rsi_with(X_local, n, nu, q, seed, comm, ops, row0, Olt, Orl, Xp):
+    L, Rt, status = _rsi_loop(X_local, q, comm, ops, row0, Olt, Orl, Xp)
+    ops.check_status(status, "subspace iteration")
+    return ShardedSketch(L_local=L, Rt=Rt, n=n, row0=row0, nu=nu, q=q, seed=seed, prepared=Xp)
+
+
 @dataclass
 class ShardedSketch:
     """This rank's part of a sketch: L_r (nu x n_r, its columns of L) and the
@@ -183,25 +219,15 @@ def subspace_iteration_pair_sharded(X_local, n: int, nu: int, q: int, seed: int,
     nz = ops.sumsq(X_local)
     comm.all_reduce(nz)
     _check_iteration_inputs(n, m, nu, q, bool(float(nz[0]) > 0.0))
-    omega_l, omega_r = sketch_draws(n, m, nu, seed)          # every rank draws the full stream
-    Olt = ops.tensor(omega_l.T, X_local)                      # Omega_L^T (nu x m), replicated
-    Orl = ops.tensor(omega_r[:, row0:row0 + n_r], X_local)   # this rank's columns of Omega_R
+    # every rank draws the full stream (compression.py:130-132), on the device when it can
+    Olt, Or, ok = ops.draws(n, m, nu, seed, X_local)
+    Orl = Or[:, row0:row0 + n_r].contiguous()                 # this rank's columns of Omega_R
     Xp = ops.prepare(X_local, nu)
-    status = ops.new_status()
-    # start: L = (X Omega_L)^T (local columns), R^T = Omega_R X (all-reduced)
-    L, Rt = ops.dual_pass(X_local, Xp, Olt, Orl)
-    comm.all_reduce(Rt)
-    _qr_rows(ops, comm, L, row0, status)
-    ops.qr(Rt, status)
-    for _ in range(q):
-        trow, tcol = ops.dual_pass(X_local, Xp, Rt, L)   # X Q_row (local), X^T Q_col (partial)
-        comm.all_reduce(tcol)
-        ops.qr(tcol, status)
-        _qr_rows(ops, comm, trow, row0, status)
-        L, Rt = ops.dual_pass(X_local, Xp, tcol, trow)
-        comm.all_reduce(Rt)
-        _qr_rows(ops, comm, L, row0, status)
-        ops.qr(Rt, status)
+    L, Rt, status = _rsi_loop(X_local, q, comm, ops, row0, Olt, Orl, Xp)
+    if not ops.draws_ok(ok):  # device stream not stitched (never observed): host draws, same sketch
+        omega_l, omega_r = sketch_draws(n, m, nu, seed)
+        return _rsi_with(X_local, n, nu, q, seed, comm, ops, row0, ops.tensor(omega_l.T, X_local),
+                         ops.tensor(omega_r[:, row0:row0 + n_r], X_local), Xp)
     ops.check_status(status, "subspace iteration")
     return ShardedSketch(L_local=L, Rt=Rt, n=n, row0=row0, nu=nu, q=q, seed=seed, prepared=Xp)
 

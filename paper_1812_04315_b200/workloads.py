@@ -129,3 +129,41 @@ def rsi_flops(n: int, m: int, q: int, nu: int) -> int:
 
 def snr_db(clean: np.ndarray, noisy: np.ndarray) -> float:
     return 10.0 * math.log10((np.linalg.norm(clean) / np.linalg.norm(noisy - clean)) ** 2)
+
+
+def device_shard(cfg: int, world: int, rank: int, *, n: int | None = None, m: int | None = None,
+                 seed: int = BASE_SEED, dtype: str = "fp32"):
+    """This rank's row block of config ``cfg``'s X = G F generated ON THE
+    DEVICE (BASELINE cfg 5: 40 GB, never on the host), plus the full initial
+    factors.  G (n x p) and F (p x m) are U(0,1) from a Philox generator seeded
+    with derive_seed(seed, 0) on every rank (identical on all ranks); zeros
+    are mapped to the smallest positive draw (the open-interval convention of
+    matrix.py:73-82).  X_r = G[rows] F by one plain GEMM (data setup, not the
+    hot path).  Initial factors from derive_seed(seed, 1).  Returns
+    (X_local, row0, n, m, p, nu, q, inner, outer, G0, F0, sketch_seed)."""
+    import torch
+
+    from .sharded import row_block
+
+    if cfg != 5:
+        raise ValueError("device generation is defined for config 5 (noiseless U(0,1) G F)")
+    n0, m0, p, nu, q, _dt, inner, outer = SPECS[cfg]
+    n = n0 if n is None else n
+    m = m0 if m is None else m
+    tdt = torch.float32 if dtype == "fp32" else torch.float64
+
+    def uni(gen, shape):
+        u = torch.rand(shape, generator=gen, device="cuda", dtype=torch.float64)
+        return u.clamp_(min=2.0 ** -53).to(tdt)
+
+    g = torch.Generator(device="cuda")
+    g.manual_seed(derive_seed(seed, 0) & ((1 << 63) - 1))
+    G = uni(g, (n, p))
+    F = uni(g, (p, m))
+    r0, nr = row_block(n, world, rank)
+    X_local = torch.mm(G[r0:r0 + nr], F).contiguous()
+    del G, F
+    g.manual_seed(derive_seed(seed, 1) & ((1 << 63) - 1))
+    G0 = uni(g, (n, p))
+    F0 = uni(g, (p, m))
+    return X_local, r0, n, m, p, nu, q, inner, outer, G0, F0, derive_seed(seed, 2)

@@ -30,6 +30,15 @@ class NumpyOps:
     def prepare(self, X, k):
         return None
 
+    def draws(self, n, m, nu, seed, like):
+        from paper_1812_04315_b200.compression import sketch_draws
+
+        omega_l, omega_r = sketch_draws(n, m, nu, seed)
+        return self.tensor(omega_l.T, like), self.tensor(omega_r, like), None
+
+    def draws_ok(self, ok):
+        return True
+
     def dual_pass(self, X, Xp, At, Bt):
         return (At @ X.T).contiguous(), (Bt @ X).contiguous()
 
