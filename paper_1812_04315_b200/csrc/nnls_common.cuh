@@ -28,7 +28,7 @@ constexpr unsigned long long NN_WATCHDOG_NS = 5000000000ull;
 constexpr int NN_TRACE_LEN = 4096;
 
 constexpr int NW_WIN = 32;             // iterations per window
-constexpr int NW_FLIGHT = 4;           // windows computed ahead of decisions
+constexpr int NW_FLIGHT = 8;           // windows computed ahead of decisions
 constexpr int NW_SNAP = NW_FLIGHT + 2; // rotating snapshot slots (+1 best slot)
 constexpr int NW_SLOTS = NW_FLIGHT + 3;// window-record ring
 constexpr int NW_MAXW = 16;            // warps per CTA incl. resolver

@@ -352,6 +352,28 @@ k_nnls_mma(const __grid_constant__ MmaArgs<T> A) {
         q[2] = 0.0;
       }
     };
+    // the sums of TWO iterations (ja: a0, a1; jb: b0, b1) in one transposed
+    // butterfly: 6 shuffles and a 5-level chain for 4 values instead of 20
+    // and two 5-level chains; lanes 0 / 8 / 16 / 24 end with a0 / a1 / b0 / b1
+    auto post2 = [&](int ja, T a0, T a1, int jb, T b0, T b1) {
+      const bool lo = lane < 16;
+      T k0 = lo ? a0 : b0, k1 = lo ? a1 : b1;
+      const T x0 = lo ? b0 : a0, x1 = lo ? b1 : a1;
+      k0 += __shfl_xor_sync(0xffffffffu, x0, 16);
+      k1 += __shfl_xor_sync(0xffffffffu, x1, 16);
+      const bool hi8 = (lane & 8) != 0;
+      T v = hi8 ? k1 : k0;
+      v += __shfl_xor_sync(0xffffffffu, hi8 ? k0 : k1, 8);
+      v += __shfl_xor_sync(0xffffffffu, v, 4);
+      v += __shfl_xor_sync(0xffffffffu, v, 2);
+      v += __shfl_xor_sync(0xffffffffu, v, 1);
+      if ((lane & 7) == 0) {
+        const int j = lo ? ja : jb;
+        double* q = pp + ((size_t)((j + NW_PPD) % NW_PPD) * NW_MAXW + wid) * 3;
+        q[hi8 ? 1 : 0] = (double)v;
+        if (!hi8) q[2] = 0.0;
+      }
+    };
     auto post_flag = [&](int j) {
       if (lane == 0) {
         __threadfence_block();
@@ -440,13 +462,20 @@ k_nnls_mma(const __grid_constant__ MmaArgs<T> A) {
     const bool has_cols = cblk < ncols;
     // one iteration k: F_k into fo, u_k into u2 (which held u_{k-2});
     // the sums of iteration k-1 are reduced and posted while the MMAs run
-    auto half = [&](T (&u1)[NE], T (&u2)[NE], T (&fo)[NE]) {
+    // iterations run in pairs (A: even k, B: odd k); B posts the sums of the
+    // previous B (k - 2, in ps) and of A (k - 1, in pa) while its MMAs run
+    T pa0 = T(0), pa1 = T(0);
+    auto half = [&](T (&u1)[NE], T (&u2)[NE], T (&fo)[NE], bool b_half) {
       const T w = __shfl_sync(0xffffffffu, wwin, k % NW_WIN);
       extrapolate(u1, u2, w, fo);
       T g[NE];
       grad(fo, g);
-      if (!(dbg & 4)) post(k - 1, ps0, ps1);
-      finish(fo, g, u2, ps0, ps1);
+      if (b_half) {
+        if (!(dbg & 4)) post2(k - 2, ps0, ps1, k - 1, pa0, pa1);
+        finish(fo, g, u2, ps0, ps1);
+      } else {
+        finish(fo, g, u2, pa0, pa1);
+      }
       ++k;
     };
     while (true) {
@@ -494,11 +523,12 @@ k_nnls_mma(const __grid_constant__ MmaArgs<T> A) {
       go = sh.halt == 0;  // one LDS per warp: every lane sees the same value
       // k is even here (windows have even length): u_{k-1} in ua, F_{k-1} in fa;
       // the pair leaves the roles canonical again, so the loop has no moves
-      half(ua, ub, fb);
-      if (k > 1 && (k - 1) % NW_WIN == 0) post_flag(k - 2);  // last iteration of the previous window
-      half(ub, ua, fa);
+      half(ua, ub, fb, false);
+      half(ub, ua, fa, true);
+      if (k > 2 && (k - 2) % NW_WIN == 0) post_flag(k - 2);  // covers the last iteration of the previous window
       if (k == max_iter || !go) break;
     }
+    bool tail = false;
     if (go && k == max_iter - 1) {
       // odd max_iter: the last iteration alone, then the canonical roles back
       // (a snapshot is not needed: a best iterate in this window is F_k itself)
@@ -510,8 +540,8 @@ k_nnls_mma(const __grid_constant__ MmaArgs<T> A) {
         }
         __syncwarp();
       }
-      half(ua, ub, fb);
-      if (k > 1 && (k - 1) % NW_WIN == 0) post_flag(k - 2);
+      half(ua, ub, fb, false);
+      tail = true;
 #pragma unroll
       for (int e = 0; e < NE; ++e) {
         T t = ua[e];
@@ -527,8 +557,12 @@ k_nnls_mma(const __grid_constant__ MmaArgs<T> A) {
       tracebuf[NN_TRACE_LEN + 51] = gtimer_ns();
       tracebuf[NN_TRACE_LEN + 54] = k;
     }
-    // the last iteration's sums and the final window flag
-    if (k > 0) {
+    // the last (one or two) iterations' sums and the final window flag
+    if (tail) {
+      post(k - 2, ps0, ps1);  // the last B (when k - 2 = -1: the start point again, same values)
+      post(k - 1, pa0, pa1);  // the odd tail iteration
+      post_flag(k - 1);
+    } else if (k > 0) {
       post(k - 1, ps0, ps1);
       post_flag(k - 1);
     }
