@@ -207,9 +207,17 @@ __global__ void k_presplit_x(const float* __restrict__ X, int64_t n, int64_t m, 
 // Skinny operand S (k x len fp32 row-major) -> per 128-wide K tile:
 // [sub0 | sub1], each sub = 2 kpad rows (hi rows 0..kpad, lo rows kpad..2kpad)
 // x 128 B, swizzled; rows >= k and columns >= len are zero.
-__global__ void k_split_skinny(const float* __restrict__ S, int k, int64_t len, int kpad, int64_t total,
-                               uint8_t* __restrict__ out) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+// Both operands of a pass in one launch: items [0, ta) split A, [ta, ta + tb) split B.
+__global__ void k_split_skinny(const float* __restrict__ SA, int64_t lenA, int64_t ta, uint8_t* __restrict__ outA,
+                               const float* __restrict__ SB, int64_t lenB, int64_t tb, uint8_t* __restrict__ outB,
+                               int k, int kpad) {
+  for (int64_t ii = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; ii < ta + tb;
+       ii += (int64_t)gridDim.x * blockDim.x) {
+    const bool isA = ii < ta;
+    const int64_t i = isA ? ii : ii - ta;
+    const float* __restrict__ S = isA ? SA : SB;
+    const int64_t len = isA ? lenA : lenB;
+    uint8_t* __restrict__ out = isA ? outA : outB;
     const int ch = (int)(i & 7);
     const int64_t rest = i >> 3;
     const int row = (int)(rest % (2 * kpad));
@@ -245,13 +253,14 @@ k_dual_bulk(const uint8_t* __restrict__ Xs, int64_t n, int64_t m, const uint8_t*
             const uint8_t* __restrict__ B2, int k, Units U, float* __restrict__ Ypart, float* __restrict__ Zpart) {
   constexpr int SK_SUB = 2 * KPAD * 128;             // skinny sub-tile bytes (hi + lo rows x 128 B)
   constexpr int SK_TILE = 2 * SK_SUB;                // one 128-wide K tile of a skinny operand
-  constexpr int STAGE = XTILE_BYTES + 2 * SK_TILE;   // X tile | A tile | B tile
+  constexpr int STAGE = XTILE_BYTES + SK_TILE;       // X tile | A tile (B: per tile row, below)
   constexpr uint32_t ID_Y = idesc_bf16(KPAD, false), ID_Z = idesc_bf16(KPAD, true);
   constexpr uint32_t LO_OFF = KPAD * 128;            // lo rows of a skinny sub-tile
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  uint8_t* bbuf = smem + (size_t)NSTAGE * STAGE;  // [2][SK_TILE]: B tile of the current / next tile row
   __shared__ __align__(8) uint64_t bar_full[NSTAGE], bar_empty[NSTAGE], bar_yfull[2], bar_yempty[2], bar_zfull,
-      bar_zempty;
+      bar_zempty, bar_bfull[2], bar_bempty[2];
   __shared__ uint32_t tmem_base_sh;
 
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -259,6 +268,10 @@ k_dual_bulk(const uint8_t* __restrict__ Xs, int64_t n, int64_t m, const uint8_t*
     for (int s = 0; s < NSTAGE; ++s) {
       mbar_init(&bar_full[s], 1);
       mbar_init(&bar_empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&bar_bfull[b], 1);
+      mbar_init(&bar_bempty[b], 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&bar_yfull[b], 1);
@@ -284,11 +297,15 @@ k_dual_bulk(const uint8_t* __restrict__ Xs, int64_t n, int64_t m, const uint8_t*
     // ------------------------------------------------------------ producer
     if (lane == 0) {
       const uint64_t pol_x = policy_evict_first(), pol_s = policy_evict_last();
-      int t = 0;
+      int t = 0, row_count = 0;
       for (int u = blockIdx.x; u < U.units; u += gridDim.x) {
         int rt0, rt1, ct0, ct1, rc, cb;
         unit_bounds(U, u, rt0, rt1, ct0, ct1, rc, cb);
-        for (int rt = rt0; rt < rt1; ++rt)
+        for (int rt = rt0; rt < rt1; ++rt, ++row_count) {
+          const int rb = row_count & 1;
+          mbar_wait(&bar_bempty[rb], ((row_count >> 1) & 1) ^ 1);
+          mbar_expect_tx(&bar_bfull[rb], (uint32_t)SK_TILE);
+          bulk_g2s(bbuf + (size_t)rb * SK_TILE, B2 + (int64_t)rt * SK_TILE, SK_TILE, &bar_bfull[rb], pol_s);
           for (int ct = ct0; ct < ct1; ++ct, ++t) {
             const int s = t % NSTAGE;
             mbar_wait(&bar_empty[s], ((t / NSTAGE) & 1) ^ 1);
@@ -296,8 +313,8 @@ k_dual_bulk(const uint8_t* __restrict__ Xs, int64_t n, int64_t m, const uint8_t*
             mbar_expect_tx(&bar_full[s], (uint32_t)STAGE);
             bulk_g2s(st, Xs + ((int64_t)rt * U.n_ct + ct) * XTILE_BYTES, XTILE_BYTES, &bar_full[s], pol_x);
             bulk_g2s(st + XTILE_BYTES, A2 + (int64_t)ct * SK_TILE, SK_TILE, &bar_full[s], pol_s);
-            bulk_g2s(st + XTILE_BYTES + SK_TILE, B2 + (int64_t)rt * SK_TILE, SK_TILE, &bar_full[s], pol_s);
           }
+        }
       }
     }
   } else if (wid == MMA_WARP) {
@@ -309,7 +326,10 @@ k_dual_bulk(const uint8_t* __restrict__ Xs, int64_t n, int64_t m, const uint8_t*
       if (lane == 0) mbar_wait(&bar_zempty, (unit_count & 1) ^ 1);
       for (int rt = rt0; rt < rt1; ++rt, ++row_count) {
         const int yb = row_count & 1;
-        if (lane == 0) mbar_wait(&bar_yempty[yb], ((row_count >> 1) & 1) ^ 1);
+        if (lane == 0) {
+          mbar_wait(&bar_yempty[yb], ((row_count >> 1) & 1) ^ 1);
+          mbar_wait(&bar_bfull[yb], (row_count >> 1) & 1);
+        }
         for (int ct = ct0; ct < ct1; ++ct, ++t) {
           const int s = t % NSTAGE;
           if (lane == 0) mbar_wait(&bar_full[s], (t / NSTAGE) & 1);
@@ -317,7 +337,8 @@ k_dual_bulk(const uint8_t* __restrict__ Xs, int64_t n, int64_t m, const uint8_t*
           tc_fence_after();
           if (lane == 0) {
             const uint32_t st = smem_u32(smem + (size_t)s * STAGE);
-            const uint32_t xhi = st, xlo = st + 2 * SUB_BYTES, a2 = st + XTILE_BYTES, b2 = a2 + SK_TILE;
+            const uint32_t xhi = st, xlo = st + 2 * SUB_BYTES, a2 = st + XTILE_BYTES;
+            const uint32_t b2 = smem_u32(bbuf + (size_t)yb * SK_TILE);
             const uint32_t dy = tmem + ycol0 + (uint32_t)yb * KPAD;
             const uint32_t dz = tmem + zcol0 + (uint32_t)(ct - ct0) * KPAD;
             // Y: K = 128 columns of X = 2 sub-tiles x 4 chunks of 16
@@ -345,7 +366,10 @@ k_dual_bulk(const uint8_t* __restrict__ Xs, int64_t n, int64_t m, const uint8_t*
               umma(dz, al, bh, ID_Z, 1u);
             }
             umma_commit(&bar_empty[s]);
-            if (ct == ct1 - 1) umma_commit(&bar_yfull[yb]);
+            if (ct == ct1 - 1) {
+              umma_commit(&bar_yfull[yb]);
+              umma_commit(&bar_bempty[yb]);
+            }
             if (ct == ct1 - 1 && rt == rt1 - 1) umma_commit(&bar_zfull);
           }
           __syncwarp();
@@ -400,12 +424,18 @@ k_dual_bulk(const uint8_t* __restrict__ Xs, int64_t n, int64_t m, const uint8_t*
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
 }
 
-__global__ void k_slabs(const float* __restrict__ part, int nslab, int64_t count, float* __restrict__ out) {
-  int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (o >= count) return;
+// fixed-order slab sums of both products in one launch: [0, cy) -> Y, [cy, cy + cz) -> Z
+__global__ void k_slabs(const float* __restrict__ py, int ny, int64_t cy, float* __restrict__ oy,
+                        const float* __restrict__ pz, int nz, int64_t cz, float* __restrict__ oz) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= cy + cz) return;
+  const bool isY = i < cy;
+  const float* __restrict__ part = isY ? py : pz;
+  const int nslab = isY ? ny : nz;
+  const int64_t count = isY ? cy : cz, o = isY ? i : i - cy;
   float s = part[o];
   for (int c = 1; c < nslab; ++c) s += part[(int64_t)c * count + o];
-  out[o] = s;
+  (isY ? oy : oz)[o] = s;
 }
 
 // Unit grid: balance tiles per CTA (units are dealt round-robin to the
@@ -495,13 +525,12 @@ int dual_pass_tc_pre(Arena& ws, const uint8_t* Xs, int64_t n, int64_t m, const f
   if (!ws.ok) return NENMF_ERR_WORKSPACE;
   {
     const int64_t ta = (int64_t)U.n_ct * 2 * 2 * kpad * 8, tb = (int64_t)U.n_rt * 2 * 2 * kpad * 8;
-    k_split_skinny<<<(unsigned)imin(cdiv(ta, 256), 1184), 256, 0, s>>>(At, (int)k, m, kpad, ta, A2);
-    NENMF_LAUNCH_CHECK();
-    k_split_skinny<<<(unsigned)imin(cdiv(tb, 256), 1184), 256, 0, s>>>(Bt, (int)k, n, kpad, tb, B2);
+    k_split_skinny<<<(unsigned)imin(cdiv(ta + tb, 256), 2368), 256, 0, s>>>(At, m, ta, A2, Bt, n, tb, B2, (int)k,
+                                                                             kpad);
     NENMF_LAUNCH_CHECK();
   }
-  const size_t stage = XTILE_BYTES + 2 * (size_t)sk_tile;
-  const size_t smem = NSTAGE * stage + 1024;
+  const size_t stage = XTILE_BYTES + (size_t)sk_tile;
+  const size_t smem = NSTAGE * stage + 2 * (size_t)sk_tile + 1024;
   const unsigned grid = (unsigned)imin(U.units, sms);
   float* Yo = Ypart ? Ypart : Yt;
   float* Zo = Zpart ? Zpart : Zt;
@@ -513,12 +542,9 @@ int dual_pass_tc_pre(Arena& ws, const uint8_t* Xs, int64_t n, int64_t m, const f
     k_dual_bulk<16><<<grid, NWARPS * 32, smem, s>>>(Xs, n, m, A2, B2, (int)k, U, Yo, Zo);
   }
   NENMF_LAUNCH_CHECK();
-  if (Ypart) {
-    k_slabs<<<(unsigned)cdiv(k * n, 256), 256, 0, s>>>(Ypart, U.n_cb, k * n, Yt);
-    NENMF_LAUNCH_CHECK();
-  }
-  if (Zpart) {
-    k_slabs<<<(unsigned)cdiv(k * m, 256), 256, 0, s>>>(Zpart, U.n_rc, k * m, Zt);
+  if (Ypart || Zpart) {
+    const int64_t cy = Ypart ? k * n : 0, cz = Zpart ? k * m : 0;
+    k_slabs<<<(unsigned)cdiv(cy + cz, 256), 256, 0, s>>>(Ypart, U.n_cb, cy, Yt, Zpart, U.n_rc, cz, Zt);
     NENMF_LAUNCH_CHECK();
   }
   return NENMF_OK;

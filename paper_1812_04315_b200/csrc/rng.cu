@@ -141,53 +141,75 @@ __global__ void k_zig_scan(const Tables* __restrict__ T, uint64_t s_lo, uint64_t
   out[c].exit = pos - S;
 }
 
-// one thread: true entry offset and first draw index of every chunk
-__global__ void k_zig_link(const Tables* __restrict__ T, uint64_t s_lo, uint64_t s_hi, uint64_t i_lo, uint64_t i_hi,
-                           const ChunkScan* __restrict__ sc, int64_t nchunks, int S, int64_t need,
-                           int* __restrict__ entry, int64_t* __restrict__ base, int* __restrict__ ok) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  int e = 0;
-  int64_t b = 0;
-  int good = 1;
-  for (int64_t c = 0; c < nchunks; ++c) {
-    const ChunkScan s = sc[c];
-    entry[c] = e;
-    base[c] = b;
-    if (e == 0) {  // the common case: the chunk's own walk
-      b += s.count;
-      e = s.exit;
-      continue;
-    }
-    if (e < 64 && ((s.mask >> e) & 1ull)) {  // merged with the chunk's walk
-      b += s.count - __popcll(s.mask & ((1ull << e) - 1ull));
-      e = s.exit;
-      continue;
-    }
-    // re-walk from the true entry until it meets the chunk's walk (rare)
-    Stream g;
-    g.inc = ((u128)i_hi << 64) | i_lo;
-    g.s = advance(((u128)s_hi << 64) | s_lo, g.inc, (uint64_t)c * (uint64_t)S + (uint64_t)e);
-    int pos = e, extra = 0;
-    while (pos < S && !(pos < 64 && ((s.mask >> pos) & 1ull))) {
-      if (pos >= 64) break;
-      int used;
-      draw(g, *T, used);
-      pos += used;
-      ++extra;
-    }
-    if (pos >= S) {  // the whole chunk walked from the entry
-      b += extra;
-      e = pos - S;
-    } else if (pos < 64 && ((s.mask >> pos) & 1ull)) {
-      b += extra + s.count - __popcll(s.mask & ((1ull << pos) - 1ull));
-      e = s.exit;
-    } else {
-      good = 0;
-      break;
-    }
+// one thread chains the chunks (true entry offset and first draw index of
+// each); the block stages the chunk summaries through shared memory so the
+// sequential walk reads them at LDS latency
+constexpr int LINK_TILE = 2048;
+__global__ void __launch_bounds__(256) k_zig_link(const Tables* __restrict__ T, uint64_t s_lo, uint64_t s_hi,
+                                                  uint64_t i_lo, uint64_t i_hi, const ChunkScan* __restrict__ sc,
+                                                  int64_t nchunks, int S, int64_t need, int* __restrict__ entry,
+                                                  int64_t* __restrict__ base, int* __restrict__ ok) {
+  __shared__ ChunkScan tile[LINK_TILE];
+  __shared__ int s_e, s_good;
+  __shared__ long long s_b;
+  if (threadIdx.x == 0) {
+    s_e = 0;
+    s_b = 0;
+    s_good = 1;
   }
-  if (b < need) good = 0;
-  *ok = good;
+  for (int64_t t0 = 0; t0 < nchunks; t0 += LINK_TILE) {
+    const int nt = (int)imin(LINK_TILE, nchunks - t0);
+    __syncthreads();
+    for (int i = threadIdx.x; i < nt; i += blockDim.x) tile[i] = sc[t0 + i];
+    __syncthreads();
+    if (threadIdx.x != 0 || !s_good) continue;
+    int e = s_e;
+    int64_t b = s_b;
+    int good = 1;
+    for (int i = 0; i < nt; ++i) {
+      const int64_t c = t0 + i;
+      const ChunkScan s = tile[i];
+      entry[c] = e;
+      base[c] = b;
+      if (e == 0) {  // the common case: the chunk's own walk
+        b += s.count;
+        e = s.exit;
+        continue;
+      }
+      if (e < 64 && ((s.mask >> e) & 1ull)) {  // merged with the chunk's walk
+        b += s.count - __popcll(s.mask & ((1ull << e) - 1ull));
+        e = s.exit;
+        continue;
+      }
+      // re-walk from the true entry until it meets the chunk's walk (rare)
+      Stream g;
+      g.inc = ((u128)i_hi << 64) | i_lo;
+      g.s = advance(((u128)s_hi << 64) | s_lo, g.inc, (uint64_t)c * (uint64_t)S + (uint64_t)e);
+      int pos = e, extra = 0;
+      while (pos < S && !(pos < 64 && ((s.mask >> pos) & 1ull))) {
+        if (pos >= 64) break;
+        int used;
+        draw(g, *T, used);
+        pos += used;
+        ++extra;
+      }
+      if (pos >= S) {  // the whole chunk walked from the entry
+        b += extra;
+        e = pos - S;
+      } else if (pos < 64 && ((s.mask >> pos) & 1ull)) {
+        b += extra + s.count - __popcll(s.mask & ((1ull << pos) - 1ull));
+        e = s.exit;
+      } else {
+        good = 0;
+        break;
+      }
+    }
+    s_e = e;
+    s_b = b;
+    s_good = good;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) *ok = (s_good && s_b >= need) ? 1 : 0;
 }
 
 template <typename TO>
@@ -260,7 +282,7 @@ int sketch_draws_device(int dtype, const void* tables, uint64_t s_lo, uint64_t s
   const unsigned blocks = (unsigned)cdiv(nchunks, 64);
   k_zig_scan<<<blocks, 64, 0, s>>>(T, s_lo, s_hi, i_lo, i_hi, nchunks, S, sc);
   NENMF_LAUNCH_CHECK();
-  k_zig_link<<<1, 32, 0, s>>>(T, s_lo, s_hi, i_lo, i_hi, sc, nchunks, S, need, entry, base, ok);
+  k_zig_link<<<1, 256, 0, s>>>(T, s_lo, s_hi, i_lo, i_hi, sc, nchunks, S, need, entry, base, ok);
   NENMF_LAUNCH_CHECK();
   if (dtype == NENMF_F64)
     k_zig_emit<double><<<blocks, 64, 0, s>>>(T, s_lo, s_hi, i_lo, i_hi, nchunks, S, entry, base, ok, n, m, nu,

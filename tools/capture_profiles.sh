@@ -9,7 +9,7 @@ python bench.py --steps 3 --warmup 3 > gpurun_out/prof/bench.json 2> gpurun_out/
 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file gpurun_out/prof/launches.csv python bench.py --steps 1 --warmup 3 --no-cpu-baseline \
     > gpurun_out/prof/ncu_launch.log 2>&1
-for k in k_dual_bulk k_nnls_mma k_qr2 k_presplit_x; do
+for k in k_dual_bulk k_nnls_mma k_gram_factor k_presplit_x k_zig_emit; do
   ncu --set full --clock-control none --import-source on -k regex:$k -s 2 -c 1 \
       -o gpurun_out/prof/full_$k python tools/profile_step.py 2 > gpurun_out/prof/ncu_full_$k.log 2>&1
 done
