@@ -227,52 +227,105 @@ int ab(Arena& ws, const T* At, int64_t p, int64_t r, const T* B, int64_t c, int6
 // --------------------------------------------------------------- resid ----
 constexpr int RS_THREADS = 256;  // 64 columns x 4 row groups
 
-template <typename T, bool TRANS>
+// Explicit residual sums ||A F - B||^2 for one or two candidates F (the
+// reference's _true_objective, nnls.py:115-116, and the RRE of
+// tracing.py:45-57 with A^T = G^T, B = X).  Register-blocked: each thread
+// keeps its column of F (p values per candidate) in registers for the whole
+// row chunk and reads A^T columns as broadcast 16-byte shared-memory loads,
+// so the inner product is FMA-bound and B (X) is streamed once, coalesced.
+template <typename T, int PM, bool TRANS>
 __global__ void __launch_bounds__(RS_THREADS)
 k_resid(const T* __restrict__ At, int p, int64_t r, const T* __restrict__ B, int64_t c, int64_t ldb,
         const T* __restrict__ F1, const T* __restrict__ F2, int64_t rchunk,
         double* __restrict__ part, const int* __restrict__ gate) {
   if (gate != nullptr && *gate == 0) return;
-  extern __shared__ double smem_d[];
+  constexpr int G = RS_THREADS / AB_CB;          // row groups
+  constexpr int RPT = AB_RT / G;                 // rows per thread per tile
+  constexpr int PS = PM + 4;                     // row stride: 16-byte aligned, fewer store conflicts
+  __shared__ __align__(16) T AtT[AB_RT * PS];    // A^T columns of the tile, a contiguous
   __shared__ double red[33];
-  const int nc = F2 != nullptr ? 2 : 1;
-  T* Bs = reinterpret_cast<T*>(smem_d);          // [RT][CB+1]
-  T* Ats = Bs + AB_RT * (AB_CB + 1);             // [p][RT+1]
-  T* Fs = Ats + p * (AB_RT + 1);                 // [nc][p][CB]
   const int jj = threadIdx.x % AB_CB, g = threadIdx.x / AB_CB;
   const int64_t j0 = (int64_t)blockIdx.x * AB_CB;
   const int64_t tc0 = (int64_t)blockIdx.y * rchunk, tc1 = min(r, tc0 + rchunk);
-  for (int idx = threadIdx.x; idx < nc * p * AB_CB; idx += blockDim.x) {
-    int cand = idx / (p * AB_CB), rem = idx % (p * AB_CB), a = rem / AB_CB, j2 = rem % AB_CB;
-    const T* F = cand == 0 ? F1 : F2;
-    int64_t j = j0 + j2;
-    Fs[idx] = j < c ? F[(int64_t)a * c + j] : T(0);
+  const bool two = F2 != nullptr;
+  const int64_t j = j0 + jj;
+  const bool live = j < c;
+  T f1[PM], f2[PM];
+#pragma unroll
+  for (int a = 0; a < PM; ++a) {
+    f1[a] = (live && a < p) ? F1[(int64_t)a * c + j] : T(0);
+    f2[a] = (two && live && a < p) ? F2[(int64_t)a * c + j] : T(0);
   }
+  // B(t, j) for this thread's rows g, g + G, ... of a tile, loaded one tile ahead
+  auto bload = [&](int64_t t0, T (&v)[RPT]) {
+#pragma unroll
+    for (int i = 0; i < RPT; ++i) {
+      const int64_t t = t0 + g + G * i;
+      v[i] = (live && t < tc1) ? (TRANS ? B[j * ldb + t] : __ldcs(&B[t * ldb + j])) : T(0);
+    }
+  };
+  auto dot = [&](const T* w, const T (&f)[PM]) -> T {
+    T s = T(0);
+    if constexpr (sizeof(T) == 4) {
+#pragma unroll
+      for (int a = 0; a < PM; a += 4) {
+        const float4 w4 = *reinterpret_cast<const float4*>(w + a);
+        s = fmaf(w4.x, f[a], s);
+        s = fmaf(w4.y, f[a + 1], s);
+        s = fmaf(w4.z, f[a + 2], s);
+        s = fmaf(w4.w, f[a + 3], s);
+      }
+    } else {
+#pragma unroll
+      for (int a = 0; a < PM; a += 2) {
+        const double2 w2 = *reinterpret_cast<const double2*>(w + a);
+        s = fma(w2.x, f[a], s);
+        s = fma(w2.y, f[a + 1], s);
+      }
+    }
+    return s;
+  };
+  T bc[RPT], bn[RPT];
+  bload(tc0, bc);
   double acc0 = 0.0, acc1 = 0.0;
-  const bool live = (j0 + jj) < c;
   for (int64_t t0 = tc0; t0 < tc1; t0 += AB_RT) {
     const int nt = (int)imin(AB_RT, tc1 - t0);
-    load_b_tile<T, TRANS>(Bs, B, ldb, r, c, t0, nt, j0);
-    load_at_tile<T>(Ats, At, p, r, t0, nt);
     __syncthreads();
+    for (int idx = threadIdx.x; idx < AB_RT * PM; idx += blockDim.x) {
+      const int a = idx / AB_RT, tt = idx % AB_RT;  // coalesced along the rows of A
+      AtT[tt * PS + a] = (tt < nt && a < p) ? At[(int64_t)a * r + t0 + tt] : T(0);
+    }
+    __syncthreads();
+    if (t0 + AB_RT < tc1) bload(t0 + AB_RT, bn);
     if (live) {
-      for (int tt = g; tt < nt; tt += 4) {
-        const T b = Bs[tt * (AB_CB + 1) + jj];
-        T s0 = T(0), s1 = T(0);
-        for (int a = 0; a < p; ++a) {
-          const T w = Ats[a * (AB_RT + 1) + tt];
-          s0 = fma_acc(w, Fs[a * AB_CB + jj], s0);
-          if (nc == 2) s1 = fma_acc(w, Fs[(p + a) * AB_CB + jj], s1);
+      // four rows at a time: four independent FMA chains per candidate
+#pragma unroll
+      for (int i0 = 0; i0 < RPT; i0 += 4) {
+        T s[4] = {T(0), T(0), T(0), T(0)}, s2[4] = {T(0), T(0), T(0), T(0)};
+#pragma unroll
+        for (int a = 0; a < PM; ++a) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const T wa = AtT[(g + G * (i0 + u)) * PS + a];
+            s[u] = fma_acc(wa, f1[a], s[u]);
+            if (two) s2[u] = fma_acc(wa, f2[a], s2[u]);
+          }
         }
-        double d0 = (double)(s0 - b);
-        acc0 += d0 * d0;
-        if (nc == 2) {
-          double d1 = (double)(s1 - b);
-          acc1 += d1 * d1;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (g + G * (i0 + u) < nt) {
+            const double d0 = (double)(s[u] - bc[i0 + u]);
+            acc0 += d0 * d0;
+            if (two) {
+              const double d1 = (double)(s2[u] - bc[i0 + u]);
+              acc1 += d1 * d1;
+            }
+          }
         }
       }
     }
-    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < RPT; ++i) bc[i] = bn[i];
   }
   const int64_t bid = (int64_t)blockIdx.y * gridDim.x + blockIdx.x;
   double s0 = block_sum(acc0, red);
@@ -311,15 +364,17 @@ int resid(Arena& ws, const T* At, int64_t p, int64_t r, const T* B, int64_t c, i
   double* part = ws.take<double>((size_t)grid.x * grid.y * 2);
   if (ws.base == nullptr) return NENMF_OK;
   if (!ws.ok) return NENMF_ERR_WORKSPACE;
-  const int nc = F2 != nullptr ? 2 : 1;
-  size_t smem = ((size_t)AB_RT * (AB_CB + 1) + (size_t)p * (AB_RT + 1) + (size_t)nc * p * AB_CB) * sizeof(T);
-  if (trans) {
-    NENMF_CUDA_TRY(cudaFuncSetAttribute(k_resid<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_resid<T, true><<<grid, RS_THREADS, smem, st>>>(At, (int)p, r, B, c, ldb, F1, F2, AB_RCHUNK, part, gate);
-  } else {
-    NENMF_CUDA_TRY(cudaFuncSetAttribute(k_resid<T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_resid<T, false><<<grid, RS_THREADS, smem, st>>>(At, (int)p, r, B, c, ldb, F1, F2, AB_RCHUNK, part, gate);
-  }
+  auto go = [&](auto kern, int) -> int {
+    kern<<<grid, RS_THREADS, 0, st>>>(At, (int)p, r, B, c, ldb, F1, F2, AB_RCHUNK, part, gate);
+    return NENMF_OK;
+  };
+  int rc;
+  if (p <= 8) rc = trans ? go(k_resid<T, 8, true>, 8) : go(k_resid<T, 8, false>, 8);
+  else if (p <= 16) rc = trans ? go(k_resid<T, 16, true>, 16) : go(k_resid<T, 16, false>, 16);
+  else if (p <= 24) rc = trans ? go(k_resid<T, 24, true>, 24) : go(k_resid<T, 24, false>, 24);
+  else if (p <= 32) rc = trans ? go(k_resid<T, 32, true>, 32) : go(k_resid<T, 32, false>, 32);
+  else rc = trans ? go(k_resid<T, 64, true>, 64) : go(k_resid<T, 64, false>, 64);
+  if (rc != NENMF_OK) return rc;
   NENMF_LAUNCH_CHECK();
   k_pair_final<<<1, 256, 0, st>>>(part, (int64_t)grid.x * grid.y, out2, gate);
   NENMF_LAUNCH_CHECK();
