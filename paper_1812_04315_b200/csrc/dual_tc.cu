@@ -487,7 +487,7 @@ inline Units choose_units(int64_t n, int64_t m, int64_t k, int ctmax, int sms) {
 }  // namespace tc
 
 bool tc_pass_eligible(int64_t n, int64_t m, int64_t k) {
-  if (k < 1 || k > 32 || n < tc::TILE || m < tc::TILE) return false;
+  if (k < 1 || k > 128 || n < tc::TILE || m < tc::TILE) return false;
   return getenv("NENMF_NO_TC") == nullptr;
 }
 
@@ -506,11 +506,33 @@ int tc_presplit(const float* X, int64_t n, int64_t m, int64_t ldx, uint8_t* Xs, 
   return NENMF_OK;
 }
 
+static int dual_pass_tc_chunk(Arena& ws, const uint8_t* Xs, int64_t n, int64_t m, const float* At, const float* Bt,
+                              int64_t k, float* Yt, float* Zt, cudaStream_t s);
+
 // One pass over a pre-split X (tc_presplit): Yt = At X^T (k x n), Zt = Bt X (k x m).
+// k > 32 (cfg3's p' = 60, cfg4's 40): the skinny operands are processed in
+// row blocks of 32 (short-major storage: a block is a contiguous slice), one
+// X stream per block.
 int dual_pass_tc_pre(Arena& ws, const uint8_t* Xs, int64_t n, int64_t m, const float* At, const float* Bt,
                      int64_t k, float* Yt, float* Zt, cudaStream_t s) {
-  using namespace tc;
   if (At == nullptr || Bt == nullptr || !tc_pass_eligible(n, m, k)) return NENMF_ERR_UNSUPPORTED;
+  if (k <= 32) return dual_pass_tc_chunk(ws, Xs, n, m, At, Bt, k, Yt, Zt, s);
+  const bool dry = ws.base == nullptr;
+  size_t need = 0;
+  for (int64_t k0 = 0; k0 < k; k0 += 32) {
+    const int64_t kc = imin(32, k - k0);
+    Arena a = dry ? Arena(nullptr, 0) : ws;
+    NENMF_TRY(dual_pass_tc_chunk(a, Xs, n, m, At + k0 * m, Bt + k0 * n, kc, Yt ? Yt + k0 * n : nullptr,
+                                 Zt ? Zt + k0 * m : nullptr, s));
+    if (a.used - (dry ? 0 : ws.used) > need) need = a.used - (dry ? 0 : ws.used);
+  }
+  if (dry) ws.take<char>(need);
+  return NENMF_OK;
+}
+
+static int dual_pass_tc_chunk(Arena& ws, const uint8_t* Xs, int64_t n, int64_t m, const float* At, const float* Bt,
+                              int64_t k, float* Yt, float* Zt, cudaStream_t s) {
+  using namespace tc;
   const int kpad = k <= 16 ? 16 : 32;
   const int ctmax = (512 - 2 * kpad) / kpad;
   int sms = sm_count();

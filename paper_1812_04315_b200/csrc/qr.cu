@@ -25,7 +25,7 @@
 
 namespace nenmf {
 
-constexpr int QC_KMAX = 32;  // the register-row factorisation holds k <= 32
+constexpr int QC_KMAX = 64;  // panels of up to 64 columns (BASELINE cfg3's p' = 60)
 
 // (Pivoted) Cholesky of a k x k Gram matrix (k <= 32), right-looking, by the
 // whole CTA: the Schur complement stays in shared memory S; per step the
@@ -36,13 +36,14 @@ constexpr int QC_KMAX = 32;  // the register-row factorisation holds k <= 32
 // the original index space: P[:, perm] = Q R11 (R11[j][l] = R[j*k + perm[l]]).
 // Without pivoting perm is the identity.  A pivot <= rel_tol * max(diag) ends
 // it (rank).  R (k*k) is shared scratch.
-__device__ void block_factor(double* S_in, double* /*R scratch (unused)*/, int k, int pivot, double rel_tol,
-                             double* __restrict__ Rout, int* __restrict__ meta, nenmf_device_status* st) {
-  // row stride 32 inside: element (a, b) at a * 32 + b, no integer division
-  __shared__ double S[QC_KMAX * QC_KMAX];
-  __shared__ double Rc[QC_KMAX];  // the current column of R (remaining rows)
-  __shared__ int perm[QC_KMAX];
-  __shared__ int rem[QC_KMAX];
+__device__ void block_factor(double* S_in, int k, int pivot, double rel_tol, double* __restrict__ Rout,
+                             int* __restrict__ meta, nenmf_device_status* st) {
+  // row stride 64 inside: element (a, b) at a * 64 + b, no integer division
+  constexpr int KS = QC_KMAX;
+  __shared__ double S[KS * KS];
+  __shared__ double Rc[KS];  // the current column of R (remaining rows)
+  __shared__ int perm[KS];
+  __shared__ int rem[KS];
   __shared__ int s_piv, s_stop, s_bad;
   __shared__ double s_rjj, s_inv, s_tau;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nwarp = blockDim.x >> 5;
@@ -50,16 +51,17 @@ __device__ void block_factor(double* S_in, double* /*R scratch (unused)*/, int k
   const int kk = k * k;
   if (tid == 0) s_bad = 0;
   __syncthreads();
-  for (int a = wid; a < QC_KMAX; a += nwarp) {
-    const double v = (a < k && lane < k) ? S_in[a * k + lane] : 0.0;
-    S[a * 32 + lane] = v;
-    if (!isfinite(v)) s_bad = 1;
-  }
+  for (int a = wid; a < KS; a += nwarp)
+    for (int b = lane; b < KS; b += 32) {
+      const double v = (a < k && b < k) ? S_in[a * k + b] : 0.0;
+      S[a * KS + b] = v;
+      if (!isfinite(v)) s_bad = 1;
+    }
   for (int e = tid; e < kk; e += blockDim.x) Rout[e] = 0.0;
-  if (tid < QC_KMAX) rem[tid] = tid < k ? 1 : 0;
+  if (tid < KS) rem[tid] = tid < k ? 1 : 0;
   __syncthreads();
   if (tid < 32) {
-    double mx = lane < k ? S[lane * 33] : 0.0;
+    double mx = fmax(lane < k ? S[lane * (KS + 1)] : 0.0, lane + 32 < k ? S[(lane + 32) * (KS + 1)] : 0.0);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(FULL, mx, o));
     if (lane == 0) {
@@ -75,19 +77,23 @@ __device__ void block_factor(double* S_in, double* /*R scratch (unused)*/, int k
   } else {
     for (int j = 0; j < k; ++j) {
       if (tid < 32) {
-        const bool live = lane < k && rem[lane];
-        const double d = live ? S[lane * 33] : -1.0;
+        // lane holds candidate rows lane and lane + 32
+        const bool live0 = lane < k && rem[lane], live1 = lane + 32 < k && rem[lane + 32];
+        const double d0 = live0 ? S[lane * (KS + 1)] : -1.0;
+        const double d1 = live1 ? S[(lane + 32) * (KS + 1)] : -1.0;
         int pj;
         if (pivot) {
           // positive doubles order like their bit patterns: compare the top 32 bits
-          const unsigned key = d > 0.0 ? (unsigned)(__double_as_longlong(d) >> 32) : 0u;
-          const unsigned best = __reduce_max_sync(FULL, key);
-          const unsigned cand = __ballot_sync(FULL, live && key == best);
-          pj = cand ? __ffs(cand) - 1 : j;
+          const unsigned k0 = d0 > 0.0 ? (unsigned)(__double_as_longlong(d0) >> 32) : 0u;
+          const unsigned k1 = d1 > 0.0 ? (unsigned)(__double_as_longlong(d1) >> 32) : 0u;
+          const unsigned best = __reduce_max_sync(FULL, k0 > k1 ? k0 : k1);
+          const unsigned c0 = __ballot_sync(FULL, live0 && k0 == best);
+          const unsigned c1 = __ballot_sync(FULL, live1 && k1 == best);
+          pj = c0 ? __ffs(c0) - 1 : (c1 ? 32 + __ffs(c1) - 1 : j);
         } else {
           pj = j;
         }
-        const double bv = __shfl_sync(FULL, d, pj);
+        const double bv = S[pj * (KS + 1)];
         const bool stop = !(bv > s_tau);
         double rjj = 0.0, inv = 0.0;
         if (!stop) {
@@ -95,30 +101,38 @@ __device__ void block_factor(double* S_in, double* /*R scratch (unused)*/, int k
           inv = 1.0 / rjj;
         }
         // R[j][a] = S[a][pj] / rjj for the remaining rows, rjj at the pivot
-        const bool other = live && lane != pj;
-        const double ra = other ? S[lane * 32 + pj] * inv : (lane == pj ? rjj : 0.0);
-        if (!stop) {
-          Rc[lane] = other ? ra : 0.0;
-          if (lane < k) Rout[j * k + lane] = ra;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int a = lane + 32 * h;
+          const bool live = h == 0 ? live0 : live1;
+          const bool other = live && a != pj;
+          const double ra = other ? S[a * KS + pj] * inv : (a == pj ? rjj : 0.0);
+          if (!stop) {
+            Rc[a] = other ? ra : 0.0;
+            if (a < k) Rout[j * k + a] = ra;
+          }
         }
         if (lane == 0) {
           s_stop = stop;
           s_piv = pj;
           perm[j] = pj;
         }
-        if (lane == pj) rem[lane] = 0;
       }
       __syncthreads();
       if (s_stop) {
         rank = j;
         break;
       }
+      if (tid == s_piv) rem[tid] = 0;
       // rank-1 update of the remaining block (Rc is 0 outside it)
       {
-        const double rb = Rc[lane];
+        const double rb0 = Rc[lane], rb1 = Rc[lane + 32];
         for (int a = wid; a < k; a += nwarp) {
           const double ra = Rc[a];
-          if (ra != 0.0 && rb != 0.0) S[a * 32 + lane] = fma(-ra, rb, S[a * 32 + lane]);
+          if (ra != 0.0) {
+            if (rb0 != 0.0) S[a * KS + lane] = fma(-ra, rb0, S[a * KS + lane]);
+            if (rb1 != 0.0) S[a * KS + lane + 32] = fma(-ra, rb1, S[a * KS + lane + 32]);
+          }
         }
       }
       __syncthreads();
@@ -201,64 +215,68 @@ __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
       : "d"(a), "d"(b));
 }
 
-template <typename T>
+template <typename T, int NB>
 __global__ void __launch_bounds__(256) k_gram_part(PanelSet P, int k) {
-  extern __shared__ double qsm[];  // [8 warps][32][32]
+  constexpr int NT = NB * (NB + 1) / 2;  // upper-triangle 8 x 8 tiles
+  constexpr int KS = 8 * NB;
+  extern __shared__ double qsm[];        // [KS][KS]: the CTA's partial, warps added in order
   const int pi = (P.npan > 1 && (int)blockIdx.x >= P.cta0[1]) ? 1 : 0;
   const int local = (int)blockIdx.x - P.cta0[pi];
   const int64_t rows = P.rows[pi];
   const int64_t r0 = (int64_t)local * rows / P.ncta[pi], r1 = (int64_t)(local + 1) * rows / P.ncta[pi];
   const T* __restrict__ Pt = reinterpret_cast<const T*>(P.in[pi]);
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, gq = lane >> 2, tq = lane & 3;
-  const int nb = (k + 7) >> 3;  // 8-column blocks
-  double acc[10][2];
+  const int nb = (k + 7) >> 3;  // 8-column blocks in use
+  double acc[NT][2];
 #pragma unroll
-  for (int t = 0; t < 10; ++t) acc[t][0] = acc[t][1] = 0.0;
-  auto load = [&](int64_t r, double (&f)[4]) {
+  for (int t = 0; t < NT; ++t) acc[t][0] = acc[t][1] = 0.0;
+  auto load = [&](int64_t r, double (&f)[NB]) {
     const int64_t row = r + tq;
 #pragma unroll
-    for (int b = 0; b < 4; ++b) {
+    for (int b = 0; b < NB; ++b) {
       const int col = 8 * b + gq;
       f[b] = (b < nb && col < k && row < r1) ? (double)__ldg(&Pt[(int64_t)col * rows + row]) : 0.0;
     }
   };
-  double fn[4];
+  double fn[NB];
   load(r0 + 4 * wid, fn);  // software pipelined: the next step's loads are in flight during the DMMAs
   for (int64_t r = r0 + 4 * wid; r < r1; r += 32) {
-    double f[4];
+    double f[NB];
 #pragma unroll
-    for (int b = 0; b < 4; ++b) f[b] = fn[b];
+    for (int b = 0; b < NB; ++b) f[b] = fn[b];
     if (r + 32 < r1) load(r + 32, fn);
     int t = 0;
 #pragma unroll
-    for (int ma = 0; ma < 4; ++ma)
+    for (int ma = 0; ma < NB; ++ma)
 #pragma unroll
-      for (int na = ma; na < 4; ++na, ++t)
+      for (int na = ma; na < NB; ++na, ++t)
         if (na < nb) dmma(acc[t], f[ma], f[na]);
   }
-  double* W = qsm + (size_t)wid * 1024;
-  {
-    int t = 0;
+  for (int e = threadIdx.x; e < KS * KS; e += blockDim.x) qsm[e] = 0.0;
+  for (int w = 0; w < 8; ++w) {
+    __syncthreads();
+    if (wid == w) {
+      int t = 0;
 #pragma unroll
-    for (int ma = 0; ma < 4; ++ma)
+      for (int ma = 0; ma < NB; ++ma)
 #pragma unroll
-      for (int na = ma; na < 4; ++na, ++t) {
-        if (na >= nb) continue;
-        const int i = 8 * ma + gq, j = 8 * na + 2 * tq;
-        W[i * 32 + j] = acc[t][0];
-        W[i * 32 + j + 1] = acc[t][1];
-        W[j * 32 + i] = acc[t][0];
-        W[(j + 1) * 32 + i] = acc[t][1];
-      }
+        for (int na = ma; na < NB; ++na, ++t) {
+          if (na >= nb) continue;
+          const int i = 8 * ma + gq, j = 8 * na + 2 * tq;
+          qsm[i * KS + j] += acc[t][0];
+          qsm[i * KS + j + 1] += acc[t][1];
+          if (ma != na) {  // mirror (G is exactly symmetric)
+            qsm[j * KS + i] += acc[t][0];
+            qsm[(j + 1) * KS + i] += acc[t][1];
+          }
+        }
+    }
   }
   __syncthreads();
   double* out = P.part[pi] + (int64_t)local * k * k;
   for (int e = threadIdx.x; e < k * k; e += blockDim.x) {
     const int a = e / k, b = e - a * k;
-    double v = 0.0;
-#pragma unroll
-    for (int w = 0; w < 8; ++w) v += qsm[(size_t)w * 1024 + a * 32 + b];
-    out[e] = v;
+    out[e] = qsm[a * KS + b];
   }
 }
 
@@ -269,7 +287,6 @@ __global__ void __launch_bounds__(256) k_gram_factor(PanelSet P, int k, int pivo
                                                      nenmf_device_status* st) {
   extern __shared__ double qsm[];
   double* S = qsm;
-  double* Rw = S + k * k;
   const int pi = blockIdx.x;
   const int kk = k * k;
   if (st != nullptr && st->code != 0) {
@@ -301,7 +318,7 @@ __global__ void __launch_bounds__(256) k_gram_factor(PanelSet P, int k, int pivo
   }
   __syncthreads();
   if (pivot < 0) return;
-  block_factor(S, Rw, k, pivot, tol, P.R[pi], P.meta[pi], st);
+  block_factor(S, k, pivot, tol, P.R[pi], P.meta[pi], st);
 }
 
 template <typename T, int KM>
@@ -327,8 +344,8 @@ __global__ void __launch_bounds__(256) k_trsm(PanelSet P, int k, int full_only) 
     trsm_row<T, KM>(in_t, rows, k, R, perm, rdinv, r, i, out_t, P.row0[pi]);
 }
 
-inline size_t gram_smem(int) { return (size_t)8 * 1024 * sizeof(double); }
-inline size_t factor_smem(int k) { return (size_t)2 * k * k * sizeof(double); }
+inline size_t gram_smem(int k) { return (size_t)(k <= 32 ? 32 * 32 : 64 * 64) * sizeof(double); }
+inline size_t factor_smem(int k) { return (size_t)k * k * sizeof(double); }
 
 // CTAs per panel: the whole GPU shared by the panels, >= 256 rows per CTA
 // (the one-CTA factor kernel reduces the per-CTA Gram partials)
@@ -349,14 +366,21 @@ inline void split_ctas(PanelSet& P) {
 template <typename T>
 int launch_gram_part(PanelSet& P, int k, cudaStream_t s) {
   const size_t smem = gram_smem(k);
-  NENMF_CUDA_TRY(set_smem(k_gram_part<T>, smem));
-  k_gram_part<T><<<P.cta0[P.npan - 1] + P.ncta[P.npan - 1], 256, smem, s>>>(P, k);
+  const unsigned grid = P.cta0[P.npan - 1] + P.ncta[P.npan - 1];
+  if (k <= 32) {
+    NENMF_CUDA_TRY(set_smem(k_gram_part<T, 4>, smem));
+    k_gram_part<T, 4><<<grid, 256, smem, s>>>(P, k);
+  } else {
+    NENMF_CUDA_TRY(set_smem(k_gram_part<T, 8>, smem));
+    k_gram_part<T, 8><<<grid, 256, smem, s>>>(P, k);
+  }
   NENMF_LAUNCH_CHECK();
   return NENMF_OK;
 }
 
 int launch_gram_factor(PanelSet& P, int k, int pivot, double tol, int gin, nenmf_device_status* st,
                        cudaStream_t s) {
+  NENMF_CUDA_TRY(set_smem(k_gram_factor, factor_smem(k)));
   k_gram_factor<<<P.npan, 256, factor_smem(k), s>>>(P, k, pivot, tol, gin, st);
   NENMF_LAUNCH_CHECK();
   return NENMF_OK;
@@ -364,7 +388,9 @@ int launch_gram_factor(PanelSet& P, int k, int pivot, double tol, int gin, nenmf
 
 template <typename T>
 int launch_trsm(PanelSet& P, int k, int full_only, cudaStream_t s) {
-  k_trsm<T, QC_KMAX><<<P.cta0[P.npan - 1] + P.ncta[P.npan - 1], 256, 0, s>>>(P, k, full_only);
+  const unsigned grid = P.cta0[P.npan - 1] + P.ncta[P.npan - 1];
+  if (k <= 32) k_trsm<T, 32><<<grid, 256, 0, s>>>(P, k, full_only);
+  else k_trsm<T, 64><<<grid, 256, 0, s>>>(P, k, full_only);
   NENMF_LAUNCH_CHECK();
   return NENMF_OK;
 }
@@ -430,6 +456,7 @@ int panel_gram(Arena& ws, const T* Pt, int64_t rows, int64_t k, double* G, cudaS
   NENMF_TRY(launch_gram_part<T>(P, (int)k, s));
   // reduce only (the factorisation runs after the cross-rank all-reduce):
   // k_gram_factor with pivot = -1 stops after writing G
+  NENMF_CUDA_TRY(set_smem(k_gram_factor, factor_smem((int)k)));
   k_gram_factor<<<1, 256, factor_smem((int)k), s>>>(P, (int)k, -1, 0.0, 0, nullptr);
   NENMF_LAUNCH_CHECK();
   return NENMF_OK;

@@ -412,7 +412,7 @@ int orthonormalize_tsqr(Arena& ws, T* Pt, int64_t rows, int64_t k, nenmf_device_
 template <typename T>
 int orthonormalize(Arena& ws, T* Pt, int64_t rows, int64_t k, nenmf_device_status* st, cudaStream_t s) {
   const char* e = getenv("NENMF_QR");
-  if ((e != nullptr && e[0] == 't') || k > 32) return orthonormalize_tsqr<T>(ws, Pt, rows, k, st, s);
+  if ((e != nullptr && e[0] == 't') || k > 64) return orthonormalize_tsqr<T>(ws, Pt, rows, k, st, s);
   return orthonormalize_cholqr<T>(ws, Pt, rows, k, st, s);
 }
 
@@ -481,7 +481,7 @@ int rsi(Arena& ws, const T* X, int64_t n, int64_t m, int64_t ldx, const T* omega
   auto qr2 = [&](T* A, int64_t ra, T* B, int64_t rb) -> int {
     Arena a = fresh();
     const char* e = getenv("NENMF_QR");
-    if ((e != nullptr && e[0] == 't') || nu > 32) {  // CholeskyQR2 path holds k <= 32
+    if ((e != nullptr && e[0] == 't') || nu > 64) {  // CholeskyQR2 path holds k <= 64
       NENMF_TRY(orthonormalize<T>(a, A, ra, nu, st, s));
       Arena b = fresh();
       return orthonormalize<T>(b, B, rb, nu, st, s);
