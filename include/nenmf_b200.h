@@ -114,6 +114,19 @@ int nenmf_solve_nnls(int dtype, const void* At, int64_t r, int64_t p,
  * G-half.  Formed inside the solver launch when it is fused (r <= 64); same
  * result as a separate nenmf_abt(F_out, next_bt) up to summation order. */
 size_t nenmf_solve_nnls_next_workspace_bytes(int dtype, int64_t r, int64_t p, int64_t c, int64_t next_k);
+
+/* Vanilla half-steps on FP32 data (factorize.py:94-98): as nenmf_solve_nnls,
+ * with Xp = nenmf_prepare_x(X) of the X that B is (trans_b = 0: B = X, r x c)
+ * or whose transpose B is (trans_b = 1: X is c x r).  V = A^T B then comes
+ * from one tensor-core pass over Xp; B itself is still read by the
+ * explicit-residual tie-break (nnls.py:219-227).  Xp = NULL: plain solve. */
+size_t nenmf_solve_nnls_prepared_workspace_bytes(int dtype, int64_t r, int64_t p, int64_t c);
+int nenmf_solve_nnls_prepared(int dtype, const void* At, int64_t r, int64_t p, const void* B,
+                              int64_t c, int64_t ldb, int trans_b, const void* Xp, const void* F0,
+                              void* F_out, int max_iter, double grad_tol, double lipschitz_safety,
+                              const double* power_vectors, int power_count, int power_max_iters,
+                              double power_tol, nenmf_device_status* status, void* ws,
+                              size_t ws_bytes, void* stream);
 int nenmf_solve_nnls_next(int dtype, const void* At, int64_t r, int64_t p,
                           const void* B, int64_t c, int64_t ldb, int trans_b,
                           const void* F0, void* F_out,

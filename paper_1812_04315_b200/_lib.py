@@ -36,6 +36,9 @@ _SIGS = {
     "nenmf_solve_nnls_next_workspace_bytes": (_sz, [_i32, _i64, _i64, _i64, _i64]),
     "nenmf_solve_nnls_next": (_i32, [_i32, _vp, _i64, _i64, _vp, _i64, _i64, _i32, _vp, _vp, _i32, _dbl, _dbl,
                                      _vp, _i32, _i32, _dbl, _vp, _i64, _vp, _vp, _vp, _sz, _vp]),
+    "nenmf_solve_nnls_prepared_workspace_bytes": (_sz, [_i32, _i64, _i64, _i64]),
+    "nenmf_solve_nnls_prepared": (_i32, [_i32, _vp, _i64, _i64, _vp, _i64, _i64, _i32, _vp, _vp, _vp, _i32, _dbl,
+                                         _dbl, _vp, _i32, _i32, _dbl, _vp, _vp, _sz, _vp]),
     "nenmf_spectral_norm_sq_workspace_bytes": (_sz, [_i32, _i64, _i64]),
     "nenmf_spectral_norm_sq": (_i32, [_i32, _vp, _i64, _i64, _vp, _i32, _i32, _dbl, _vp, _vp, _vp, _sz, _vp]),
     "nenmf_gradient_workspace_bytes": (_sz, [_i32, _i64, _i64, _i64]),

@@ -24,7 +24,7 @@ def _dt(t) -> str:
 
 
 def solve(At, B, F0, Fout, *, trans_b: bool, max_iter: int, grad_tol: float, lipschitz_safety: float,
-          status, status_index: int = 0, next_bt=None, next_out=None) -> None:
+          status, status_index: int = 0, next_bt=None, next_out=None, Xp=None) -> None:
     """nenmf_solve_nnls: At (p x r), B (r x c) or, with trans_b, the (c x r)
     matrix whose transpose is B; F0/Fout (p x c).  With next_bt (k x c) also
     next_out (p x k) = Fout next_bt^T (nenmf_solve_nnls_next)."""
@@ -40,7 +40,15 @@ def solve(At, B, F0, Fout, *, trans_b: bool, max_iter: int, grad_tol: float, lip
     k = min(r, p)
     pv = _lib.power_vectors(k)
     code = _lib.code_of(dt)
-    if next_bt is None:
+    if Xp is not None:
+        assert next_bt is None
+        ws = _lib.workspace(lib.nenmf_solve_nnls_prepared_workspace_bytes(code, r, p, c))
+        rc = lib.nenmf_solve_nnls_prepared(code, At.data_ptr(), r, p, B.data_ptr(), c, ldb, 1 if trans_b else 0,
+                                           Xp.data_ptr(), F0.data_ptr(), Fout.data_ptr(), int(max_iter),
+                                           float(grad_tol), float(lipschitz_safety), pv.data_ptr(), pv.shape[0],
+                                           POWER_MAX_ITERS, POWER_TOL, _lib.status_ptr(status, status_index),
+                                           ws.data_ptr(), ws.numel(), _lib.stream_handle())
+    elif next_bt is None:
         nbytes = lib.nenmf_solve_nnls_workspace_bytes(code, r, p, c)
         ws = _lib.workspace(nbytes)
         rc = lib.nenmf_solve_nnls(code, At.data_ptr(), r, p, B.data_ptr(), c, ldb, 1 if trans_b else 0,

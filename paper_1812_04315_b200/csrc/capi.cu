@@ -91,6 +91,37 @@ size_t nenmf_solve_nnls_next_workspace_bytes(int dtype, int64_t r, int64_t p, in
   return best + 256;
 }
 
+size_t nenmf_solve_nnls_prepared_workspace_bytes(int dtype, int64_t r, int64_t p, int64_t c) {
+  size_t best = 0;
+  for (int mi : {1, (1 << 16) + 1}) {
+    Arena a(nullptr, 0);
+    NENMF_DISPATCH(dtype, [&] {
+      const scalar_t* sent = reinterpret_cast<const scalar_t*>(256);
+      return solve_nnls<scalar_t>(a, sent, r, p, sent, c, c, false, sent, nullptr, mi, 1e-4, 1.0, nullptr, 1, 100,
+                                  1e-9, nullptr, nullptr, nullptr, 0, nullptr,
+                                  reinterpret_cast<const uint8_t*>(256));
+    });
+    best = a.used > best ? a.used : best;
+  }
+  const size_t plain = nenmf_solve_nnls_next_workspace_bytes(dtype, r, p, c, 0);
+  return (best > plain ? best : plain) + 256;
+}
+
+int nenmf_solve_nnls_prepared(int dtype, const void* At, int64_t r, int64_t p, const void* B, int64_t c,
+                              int64_t ldb, int trans_b, const void* Xp, const void* F0, void* F_out, int max_iter,
+                              double grad_tol, double lipschitz_safety, const double* power_vectors,
+                              int power_count, int power_max_iters, double power_tol, nenmf_device_status* status,
+                              void* ws, size_t ws_bytes, void* stream) {
+  if (ws == nullptr || status == nullptr) return NENMF_ERR_VALUE;
+  Arena a(ws, ws_bytes);
+  return NENMF_DISPATCH(dtype, [&] {
+    return solve_nnls<scalar_t>(a, C<scalar_t>(At), r, p, C<scalar_t>(B), c, ldb, trans_b != 0, C<scalar_t>(F0),
+                                M<scalar_t>(F_out), max_iter, grad_tol, lipschitz_safety, power_vectors,
+                                power_count, power_max_iters, power_tol, status, S(stream), nullptr, 0, nullptr,
+                                static_cast<const uint8_t*>(Xp));
+  });
+}
+
 size_t nenmf_solve_nnls_workspace_bytes(int dtype, int64_t r, int64_t p, int64_t c) {
   return nenmf_solve_nnls_next_workspace_bytes(dtype, r, p, c, 0);
 }

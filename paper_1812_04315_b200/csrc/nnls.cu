@@ -19,6 +19,7 @@
 // same decisions; the best iterate is recomputed from a window snapshot when
 // it is no longer live.  See nnls_kernel.cuh.
 #include "nnls.cuh"
+#include "rsi.cuh"
 #include "nnls_common.cuh"
 #include "skinny.cuh"
 
@@ -195,7 +196,7 @@ template <typename T>
 int solve_nnls(Arena& ws, const T* At, int64_t r, int64_t p, const T* B, int64_t c, int64_t ldb, bool trans,
                const T* F0, T* Fout, int max_iter, double grad_tol, double safety, const double* pvec,
                int pcount, int pmax, double ptol, nenmf_device_status* st, cudaStream_t s, const T* Pt,
-               int64_t nup, T* Pout) {
+               int64_t nup, T* Pout, const uint8_t* Xpre) {
   if (r < 1 || p < 1 || c < 1) return NENMF_ERR_DIM;
   if (Pt != nullptr && (nup < 1 || Pout == nullptr)) return NENMF_ERR_VALUE;
   if (p > 64) return NENMF_ERR_UNSUPPORTED;
@@ -241,7 +242,25 @@ int solve_nnls(Arena& ws, const T* At, int64_t r, int64_t p, const T* B, int64_t
   if (!dry && !ws.ok) return NENMF_ERR_WORKSPACE;
   if (!fused) {
     NENMF_TRY(abt<T>(ws, At, p, At, p, r, W, s));                       // W = A^T A   (nnls.py:157)
-    NENMF_TRY(ab<T>(ws, At, p, r, B, c, ldb, trans, V, s));             // V = A^T B   (nnls.py:158)
+    bool vdone = false;
+    if constexpr (sizeof(T) == 4) {
+      // V = A^T B from one tensor-core pass over the prepared X: the Y side when
+      // B = X^T (X is c x r), the Z side when B = X (r x c); the other side of
+      // the pass is discarded
+      const int64_t nx = trans ? c : r, mx = trans ? r : c;
+      if (Xpre != nullptr && tc_pass_eligible(nx, mx, p)) {
+        float* junk = ws.take<float>((size_t)p * (trans ? r : r));
+        const float* A_f = reinterpret_cast<const float*>(At);
+        const float* F0_f = reinterpret_cast<const float*>(F0);
+        float* V_f = reinterpret_cast<float*>(V);
+        if (trans)  // Y (p x nx = c) = At X^T with At (p x mx = r); Z side fed F0 (p x c)
+          NENMF_TRY(dual_pass_tc_pre(ws, Xpre, nx, mx, A_f, dry ? A_f : F0_f, p, V_f, junk, s));
+        else        // Z (p x mx = c) = At X with At (p x nx = r); Y side fed F0 (p x c)
+          NENMF_TRY(dual_pass_tc_pre(ws, Xpre, nx, mx, dry ? A_f : F0_f, A_f, p, junk, V_f, s));
+        vdone = true;
+      }
+    }
+    if (!vdone) NENMF_TRY(ab<T>(ws, At, p, r, B, c, ldb, trans, V, s));  // V = A^T B   (nnls.py:158)
     NENMF_TRY(lipschitz<T>(ws, At, r, p, W, pvec, pcount, pmax, ptol, safety, Lbuf, st, s));  // (nnls.py:159)
   }
   if (!dry) {
@@ -346,7 +365,7 @@ namespace nenmf {
 #define NENMF_INST_NNLS(T)                                                                                    \
   template int solve_nnls<T>(Arena&, const T*, int64_t, int64_t, const T*, int64_t, int64_t, bool, const T*,  \
                              T*, int, double, double, const double*, int, int, double, nenmf_device_status*,   \
-                             cudaStream_t, const T*, int64_t, T*);                                           \
+                             cudaStream_t, const T*, int64_t, T*, const uint8_t*);                           \
   template int spectral_norm_sq<T>(Arena&, const T*, int64_t, int64_t, const double*, int, int, double, double*, \
                                    nenmf_device_status*, cudaStream_t);                                      \
   template int gradient<T>(Arena&, const T*, int64_t, int64_t, const T*, int64_t, int64_t, bool, const T*,    \

@@ -15,6 +15,8 @@
 // NeNMF exactly (reference test_factorize.py:161-176).
 #include "skinny.cuh"
 
+#include <cstdlib>
+
 namespace nenmf {
 
 // ----------------------------------------------------------------- abt ----
@@ -336,6 +338,120 @@ k_resid(const T* __restrict__ At, int p, int64_t r, const T* __restrict__ B, int
   }
 }
 
+// FP32 residual sums on the tensor pipe, X-oriented: for X (nx x mx, ld ldx)
+// and candidates (U1, V1), (U2, V2) (p x nx and p x mx, p <= 32), part sums
+// of ||U^T V - X||^2.  Warp tile 16 rows x 64 columns: the 16 x 8 blocks of
+// U^T V come from m16n8k8 TF32 MMAs in 3xTF32 split precision (hi by
+// truncation, lo = x - hi raw; relative error ~2^-20), the X values of the
+// tile are loaded (two floats per thread per block) before the MMAs so the
+// DRAM stream overlaps them.  Row/column tails are masked.
+__device__ __forceinline__ void mma_tf32_r(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm("mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t tf_hi(float x) { return __float_as_uint(x) & 0xffffe000u; }
+__device__ __forceinline__ uint32_t tf_lo(float x) { return __float_as_uint(x - __uint_as_float(tf_hi(x))); }
+
+template <int KT>
+__global__ void __launch_bounds__(256)
+k_resid_mma(const float* __restrict__ X, int64_t nx, int64_t mx, int64_t ldx, int p,
+            const float* __restrict__ U1, const float* __restrict__ V1, const float* __restrict__ U2,
+            const float* __restrict__ V2, double* __restrict__ part, const int* __restrict__ gate) {
+  if (gate != nullptr && *gate == 0) return;
+  __shared__ double red[33];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, gq = lane >> 2, tq = lane & 3;
+  const bool two = U2 != nullptr;
+  const int64_t ntr = (nx + 15) / 16, ntc = (mx + 63) / 64;
+  const int64_t tiles = ntr * ntc;
+  double acc0 = 0.0, acc1 = 0.0;
+  for (int64_t tile = (int64_t)blockIdx.x * 8 + wid; tile < tiles; tile += (int64_t)gridDim.x * 8) {
+    const int64_t i0 = (tile / ntc) * 16, j0 = (tile % ntc) * 64;
+    // X of the warp tile: rows i0 + gq (+8), columns j0 + 8 nt + 2 tq (+1)
+    float2 xv[8][2];
+#pragma unroll
+    for (int nt = 0; nt < 8; ++nt)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int64_t i = i0 + gq + 8 * h, j = j0 + 8 * nt + 2 * tq;
+        float2 v = make_float2(0.f, 0.f);
+        if (i < nx) {
+          const float* px = X + i * ldx + j;
+          if (j + 1 < mx && ((reinterpret_cast<uintptr_t>(px) & 7) == 0)) v = __ldcs(reinterpret_cast<const float2*>(px));
+          else {
+            if (j < mx) v.x = __ldcs(px);
+            if (j + 1 < mx) v.y = __ldcs(px + 1);
+          }
+        }
+        xv[nt][h] = v;
+      }
+    // A fragments (rows of U^T): a0 (gq, tq), a1 (gq+8, tq), a2 (gq, tq+4), a3 (gq+8, tq+4)
+    auto afrag = [&](const float* U, uint32_t (&ah)[KT][4], uint32_t (&al)[KT][4]) {
+#pragma unroll
+      for (int kt = 0; kt < KT; ++kt)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int a = 8 * kt + tq + ((q & 2) ? 4 : 0);
+          const int64_t i = i0 + gq + ((q & 1) ? 8 : 0);
+          const float u = (a < p && i < nx) ? __ldg(&U[(int64_t)a * nx + i]) : 0.f;
+          ah[kt][q] = tf_hi(u);
+          al[kt][q] = tf_lo(u);
+        }
+    };
+    uint32_t a1h[KT][4], a1l[KT][4], a2h[KT][4], a2l[KT][4];
+    afrag(U1, a1h, a1l);
+    if (two) {
+      if (U2 != U1) afrag(U2, a2h, a2l);
+      else {
+#pragma unroll
+        for (int kt = 0; kt < KT; ++kt)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            a2h[kt][q] = a1h[kt][q];
+            a2l[kt][q] = a1l[kt][q];
+          }
+      }
+    }
+    float s0 = 0.f, s1 = 0.f;
+#pragma unroll
+    for (int nt = 0; nt < 8; ++nt) {
+      const int64_t jb = j0 + 8 * nt + gq;  // B fragment column
+      auto prod = [&](const float* V, const uint32_t (&ah)[KT][4], const uint32_t (&al)[KT][4], float (&c)[4]) {
+#pragma unroll
+        for (int kt = 0; kt < KT; ++kt) {
+          const int a0 = 8 * kt + tq, a1 = a0 + 4;
+          const float v0 = (a0 < p && jb < mx) ? __ldg(&V[(int64_t)a0 * mx + jb]) : 0.f;
+          const float v1 = (a1 < p && jb < mx) ? __ldg(&V[(int64_t)a1 * mx + jb]) : 0.f;
+          const uint32_t b0h = tf_hi(v0), b1h = tf_hi(v1), b0l = tf_lo(v0), b1l = tf_lo(v1);
+          mma_tf32_r(c, al[kt], b0h, b1h);
+          mma_tf32_r(c, ah[kt], b0l, b1l);
+          mma_tf32_r(c, ah[kt], b0h, b1h);
+        }
+      };
+      float c1[4] = {0.f, 0.f, 0.f, 0.f};
+      prod(V1, a1h, a1l, c1);
+      const float d0 = c1[0] - xv[nt][0].x, d1 = c1[1] - xv[nt][0].y, d2 = c1[2] - xv[nt][1].x,
+                  d3 = c1[3] - xv[nt][1].y;
+      s0 = fmaf(d0, d0, fmaf(d1, d1, fmaf(d2, d2, fmaf(d3, d3, s0))));
+      if (two) {
+        float c2[4] = {0.f, 0.f, 0.f, 0.f};
+        prod(V2, a2h, a2l, c2);
+        const float e0 = c2[0] - xv[nt][0].x, e1 = c2[1] - xv[nt][0].y, e2 = c2[2] - xv[nt][1].x,
+                    e3 = c2[3] - xv[nt][1].y;
+        s1 = fmaf(e0, e0, fmaf(e1, e1, fmaf(e2, e2, fmaf(e3, e3, s1))));
+      }
+    }
+    acc0 += (double)s0;
+    acc1 += (double)s1;
+  }
+  const double b0 = block_sum(acc0, red);
+  const double b1 = block_sum(acc1, red);
+  if (threadIdx.x == 0) {
+    part[2 * blockIdx.x] = b0;
+    part[2 * blockIdx.x + 1] = b1;
+  }
+}
+
 // fixed-order sum of `n` pairs -> out[0..1]; optional gate
 __global__ void k_pair_final(const double* __restrict__ part, int64_t n, double* __restrict__ out,
                              const int* __restrict__ gate) {
@@ -359,6 +475,33 @@ int resid(Arena& ws, const T* At, int64_t p, int64_t r, const T* B, int64_t c, i
           const T* F1, const T* F2, double* out2, const int* gate, cudaStream_t st) {
   if (p < 1 || r < 1 || c < 1) return NENMF_ERR_DIM;
   if (p > 64) return NENMF_ERR_UNSUPPORTED;
+  if constexpr (sizeof(T) == 4) {
+    if (p <= 32 && getenv("NENMF_RESID_SIMT") == nullptr) {
+      // X-oriented tensor-core kernel: B is X (r x c) or, transposed, X (c x r)
+      const int64_t nx = trans ? c : r, mx = trans ? r : c;
+      const float* U1 = reinterpret_cast<const float*>(trans ? F1 : At);
+      const float* U2 = F2 == nullptr ? nullptr : reinterpret_cast<const float*>(trans ? F2 : At);
+      const float* V1 = reinterpret_cast<const float*>(trans ? At : F1);
+      const float* V2 = F2 == nullptr ? nullptr : reinterpret_cast<const float*>(trans ? At : F2);
+      int sms = sm_count();
+      if (sms <= 0) sms = 148;
+      const int64_t tiles = cdiv(nx, 16) * cdiv(mx, 64);
+      const unsigned grid = (unsigned)imax(1, imin((int64_t)sms * 8, cdiv(tiles, 8)));
+      double* part = ws.take<double>((size_t)grid * 2);
+      if (ws.base == nullptr) return NENMF_OK;
+      if (!ws.ok) return NENMF_ERR_WORKSPACE;
+      const float* Xf = reinterpret_cast<const float*>(B);
+      const int kt = (int)cdiv(p, 8);
+      if (kt == 1) k_resid_mma<1><<<grid, 256, 0, st>>>(Xf, nx, mx, ldb, (int)p, U1, V1, U2, V2, part, gate);
+      else if (kt == 2) k_resid_mma<2><<<grid, 256, 0, st>>>(Xf, nx, mx, ldb, (int)p, U1, V1, U2, V2, part, gate);
+      else if (kt == 3) k_resid_mma<3><<<grid, 256, 0, st>>>(Xf, nx, mx, ldb, (int)p, U1, V1, U2, V2, part, gate);
+      else k_resid_mma<4><<<grid, 256, 0, st>>>(Xf, nx, mx, ldb, (int)p, U1, V1, U2, V2, part, gate);
+      NENMF_LAUNCH_CHECK();
+      k_pair_final<<<1, 256, 0, st>>>(part, (int64_t)grid, out2, gate);
+      NENMF_LAUNCH_CHECK();
+      return NENMF_OK;
+    }
+  }
   const int64_t nchunk = cdiv(r, AB_RCHUNK);
   dim3 grid((unsigned)cdiv(c, AB_CB), (unsigned)nchunk);
   double* part = ws.take<double>((size_t)grid.x * grid.y * 2);

@@ -154,13 +154,16 @@ class _DeviceLoop:
                        status_index=self._slot(t, "F"), next_bt=self.Rt, next_out=self.FR, **kw)
             self.fr_ready = True
         else:
+            # FP32: V = A^T B from one tensor-core pass over the prepared X
+            if not hasattr(self, "Xp"):
+                self.Xp = _ops.prepare_x(self.X, self.p)
             # G-half: A = F^T, B = X^T read in place (factorize.py:94-95)
             _ops.solve(self.F, self.X, self.Gt, self.Gt_alt, trans_b=True,
-                       status_index=self._slot(t, "G"), **kw)
+                       status_index=self._slot(t, "G"), Xp=self.Xp, **kw)
             self.Gt, self.Gt_alt = self.Gt_alt, self.Gt
             # F-half: A = G, B = X (factorize.py:97-98)
             _ops.solve(self.Gt, self.X, self.F, self.F_alt, trans_b=False,
-                       status_index=self._slot(t, "F"), **kw)
+                       status_index=self._slot(t, "F"), Xp=self.Xp, **kw)
         self.F, self.F_alt = self.F_alt, self.F
 
     def drain(self) -> None:
