@@ -463,7 +463,7 @@ int rsi(Arena& ws, const T* X, int64_t n, int64_t m, int64_t ldx, const T* omega
     orthonormalize<T>(c, L, m, nu, st, s);
     need = max(need, c.used);
     Arena d(nullptr, 0);
-    orthonormalize_pair<T>(d, L, n, Rt, m, nu, st, s);
+    orthonormalize_pair<T>(d, const_cast<T*>(sent), n, const_cast<T*>(sent), m, nu, st, s);  // both panels counted
     need = max(need, d.used);
   }
   char* sbase = scratch.take<char>(need);

@@ -11,7 +11,8 @@ w = workloads.make_workload(2, dtype=dtype)
 Xd = _lib.to_device(w.X, dtype); G0 = _lib.to_device(w.G0, dtype); F0 = _lib.to_device(w.F0, dtype)
 cfg = nm.OuterConfig(inner=nm.InnerSolverConfig(max_iter=w.inner), time_budget_seconds=0.0,
                      max_outer_iterations=outer, trace_every=outer)
-run = lambda: nm.factorize_vanilla(Xd, nm.FactorPair(G=G0, F=F0, p=w.p), cfg, return_device=True)
+tv = len(sys.argv) > 3
+run = lambda: nm.factorize_vanilla(Xd, nm.FactorPair(G=G0, F=F0, p=w.p), cfg, return_device=True, tensor_v=tv)
 run(); torch.cuda.synchronize()
 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 a.record(); run(); b.record(); torch.cuda.synchronize()
