@@ -340,11 +340,23 @@ def kernel_rooflines(w, Xd, dtype):
         # FP32: the passes of a sketch stream the prepared (tile-major bf16 hi/lo) copy of X,
         # 4 bytes per element like X itself; it is made once per sketch (timed separately)
         ms_prep = ev_time(lambda: _ops.prepare_x(Xd, w.nu), 5)
-        ms_pass = ev_time(lambda: _ops.dual_pass_prepared(Xp, w.n, w.m, Rt, L, Yt, Zt), 20)
+        ms_op = ev_time(lambda: _ops.dual_pass_prepared(Xp, w.n, w.m, Rt, L, Yt, Zt), 20)
+        # the kernel alone: CUDA events around each k_dual_bulk launch on its stream
+        import ctypes
+        lib = _lib.load_library()
+        lib.nenmf_debug_xpass_ms(None)
+        lib.nenmf_debug_xpass_timing(1)
+        for _ in range(20):
+            _ops.dual_pass_prepared(Xp, w.n, w.m, Rt, L, Yt, Zt)
+        tot = ctypes.c_double(0.0)
+        cnt = lib.nenmf_debug_xpass_ms(ctypes.byref(tot))
+        lib.nenmf_debug_xpass_timing(0)
+        ms_pass = tot.value / max(cnt, 1)
         kname = "RSI X-pass (k_dual_bulk: bulk-copy stream of the prepared X -> X*A and X^T*B, tcgen05 BF16x3)"
     else:
         ms_prep = 0.0
         ms_pass = ev_time(lambda: _ops.dual_pass(Xd, Rt, L, Yt, Zt), 10)
+        ms_op = ms_pass
         kname = "RSI X-pass (k_dual: one read of X -> X*A and X^T*B)"
     del Xp
     pass_bytes = w.n * w.m * Xd.element_size()
@@ -372,7 +384,10 @@ def kernel_rooflines(w, Xd, dtype):
            "achieved": pass_gbs, "peak": hbm, "unit": "GB/s", "frac": pass_gbs / hbm,
            "traffic": _traffic("k_dual_bulk"), "peak_source": src,
            "algorithmic_bytes_per_launch": pass_bytes, "ms_per_launch": ms_pass,
-           "ms_per_launch_includes": "skinny-operand split (2 small kernels) + k_dual_bulk + slab reductions",
+           "ms_per_launch_source": "CUDA events around each k_dual_bulk launch on its stream (20 passes)",
+           "ms_per_pass_op": ms_op,
+           "pass_op_gbs": pass_bytes / (ms_op * 1e-3) / 1e9,
+           "pass_op_includes": "skinny-operand split + k_dual_bulk + slab reduction (3 launches)",
            "prepare_x_ms_once_per_sketch": ms_prep,
            "rsi_total_ms": ms_rsi, "rsi_effective_gbs": rsi_bytes / (ms_rsi * 1e-3) / 1e9,
            "rsi_bytes_model": "(2q+2)*n*m*s_X (SURVEY 8d)"}
@@ -388,7 +403,8 @@ def kernel_rooflines(w, Xd, dtype):
               "flops_per_iter": flops_it, "achieved_tflops": flops_it / (us_it * 1e-6) / 1e12,
               "hbm_floor_us_if_streamed": stream_bytes_it / (hbm * 1e9) * 1e6,
               "traffic": _traffic("k_nnls_mma")}
-    table = {"dual_pass_ms": ms_pass, "prepare_x_ms": ms_prep, "rsi_ms": ms_rsi, "solve_F_half_ms": ms_solve}
+    table = {"dual_pass_kernel_ms": ms_pass, "dual_pass_op_ms": ms_op, "prepare_x_ms": ms_prep, "rsi_ms": ms_rsi,
+             "solve_F_half_ms": ms_solve}
     return {"rsi": rsi, "solver": solver, "table": table}
 
 

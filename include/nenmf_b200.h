@@ -270,6 +270,15 @@ int nenmf_compress_prepared(int dtype, const void* X, const void* Xp, int64_t n,
                             int64_t ldx, const void* L, const void* Rt, int64_t nu,
                             void* XL, void* XRt, void* ws, size_t ws_bytes, void* stream);
 
+/* ---- measurement hooks (not part of the reference interface) ------------
+ * While enabled, every tensor-core X-pass kernel launch is bracketed by CUDA
+ * events on its stream; nenmf_debug_xpass_ms waits for them and returns the
+ * number of launches timed and their total duration (the roofline of
+ * bench.py is computed from the kernel alone, not the small launches around
+ * it).  Process-wide debug state. */
+void nenmf_debug_xpass_timing(int on);
+int nenmf_debug_xpass_ms(double* total_ms);
+
 #ifdef __cplusplus
 }
 #endif

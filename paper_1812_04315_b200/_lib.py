@@ -65,6 +65,8 @@ _SIGS = {
     "nenmf_panel_gram": (_i32, [_i32, _vp, _i64, _i64, _vp, _vp, _sz, _vp]),
     "nenmf_panel_factor": (_i32, [_vp, _i64, _i32, _vp, _vp, _vp, _vp]),
     "nenmf_panel_trsm": (_i32, [_i32, _vp, _i64, _i64, _vp, _vp, _vp, _i64, _i32, _vp]),
+    "nenmf_debug_xpass_timing": (None, [_i32]),
+    "nenmf_debug_xpass_ms": (_i32, [C.POINTER(C.c_double)]),
     "nenmf_prepared_x_bytes": (_sz, [_i32, _i64, _i64, _i64]),
     "nenmf_prepare_x": (_i32, [_i32, _vp, _i64, _i64, _i64, _i64, _vp, _vp]),
     "nenmf_dual_pass_prepared_workspace_bytes": (_sz, [_i32, _i64, _i64, _i64]),

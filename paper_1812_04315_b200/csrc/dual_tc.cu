@@ -289,6 +289,10 @@ k_dual_bulk(const uint8_t* __restrict__ Xs, int64_t n, int64_t m, const uint8_t*
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  // programmatic dependent launch: the slab reduction may be scheduled now
+  // (it waits for this grid's completion); this grid's prologue above ran
+  // while the skinny-split kernel was finishing
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const uint32_t tmem = tmem_base_sh;
   // TMEM columns: Y buffers [0, 2 KPAD), Z accumulators [2 KPAD, 2 KPAD + CT KPAD)
   const uint32_t ycol0 = 0, zcol0 = 2 * KPAD;
@@ -296,6 +300,7 @@ k_dual_bulk(const uint8_t* __restrict__ Xs, int64_t n, int64_t m, const uint8_t*
   if (wid == PROD_WARP) {
     // ------------------------------------------------------------ producer
     if (lane == 0) {
+      asm volatile("griddepcontrol.wait;" ::: "memory");  // the split skinny operands are complete
       const uint64_t pol_x = policy_evict_first(), pol_s = policy_evict_last();
       int t = 0, row_count = 0;
       for (int u = blockIdx.x; u < U.units; u += gridDim.x) {
@@ -427,6 +432,7 @@ k_dual_bulk(const uint8_t* __restrict__ Xs, int64_t n, int64_t m, const uint8_t*
 // fixed-order slab sums of both products in one launch: [0, cy) -> Y, [cy, cy + cz) -> Z
 __global__ void k_slabs(const float* __restrict__ py, int ny, int64_t cy, float* __restrict__ oy,
                         const float* __restrict__ pz, int nz, int64_t cz, float* __restrict__ oz) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // programmatic launch after the pass kernel
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= cy + cz) return;
   const bool isY = i < cy;
@@ -485,6 +491,24 @@ inline Units choose_units(int64_t n, int64_t m, int64_t k, int ctmax, int sms) {
 }
 
 }  // namespace tc
+
+// Measurement hook (bench.py's roofline): while enabled, every k_dual_bulk
+// launch is bracketed by CUDA events on its own stream, so the kernel's
+// duration is known without the small launches around it.  Debug facility:
+// process-wide, guarded by a mutex.
+namespace {
+std::mutex g_xt_mu;
+bool g_xt_on = false;
+std::vector<std::pair<cudaEvent_t, cudaEvent_t>> g_xt_ev;
+}  // namespace
+
+bool xpass_timing_begin(cudaEvent_t* e0, cudaEvent_t* e1) {
+  std::lock_guard<std::mutex> g(g_xt_mu);
+  if (!g_xt_on) return false;
+  if (cudaEventCreate(e0) != cudaSuccess || cudaEventCreate(e1) != cudaSuccess) return false;
+  g_xt_ev.emplace_back(*e0, *e1);
+  return true;
+}
 
 bool tc_pass_eligible(int64_t n, int64_t m, int64_t k) {
   if (k < 1 || k > 128 || n < tc::TILE || m < tc::TILE) return false;
@@ -556,17 +580,40 @@ static int dual_pass_tc_chunk(Arena& ws, const uint8_t* Xs, int64_t n, int64_t m
   const unsigned grid = (unsigned)imin(U.units, sms);
   float* Yo = Ypart ? Ypart : Yt;
   float* Zo = Zpart ? Zpart : Zt;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  const bool timed = xpass_timing_begin(&ev0, &ev1);
+  if (timed) cudaEventRecord(ev0, s);
+  cudaLaunchAttribute pdl[1];
+  pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  pdl[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(NWARPS * 32);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cfg.attrs = pdl;
+  cfg.numAttrs = 1;
   if (kpad == 32) {
     NENMF_CUDA_TRY(set_smem(k_dual_bulk<32>, smem));
-    k_dual_bulk<32><<<grid, NWARPS * 32, smem, s>>>(Xs, n, m, A2, B2, (int)k, U, Yo, Zo);
+    NENMF_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_dual_bulk<32>, Xs, n, m, (const uint8_t*)A2, (const uint8_t*)B2, (int)k,
+                                      U, Yo, Zo));
   } else {
     NENMF_CUDA_TRY(set_smem(k_dual_bulk<16>, smem));
-    k_dual_bulk<16><<<grid, NWARPS * 32, smem, s>>>(Xs, n, m, A2, B2, (int)k, U, Yo, Zo);
+    NENMF_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_dual_bulk<16>, Xs, n, m, (const uint8_t*)A2, (const uint8_t*)B2, (int)k,
+                                      U, Yo, Zo));
   }
   NENMF_LAUNCH_CHECK();
+  if (timed) cudaEventRecord(ev1, s);
   if (Ypart || Zpart) {
     const int64_t cy = Ypart ? k * n : 0, cz = Zpart ? k * m : 0;
-    k_slabs<<<(unsigned)cdiv(cy + cz, 256), 256, 0, s>>>(Ypart, U.n_cb, cy, Yt, Zpart, U.n_rc, cz, Zt);
+    cudaLaunchConfig_t c2 = {};
+    c2.gridDim = dim3((unsigned)cdiv(cy + cz, 256));
+    c2.blockDim = dim3(256);
+    c2.stream = s;
+    c2.attrs = pdl;
+    c2.numAttrs = 1;
+    NENMF_CUDA_TRY(cudaLaunchKernelEx(&c2, k_slabs, (const float*)Ypart, (int)U.n_cb, cy, Yt, (const float*)Zpart,
+                                      (int)U.n_rc, cz, Zt));
     NENMF_LAUNCH_CHECK();
   }
   return NENMF_OK;
@@ -588,3 +635,30 @@ int dual_pass_tc(Arena& ws, const float* X, int64_t n, int64_t m, int64_t ldx, c
 }
 
 }  // namespace nenmf
+
+extern "C" {
+void nenmf_debug_xpass_timing(int on) {
+  std::lock_guard<std::mutex> g(nenmf::g_xt_mu);
+  nenmf::g_xt_on = on != 0;
+}
+
+// Total duration (ms) and count of the k_dual_bulk launches timed since the
+// last call (waits for them); clears the list.
+int nenmf_debug_xpass_ms(double* total_ms) {
+  std::lock_guard<std::mutex> g(nenmf::g_xt_mu);
+  double tot = 0.0;
+  int cnt = 0;
+  for (auto& pr : nenmf::g_xt_ev) {
+    float ms = 0.f;
+    if (cudaEventSynchronize(pr.second) == cudaSuccess && cudaEventElapsedTime(&ms, pr.first, pr.second) == cudaSuccess) {
+      tot += ms;
+      ++cnt;
+    }
+    cudaEventDestroy(pr.first);
+    cudaEventDestroy(pr.second);
+  }
+  nenmf::g_xt_ev.clear();
+  if (total_ms != nullptr) *total_ms = tot;
+  return cnt;
+}
+}  // extern "C"
