@@ -266,6 +266,17 @@ int nenmf_rsi_prepared(int dtype, const void* X, const void* Xp, int64_t n, int6
                        int64_t ldx, const void* omega_l_t, const void* omega_r, int64_t nu,
                        int q, void* L, void* Rt, nenmf_device_status* status,
                        void* ws, size_t ws_bytes, void* stream);
+/* Randomized power iteration (compression.py:144-176): the products of
+ * nenmf_rsi without the intermediate orthonormalisations, one at the end.
+ * Status NUMERICAL_COLLAPSE with iteration k when an iterate overflows at
+ * step k (FP32 tracks power-of-two scale factors so the fp64 overflow point
+ * is reproduced) or, with iteration q, when a column is entirely zero.  Xp
+ * may be NULL; workspace: nenmf_rsi_prepared_workspace_bytes (Xp given) or
+ * nenmf_rsi_workspace_bytes. */
+int nenmf_power_iteration(int dtype, const void* X, const void* Xp, int64_t n, int64_t m, int64_t ldx,
+                          const void* omega_l_t, const void* omega_r, int64_t nu, int q, void* L,
+                          void* Rt, nenmf_device_status* status, void* ws, size_t ws_bytes,
+                          void* stream);
 int nenmf_compress_prepared(int dtype, const void* X, const void* Xp, int64_t n, int64_t m,
                             int64_t ldx, const void* L, const void* Rt, int64_t nu,
                             void* XL, void* XRt, void* ws, size_t ws_bytes, void* stream);

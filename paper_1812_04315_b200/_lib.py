@@ -74,6 +74,8 @@ _SIGS = {
     "nenmf_rsi_prepared_workspace_bytes": (_sz, [_i32, _i64, _i64, _i64]),
     "nenmf_rsi_prepared": (_i32, [_i32, _vp, _vp, _i64, _i64, _i64, _vp, _vp, _i64, _i32, _vp, _vp, _vp, _vp, _sz,
                                   _vp]),
+    "nenmf_power_iteration": (_i32, [_i32, _vp, _vp, _i64, _i64, _i64, _vp, _vp, _i64, _i32, _vp, _vp, _vp, _vp,
+                                     _sz, _vp]),
     "nenmf_compress_prepared": (_i32, [_i32, _vp, _vp, _i64, _i64, _i64, _vp, _vp, _i64, _vp, _vp, _vp, _sz, _vp]),
 }
 

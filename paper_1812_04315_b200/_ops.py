@@ -197,6 +197,20 @@ def rsi(X, omega_l_t, omega_r, q: int, L, Rt, status, Xp=None) -> None:
     _lib.check(rc, "subspace_iteration_pair")
 
 
+def power_iteration(X, omega_l_t, omega_r, q: int, L, Rt, status, Xp=None) -> None:
+    lib, _ = _lib.require_device()
+    code = _lib.code_of(_dt(X))
+    n, m = X.shape
+    nu = omega_r.shape[0]
+    nbytes = (lib.nenmf_rsi_prepared_workspace_bytes(code, n, m, nu) if Xp is not None
+              else lib.nenmf_rsi_workspace_bytes(code, n, m, nu))
+    ws = _lib.workspace(nbytes)
+    rc = lib.nenmf_power_iteration(code, X.data_ptr(), _lib.ptr(Xp), n, m, X.stride(0), omega_l_t.data_ptr(),
+                                   omega_r.data_ptr(), nu, int(q), L.data_ptr(), Rt.data_ptr(),
+                                   _lib.status_ptr(status), ws.data_ptr(), ws.numel(), _lib.stream_handle())
+    _lib.check(rc, "power_iteration_pair")
+
+
 def compress(X, L, Rt, XL, XRt, Xp=None) -> None:
     lib, _ = _lib.require_device()
     code = _lib.code_of(_dt(X))

@@ -174,7 +174,7 @@ def sketch_draws_device(n: int, m: int, nu: int, seed: int, dtype: str):
     return olt, orr, ok
 
 
-def rsi_device(Xd, nu: int, q: int, seed: int, prepared=None, draws=None):
+def rsi_device(Xd, nu: int, q: int, seed: int, prepared=None, draws=None, power: bool = False):
     """Device RSI on a resident X (CUDA tensor).  Returns (L, Rt, status)
     tensors; Rt is R transposed (nu x m).  ``prepared`` is an optional
     ``_ops.prepare_x`` copy of Xd (made once, reused by the compression pass).
@@ -188,16 +188,17 @@ def rsi_device(Xd, nu: int, q: int, seed: int, prepared=None, draws=None):
     L = torch.empty((nu, n), dtype=Xd.dtype, device="cuda")
     Rt = torch.empty((nu, m), dtype=Xd.dtype, device="cuda")
     status = _lib.new_status()
+    run = _ops.power_iteration if power else _ops.rsi  # compression.py:144-176 / :120-141
     if dev is not None:
         om_lt, om_r, ok = dev
-        _ops.rsi(Xd, om_lt, om_r, q, L, Rt, status, Xp=prepared)
+        run(Xd, om_lt, om_r, q, L, Rt, status, Xp=prepared)
         if bool(ok.item()):
             return L, Rt, status
     omega_l, omega_r = sketch_draws(n, m, nu, seed)
     om_lt = _lib.to_device(np.ascontiguousarray(omega_l.T), dtype)
     om_r = _lib.to_device(omega_r, dtype)
     status.zero_()
-    _ops.rsi(Xd, om_lt, om_r, q, L, Rt, status, Xp=prepared)
+    run(Xd, om_lt, om_r, q, L, Rt, status, Xp=prepared)
     return L, Rt, status
 
 
@@ -222,6 +223,20 @@ def subspace_iteration_pair(X, nu: int, q: int, seed: int, *, dtype: str = "fp64
     """Randomized subspace iteration with a QR after every product
     (compression.py:120-141), on the GPU.  Returns NumPy L = Q_col^T and
     R = Q_row like the reference; the device copies are cached on the pair."""
+    return _iterated_pair(X, nu, q, seed, dtype, SUBSPACE_ITERATION)
+
+
+def power_iteration_pair(X, nu: int, q: int, seed: int, *, dtype: str = "fp64") -> SketchPair:
+    """Randomized power iteration: the same draws and alternating products as
+    subspace_iteration_pair, orthonormalised only once at the end
+    (compression.py:144-176), on the GPU.  An iterate that overflows at step k
+    raises NumericalCollapseError(iteration=k) (FP32 tracks power-of-two scale
+    factors so that the reference's fp64 overflow step is reproduced); a zero
+    column after the last step raises it with iteration=q."""
+    return _iterated_pair(X, nu, q, seed, dtype, POWER_ITERATION)
+
+
+def _iterated_pair(X, nu: int, q: int, seed: int, dtype: str, scheme: str) -> SketchPair:
     if _is_device_tensor(X):
         Xd = X
         dtype = "fp64" if str(X.dtype).endswith("float64") else "fp32"
@@ -240,12 +255,13 @@ def subspace_iteration_pair(X, nu: int, q: int, seed: int, *, dtype: str = "fp64
     # a device-resident X is prepared once here and the copy is kept on the
     # pair, so factorize_compressed's compression pass reuses it
     Xp = _ops.prepare_x(Xd, nu) if on_device else None
-    L, Rt, status = rsi_device(Xd, nu, q, seed, prepared=Xp)
+    power = scheme == POWER_ITERATION
+    L, Rt, status = rsi_device(Xd, nu, q, seed, prepared=Xp, power=power)
     st = _lib.read_status(status)[0]
     if st["code"] != 0:
-        raise_for_status(int(st["code"]), int(st["iteration"]), "subspace iteration")
+        raise_for_status(int(st["code"]), int(st["iteration"]), "power iteration" if power else "subspace iteration")
     pair = SketchPair(L=_lib.to_host(L), R=np.ascontiguousarray(_lib.to_host(Rt).T), nu=nu,
-                      scheme=SUBSPACE_ITERATION, q=q, seed=seed)
+                      scheme=scheme, q=q, seed=seed)
     pair.device[dtype] = (L, Rt)
     if Xp is not None:
         pair.device["prepared"] = (_x_key(Xd), Xp)

@@ -286,7 +286,8 @@ int nenmf_orthonormalize(int dtype, void* Pt, int64_t rows, int64_t k, nenmf_dev
 size_t nenmf_rsi_workspace_bytes(int dtype, int64_t n, int64_t m, int64_t nu) {
   Arena a(nullptr, 0);
   NENMF_DISPATCH(dtype, [&] {
-    return rsi<scalar_t>(a, nullptr, n, m, m, nullptr, nullptr, nu, 1, nullptr, nullptr, nullptr, nullptr);
+    return rsi<scalar_t>(a, nullptr, n, m, m, nullptr, nullptr, nu, 1, nullptr, nullptr, nullptr, nullptr, nullptr,
+                         1);  // sized for both schemes (power carves a little more)
   });
   // compress reuses the same scratch shape as one pass
   size_t c = nenmf_dual_pass_workspace_bytes(dtype, n, m, nu);
@@ -377,7 +378,7 @@ size_t nenmf_rsi_prepared_workspace_bytes(int dtype, int64_t n, int64_t m, int64
   if (nenmf_prepared_x_bytes(dtype, n, m, nu) == 0) return nenmf_rsi_workspace_bytes(dtype, n, m, nu);
   Arena a(nullptr, 0);
   rsi<float>(a, nullptr, n, m, m, nullptr, nullptr, nu, 1, nullptr, nullptr, nullptr, nullptr,
-             reinterpret_cast<const uint8_t*>(16));
+             reinterpret_cast<const uint8_t*>(16), 1);
   size_t c = nenmf_dual_pass_prepared_workspace_bytes(dtype, n, m, nu);
   return (a.used > c ? a.used : c) + 256;
 }
@@ -390,6 +391,17 @@ int nenmf_rsi_prepared(int dtype, const void* X, const void* Xp, int64_t n, int6
   return NENMF_DISPATCH(dtype, [&] {
     return rsi<scalar_t>(a, C<scalar_t>(X), n, m, ldx, C<scalar_t>(omega_l_t), C<scalar_t>(omega_r), nu, q,
                          M<scalar_t>(L), M<scalar_t>(Rt), status, S(stream), static_cast<const uint8_t*>(Xp));
+  });
+}
+
+int nenmf_power_iteration(int dtype, const void* X, const void* Xp, int64_t n, int64_t m, int64_t ldx,
+                          const void* omega_l_t, const void* omega_r, int64_t nu, int q, void* L, void* Rt,
+                          nenmf_device_status* status, void* ws, size_t ws_bytes, void* stream) {
+  if (ws == nullptr) return NENMF_ERR_VALUE;
+  Arena a(ws, ws_bytes);
+  return NENMF_DISPATCH(dtype, [&] {
+    return rsi<scalar_t>(a, C<scalar_t>(X), n, m, ldx, C<scalar_t>(omega_l_t), C<scalar_t>(omega_r), nu, q,
+                         M<scalar_t>(L), M<scalar_t>(Rt), status, S(stream), static_cast<const uint8_t*>(Xp), 1);
   });
 }
 

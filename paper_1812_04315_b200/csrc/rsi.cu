@@ -416,10 +416,95 @@ int orthonormalize(Arena& ws, T* Pt, int64_t rows, int64_t k, nenmf_device_statu
   return orthonormalize_cholqr<T>(ws, Pt, rows, k, st, s);
 }
 
+// ====================================================== power iteration ====
+// compression.py:144-176 keeps the raw power iterates and checks them for
+// overflow after every step.  FP64 runs that arithmetic as is (finiteness
+// check per step).  FP32 rescales every iterate by a power of two after each
+// pass (exact; the subspace is unchanged) and tracks the exponent per chain,
+// so the reference's fp64 overflow is reproduced: step k collapses when an
+// iterate's magnitude reaches 2^1024.
+struct PowerChains {
+  unsigned maxbits[4];  // |x| max of the two panels of the current pass (float bits)
+  int bad;              // a non-finite value was seen
+  int exp[2];           // accumulated exponents: [0] L-chain (Y), [1] R-chain (Z)
+};
+
+__global__ void k_power_stats(const float* __restrict__ P0, int64_t c0, const float* __restrict__ P1, int64_t c1,
+                              PowerChains* pc) {
+  __shared__ unsigned sm[2];
+  __shared__ int sbad;
+  if (threadIdx.x < 2) sm[threadIdx.x] = 0u;
+  if (threadIdx.x == 0) sbad = 0;
+  __syncthreads();
+  unsigned m0 = 0u, m1 = 0u;
+  bool bad = false;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < c0 + c1; i += stride) {
+    const float v = i < c0 ? P0[i] : P1[i - c0];
+    bad |= !isfinite(v);
+    const unsigned b = __float_as_uint(fabsf(v));
+    if (i < c0) m0 = b > m0 ? b : m0;
+    else m1 = b > m1 ? b : m1;
+  }
+  atomicMax(&sm[0], m0);
+  atomicMax(&sm[1], m1);
+  if (bad) sbad = 1;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    atomicMax(&pc->maxbits[0], sm[0]);
+    atomicMax(&pc->maxbits[1], sm[1]);
+    if (sbad) atomicExch(&pc->bad, 1);
+  }
+}
+
+// scale panel i by 2^-e_i (e_i = exponent of its max), add e_i to its chain;
+// block 0 / thread 0 also applies the emulated fp64 overflow rule
+__global__ void k_power_scale(float* __restrict__ P0, int64_t c0, int chain0, float* __restrict__ P1, int64_t c1,
+                              int chain1, PowerChains* pc, int step, nenmf_device_status* st) {
+  const float mx0 = __uint_as_float(pc->maxbits[0]), mx1 = __uint_as_float(pc->maxbits[1]);
+  const int e0 = mx0 > 0.f ? ilogbf(mx0) : 0, e1 = mx1 > 0.f ? ilogbf(mx1) : 0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < c0 + c1; i += stride) {
+    if (i < c0) P0[i] = ldexpf(P0[i], -e0);
+    else P1[i - c0] = ldexpf(P1[i - c0], -e1);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    const int E0 = pc->exp[chain0] + e0, E1 = pc->exp[chain1] + e1;
+    pc->exp[chain0] = E0;
+    pc->exp[chain1] = E1;
+    if (pc->bad || E0 >= 1024 || E1 >= 1024) status_fail(st, NENMF_ERR_NUMERICAL_COLLAPSE, step);
+    pc->maxbits[0] = pc->maxbits[1] = 0u;
+    pc->bad = 0;
+  }
+}
+
+template <typename T>
+__global__ void k_power_finite(const T* __restrict__ P0, int64_t c0, const T* __restrict__ P1, int64_t c1, int step,
+                               nenmf_device_status* st) {
+  bool bad = false;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < c0 + c1; i += stride)
+    bad |= !isfinite(i < c0 ? P0[i] : P1[i - c0]);
+  if (__syncthreads_or(bad) && threadIdx.x == 0) status_fail(st, NENMF_ERR_NUMERICAL_COLLAPSE, step);
+}
+
+// a panel column (row of the short-major storage) that is entirely zero
+template <typename T>
+__global__ void k_zero_rows(const T* __restrict__ P0, int64_t len0, const T* __restrict__ P1, int64_t len1, int k,
+                            int step, nenmf_device_status* st) {
+  if (st != nullptr && st->code != 0) return;
+  const int b = blockIdx.x;
+  const T* row = b < k ? P0 + (int64_t)b * len0 : P1 + (int64_t)(b - k) * len1;
+  const int64_t len = b < k ? len0 : len1;
+  bool any = false;
+  for (int64_t i = threadIdx.x; i < len; i += blockDim.x) any |= row[i] != T(0);
+  if (!__syncthreads_or(any) && threadIdx.x == 0) status_fail(st, NENMF_ERR_NUMERICAL_COLLAPSE, step);
+}
+
 // ================================================================= RSI ====
 template <typename T>
 int rsi(Arena& ws, const T* X, int64_t n, int64_t m, int64_t ldx, const T* omega_l_t, const T* omega_r, int64_t nu,
-        int q, T* L, T* Rt, nenmf_device_status* st, cudaStream_t s, const uint8_t* Xpre) {
+        int q, T* L, T* Rt, nenmf_device_status* st, cudaStream_t s, const uint8_t* Xpre, int power) {
   if (nu < 1 || nu > min(n, m)) return NENMF_ERR_DIM;
   if (q < 1) return NENMF_ERR_VALUE;
   const bool dry = ws.base == nullptr;
@@ -432,6 +517,7 @@ int rsi(Arena& ws, const T* X, int64_t n, int64_t m, int64_t ldx, const T* omega
   uint8_t* Xs = own ? ws.take<uint8_t>(tc_presplit_bytes(n, m)) : const_cast<uint8_t*>(Xpre);
   T* tcol = ws.take<T>((size_t)nu * m);  // Q~ of the L-chain (m x nu panel)
   T* trow = ws.take<T>((size_t)nu * n);  // Q~ of the R-chain (n x nu panel)
+  PowerChains* pchains = power ? ws.take<PowerChains>(1) : nullptr;
   if (!dry && !ws.ok) return NENMF_ERR_WORKSPACE;
   auto pass = [&](Arena& a, const T* At, const T* Bt, T* Yt, T* Zt) -> int {
     if constexpr (sizeof(T) == 4) {
@@ -465,6 +551,12 @@ int rsi(Arena& ws, const T* X, int64_t n, int64_t m, int64_t ldx, const T* omega
     Arena d(nullptr, 0);
     orthonormalize_pair<T>(d, const_cast<T*>(sent), n, const_cast<T*>(sent), m, nu, st, s);  // both panels counted
     need = max(need, d.used);
+    if (power) {
+      Arena e1(nullptr, 0), e2(nullptr, 0);
+      orthonormalize_tsqr<T>(e1, L, n, nu, st, s);
+      orthonormalize_tsqr<T>(e2, L, m, nu, st, s);
+      need = max(need, max(e1.used, e2.used));
+    }
   }
   char* sbase = scratch.take<char>(need);
   if (dry) {
@@ -488,14 +580,50 @@ int rsi(Arena& ws, const T* X, int64_t n, int64_t m, int64_t ldx, const T* omega
     }
     return orthonormalize_pair<T>(a, A, ra, B, rb, nu, st, s);  // both chains in one launch
   };
-  NENMF_TRY(qr2(L, n, Rt, m));
+  // power iteration (compression.py:144-176): no QR between products
+  const unsigned eg = (unsigned)imin(1184, cdiv(nu * (n + m), 256));
+  auto pscale = [&](T* Yc, int64_t ny, int cy, T* Zc, int64_t nz, int cz, int step) -> int {
+    if constexpr (sizeof(T) == 4) {
+      k_power_stats<<<eg, 256, 0, s>>>(reinterpret_cast<const float*>(Yc), nu * ny, reinterpret_cast<const float*>(Zc),
+                                       nu * nz, pchains);
+      NENMF_LAUNCH_CHECK();
+      k_power_scale<<<eg, 256, 0, s>>>(reinterpret_cast<float*>(Yc), nu * ny, cy, reinterpret_cast<float*>(Zc),
+                                       nu * nz, cz, pchains, step, st);
+      NENMF_LAUNCH_CHECK();
+    }
+    return NENMF_OK;
+  };
+  if (power) {
+    NENMF_CUDA_TRY(cudaMemsetAsync(pchains, 0, sizeof(PowerChains), s));
+    NENMF_TRY(pscale(L, n, 0, Rt, m, 1, 1));
+  } else {
+    NENMF_TRY(qr2(L, n, Rt, m));
+  }
   for (int it = 1; it <= q; ++it) {
     // pass a: X^T Q_col (-> tcol, m x nu) and X Q_row (-> trow, n x nu)  (compression.py:138-139)
     { Arena a = fresh(); NENMF_TRY(pass(a, Rt, L, trow, tcol)); }
-    NENMF_TRY(qr2(tcol, m, trow, n));
+    if (power) NENMF_TRY(pscale(tcol, m, 0, trow, n, 1, it));
+    else NENMF_TRY(qr2(tcol, m, trow, n));
     // pass b: X Q~_col (-> L) and X^T Q~_row (-> Rt)
     { Arena a = fresh(); NENMF_TRY(pass(a, tcol, trow, L, Rt)); }
-    NENMF_TRY(qr2(L, n, Rt, m));
+    if (power) {
+      if constexpr (sizeof(T) == 4) NENMF_TRY(pscale(L, n, 0, Rt, m, 1, it));
+      else {
+        k_power_finite<T><<<eg, 256, 0, s>>>(L, nu * n, Rt, nu * m, it, st);  // compression.py:164-168
+        NENMF_LAUNCH_CHECK();
+      }
+    } else {
+      NENMF_TRY(qr2(L, n, Rt, m));
+    }
+  }
+  if (power) {
+    // zero column on either side after q steps (compression.py:169-174), then one QR
+    // each: Householder TSQR (the raw power iterate has condition ~ (s1/sk)^(2q+1),
+    // beyond what a Gram-based QR resolves)
+    k_zero_rows<T><<<(unsigned)(2 * nu), 256, 0, s>>>(L, n, Rt, m, (int)nu, q, st);
+    NENMF_LAUNCH_CHECK();
+    { Arena a = fresh(); NENMF_TRY(orthonormalize_tsqr<T>(a, L, n, nu, st, s)); }
+    { Arena a = fresh(); NENMF_TRY(orthonormalize_tsqr<T>(a, Rt, m, nu, st, s)); }
   }
   return NENMF_OK;
 }
@@ -517,7 +645,7 @@ int compress(Arena& ws, const T* X, int64_t n, int64_t m, int64_t ldx, const T* 
                             T*, cudaStream_t);                                                              \
   template int orthonormalize<T>(Arena&, T*, int64_t, int64_t, nenmf_device_status*, cudaStream_t);         \
   template int rsi<T>(Arena&, const T*, int64_t, int64_t, int64_t, const T*, const T*, int64_t, int, T*, T*, \
-                      nenmf_device_status*, cudaStream_t, const uint8_t*);                                  \
+                      nenmf_device_status*, cudaStream_t, const uint8_t*, int);                             \
   template int compress<T>(Arena&, const T*, int64_t, int64_t, int64_t, const T*, const T*, int64_t, T*, T*, \
                            cudaStream_t, const uint8_t*);
 NENMF_INST_RSI(double)

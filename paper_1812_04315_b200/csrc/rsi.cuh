@@ -13,7 +13,8 @@ int orthonormalize(Arena& ws, T* Pt, int64_t rows, int64_t k, nenmf_device_statu
 
 template <typename T>
 int rsi(Arena& ws, const T* X, int64_t n, int64_t m, int64_t ldx, const T* omega_l_t, const T* omega_r, int64_t nu,
-        int q, T* L, T* Rt, nenmf_device_status* st, cudaStream_t s, const uint8_t* Xpre = nullptr);
+        int q, T* L, T* Rt, nenmf_device_status* st, cudaStream_t s, const uint8_t* Xpre = nullptr,
+        int power = 0);
 
 template <typename T>
 int compress(Arena& ws, const T* X, int64_t n, int64_t m, int64_t ldx, const T* L, const T* Rt, int64_t nu, T* XL,

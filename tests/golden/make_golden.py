@@ -131,6 +131,33 @@ def gen_rsi():
     save("rsi", names=np.array([s[0] for s in specs]), **cases)
 
 
+def gen_power():
+    """power_iteration_pair (compression.py:144-176): sketches, and the step
+    at which an overflowing iterate raises NumericalCollapseError."""
+    cases = {}
+    specs = [
+        ("noisy", nenmf.generate_problem(200, 180, 10, 30.0, seed=5).X, 20, 2, 6),
+        ("tall", nenmf.generate_problem(600, 40, 5, 20.0, seed=7).X, 12, 1, 8),
+        ("wide", nenmf.generate_problem(40, 500, 5, 20.0, seed=9).X, 10, 3, 10),
+    ]
+    for name, X, nu, q, seed in specs:
+        sk = nenmf.power_iteration_pair(X, nu, q, seed)
+        cases[f"{name}_X"] = X
+        cases[f"{name}_L"] = sk.L
+        cases[f"{name}_R"] = sk.R
+        cases[f"{name}_par"] = np.array([nu, q, seed], dtype=np.int64)
+    # overflow: a large-scale X makes X^T X ... leave the fp64 range at some step
+    Xo = nenmf.generate_problem(120, 100, 4, 30.0, seed=3).X * 1e40
+    try:
+        nenmf.power_iteration_pair(Xo, 6, 8, 4)
+        step = -1
+    except nenmf.NumericalCollapseError as exc:
+        step = exc.iteration
+    cases["overflow_X"] = Xo
+    cases["overflow_par"] = np.array([6, 8, 4, step], dtype=np.int64)
+    save("power", names=np.array([s[0] for s in specs]), **cases)
+
+
 def _trace(records):
     return np.array([[r.outer_iter, r.rre, r.objective] for r in records])
 
@@ -210,6 +237,7 @@ if __name__ == "__main__":
     gen_spectral()
     gen_nnls()
     gen_rsi()
+    gen_power()
     gen_factorize()
     gen_config1()
     gen_seeds()

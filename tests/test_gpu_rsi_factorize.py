@@ -277,3 +277,46 @@ def test_vanilla_fp32_tensor_v_vs_oracle():
         assert np.abs(got - exp).max() <= 1e-3 * exp.max()
         assert np.linalg.norm(out.F - ref.F) <= ftol * np.linalg.norm(ref.F)
         assert np.linalg.norm(out.G - ref.G) <= ftol * np.linalg.norm(ref.G)
+
+
+@pytest.mark.parametrize("dtype", ["fp64", "fp32"])
+def test_power_iteration_vs_golden(golden, dtype):
+    """power_iteration_pair (compression.py:144-176) against the reference's
+    own outputs: the raw power iterates are ill-conditioned, so the dominant
+    directions are compared (fp64: top half of the sketch at sin 1e-6; fp32:
+    the leading direction at 1e-3),
+    plus orthonormality and the overflow step of a large-scale X (fp32
+    reproduces the fp64 overflow step through its power-of-two scale factors)."""
+    d = golden("power")
+    for name in d["names"]:
+        nu, q, seed = (int(v) for v in d[f"{name}_par"])
+        X = d[f"{name}_X"]
+        if dtype == "fp32":
+            X = X.astype(np.float32).astype(np.float64)
+        sk = nm.power_iteration_pair(X, nu, q, seed, dtype=dtype)
+        assert sk.scheme == nm.POWER_ITERATION
+        tol_o = 1e-10 if dtype == "fp64" else 1e-5
+        assert np.abs(sk.L @ sk.L.T - np.eye(nu)).max() <= tol_o, name
+        assert np.abs(sk.R.T @ sk.R - np.eye(nu)).max() <= tol_o, name
+        # fp64: the top half of the sketch; fp32: the passes carry ~1e-5 relative
+        # precision, so only directions whose power-iterate weight
+        # (s_i / s_1)^(2q+1) stays well above that are determined -- on these
+        # nonnegative problems (s_1 >> s_2) the leading direction
+        top = max(1, nu // 2) if dtype == "fp64" else 1
+        tol = 1e-6 if dtype == "fp64" else 1e-3
+        assert sin_max_angle(sk.L.T, d[f"{name}_L"].T, top=top) <= tol, name
+        assert sin_max_angle(sk.R, d[f"{name}_R"], top=top) <= tol, name
+    nu, q, seed, step = (int(v) for v in d["overflow_par"])
+    X = d["overflow_X"]
+    if dtype == "fp32":
+        # entries ~1e40 do not fit fp32: scale into range; the expected step
+        # comes from the pinned oracle on the same fp32-rounded data
+        import nenmf_oracle as orc
+
+        X = (X * 1e-10).astype(np.float32).astype(np.float64)
+        with pytest.raises(orc.OracleFailure) as ref_exc:
+            orc.power_pair(X, nu, q, seed)
+        step = ref_exc.value.iteration
+    with pytest.raises(nm.NumericalCollapseError) as exc:
+        nm.power_iteration_pair(X, nu, q, seed, dtype=dtype)
+    assert exc.value.iteration == step

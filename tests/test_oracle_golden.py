@@ -101,3 +101,18 @@ def test_seeded_draws(golden):
     assert np.array_equal(pair.G, d["init_G"]) and np.array_equal(pair.F, d["init_F"])
     assert np.array_equal(uniform_matrix(5, 4, 3), d["uniform"])
     assert np.array_equal(gaussian_matrix(4, 5, 3), d["gauss"])
+
+
+def test_power_pair(golden):
+    """oracle.power_pair against the reference's power_iteration_pair
+    (compression.py:144-176): sketches bit-equal, overflow step equal."""
+    d = golden("power")
+    for name in d["names"]:
+        nu, q, seed = (int(v) for v in d[f"{name}_par"])
+        L, R = orc.power_pair(d[f"{name}_X"], nu, q, seed)
+        assert np.array_equal(L, d[f"{name}_L"]), name
+        assert np.array_equal(R, d[f"{name}_R"]), name
+    nu, q, seed, step = (int(v) for v in d["overflow_par"])
+    with pytest.raises(orc.OracleFailure) as exc:
+        orc.power_pair(d["overflow_X"], nu, q, seed)
+    assert exc.value.kind == "NumericalCollapseError" and exc.value.iteration == step
