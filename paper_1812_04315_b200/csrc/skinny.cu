@@ -452,6 +452,143 @@ k_resid_mma(const float* __restrict__ X, int64_t nx, int64_t mx, int64_t ldx, in
   }
 }
 
+// Pipelined variant (X, U, V 16-byte aligned, nx, mx, ldx multiples of 4):
+// persistent CTAs stream 128 x 64 tiles of X together with the matching
+// U (p x 128) and V (p x 64) slices through a 3-stage cp.async ring; the
+// 8 warps take 16 rows each; fragments and X values are read from shared
+// memory with conflict-free strides.  Same arithmetic as k_resid_mma.
+constexpr int RP_NS = 3, RP_XS = 72, RP_US = 136, RP_VS = 72;
+
+__device__ __forceinline__ void cp16(void* dst, const void* src, int bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+               "l"(src), "r"(bytes)
+               : "memory");
+}
+
+template <int KT>
+__global__ void __launch_bounds__(256, 1)
+k_resid_pipe(const float* __restrict__ X, int64_t nx, int64_t mx, int64_t ldx, int p,
+             const float* __restrict__ U1, const float* __restrict__ V1, const float* __restrict__ U2,
+             const float* __restrict__ V2, double* __restrict__ part, const int* __restrict__ gate) {
+  if (gate != nullptr && *gate == 0) return;
+  constexpr int KP = 8 * KT;
+  constexpr int XB = 128 * RP_XS, UB = KP * RP_US, VB = KP * RP_VS;  // floats per stage section
+  extern __shared__ __align__(16) float rsm[];
+  __shared__ double red[33];
+  const bool two = U2 != nullptr;
+  const bool u2s = two && U2 != U1, v2s = two && V2 != V1;  // second-candidate sections
+  const int stage_f = XB + UB + VB + (u2s ? UB : 0) + (v2s ? VB : 0);
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, gq = lane >> 2, tq = lane & 3;
+  const int64_t ntr = (nx + 127) / 128, ntc = (mx + 63) / 64, tiles = ntr * ntc;
+  auto issue = [&](int64_t tile, int slot) {
+    float* base = rsm + (size_t)slot * stage_f;
+    const int64_t i0 = (tile / ntc) * 128, j0 = (tile % ntc) * 64;
+    // X: 128 rows x 16 chunks
+    for (int c = tid; c < 128 * 16; c += 256) {
+      const int r = c >> 4, ch = c & 15;
+      const int64_t i = i0 + r, j = j0 + 4 * ch;
+      const int valid = (i < nx) ? (int)imax(0, imin(4, mx - j)) : 0;
+      cp16(base + r * RP_XS + 4 * ch, X + (valid ? i * ldx + j : 0), 4 * valid);
+    }
+    auto urows = [&](const float* U, float* dst) {  // p x 128 slice of U (p x nx)
+      for (int c = tid; c < KP * 32; c += 256) {
+        const int a = c >> 5, ch = c & 31;
+        const int64_t i = i0 + 4 * ch;
+        const int valid = a < p ? (int)imax(0, imin(4, nx - i)) : 0;
+        cp16(dst + a * RP_US + 4 * ch, U + (valid ? (int64_t)a * nx + i : 0), 4 * valid);
+      }
+    };
+    auto vrows = [&](const float* V, float* dst) {  // p x 64 slice of V (p x mx)
+      for (int c = tid; c < KP * 16; c += 256) {
+        const int a = c >> 4, ch = c & 15;
+        const int64_t j = j0 + 4 * ch;
+        const int valid = a < p ? (int)imax(0, imin(4, mx - j)) : 0;
+        cp16(dst + a * RP_VS + 4 * ch, V + (valid ? (int64_t)a * mx + j : 0), 4 * valid);
+      }
+    };
+    float* us = base + XB;
+    float* vs = us + UB;
+    urows(U1, us);
+    vrows(V1, vs);
+    float* extra = vs + VB;
+    if (u2s) {
+      urows(U2, extra);
+      extra += UB;
+    }
+    if (v2s) vrows(V2, extra);
+  };
+  const int64_t first = blockIdx.x, step = gridDim.x;
+  const int64_t mine = first < tiles ? (tiles - 1 - first) / step + 1 : 0;
+#pragma unroll
+  for (int sidx = 0; sidx < RP_NS - 1; ++sidx) {
+    if (sidx < mine) issue(first + sidx * step, sidx);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  double acc0 = 0.0, acc1 = 0.0;
+  for (int64_t it = 0; it < mine; ++it) {
+    if (it + RP_NS - 1 < mine) issue(first + (it + RP_NS - 1) * step, (int)((it + RP_NS - 1) % RP_NS));
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    asm volatile("cp.async.wait_group %0;" ::"n"(RP_NS - 1) : "memory");
+    __syncthreads();
+    const float* base = rsm + (size_t)(it % RP_NS) * stage_f;
+    const float* xs = base;
+    const float* us1 = base + XB;
+    const float* vs1 = us1 + UB;
+    const float* us2 = u2s ? vs1 + VB : us1;
+    const float* vs2 = v2s ? vs1 + VB + (u2s ? UB : 0) : vs1;
+    const int rw = 16 * wid;  // this warp's 16 rows of the tile
+    auto afr = [&](const float* us, uint32_t (&ah)[KT][4], uint32_t (&al)[KT][4]) {
+#pragma unroll
+      for (int kt = 0; kt < KT; ++kt)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float u = us[(8 * kt + tq + ((q & 2) ? 4 : 0)) * RP_US + rw + gq + ((q & 1) ? 8 : 0)];
+          ah[kt][q] = tf_hi(u);
+          al[kt][q] = tf_lo(u);
+        }
+    };
+    uint32_t a1h[KT][4], a1l[KT][4], a2h[KT][4], a2l[KT][4];
+    afr(us1, a1h, a1l);
+    if (two) afr(us2, a2h, a2l);
+    float s0 = 0.f, s1 = 0.f;
+#pragma unroll
+    for (int nt = 0; nt < 8; ++nt) {
+      const float2 x0 = *reinterpret_cast<const float2*>(xs + (rw + gq) * RP_XS + 8 * nt + 2 * tq);
+      const float2 x1 = *reinterpret_cast<const float2*>(xs + (rw + gq + 8) * RP_XS + 8 * nt + 2 * tq);
+      auto prod = [&](const float* vs, const uint32_t (&ah)[KT][4], const uint32_t (&al)[KT][4], float (&c)[4]) {
+#pragma unroll
+        for (int kt = 0; kt < KT; ++kt) {
+          const float v0 = vs[(8 * kt + tq) * RP_VS + 8 * nt + gq];
+          const float v1 = vs[(8 * kt + tq + 4) * RP_VS + 8 * nt + gq];
+          const uint32_t b0h = tf_hi(v0), b1h = tf_hi(v1), b0l = tf_lo(v0), b1l = tf_lo(v1);
+          mma_tf32_r(c, al[kt], b0h, b1h);
+          mma_tf32_r(c, ah[kt], b0l, b1l);
+          mma_tf32_r(c, ah[kt], b0h, b1h);
+        }
+      };
+      float c1[4] = {0.f, 0.f, 0.f, 0.f};
+      prod(vs1, a1h, a1l, c1);
+      const float d0 = c1[0] - x0.x, d1 = c1[1] - x0.y, d2 = c1[2] - x1.x, d3 = c1[3] - x1.y;
+      s0 = fmaf(d0, d0, fmaf(d1, d1, fmaf(d2, d2, fmaf(d3, d3, s0))));
+      if (two) {
+        float c2[4] = {0.f, 0.f, 0.f, 0.f};
+        prod(vs2, a2h, a2l, c2);
+        const float e0 = c2[0] - x0.x, e1 = c2[1] - x0.y, e2 = c2[2] - x1.x, e3 = c2[3] - x1.y;
+        s1 = fmaf(e0, e0, fmaf(e1, e1, fmaf(e2, e2, fmaf(e3, e3, s1))));
+      }
+    }
+    acc0 += (double)s0;
+    acc1 += (double)s1;
+    __syncthreads();  // the slot is refilled by a later issue
+  }
+  const double b0 = block_sum(acc0, red);
+  const double b1 = block_sum(acc1, red);
+  if (threadIdx.x == 0) {
+    part[2 * blockIdx.x] = b0;
+    part[2 * blockIdx.x + 1] = b1;
+  }
+}
+
 // fixed-order sum of `n` pairs -> out[0..1]; optional gate
 __global__ void k_pair_final(const double* __restrict__ part, int64_t n, double* __restrict__ out,
                              const int* __restrict__ gate) {
@@ -486,12 +623,36 @@ int resid(Arena& ws, const T* At, int64_t p, int64_t r, const T* B, int64_t c, i
       int sms = sm_count();
       if (sms <= 0) sms = 148;
       const int64_t tiles = cdiv(nx, 16) * cdiv(mx, 64);
-      const unsigned grid = (unsigned)imax(1, imin((int64_t)sms * 8, cdiv(tiles, 8)));
+      const bool pipe_ok = ((nx | mx | ldb) & 3) == 0;
+      const unsigned grid = pipe_ok ? (unsigned)imax(1, imin((int64_t)sms, cdiv(nx, 128) * cdiv(mx, 64)))
+                                    : (unsigned)imax(1, imin((int64_t)sms * 8, cdiv(tiles, 8)));
       double* part = ws.take<double>((size_t)grid * 2);
       if (ws.base == nullptr) return NENMF_OK;
       if (!ws.ok) return NENMF_ERR_WORKSPACE;
       const float* Xf = reinterpret_cast<const float*>(B);
       const int kt = (int)cdiv(p, 8);
+      auto al16 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
+      if (((nx | mx | ldb) & 3) == 0 && al16(Xf) && al16(U1) && al16(V1) && (U2 == nullptr || al16(U2)) &&
+          (V2 == nullptr || al16(V2)) && getenv("NENMF_RESID_V1") == nullptr) {
+        const int kp = 8 * kt;
+        const size_t stage_f = (size_t)128 * RP_XS + (size_t)kp * RP_US + (size_t)kp * RP_VS +
+                               ((U2 != nullptr && U2 != U1) ? (size_t)kp * RP_US : 0) +
+                               ((V2 != nullptr && V2 != V1) ? (size_t)kp * RP_VS : 0);
+        const size_t smem = stage_f * RP_NS * sizeof(float);
+        auto go = [&](auto kern) -> int {
+          NENMF_CUDA_TRY(set_smem(kern, smem));
+          kern<<<grid, 256, smem, st>>>(Xf, nx, mx, ldb, (int)p, U1, V1, U2, V2, part, gate);
+          return NENMF_OK;
+        };
+        if (kt == 1) NENMF_TRY(go(k_resid_pipe<1>));
+        else if (kt == 2) NENMF_TRY(go(k_resid_pipe<2>));
+        else if (kt == 3) NENMF_TRY(go(k_resid_pipe<3>));
+        else NENMF_TRY(go(k_resid_pipe<4>));
+        NENMF_LAUNCH_CHECK();
+        k_pair_final<<<1, 256, 0, st>>>(part, (int64_t)grid, out2, gate);
+        NENMF_LAUNCH_CHECK();
+        return NENMF_OK;
+      }
       if (kt == 1) k_resid_mma<1><<<grid, 256, 0, st>>>(Xf, nx, mx, ldb, (int)p, U1, V1, U2, V2, part, gate);
       else if (kt == 2) k_resid_mma<2><<<grid, 256, 0, st>>>(Xf, nx, mx, ldb, (int)p, U1, V1, U2, V2, part, gate);
       else if (kt == 3) k_resid_mma<3><<<grid, 256, 0, st>>>(Xf, nx, mx, ldb, (int)p, U1, V1, U2, V2, part, gate);
