@@ -211,7 +211,12 @@ int solve_nnls(Arena& ws, const T* At, int64_t r, int64_t p, const T* B, int64_t
   const int64_t mcpb = cdiv(c, mgrid);
   const bool use_mma = p <= 32 && mcpb <= nnls_mma_max_cols<T>((int)p) && max_iter <= NN_WTAB_LEN &&
                        getenv("NENMF_NNLS_SIMT") == nullptr;
-  const int grid_used = use_mma ? mgrid : pl.grid;
+  // FP32, p <= 32, too many columns for the register-resident solver: the
+  // streamed tensor-core solver (nnls_stream.cuh) keeps u_k in HBM
+  const bool use_stream = !use_mma && sizeof(T) == 4 && p <= 32 && max_iter <= NN_WTAB_LEN &&
+                          getenv("NENMF_NNLS_SIMT") == nullptr;
+  const int sgrid = (int)imax(1, imin(sms, cdiv(c, 16)));
+  const int grid_used = use_mma ? mgrid : (use_stream ? sgrid : pl.grid);
   // fused prologue/epilogue (W, V, L and the tie-break inside the solver
   // launch) for the compressed problems' short operands
   const int cbm = nnls_mma_col_block<T>();
@@ -229,8 +234,9 @@ int solve_nnls(Arena& ws, const T* At, int64_t r, int64_t p, const T* B, int64_t
   T* V = fused ? nullptr : ws.take<T>((size_t)pc);
   double* Lbuf = ws.take<double>(4);
   T* snaps = ws.take<T>((size_t)(NW_SNAP + 1) * 4 * pc);
+  T* ustate = use_stream ? ws.take<T>((size_t)2 * pc) : nullptr;
   double* salpha = use_mma ? nullptr : ws.take<double>((size_t)pl.grid * NW_MAXW * (NW_SNAP + 1) * 2);
-  T* gstate = (use_mma || pl.smem_state) ? nullptr : ws.take<T>((size_t)4 * pc);
+  T* gstate = (use_mma || use_stream || pl.smem_state) ? nullptr : ws.take<T>((size_t)4 * pc);
   double* rpart = fused ? ws.take<double>((size_t)2 * grid_used) : nullptr;
   double* npart = fused_next ? ws.take<double>((size_t)grid_used * p * nup) : nullptr;
   // window records + (fused) the grid-barrier counter, zeroed together
@@ -311,6 +317,29 @@ int solve_nnls(Arena& ws, const T* At, int64_t r, int64_t p, const T* B, int64_t
       if (fused) {
         if (Pt != nullptr && !fused_next) NENMF_TRY(abt<T>(ws, Fout, p, Pt, nup, c, Pout, s));
         return NENMF_OK;
+      }
+    } else if (use_stream) {
+      if constexpr (sizeof(T) == 4) {
+        const double* wtab = momentum_table(max_iter);
+        if (wtab == nullptr) return NENMF_ERR_CUDA;
+        StreamArgs a{};
+        a.W = W;
+        a.V = V;
+        a.L = Lbuf;
+        a.F0 = F0;
+        a.Fout = Fout;
+        a.U = ustate;
+        a.snaps = snaps;
+        a.p = (int)p;
+        a.c = c;
+        a.cpb = cdiv(c, sgrid);
+        a.max_iter = max_iter;
+        a.grad_tol = grad_tol;
+        a.wtab = wtab;
+        a.recs = recs;
+        a.results = results;
+        a.st = st;
+        NENMF_TRY(launch_nnls_stream(a, sgrid, s));
       }
     } else {
       NENMF_TRY(launch_nnls<T>(pl, W, V, F0, Fout, snaps, salpha, gstate, (int)p, c, Lbuf, max_iter, grad_tol, recs,

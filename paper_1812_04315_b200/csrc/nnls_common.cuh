@@ -349,6 +349,27 @@ struct MmaArgs {
 template <typename T>
 int launch_nnls_mma(const MmaArgs<T>& a, int grid, cudaStream_t s);
 
+// Arguments of the streamed tensor-core solver (nnls_stream.cuh, FP32).
+struct StreamArgs {
+  const float* W;   // p x p
+  const float* V;   // p x c
+  const double* L;  // [0] = Lipschitz constant
+  const float* F0;  // p x c
+  float* Fout;      // p x c
+  float* U;         // 2 x p x c: u_k lives in slot k & 1 (u_{-1}: slot 1)
+  float* snaps;     // (NW_SNAP + 1) x 2 x p x c
+  int p;
+  int64_t c, cpb;
+  int max_iter;
+  double grad_tol;
+  const double* wtab;
+  WinRec* recs;
+  WinRec* results;
+  nenmf_device_status* st;
+};
+
+int launch_nnls_stream(const StreamArgs& a, int grid, cudaStream_t s);
+
 template <typename T>
 int nnls_mma_max_cols(int p);  // columns one CTA of the tensor-core solver can hold
 template <typename T>

@@ -1,0 +1,342 @@
+// Streamed tensor-core inner solver for problems with more columns than the
+// register-resident solver holds (BASELINE cfg4's G-half: 400 000 columns,
+// cfg5's: 100 000; nnls.py:160-227).
+//
+// Same arithmetic per 16-column tile as k_nnls_mma (TF32 hi x hi + one BF16
+// correction MMA per k-tile, accumulators reused as the next A operand) and
+// the same windowed decision protocol (resolver warp, window records, fixed
+// order sums), but the iterate state lives in HBM: per iteration every warp
+// sweeps its tiles, reading u_{k-1}, u_{k-2} and V and writing u_k (16 bytes
+// per element and iteration, the streaming floor).  Window snapshots are the
+// values already loaded at a window start; the returned best iterate is
+// recomputed from its window's snapshot at the end (<= 32 on-chip steps per
+// tile).  FP32, p <= 32.
+#pragma once
+#include "nnls_mma.cuh"
+
+namespace nenmf {
+
+template <int NT>
+__host__ __device__ constexpr int stream_threads() {
+  return NT <= 2 ? 512 : 288;  // 15 or 8 compute warps + the resolver
+}
+
+template <int NT>
+__global__ void __launch_bounds__(stream_threads<NT>(), 1) k_nnls_stream(const __grid_constant__ StreamArgs A) {
+  constexpr int NE = 4 * NT;
+  constexpr int CB = 16;
+  extern __shared__ __align__(16) double smem_d[];
+  double* pp = smem_d;  // [PPD][MAXW][3]
+  __shared__ SolverShared sh;
+  const int p = A.p, max_iter = A.max_iter;
+  const int64_t c = A.c, pc = (int64_t)A.p * A.c;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int ncw = (blockDim.x >> 5) - 1;
+  const bool resolver = wid == ncw;
+  const int64_t j0 = (int64_t)blockIdx.x * A.cpb;
+  const int ncols = (int)(imin(c, j0 + A.cpb) - j0);
+  const int ntiles = ncols > 0 ? (ncols + CB - 1) / CB : 0;
+  const int gq = lane >> 2, tq = lane & 3;
+  solver_shared_init(sh);
+  __syncthreads();
+  if (A.st->code != 0) return;
+  const double L = A.L[0];
+  const float rnegL = (float)(-1.0 / L);
+
+  if (!resolver) {
+    // element e of this thread within a tile: solver row, tile-local column
+    auto erow = [&](int e) { return 8 * (e >> 2) + 2 * tq + (e & 1); };
+    auto ecol = [&](int e) { return gq + ((e & 2) ? 8 : 0); };
+    // W^T fragments, as k_nnls_mma
+    uint32_t bhi[NT][NT][2], bco[NT][NT][2];
+#pragma unroll
+    for (int kt = 0; kt < NT; ++kt)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        float wh[2], wl[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int i = 8 * nt + gq, l = 8 * kt + 2 * tq + h;
+          const float w = (i < p && l < p) ? A.W[i * p + l] : 0.f;
+          bhi[kt][nt][h] = tf32_hi(w);
+          wh[h] = __uint_as_float(bhi[kt][nt][h]);
+          wl[h] = w - wh[h];
+        }
+        bco[kt][nt][0] = pack_bf16(wh[0], wh[1]);
+        bco[kt][nt][1] = pack_bf16(wl[0], wl[1]);
+      }
+    auto grad = [&](const float (&fe)[NE], const float (&nv)[NE], float (&g)[NE]) {
+      uint32_t ahi[NT][4], aco[NT][4];
+#pragma unroll
+      for (int t = 0; t < NT; ++t) {
+        const float c0 = fe[4 * t], c1 = fe[4 * t + 1], c2 = fe[4 * t + 2], c3 = fe[4 * t + 3];
+        const uint32_t h0 = tf32_hi(c0), h1 = tf32_hi(c1), h2 = tf32_hi(c2), h3 = tf32_hi(c3);
+        ahi[t][0] = h0;
+        ahi[t][1] = h2;
+        ahi[t][2] = h1;
+        ahi[t][3] = h3;
+        const float f0 = __uint_as_float(h0), f1 = __uint_as_float(h1), f2 = __uint_as_float(h2),
+                    f3 = __uint_as_float(h3);
+        aco[t][0] = pack_bf16(c0 - f0, c1 - f1);
+        aco[t][1] = pack_bf16(c2 - f2, c3 - f3);
+        aco[t][2] = pack_bf16(f0, f1);
+        aco[t][3] = pack_bf16(f2, f3);
+      }
+      float cc[NT][4];
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int r = 0; r < 4; ++r) cc[nt][r] = nv[4 * nt + r];
+#pragma unroll
+      for (int kt = 0; kt < NT; ++kt)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) mma_bf16(cc[nt], aco[kt], bco[kt][nt][0], bco[kt][nt][1]);
+#pragma unroll
+      for (int kt = 0; kt < NT; ++kt)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) mma_tf32(cc[nt], ahi[kt], bhi[kt][nt][0], bhi[kt][nt][1]);
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int r = 0; r < 4; ++r) g[4 * nt + r] = cc[nt][r];
+    };
+    auto post = [&](int j, float s0, float s1) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+        s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+      }
+      if (lane == 0) {
+        double* q = pp + ((size_t)((j + NW_PPD) % NW_PPD) * NW_MAXW + wid) * 3;
+        q[0] = s0;
+        q[1] = s1;
+        q[2] = 0.0;
+      }
+    };
+    auto post_flag = [&](int j) {
+      if (lane == 0) {
+        __threadfence_block();
+        sh.posted[wid] = j;
+      }
+    };
+    auto wload = [&](int base) -> double {
+      const int i = base - 1 + lane;
+      return (i >= 0 && i < max_iter) ? A.wtab[i] : 0.0;
+    };
+    // one tile of one iteration k (k = -1: the start point), in two halves so
+    // that the next tile's loads are in flight while this one computes
+    const float* __restrict__ V = A.V;
+    const int64_t jend = j0 + ncols;
+    auto eoff = [&](int64_t cb, int e) -> int64_t {
+      return (int64_t)(8 * (e >> 2) + (e & 1)) * c + ((e & 2) ? 8 : 0) + (int64_t)(2 * tq) * c + cb + gq;
+    };
+    auto eok = [&](int64_t cb, int e) -> bool {
+      return erow(e) < p && cb + ecol(e) < jend;
+    };
+    struct Tile {
+      float u1[NE], u2[NE], nv[NE];
+    };
+    auto tload = [&](int tile, int k, Tile& T) {
+      const int64_t cb = j0 + (int64_t)tile * CB;
+      const float* __restrict__ Uw = A.U + (int64_t)(k & 1) * pc;
+      const float* __restrict__ Ur = A.U + (int64_t)((k + 1) & 1) * pc;
+#pragma unroll
+      for (int e = 0; e < NE; ++e) {
+        const bool ok = eok(cb, e);
+        const int64_t o = eoff(cb, e);
+        T.nv[e] = ok ? -__ldcs(&V[o]) : 0.f;
+        if (k < 0) {
+          T.u1[e] = ok ? A.F0[o] : 0.f;
+          T.u2[e] = T.u1[e];
+        } else {
+          T.u1[e] = ok ? Ur[o] : 0.f;
+          T.u2[e] = (ok && k > 0) ? Uw[o] : T.u1[e];
+        }
+      }
+    };
+    auto tcompute = [&](int tile, int k, float w, bool snap, int slot, bool save, const Tile& T, float& s0,
+                        float& s1) {
+      const int64_t cb = j0 + (int64_t)tile * CB;
+      float fe[NE], g[NE];
+      if (k >= 0) {
+        if (snap) {
+          float* sp = A.snaps + (int64_t)(slot * 2) * pc;
+          float* bp = A.snaps + (int64_t)(NW_SNAP * 2) * pc;
+#pragma unroll
+          for (int e = 0; e < NE; ++e)
+            if (eok(cb, e)) {
+              const int64_t o = eoff(cb, e);
+              if (save) {
+                bp[o] = sp[o];
+                bp[pc + o] = sp[pc + o];
+              }
+              sp[o] = T.u1[e];
+              sp[pc + o] = T.u2[e];
+            }
+        }
+#pragma unroll
+        for (int e = 0; e < NE; ++e) fe[e] = relu_nan_fast(fmaf(T.u1[e] - T.u2[e], w, T.u1[e]));
+      } else {
+#pragma unroll
+        for (int e = 0; e < NE; ++e) fe[e] = T.u1[e];  // F0
+      }
+      grad(fe, T.nv, g);
+      float* __restrict__ Uo = A.U + (int64_t)(k < 0 ? 1 : (k & 1)) * pc;  // u_{-1} -> slot 1
+#pragma unroll
+      for (int e = 0; e < NE; ++e) {
+        const bool ok = eok(cb, e);
+        const float u = fmaf(g[e], rnegL, fe[e]);
+        if (ok) Uo[eoff(cb, e)] = u;
+        const float pgv = ok ? (fe[e] > 0.f ? g[e] : min0_nan(g[e])) : 0.f;
+        s0 = fmaf(pgv, pgv, s0);
+        s1 = ok ? fmaf(fe[e], g[e] + T.nv[e], s1) : s1;
+      }
+    };
+    // all of this warp's tiles for iteration k, loads one tile ahead
+    // (NT <= 2; with NT >= 3 the extra registers would spill, and 8 warps per
+    // SM keep enough loads in flight without it)
+    auto sweep = [&](int k, float w, bool snap, int slot, bool save, float& s0, float& s1) {
+      if constexpr (NT <= 2) {
+        int t = wid;
+        if (t >= ntiles) return;
+        Tile cur, nxt;
+        tload(t, k, cur);
+        for (; t < ntiles; t += ncw) {
+          const bool more = t + ncw < ntiles;
+          if (more) tload(t + ncw, k, nxt);
+          tcompute(t, k, w, snap, slot, save, cur, s0, s1);
+          if (more) cur = nxt;
+        }
+      } else {
+        for (int t = wid; t < ntiles; t += ncw) {
+          Tile cur;
+          tload(t, k, cur);
+          tcompute(t, k, w, snap, slot, save, cur, s0, s1);
+        }
+      }
+    };
+    // start point (nnls.py:163-178)
+    {
+      float s0 = 0.f, s1 = 0.f;
+      sweep(-1, 0.f, false, 0, false, s0, s1);
+      post(-1, s0, s1);
+      post_flag(-1);
+    }
+    double wwin = 0.0, wnext = wload(0);
+    int k = 0;
+    for (; k < max_iter; ++k) {
+      bool snap = false, save = false;
+      int slot = 0;
+      if (k % NW_WIN == 0) {
+        const int w = k / NW_WIN;
+        wwin = wnext;
+        wnext = wload(k + NW_WIN);
+        int ok = 1;
+        if (lane == 0) {
+          const int need = (w - NW_FLIGHT) * NW_WIN - 1;
+          while (sh.resolved < need && !sh.halt) __nanosleep(64);
+          ok = sh.halt ? 0 : 1;
+        }
+        ok = __shfl_sync(0xffffffffu, ok, 0);
+        if (!ok) break;
+        slot = w % NW_SNAP;
+        const int evicted = w - NW_SNAP;
+        const int bj = sh.best_j;
+        save = evicted >= 0 && bj >= 0 && bj / NW_WIN == evicted;
+        snap = true;
+        if (lane == 0 && save) sh.bsw[wid] = evicted;
+        __syncwarp();
+      } else if (sh.halt) {
+        break;
+      }
+      const float w = (float)__shfl_sync(0xffffffffu, wwin, k % NW_WIN);
+      float s0 = 0.f, s1 = 0.f;
+      sweep(k, w, snap, slot, save, s0, s1);
+      post(k, s0, s1);
+      if ((k + 1) % NW_WIN == 0) post_flag(k);
+    }
+    if (k > 0) post_flag(k - 1);
+    if (lane == 0) sh.kdone[wid] = k;
+    __syncwarp();
+    asm volatile("bar.sync 1, %0;" ::"r"(blockDim.x) : "memory");
+    // ---- the best iterate, recomputed from its window's snapshot
+    const int bj = sh.best_j;
+    if (bj >= 0 && sh.fail_at == -1) {
+      const int kd = sh.kdone[wid];
+      const int wb = bj / NW_WIN;
+      const int slot = (sh.bsw[wid] == wb && wb + NW_SNAP <= (kd - 1) / NW_WIN) ? NW_SNAP : wb % NW_SNAP;
+      const float* sp = A.snaps + (int64_t)(slot * 2) * pc;
+      const double wrec = wload(wb * NW_WIN);
+      for (int t = wid; t < ntiles; t += ncw) {
+        const int64_t cb = j0 + (int64_t)t * CB;
+        float ua[NE], ub[NE], nv[NE], fe[NE], g[NE];
+        int64_t off[NE];
+        bool ok[NE];
+#pragma unroll
+        for (int e = 0; e < NE; ++e) {
+          const int r = erow(e);
+          const int64_t col = cb + ecol(e);
+          ok[e] = r < p && col < j0 + ncols;
+          off[e] = (int64_t)r * c + col;
+          ua[e] = ok[e] ? sp[off[e]] : 0.f;
+          ub[e] = ok[e] ? sp[pc + off[e]] : 0.f;
+          nv[e] = ok[e] ? -V[off[e]] : 0.f;
+        }
+        for (int kk = wb * NW_WIN; kk <= bj; ++kk) {
+          const float w = (float)__shfl_sync(0xffffffffu, wrec, kk % NW_WIN);
+#pragma unroll
+          for (int e = 0; e < NE; ++e) fe[e] = relu_nan_fast(fmaf(ua[e] - ub[e], w, ua[e]));
+          grad(fe, nv, g);
+#pragma unroll
+          for (int e = 0; e < NE; ++e) {
+            ub[e] = ua[e];
+            ua[e] = fmaf(g[e], rnegL, fe[e]);
+          }
+        }
+#pragma unroll
+        for (int e = 0; e < NE; ++e)
+          if (ok[e]) A.Fout[off[e]] = fe[e];
+      }
+    }
+  } else {
+    resolver_warp(sh, pp, ncw, max_iter, A.grad_tol, L, A.recs, A.results, nullptr);
+    asm volatile("bar.sync 1, %0;" ::"r"(blockDim.x) : "memory");
+  }
+  __syncthreads();
+  if (blockIdx.x == 0 && tid == 0) {
+    nenmf_device_status* st = A.st;
+    if (sh.fail_at >= 0) status_fail(st, NENMF_ERR_NUMERICAL_FAILURE, sh.fail_at);
+    if (sh.fail_at == -2) status_fail(st, NENMF_ERR_CUDA, -2);
+    st->inner_iters = sh.stop_at >= 0 ? sh.stop_at + 1 : (sh.fail_at >= 0 ? sh.fail_at : max_iter);
+    st->returned_best = sh.best_j >= 0 ? 1 : 0;
+    st->best_partial = sh.best_part;
+    st->pg_ref = sh.pg_ref;
+  }
+}
+
+// grid: one CTA per SM (cooperative); returns NENMF_ERR_UNSUPPORTED outside FP32, p <= 32
+int launch_nnls_stream(const StreamArgs& a, int grid, cudaStream_t s) {
+  const int nt = (a.p + 7) / 8;
+  const size_t smem = (size_t)NW_PPD * NW_MAXW * 3 * sizeof(double);
+  void* args[] = {(void*)&a};
+  switch (nt) {
+#define NENMF_STREAM_CASE(N)                                                                               \
+  case N: {                                                                                                \
+    NENMF_CUDA_TRY(set_smem(k_nnls_stream<N>, smem));                                                      \
+    NENMF_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k_nnls_stream<N>, dim3(grid),                  \
+                                               dim3(stream_threads<N>()), args, smem, s));                 \
+    break;                                                                                                 \
+  }
+    NENMF_STREAM_CASE(1)
+    NENMF_STREAM_CASE(2)
+    NENMF_STREAM_CASE(3)
+    NENMF_STREAM_CASE(4)
+#undef NENMF_STREAM_CASE
+    default:
+      return NENMF_ERR_UNSUPPORTED;
+  }
+  launch_counter_add(1);
+  return NENMF_OK;
+}
+
+}  // namespace nenmf

@@ -174,3 +174,25 @@ def test_frobenius_and_rre():
     assert nm.rre(X, np.zeros((15, 2)), np.zeros((2, 15))) == 1.0
     with pytest.raises(nm.ZeroMatrixError):
         nm.rre(np.zeros((4, 4)), np.ones((4, 2)), np.ones((2, 4)))
+
+
+@pytest.mark.parametrize("p,c,max_iter", [(20, 20000, 100), (9, 40000, 70), (30, 17000, 45)])
+def test_streamed_solver_many_columns(monkeypatch, p, c, max_iter):
+    """FP32 solves with more columns than the register-resident tensor-core
+    solver holds use the streamed tensor-core solver (nnls_stream.cuh):
+    within the FP32 tolerance of the fp64 oracle, and of the SIMT solver;
+    same inner-iteration count and returned iterate kind."""
+    rng = np.random.default_rng(c + p)
+    r = 30
+    A = rng.random((r, p))
+    B = A @ rng.random((p, c)) + 0.05 * rng.standard_normal((r, c))
+    F0 = rng.random((p, c))
+    cfg = nm.InnerSolverConfig(max_iter=max_iter, grad_tol=1e-9)
+    rep_s, rep_simt = [], []
+    Fs = nm.solve_nnls(A, B, F0, cfg, dtype="fp32", report=rep_s)
+    monkeypatch.setenv("NENMF_NNLS_SIMT", "1")
+    Fsimt = nm.solve_nnls(A, B, F0, cfg, dtype="fp32", report=rep_simt)
+    Fr = orc.nesterov_nnls(A, B, F0, max_iter=max_iter, grad_tol=1e-9)
+    assert rep_s[0].inner_iters == rep_simt[0].inner_iters
+    assert np.linalg.norm(Fs - Fr) <= 1e-3 * np.linalg.norm(Fr)
+    assert np.linalg.norm(Fs - Fsimt) <= 1e-3 * np.linalg.norm(Fsimt)
