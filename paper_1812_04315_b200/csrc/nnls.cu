@@ -215,7 +215,9 @@ int solve_nnls(Arena& ws, const T* At, int64_t r, int64_t p, const T* B, int64_t
   // streamed tensor-core solver (nnls_stream.cuh) keeps u_k in HBM
   const bool use_stream = !use_mma && sizeof(T) == 4 && p <= 32 && max_iter <= NN_WTAB_LEN &&
                           getenv("NENMF_NNLS_SIMT") == nullptr;
-  const int sgrid = (int)imax(1, imin(sms, cdiv(c, 16)));
+  // streamed solver: column blocks of whole 16-column tiles (16-byte aligned rows for cp.async)
+  const int64_t scpb = cdiv(cdiv(c, imax(1, imin(sms, cdiv(c, 16)))), 16) * 16;
+  const int sgrid = (int)imax(1, cdiv(c, scpb));
   const int grid_used = use_mma ? mgrid : (use_stream ? sgrid : pl.grid);
   // fused prologue/epilogue (W, V, L and the tie-break inside the solver
   // launch) for the compressed problems' short operands
@@ -332,7 +334,7 @@ int solve_nnls(Arena& ws, const T* At, int64_t r, int64_t p, const T* B, int64_t
         a.snaps = snaps;
         a.p = (int)p;
         a.c = c;
-        a.cpb = cdiv(c, sgrid);
+        a.cpb = scpb;
         a.max_iter = max_iter;
         a.grad_tol = grad_tol;
         a.wtab = wtab;

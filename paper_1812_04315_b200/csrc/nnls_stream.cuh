@@ -16,10 +16,13 @@
 
 namespace nenmf {
 
+// 4 compute warps + the resolver; each compute warp streams its tiles through
+// a 3-stage shared-memory ring (stage: u_{k-1}, u_{k-2}, V tiles of 32 x 16)
 template <int NT>
 __host__ __device__ constexpr int stream_threads() {
-  return NT <= 2 ? 512 : 288;  // 15 or 8 compute warps + the resolver
+  return 5 * 32;
 }
+constexpr int SS_STAGES = 3, SS_ROW = 20, SS_ARR_F = 32 * SS_ROW, SS_STAGE_F = 3 * SS_ARR_F;
 
 template <int NT>
 __global__ void __launch_bounds__(stream_threads<NT>(), 1) k_nnls_stream(const __grid_constant__ StreamArgs A) {
@@ -133,31 +136,53 @@ __global__ void __launch_bounds__(stream_threads<NT>(), 1) k_nnls_stream(const _
     auto eok = [&](int64_t cb, int e) -> bool {
       return erow(e) < p && cb + ecol(e) < jend;
     };
-    struct Tile {
-      float u1[NE], u2[NE], nv[NE];
-    };
-    auto tload = [&](int tile, int k, Tile& T) {
+    // Per-warp 3-stage cp.async ring in shared memory: a stage holds one tile
+    // of u_{k-1}, u_{k-2} and V (32 rows x 16 columns each, row stride 20:
+    // the accumulator-layout reads are bank-conflict free), two tiles ahead
+    // of the one being computed.
+    float* ring = reinterpret_cast<float*>(smem_d + (size_t)NW_PPD * NW_MAXW * 3) +
+                  (size_t)wid * SS_STAGES * SS_STAGE_F;
+    const bool vec = (c & 3) == 0;  // 16-byte rows: cp.async; otherwise plain loads
+    auto issue = [&](int tile, int k, int stg) {
       const int64_t cb = j0 + (int64_t)tile * CB;
-      const float* __restrict__ Uw = A.U + (int64_t)(k & 1) * pc;
-      const float* __restrict__ Ur = A.U + (int64_t)((k + 1) & 1) * pc;
+      float* st = ring + stg * SS_STAGE_F;
+      const float* src[3] = {k < 0 ? A.F0 : A.U + (int64_t)((k + 1) & 1) * pc,  // u_{k-1} (F0 at the start)
+                             A.U + (int64_t)(k & 1) * pc,                        // u_{k-2}
+                             V};
+      const int narr = (k <= 0) ? 1 : 2;  // k <= 0: u_{k-2} := u_{k-1}
+      for (int arr = 0; arr < 3; ++arr) {
+        if (arr == 1 && narr == 1) continue;
+        float* dst = st + arr * SS_ARR_F;
+        for (int q = lane; q < 32 * 4; q += 32) {
+          const int r = q >> 2, ch = q & 3;
+          const int64_t col = cb + 4 * ch;
+          const int valid = r < p ? (int)imax(0, imin(4, jend - col)) : 0;
+          if (vec) {
+            const float* g = src[arr] + (valid ? (int64_t)r * c + col : 0);
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(
+                             (uint32_t)__cvta_generic_to_shared(dst + r * SS_ROW + 4 * ch)),
+                         "l"(g), "r"(4 * valid)
+                         : "memory");
+          } else {
 #pragma unroll
-      for (int e = 0; e < NE; ++e) {
-        const bool ok = eok(cb, e);
-        const int64_t o = eoff(cb, e);
-        T.nv[e] = ok ? -__ldcs(&V[o]) : 0.f;
-        if (k < 0) {
-          T.u1[e] = ok ? A.F0[o] : 0.f;
-          T.u2[e] = T.u1[e];
-        } else {
-          T.u1[e] = ok ? Ur[o] : 0.f;
-          T.u2[e] = (ok && k > 0) ? Uw[o] : T.u1[e];
+            for (int i = 0; i < 4; ++i)
+              dst[r * SS_ROW + 4 * ch + i] = i < valid ? src[arr][(int64_t)r * c + col + i] : 0.f;
+          }
         }
       }
+      asm volatile("cp.async.commit_group;" ::: "memory");
     };
-    auto tcompute = [&](int tile, int k, float w, bool snap, int slot, bool save, const Tile& T, float& s0,
+    auto tcompute = [&](int tile, int k, float w, bool snap, int slot, bool save, const float* st, float& s0,
                         float& s1) {
       const int64_t cb = j0 + (int64_t)tile * CB;
-      float fe[NE], g[NE];
+      float u1[NE], u2[NE], nv[NE], fe[NE], g[NE];
+#pragma unroll
+      for (int e = 0; e < NE; ++e) {
+        const int sidx = erow(e) * SS_ROW + ecol(e);
+        u1[e] = st[sidx];
+        u2[e] = k <= 0 ? u1[e] : st[SS_ARR_F + sidx];
+        nv[e] = -st[2 * SS_ARR_F + sidx];
+      }
       if (k >= 0) {
         if (snap) {
           float* sp = A.snaps + (int64_t)(slot * 2) * pc;
@@ -170,17 +195,17 @@ __global__ void __launch_bounds__(stream_threads<NT>(), 1) k_nnls_stream(const _
                 bp[o] = sp[o];
                 bp[pc + o] = sp[pc + o];
               }
-              sp[o] = T.u1[e];
-              sp[pc + o] = T.u2[e];
+              sp[o] = u1[e];
+              sp[pc + o] = u2[e];
             }
         }
 #pragma unroll
-        for (int e = 0; e < NE; ++e) fe[e] = relu_nan_fast(fmaf(T.u1[e] - T.u2[e], w, T.u1[e]));
+        for (int e = 0; e < NE; ++e) fe[e] = relu_nan_fast(fmaf(u1[e] - u2[e], w, u1[e]));
       } else {
 #pragma unroll
-        for (int e = 0; e < NE; ++e) fe[e] = T.u1[e];  // F0
+        for (int e = 0; e < NE; ++e) fe[e] = u1[e];  // F0
       }
-      grad(fe, T.nv, g);
+      grad(fe, nv, g);
       float* __restrict__ Uo = A.U + (int64_t)(k < 0 ? 1 : (k & 1)) * pc;  // u_{-1} -> slot 1
 #pragma unroll
       for (int e = 0; e < NE; ++e) {
@@ -189,31 +214,26 @@ __global__ void __launch_bounds__(stream_threads<NT>(), 1) k_nnls_stream(const _
         if (ok) Uo[eoff(cb, e)] = u;
         const float pgv = ok ? (fe[e] > 0.f ? g[e] : min0_nan(g[e])) : 0.f;
         s0 = fmaf(pgv, pgv, s0);
-        s1 = ok ? fmaf(fe[e], g[e] + T.nv[e], s1) : s1;
+        s1 = ok ? fmaf(fe[e], g[e] + nv[e], s1) : s1;
       }
     };
-    // all of this warp's tiles for iteration k, loads one tile ahead
-    // (NT <= 2; with NT >= 3 the extra registers would spill, and 8 warps per
-    // SM keep enough loads in flight without it)
+    // all of this warp's tiles for iteration k through the ring
     auto sweep = [&](int k, float w, bool snap, int slot, bool save, float& s0, float& s1) {
-      if constexpr (NT <= 2) {
-        int t = wid;
-        if (t >= ntiles) return;
-        Tile cur, nxt;
-        tload(t, k, cur);
-        for (; t < ntiles; t += ncw) {
-          const bool more = t + ncw < ntiles;
-          if (more) tload(t + ncw, k, nxt);
-          tcompute(t, k, w, snap, slot, save, cur, s0, s1);
-          if (more) cur = nxt;
-        }
-      } else {
-        for (int t = wid; t < ntiles; t += ncw) {
-          Tile cur;
-          tload(t, k, cur);
-          tcompute(t, k, w, snap, slot, save, cur, s0, s1);
-        }
+      __syncwarp();  // this warp's u stores of iteration k - 1 are visible to its cp.async reads
+      const int nmine = wid < ntiles ? (ntiles - 1 - wid) / ncw + 1 : 0;
+      for (int i = 0; i < SS_STAGES - 1; ++i) {
+        if (i < nmine) issue(wid + i * ncw, k, i);
+        else asm volatile("cp.async.commit_group;" ::: "memory");
       }
+      for (int i = 0; i < nmine; ++i) {
+        asm volatile("cp.async.wait_group %0;" ::"n"(SS_STAGES - 2) : "memory");
+        __syncwarp();
+        tcompute(wid + i * ncw, k, w, snap, slot, save, ring + (i % SS_STAGES) * SS_STAGE_F, s0, s1);
+        __syncwarp();  // the stage is refilled below
+        if (i + SS_STAGES - 1 < nmine) issue(wid + (i + SS_STAGES - 1) * ncw, k, (i + SS_STAGES - 1) % SS_STAGES);
+        else asm volatile("cp.async.commit_group;" ::: "memory");
+      }
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
     };
     // start point (nnls.py:163-178)
     {
@@ -317,7 +337,8 @@ __global__ void __launch_bounds__(stream_threads<NT>(), 1) k_nnls_stream(const _
 // grid: one CTA per SM (cooperative); returns NENMF_ERR_UNSUPPORTED outside FP32, p <= 32
 int launch_nnls_stream(const StreamArgs& a, int grid, cudaStream_t s) {
   const int nt = (a.p + 7) / 8;
-  const size_t smem = (size_t)NW_PPD * NW_MAXW * 3 * sizeof(double);
+  const size_t smem = (size_t)NW_PPD * NW_MAXW * 3 * sizeof(double) +
+                      (size_t)4 * SS_STAGES * SS_STAGE_F * sizeof(float);
   void* args[] = {(void*)&a};
   switch (nt) {
 #define NENMF_STREAM_CASE(N)                                                                               \
