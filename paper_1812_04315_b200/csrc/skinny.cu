@@ -198,10 +198,301 @@ __global__ void k_chunk_reduce(const T* __restrict__ part, int nchunk, int64_t c
   out[o] = s;
 }
 
+__device__ __forceinline__ void mma_tf32_r(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm("mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t tf_hi(float x) { return __float_as_uint(x) & 0xffffe000u; }
+__device__ __forceinline__ uint32_t tf_lo(float x) { return __float_as_uint(x - __uint_as_float(tf_hi(x))); }
+
+// ---------------------------------------------------------------------------
+// FP32 V = A^T B on the tensor pipe (3xTF32 m16n8k8), X streamed through a
+// 3-stage cp.async ring, fixed-order partial sums (deterministic).
+//   k_ux  ("Z side", B = X):    out (p x mx) = U (p x nx) X (nx x mx); units =
+//         (64-column band, row chunk); a warp owns 16 rows of each 128-row
+//         tile and accumulates the band's p x 64 partial in registers; the 8
+//         warps are summed in order at the end of the unit.
+//   k_xv  ("Y side", B = X^T):  out (p x nx) = V (p x mx) X^T; units =
+//         (128-row band, column chunk); a warp owns 16 rows and accumulates
+//         its 16 x p block over the chunk's 64-column tiles.
+// Partials of the chunks go to slabs summed by k_chunk_reduce (chunk order).
+constexpr int VP_NS = 3, VP_XS = 72, VP_US = 136, VP_VS = 72;
+
+template <int MT>  // MT = m16 tiles of p (p <= 16 MT)
+__global__ void __launch_bounds__(256, 1)
+k_ux(const float* __restrict__ X, int64_t nx, int64_t mx, int64_t ldx, const float* __restrict__ U, int p,
+     int64_t nbands, int64_t rchunk, int64_t nunits, float* __restrict__ slab) {
+  constexpr int KP = 16 * MT;
+  constexpr int XB = 128 * VP_XS, UB = KP * VP_US, SF = XB + UB;
+  extern __shared__ __align__(16) float vsm[];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, gq = lane >> 2, tq = lane & 3;
+  float* red = vsm + VP_NS * SF;  // [KP][64] cross-warp sums
+  for (int64_t u = blockIdx.x; u < nunits; u += gridDim.x) {
+    const int64_t cb = u % nbands, rc = u / nbands;
+    const int64_t j0 = cb * 64, r0 = rc * rchunk, r1 = imin(nx, r0 + rchunk);
+    const int ntl = (int)((r1 - r0 + 127) / 128);
+    auto issue = [&](int t, int stg) {
+      float* xs = vsm + stg * SF;
+      float* us = xs + XB;
+      const int64_t i0 = r0 + (int64_t)t * 128;
+      for (int c = tid; c < 128 * 16; c += 256) {
+        const int r = c >> 4, ch = c & 15;
+        const int64_t i = i0 + r, j = j0 + 4 * ch;
+        const int valid = (i < r1) ? (int)imax(0, imin(4, mx - j)) : 0;
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(
+                         (uint32_t)__cvta_generic_to_shared(xs + r * VP_XS + 4 * ch)),
+                     "l"(X + (valid ? i * ldx + j : 0)), "r"(4 * valid)
+                     : "memory");
+      }
+      for (int c = tid; c < KP * 32; c += 256) {
+        const int a = c >> 5, ch = c & 31;
+        const int64_t i = i0 + 4 * ch;
+        const int valid = a < p ? (int)imax(0, imin(4, r1 - i)) : 0;
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(
+                         (uint32_t)__cvta_generic_to_shared(us + a * VP_US + 4 * ch)),
+                     "l"(U + (valid ? (int64_t)a * nx + i : 0)), "r"(4 * valid)
+                     : "memory");
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    float acc[MT][8][4];
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 8; ++nt)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[mt][nt][q] = 0.f;
+    __syncthreads();  // the ring is free (previous unit done)
+    for (int i = 0; i < VP_NS - 1; ++i) {
+      if (i < ntl) issue(i, i);
+      else asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+    for (int t = 0; t < ntl; ++t) {
+      asm volatile("cp.async.wait_group %0;" ::"n"(VP_NS - 2) : "memory");
+      __syncthreads();
+      const float* xs = vsm + (t % VP_NS) * SF;
+      const float* us = xs + XB;
+#pragma unroll
+      for (int kt = 0; kt < 2; ++kt) {
+        const int ib = 16 * wid + 8 * kt;  // 8 rows of the tile (K)
+        uint32_t ah[MT][4], al[MT][4];
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const float v = us[(16 * mt + gq + ((q & 1) ? 8 : 0)) * VP_US + ib + tq + ((q & 2) ? 4 : 0)];
+            ah[mt][q] = tf_hi(v);
+            al[mt][q] = tf_lo(v);
+          }
+#pragma unroll
+        for (int nt = 0; nt < 8; ++nt) {
+          const float b0 = xs[(ib + tq) * VP_XS + 8 * nt + gq], b1 = xs[(ib + tq + 4) * VP_XS + 8 * nt + gq];
+          const uint32_t b0h = tf_hi(b0), b1h = tf_hi(b1), b0l = tf_lo(b0), b1l = tf_lo(b1);
+#pragma unroll
+          for (int mt = 0; mt < MT; ++mt) {
+            mma_tf32_r(acc[mt][nt], al[mt], b0h, b1h);
+            mma_tf32_r(acc[mt][nt], ah[mt], b0l, b1l);
+            mma_tf32_r(acc[mt][nt], ah[mt], b0h, b1h);
+          }
+        }
+      }
+      __syncthreads();
+      if (t + VP_NS - 1 < ntl) issue(t + VP_NS - 1, (t + VP_NS - 1) % VP_NS);
+      else asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    // warps summed in order: C (a, j): rows gq / gq+8 of m-tile mt, columns 2tq, 2tq+1 of n-tile nt
+    for (int w = 0; w < 8; ++w) {
+      __syncthreads();
+      if (wid == w) {
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+          for (int nt = 0; nt < 8; ++nt)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const int a = 16 * mt + gq + ((q & 2) ? 8 : 0), j = 8 * nt + 2 * tq + (q & 1);
+              red[a * 64 + j] = (w == 0 ? 0.f : red[a * 64 + j]) + acc[mt][nt][q];
+            }
+      }
+    }
+    __syncthreads();
+    for (int e = tid; e < p * 64; e += 256) {
+      const int a = e >> 6, j = e & 63;
+      if (j0 + j < mx) slab[(rc * p + a) * mx + j0 + j] = red[a * 64 + j];
+    }
+  }
+}
+
+template <int NTP>  // NTP = n8 tiles of p (p <= 8 NTP)
+__global__ void __launch_bounds__(256, 1)
+k_xv(const float* __restrict__ X, int64_t nx, int64_t mx, int64_t ldx, const float* __restrict__ V, int p,
+     int64_t nbands, int64_t cchunk, int64_t nunits, float* __restrict__ slab) {
+  constexpr int KP = 8 * NTP;
+  constexpr int XB = 128 * VP_XS, VB = KP * VP_VS, SF = XB + VB;
+  extern __shared__ __align__(16) float vsm[];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, gq = lane >> 2, tq = lane & 3;
+  for (int64_t u = blockIdx.x; u < nunits; u += gridDim.x) {
+    const int64_t rb = u % nbands, cc = u / nbands;
+    const int64_t i0 = rb * 128, c0 = cc * cchunk, c1 = imin(mx, c0 + cchunk);
+    const int ntl = (int)((c1 - c0 + 63) / 64);
+    auto issue = [&](int t, int stg) {
+      float* xs = vsm + stg * SF;
+      float* vs = xs + XB;
+      const int64_t j0 = c0 + (int64_t)t * 64;
+      for (int c = tid; c < 128 * 16; c += 256) {
+        const int r = c >> 4, ch = c & 15;
+        const int64_t i = i0 + r, j = j0 + 4 * ch;
+        const int valid = (i < nx) ? (int)imax(0, imin(4, c1 - j)) : 0;
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(
+                         (uint32_t)__cvta_generic_to_shared(xs + r * VP_XS + 4 * ch)),
+                     "l"(X + (valid ? i * ldx + j : 0)), "r"(4 * valid)
+                     : "memory");
+      }
+      for (int c = tid; c < KP * 16; c += 256) {
+        const int a = c >> 4, ch = c & 15;
+        const int64_t j = j0 + 4 * ch;
+        const int valid = a < p ? (int)imax(0, imin(4, c1 - j)) : 0;
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(
+                         (uint32_t)__cvta_generic_to_shared(vs + a * VP_VS + 4 * ch)),
+                     "l"(V + (valid ? (int64_t)a * mx + j : 0)), "r"(4 * valid)
+                     : "memory");
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    float acc[NTP][4];
+#pragma unroll
+    for (int nt = 0; nt < NTP; ++nt)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[nt][q] = 0.f;
+    __syncthreads();
+    for (int i = 0; i < VP_NS - 1; ++i) {
+      if (i < ntl) issue(i, i);
+      else asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+    for (int t = 0; t < ntl; ++t) {
+      asm volatile("cp.async.wait_group %0;" ::"n"(VP_NS - 2) : "memory");
+      __syncthreads();
+      const float* xs = vsm + (t % VP_NS) * SF;
+      const float* vs = xs + XB;
+      const int rw = 16 * wid;
+#pragma unroll
+      for (int kt = 0; kt < 8; ++kt) {
+        uint32_t ah[4], al[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float v = xs[(rw + gq + ((q & 1) ? 8 : 0)) * VP_XS + 8 * kt + tq + ((q & 2) ? 4 : 0)];
+          ah[q] = tf_hi(v);
+          al[q] = tf_lo(v);
+        }
+#pragma unroll
+        for (int nt = 0; nt < NTP; ++nt) {
+          const float b0 = vs[(8 * nt + gq) * VP_VS + 8 * kt + tq], b1 = vs[(8 * nt + gq) * VP_VS + 8 * kt + tq + 4];
+          const uint32_t b0h = tf_hi(b0), b1h = tf_hi(b1), b0l = tf_lo(b0), b1l = tf_lo(b1);
+          mma_tf32_r(acc[nt], al, b0h, b1h);
+          mma_tf32_r(acc[nt], ah, b0l, b1l);
+          mma_tf32_r(acc[nt], ah, b0h, b1h);
+        }
+      }
+      __syncthreads();
+      if (t + VP_NS - 1 < ntl) issue(t + VP_NS - 1, (t + VP_NS - 1) % VP_NS);
+      else asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    // C (row, a): rows gq / gq+8 of the warp's 16, a = 8 nt + 2 tq (+1)
+#pragma unroll
+    for (int nt = 0; nt < NTP; ++nt)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int a = 8 * nt + 2 * tq + (q & 1);
+        const int64_t i = i0 + 16 * wid + gq + ((q & 2) ? 8 : 0);
+        if (a < p && i < nx) slab[(cc * p + a) * nx + i] = acc[nt][q];
+      }
+  }
+}
+
+// FP32 tensor-core V = A^T B; NENMF_ERR_UNSUPPORTED outside p <= 32 or
+// unaligned operands (the caller then uses the CUDA-core kernel)
+static int ab_mma(Arena& ws, const float* At, int64_t p, int64_t r, const float* B, int64_t c, int64_t ldb,
+                  bool trans, float* V, cudaStream_t st) {
+  if (p > 32 || getenv("NENMF_AB_SIMT") != nullptr) return NENMF_ERR_UNSUPPORTED;
+  // X is B (r x c) or, transposed, the c x r matrix whose transpose B is
+  const int64_t nx = trans ? c : r, mx = trans ? r : c;
+  auto al16 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
+  if (((nx | mx | ldb) & 3) != 0 || !al16(B) || !al16(At)) return NENMF_ERR_UNSUPPORTED;
+  int sms = sm_count();
+  if (sms <= 0) sms = 148;
+  // scratch sized for either orientation of (r, c), so that sizing dry runs
+  // (which do not know the orientation of the later call) always suffice
+  auto zslab = [&](int64_t zx, int64_t zm) {
+    const int64_t nb = cdiv(zm, 64);
+    int64_t k = imax(1, imin(cdiv(zx, 128), cdiv(4 * sms, nb)));
+    return cdiv(zx, cdiv(cdiv(zx, k), 128) * 128) * p * zm;
+  };
+  auto yslab = [&](int64_t yx, int64_t ym) {
+    const int64_t nb = cdiv(yx, 128);
+    int64_t k = imax(1, imin(cdiv(ym, 64), cdiv(4 * sms, nb)));
+    return cdiv(ym, cdiv(cdiv(ym, k), 64) * 64) * p * yx;
+  };
+  const int64_t need = imax(imax(zslab(r, c), zslab(c, r)), imax(yslab(c, r), yslab(r, c)));
+  float* slab = ws.take<float>((size_t)need);
+  if (ws.base == nullptr) return NENMF_OK;
+  if (!ws.ok) return NENMF_ERR_WORKSPACE;
+  if (!trans) {
+    const int64_t nbands = cdiv(mx, 64);
+    // row chunks: ~4 units per SM, chunks of whole 128-row tiles
+    int64_t nch = imax(1, imin(cdiv(nx, 128), cdiv(4 * sms, nbands)));
+    const int64_t rchunk = cdiv(cdiv(nx, nch), 128) * 128;
+    nch = cdiv(nx, rchunk);
+    const int mt = (int)cdiv(p, 16);
+    const size_t smem = ((size_t)VP_NS * (128 * VP_XS + 16 * mt * VP_US) + (size_t)16 * mt * 64) * sizeof(float);
+    const int64_t nunits = nbands * nch;
+    const unsigned grid = (unsigned)imin(nunits, (int64_t)sms);
+    if (mt == 1) {
+      NENMF_CUDA_TRY(set_smem(k_ux<1>, smem));
+      k_ux<1><<<grid, 256, smem, st>>>(B, nx, mx, ldb, At, (int)p, nbands, rchunk, nunits, slab);
+    } else {
+      NENMF_CUDA_TRY(set_smem(k_ux<2>, smem));
+      k_ux<2><<<grid, 256, smem, st>>>(B, nx, mx, ldb, At, (int)p, nbands, rchunk, nunits, slab);
+    }
+    NENMF_LAUNCH_CHECK();
+    k_chunk_reduce<float><<<(unsigned)cdiv(p * mx, 256), 256, 0, st>>>(slab, (int)nch, p * mx, V);
+    NENMF_LAUNCH_CHECK();
+  } else {
+    const int64_t nbands = cdiv(nx, 128);
+    int64_t nch = imax(1, imin(cdiv(mx, 64), cdiv(4 * sms, nbands)));
+    const int64_t cchunk = cdiv(cdiv(mx, nch), 64) * 64;
+    nch = cdiv(mx, cchunk);
+    const int ntp = (int)cdiv(p, 8);
+    const size_t smem = (size_t)VP_NS * (128 * VP_XS + 8 * ntp * VP_VS) * sizeof(float);
+    const int64_t nunits = nbands * nch;
+    const unsigned grid = (unsigned)imin(nunits, (int64_t)sms);
+    auto go = [&](auto kern) -> int {
+      NENMF_CUDA_TRY(set_smem(kern, smem));
+      kern<<<grid, 256, smem, st>>>(B, nx, mx, ldb, At, (int)p, nbands, cchunk, nunits, slab);
+      return NENMF_OK;
+    };
+    if (ntp == 1) NENMF_TRY(go(k_xv<1>));
+    else if (ntp == 2) NENMF_TRY(go(k_xv<2>));
+    else if (ntp == 3) NENMF_TRY(go(k_xv<3>));
+    else NENMF_TRY(go(k_xv<4>));
+    NENMF_LAUNCH_CHECK();
+    k_chunk_reduce<float><<<(unsigned)cdiv(p * nx, 256), 256, 0, st>>>(slab, (int)nch, p * nx, V);
+    NENMF_LAUNCH_CHECK();
+  }
+  return NENMF_OK;
+}
+
 template <typename T>
 int ab(Arena& ws, const T* At, int64_t p, int64_t r, const T* B, int64_t c, int64_t ldb, bool trans,
        T* V, cudaStream_t st) {
   if (p < 1 || r < 1 || c < 1) return NENMF_ERR_DIM;
+  if constexpr (sizeof(T) == 4) {
+    const int rc = ab_mma(ws, reinterpret_cast<const float*>(At), p, r, reinterpret_cast<const float*>(B), c, ldb,
+                          trans, reinterpret_cast<float*>(V), st);
+    if (rc != NENMF_ERR_UNSUPPORTED) return rc;
+  }
   if (p > 4 * AB_MAXA) return NENMF_ERR_UNSUPPORTED;
   const int64_t nchunk = cdiv(r, AB_RCHUNK);
   T* part = nchunk > 1 ? ws.take<T>((size_t)nchunk * p * c) : nullptr;
@@ -345,13 +636,6 @@ k_resid(const T* __restrict__ At, int p, int64_t r, const T* __restrict__ B, int
 // truncation, lo = x - hi raw; relative error ~2^-20), the X values of the
 // tile are loaded (two floats per thread per block) before the MMAs so the
 // DRAM stream overlaps them.  Row/column tails are masked.
-__device__ __forceinline__ void mma_tf32_r(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
-  asm("mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
-      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
-      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
-}
-__device__ __forceinline__ uint32_t tf_hi(float x) { return __float_as_uint(x) & 0xffffe000u; }
-__device__ __forceinline__ uint32_t tf_lo(float x) { return __float_as_uint(x - __uint_as_float(tf_hi(x))); }
 
 template <int KT>
 __global__ void __launch_bounds__(256)
