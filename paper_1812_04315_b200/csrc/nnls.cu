@@ -240,7 +240,7 @@ int solve_nnls(Arena& ws, const T* At, int64_t r, int64_t p, const T* B, int64_t
   double* salpha = use_mma ? nullptr : ws.take<double>((size_t)pl.grid * NW_MAXW * (NW_SNAP + 1) * 2);
   T* gstate = (use_mma || use_stream || pl.smem_state) ? nullptr : ws.take<T>((size_t)4 * pc);
   double* rpart = fused ? ws.take<double>((size_t)2 * grid_used) : nullptr;
-  double* npart = fused_next ? ws.take<double>((size_t)grid_used * p * nup) : nullptr;
+  double* npart = fused_next ? ws.take<double>((size_t)grid_used * 2 * p * nup) : nullptr;  // [grid][best, start]
   // window records + (fused) the grid-barrier counter, zeroed together
   const size_t rec_bytes = sizeof(WinRec) * ((size_t)NW_SLOTS * grid_used + NW_SLOTS) + 64;
   unsigned char* recmem = ws.take<unsigned char>(rec_bytes);

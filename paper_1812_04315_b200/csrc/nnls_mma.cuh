@@ -678,24 +678,59 @@ k_nnls_mma(const __grid_constant__ MmaArgs<T> A) {
   int start_wins = 0;
   if (tracebuf != nullptr && blockIdx.x == 0 && tid == 0) tracebuf[NN_TRACE_LEN + 60 + 8] = gtimer_ns();
   if (fused && sh.fail_at == -1) {
-    // tie-break (nnls.py:219-227): fixed-order sums over warps, then over CTAs
-    // after a grid barrier; every CTA reaches the same decision
-    start_wins = 1;
-    if (ok_best) {
-      if (tid == 0) {
-        double a0 = 0.0, a1 = 0.0;
-        for (int w = 0; w < ncw; ++w) {
-          a0 += s_red[w][0];
-          a1 += s_red[w][1];
+    // tie-break (nnls.py:219-227) and the next product Pout = F_out Pt^T
+    // (factorize.py:110,113) behind ONE grid barrier: each CTA posts its
+    // residual partials of best and start and, for the next product, its
+    // partials for both candidates; after the barrier every CTA reaches the
+    // same decision (fixed-order sums) and reduces the chosen candidate's slice
+    const bool next = A.Pt != nullptr;
+    const int nup = next ? (int)A.nup : 0, no = p * nup;
+    if (next) {
+      T* Fs = Bs + (size_t)r * cpb;  // [p][cpb]
+      T* Ps = Fs + (size_t)p * cpb;  // [nup][cpb]
+      for (int i = tid; i < nup * ncols; i += blockDim.x) {
+        const int b = i / ncols, jl = i % ncols;
+        Ps[(size_t)b * cpb + jl] = A.Pt[(int64_t)b * c + j0 + jl];
+      }
+      for (int cand = ok_best ? 0 : 1; cand < 2; ++cand) {  // 0: best, 1: start
+        __syncthreads();
+        for (int i = tid; i < p * ncols; i += blockDim.x) {
+          const int a2 = i / ncols, jl = i % ncols;
+          Fs[(size_t)a2 * cpb + jl] =
+              cand == 0 ? ftile_all[(size_t)(jl / S::CB) * 2 * 32 * S::CB + a2 * S::CB + jl % S::CB]
+                        : F0[(int64_t)a2 * c + j0 + jl];
         }
-        A.rpart[2 * blockIdx.x] = a0;
-        A.rpart[2 * blockIdx.x + 1] = a1;
+        __syncthreads();
+        for (int o = tid; o < no; o += blockDim.x) {
+          const int a2 = o / nup, b = o % nup;
+          double acc2 = 0.0;
+          for (int jl = 0; jl < ncols; ++jl)
+            acc2 = fma((double)Fs[(size_t)a2 * cpb + jl], (double)Ps[(size_t)b * cpb + jl], acc2);
+          A.npart[((size_t)blockIdx.x * 2 + cand) * no + o] = acc2;
+        }
+      }
+    }
+    start_wins = 1;
+    if (ok_best || next) {
+      __syncthreads();
+      if (tid == 0) {
+        if (ok_best) {
+          double a0 = 0.0, a1 = 0.0;
+          for (int w = 0; w < ncw; ++w) {
+            a0 += s_red[w][0];
+            a1 += s_red[w][1];
+          }
+          A.rpart[2 * blockIdx.x] = a0;
+          A.rpart[2 * blockIdx.x + 1] = a1;
+        }
         __threadfence();
         atomicAdd(A.bar, 1u);
         while (ld_acquire_u32(A.bar) < gridDim.x) __nanosleep(32);
       }
+      __syncthreads();
+    }
+    if (ok_best) {
       if (wid == 0) {
-        __syncwarp();
         // CTA partials summed lane-strided then by a fixed butterfly: the same
         // order (and value) in every CTA
         double b0 = 0.0, b1 = 0.0;
@@ -725,48 +760,17 @@ k_nnls_mma(const __grid_constant__ MmaArgs<T> A) {
       for (int e = 0; e < NE; ++e)
         if (evalid(e)) Fout[eoff(e)] = F0[eoff(e)];
     }
-  }
-  if (fused && A.Pt != nullptr && sh.fail_at == -1) {
-    // ---- next product Pout = F_out Pt^T (factorize.py:110,113): per-CTA
-    // partials over its columns, a grid barrier, then each CTA reduces a
-    // slice of the p x nup outputs in fixed CTA order
-    const int nup = (int)A.nup, no = p * nup;
-    T* Fs = Bs + (size_t)r * cpb;  // [p][cpb]
-    T* Ps = Fs + (size_t)p * cpb;  // [nup][cpb]
-    const bool use_best = ok_best && !start_wins;
-    for (int i = tid; i < p * ncols; i += blockDim.x) {
-      const int a2 = i / ncols, jl = i % ncols;
-      Fs[(size_t)a2 * cpb + jl] =
-          use_best ? ftile_all[(size_t)(jl / S::CB) * 2 * 32 * S::CB + a2 * S::CB + jl % S::CB]
-                   : F0[(int64_t)a2 * c + j0 + jl];
-    }
-    for (int i = tid; i < nup * ncols; i += blockDim.x) {
-      const int b = i / ncols, jl = i % ncols;
-      Ps[(size_t)b * cpb + jl] = A.Pt[(int64_t)b * c + j0 + jl];
-    }
-    __syncthreads();
-    for (int o = tid; o < no; o += blockDim.x) {
-      const int a2 = o / nup, b = o % nup;
-      double acc2 = 0.0;
-      for (int jl = 0; jl < ncols; ++jl)
-        acc2 = fma((double)Fs[(size_t)a2 * cpb + jl], (double)Ps[(size_t)b * cpb + jl], acc2);
-      A.npart[(size_t)blockIdx.x * no + o] = acc2;
-    }
-    __syncthreads();
-    if (tid == 0) {
-      __threadfence();
-      atomicAdd(A.bar + 1, 1u);
-      while (ld_acquire_u32(A.bar + 1) < gridDim.x) __nanosleep(32);
-    }
-    __syncthreads();
-    const int per = (no + (int)gridDim.x - 1) / (int)gridDim.x;
-    const int o0 = (int)blockIdx.x * per, o1 = min(no, o0 + per);
-    const int nwarps = blockDim.x >> 5;
-    for (int o = o0 + wid; o < o1; o += nwarps) {
-      double sacc = 0.0;
-      for (int g = lane; g < (int)gridDim.x; g += 32) sacc += __ldcg(&A.npart[(size_t)g * no + o]);
-      sacc = warp_sum(sacc);
-      if (lane == 0) A.Pout[o] = (T)sacc;
+    if (next) {
+      const int cand = (ok_best && !start_wins) ? 0 : 1;
+      const int per = (no + (int)gridDim.x - 1) / (int)gridDim.x;
+      const int o0 = (int)blockIdx.x * per, o1 = min(no, o0 + per);
+      const int nwarps = blockDim.x >> 5;
+      for (int o = o0 + wid; o < o1; o += nwarps) {
+        double sacc = 0.0;
+        for (int g = lane; g < (int)gridDim.x; g += 32) sacc += __ldcg(&A.npart[((size_t)g * 2 + cand) * no + o]);
+        sacc = warp_sum(sacc);
+        if (lane == 0) A.Pout[o] = (T)sacc;
+      }
     }
   }
   if (tracebuf != nullptr && blockIdx.x == 0 && tid == 0) tracebuf[NN_TRACE_LEN + 60 + 10] = gtimer_ns();
