@@ -167,13 +167,21 @@ k_nnls_mma(const __grid_constant__ MmaArgs<T> A) {
       double* v = pv;
       if (lane < k) v[lane] = A.pvec[lane];
       __syncwarp();
+      // this lane's Gram row in registers (the row reads from shared memory
+      // would conflict: rows are k doubles apart); same arithmetic as k_power
+      double grow[32];
+#pragma unroll
+      for (int l = 0; l < 32; ++l) grow[l] = (lane < k && l < k) ? gram[lane * k + l] : 0.0;
       int draw = 1;
       double est = 0.0;
       bool conv_any = false;
       for (int it = 0; it < A.pmax; ++it) {
         double wi = 0.0;
-        if (lane < k)
-          for (int l = 0; l < k; ++l) wi = fma(gram[lane * k + l], v[l], wi);
+        if (lane < k) {
+#pragma unroll
+          for (int l = 0; l < 32; ++l)
+            if (l < k) wi = fma(grow[l], v[l], wi);
+        }
         const double nw = sqrt(warp_sum(lane < k ? fma(wi, wi, 0.0) : 0.0));
         __syncwarp();
         if (nw == 0.0) {
