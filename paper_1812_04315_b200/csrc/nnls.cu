@@ -213,7 +213,7 @@ int solve_nnls(Arena& ws, const T* At, int64_t r, int64_t p, const T* B, int64_t
                        getenv("NENMF_NNLS_SIMT") == nullptr;
   // FP32, p <= 32, too many columns for the register-resident solver: the
   // streamed tensor-core solver (nnls_stream.cuh) keeps u_k in HBM
-  const bool use_stream = !use_mma && sizeof(T) == 4 && p <= 32 && max_iter <= NN_WTAB_LEN &&
+  const bool use_stream = !use_mma && sizeof(T) == 4 && p <= 64 && max_iter <= NN_WTAB_LEN &&
                           getenv("NENMF_NNLS_SIMT") == nullptr;
   // streamed solver: column blocks of whole 16-column tiles (16-byte aligned rows for cp.async)
   const int64_t scpb = cdiv(cdiv(c, imax(1, imin(sms, cdiv(c, 16)))), 16) * 16;

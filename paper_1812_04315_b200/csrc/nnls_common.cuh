@@ -136,7 +136,7 @@ __device__ __forceinline__ void solver_shared_init(SolverShared& sh) {
 // order.  `pp` holds the compute warps' per-iteration sums [PPD][MAXW][3].
 static __device__ void resolver_warp(SolverShared& sh, const double* pp, int ncw, int max_iter, double grad_tol, double L,
                               WinRec* __restrict__ recs, WinRec* __restrict__ results,
-                              unsigned long long* __restrict__ tracebuf) {
+                              unsigned long long* __restrict__ tracebuf, int ppw = NW_MAXW) {
   const int lane = threadIdx.x & 31;
   const int G = gridDim.x;
   const bool trace = tracebuf != nullptr;
@@ -165,7 +165,7 @@ static __device__ void resolver_warp(SolverShared& sh, const double* pp, int ncw
           WinRec* rec = recs + (int64_t)rec_idx(pubw) * G + blockIdx.x;
           const int j = win_first(pubw) + lane;
           if (j <= last) {
-            const double* q = pp + (size_t)((j + NW_PPD) % NW_PPD) * NW_MAXW * 3;
+            const double* q = pp + (size_t)((j + NW_PPD) % NW_PPD) * ppw * 3;
             double v0 = 0.0, v1 = 0.0, v2 = 0.0;
             for (int w = 0; w < ncw; ++w) {
               v0 += q[w * 3 + 0];

@@ -10,19 +10,32 @@
 // per element and iteration, the streaming floor).  Window snapshots are the
 // values already loaded at a window start; the returned best iterate is
 // recomputed from its window's snapshot at the end (<= 32 on-chip steps per
-// tile).  FP32, p <= 32.
+// tile).  FP32, p <= 64.
 #pragma once
 #include "nnls_mma.cuh"
 
 namespace nenmf {
 
 // 4 compute warps + the resolver; each compute warp streams its tiles through
-// a 3-stage shared-memory ring (stage: u_{k-1}, u_{k-2}, V tiles of 32 x 16)
+// a shared-memory ring (stage: u_{k-1}, u_{k-2}, V tiles of 8 NT x 16);
+// NT <= 4 (p <= 32): 3 stages, W^T fragments in registers; NT 5..8
+// (p <= 64, BASELINE cfg3's p = 50): 2 stages, W^T fragments in shared memory.
 template <int NT>
 __host__ __device__ constexpr int stream_threads() {
   return 5 * 32;
 }
-constexpr int SS_STAGES = 3, SS_ROW = 20, SS_ARR_F = 32 * SS_ROW, SS_STAGE_F = 3 * SS_ARR_F;
+constexpr int SS_ROW = 20, SS_PPW = 8;  // ring row stride (floats); pp ring stride (warps)
+template <int NT>
+struct SS {
+  static constexpr bool WSM = NT > 4;
+  static constexpr int STAGES = WSM ? 2 : 3;
+  static constexpr int ARR_F = 8 * NT * SS_ROW;
+  static constexpr int STAGE_F = 3 * ARR_F;
+  static constexpr size_t smem() {
+    return (size_t)NW_PPD * SS_PPW * 3 * sizeof(double) + (size_t)4 * STAGES * STAGE_F * sizeof(float) +
+           (WSM ? (size_t)NT * NT * 32 * 16 : 0);
+  }
+};
 
 template <int NT>
 __global__ void __launch_bounds__(stream_threads<NT>(), 1) k_nnls_stream(const __grid_constant__ StreamArgs A) {
@@ -50,24 +63,38 @@ __global__ void __launch_bounds__(stream_threads<NT>(), 1) k_nnls_stream(const _
     // element e of this thread within a tile: solver row, tile-local column
     auto erow = [&](int e) { return 8 * (e >> 2) + 2 * tq + (e & 1); };
     auto ecol = [&](int e) { return gq + ((e & 2) ? 8 : 0); };
-    // W^T fragments, as k_nnls_mma
-    uint32_t bhi[NT][NT][2], bco[NT][NT][2];
+    // W^T fragments, as k_nnls_mma: in registers (NT <= 4) or shared memory
+    constexpr bool WSM = SS<NT>::WSM;
+    constexpr int NTR = WSM ? 1 : NT;  // register array extent
+    uint32_t bhi[NTR][NTR][2], bco[NTR][NTR][2];
+    uint4* wf = reinterpret_cast<uint4*>(reinterpret_cast<float*>(smem_d + (size_t)NW_PPD * SS_PPW * 3) +
+                                         (size_t)4 * SS<NT>::STAGES * SS<NT>::STAGE_F);  // [NT][NT][32]
 #pragma unroll
     for (int kt = 0; kt < NT; ++kt)
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) {
+        if (WSM && (kt * NT + nt) % ncw != wid) continue;  // fill the shared copy cooperatively
         float wh[2], wl[2];
+        uint32_t h2[2];
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int i = 8 * nt + gq, l = 8 * kt + 2 * tq + h;
           const float w = (i < p && l < p) ? A.W[i * p + l] : 0.f;
-          bhi[kt][nt][h] = tf32_hi(w);
-          wh[h] = __uint_as_float(bhi[kt][nt][h]);
+          h2[h] = tf32_hi(w);
+          wh[h] = __uint_as_float(h2[h]);
           wl[h] = w - wh[h];
         }
-        bco[kt][nt][0] = pack_bf16(wh[0], wh[1]);
-        bco[kt][nt][1] = pack_bf16(wl[0], wl[1]);
+        const uint32_t c0 = pack_bf16(wh[0], wh[1]), c1 = pack_bf16(wl[0], wl[1]);
+        if constexpr (WSM) {
+          wf[(kt * NT + nt) * 32 + lane] = make_uint4(h2[0], h2[1], c0, c1);
+        } else {
+          bhi[kt % NTR][nt % NTR][0] = h2[0];
+          bhi[kt % NTR][nt % NTR][1] = h2[1];
+          bco[kt % NTR][nt % NTR][0] = c0;
+          bco[kt % NTR][nt % NTR][1] = c1;
+        }
       }
+    if constexpr (WSM) asm volatile("bar.sync 2, %0;" ::"r"(ncw * 32) : "memory");
     auto grad = [&](const float (&fe)[NE], const float (&nv)[NE], float (&g)[NE]) {
       uint32_t ahi[NT][4], aco[NT][4];
 #pragma unroll
@@ -90,14 +117,26 @@ __global__ void __launch_bounds__(stream_threads<NT>(), 1) k_nnls_stream(const _
       for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
         for (int r = 0; r < 4; ++r) cc[nt][r] = nv[4 * nt + r];
+      if constexpr (WSM) {
 #pragma unroll
-      for (int kt = 0; kt < NT; ++kt)
+        for (int kt = 0; kt < NT; ++kt)
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt) mma_bf16(cc[nt], aco[kt], bco[kt][nt][0], bco[kt][nt][1]);
+          for (int nt = 0; nt < NT; ++nt) {
+            const uint4 b = wf[(kt * NT + nt) * 32 + lane];
+            mma_bf16(cc[nt], aco[kt], b.z, b.w);
+            mma_tf32(cc[nt], ahi[kt], b.x, b.y);
+          }
+      } else {
 #pragma unroll
-      for (int kt = 0; kt < NT; ++kt)
+        for (int kt = 0; kt < NT; ++kt)
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt) mma_tf32(cc[nt], ahi[kt], bhi[kt][nt][0], bhi[kt][nt][1]);
+          for (int nt = 0; nt < NT; ++nt)
+            mma_bf16(cc[nt], aco[kt], bco[kt % NTR][nt % NTR][0], bco[kt % NTR][nt % NTR][1]);
+#pragma unroll
+        for (int kt = 0; kt < NT; ++kt)
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) mma_tf32(cc[nt], ahi[kt], bhi[kt % NTR][nt % NTR][0], bhi[kt % NTR][nt % NTR][1]);
+      }
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
@@ -110,7 +149,7 @@ __global__ void __launch_bounds__(stream_threads<NT>(), 1) k_nnls_stream(const _
         s1 += __shfl_xor_sync(0xffffffffu, s1, o);
       }
       if (lane == 0) {
-        double* q = pp + ((size_t)((j + NW_PPD) % NW_PPD) * NW_MAXW + wid) * 3;
+        double* q = pp + ((size_t)((j + NW_PPD) % NW_PPD) * SS_PPW + wid) * 3;
         q[0] = s0;
         q[1] = s1;
         q[2] = 0.0;
@@ -140,7 +179,8 @@ __global__ void __launch_bounds__(stream_threads<NT>(), 1) k_nnls_stream(const _
     // of u_{k-1}, u_{k-2} and V (32 rows x 16 columns each, row stride 20:
     // the accumulator-layout reads are bank-conflict free), two tiles ahead
     // of the one being computed.
-    float* ring = reinterpret_cast<float*>(smem_d + (size_t)NW_PPD * NW_MAXW * 3) +
+    constexpr int SS_STAGES = SS<NT>::STAGES, SS_ARR_F = SS<NT>::ARR_F, SS_STAGE_F = SS<NT>::STAGE_F;
+    float* ring = reinterpret_cast<float*>(smem_d + (size_t)NW_PPD * SS_PPW * 3) +
                   (size_t)wid * SS_STAGES * SS_STAGE_F;
     const bool vec = (c & 3) == 0;  // 16-byte rows: cp.async; otherwise plain loads
     auto issue = [&](int tile, int k, int stg) {
@@ -153,7 +193,7 @@ __global__ void __launch_bounds__(stream_threads<NT>(), 1) k_nnls_stream(const _
       for (int arr = 0; arr < 3; ++arr) {
         if (arr == 1 && narr == 1) continue;
         float* dst = st + arr * SS_ARR_F;
-        for (int q = lane; q < 32 * 4; q += 32) {
+        for (int q = lane; q < 8 * NT * 4; q += 32) {
           const int r = q >> 2, ch = q & 3;
           const int64_t col = cb + 4 * ch;
           const int valid = r < p ? (int)imax(0, imin(4, jend - col)) : 0;
@@ -319,7 +359,7 @@ __global__ void __launch_bounds__(stream_threads<NT>(), 1) k_nnls_stream(const _
       }
     }
   } else {
-    resolver_warp(sh, pp, ncw, max_iter, A.grad_tol, L, A.recs, A.results, nullptr);
+    resolver_warp(sh, pp, ncw, max_iter, A.grad_tol, L, A.recs, A.results, nullptr, SS_PPW);
     asm volatile("bar.sync 1, %0;" ::"r"(blockDim.x) : "memory");
   }
   __syncthreads();
@@ -337,21 +377,23 @@ __global__ void __launch_bounds__(stream_threads<NT>(), 1) k_nnls_stream(const _
 // grid: one CTA per SM (cooperative); returns NENMF_ERR_UNSUPPORTED outside FP32, p <= 32
 int launch_nnls_stream(const StreamArgs& a, int grid, cudaStream_t s) {
   const int nt = (a.p + 7) / 8;
-  const size_t smem = (size_t)NW_PPD * NW_MAXW * 3 * sizeof(double) +
-                      (size_t)4 * SS_STAGES * SS_STAGE_F * sizeof(float);
   void* args[] = {(void*)&a};
   switch (nt) {
 #define NENMF_STREAM_CASE(N)                                                                               \
   case N: {                                                                                                \
-    NENMF_CUDA_TRY(set_smem(k_nnls_stream<N>, smem));                                                      \
+    NENMF_CUDA_TRY(set_smem(k_nnls_stream<N>, SS<N>::smem()));                                             \
     NENMF_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k_nnls_stream<N>, dim3(grid),                  \
-                                               dim3(stream_threads<N>()), args, smem, s));                 \
+                                               dim3(stream_threads<N>()), args, SS<N>::smem(), s));        \
     break;                                                                                                 \
   }
     NENMF_STREAM_CASE(1)
     NENMF_STREAM_CASE(2)
     NENMF_STREAM_CASE(3)
     NENMF_STREAM_CASE(4)
+    NENMF_STREAM_CASE(5)
+    NENMF_STREAM_CASE(6)
+    NENMF_STREAM_CASE(7)
+    NENMF_STREAM_CASE(8)
 #undef NENMF_STREAM_CASE
     default:
       return NENMF_ERR_UNSUPPORTED;

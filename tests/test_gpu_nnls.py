@@ -176,14 +176,16 @@ def test_frobenius_and_rre():
         nm.rre(np.zeros((4, 4)), np.ones((4, 2)), np.ones((2, 4)))
 
 
-@pytest.mark.parametrize("p,c,max_iter", [(20, 20000, 100), (9, 40000, 70), (30, 17000, 45)])
+@pytest.mark.parametrize("p,c,max_iter", [(20, 20000, 100), (9, 40000, 70), (30, 17000, 45), (50, 3000, 60),
+                                          (61, 2500, 40)])
 def test_streamed_solver_many_columns(monkeypatch, p, c, max_iter):
     """FP32 solves with more columns than the register-resident tensor-core
-    solver holds use the streamed tensor-core solver (nnls_stream.cuh):
+    solver holds, or 32 < p <= 64 (BASELINE cfg3's p = 50), use the streamed
+    tensor-core solver (nnls_stream.cuh):
     within the FP32 tolerance of the fp64 oracle, and of the SIMT solver;
     same inner-iteration count and returned iterate kind."""
     rng = np.random.default_rng(c + p)
-    r = 30
+    r = max(30, p + 10)
     A = rng.random((r, p))
     B = A @ rng.random((p, c)) + 0.05 * rng.standard_normal((r, c))
     F0 = rng.random((p, c))
