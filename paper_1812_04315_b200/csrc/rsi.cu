@@ -156,6 +156,19 @@ int dual_pass(Arena& ws, const T* X, int64_t n, int64_t m, int64_t ldx, const T*
                           reinterpret_cast<float*>(Zt), s);
     if (rc != NENMF_ERR_UNSUPPORTED) return rc;
   }
+  if constexpr (sizeof(T) == 8) {
+    // FP64: the two products on the FP64 tensor pipe (skinny.cu ab -> k_xv64 /
+    // k_ux64), one X stream each: Yt = At X^T (B = X^T), Zt = Bt X (B = X)
+    if (k <= 32 && getenv("NENMF_DUAL_SIMT") == nullptr) {
+      Arena a0 = ws;
+      if (At != nullptr) NENMF_TRY(ab<T>(a0, At, k, m, X, n, ldx, true, Yt, s));
+      Arena a1 = ws;
+      if (Bt != nullptr) NENMF_TRY(ab<T>(a1, Bt, k, n, X, m, ldx, false, Zt, s));
+      ws.used = a0.used > a1.used ? a0.used : a1.used;
+      if (!ws.ok || !a0.ok || !a1.ok) ws.ok = false;
+      return ws.base == nullptr || ws.ok ? NENMF_OK : NENMF_ERR_WORKSPACE;
+    }
+  }
   if (k > DU_KMAX) return NENMF_ERR_UNSUPPORTED;
   const int BC = dual_block_cols<T>(k);
   const int64_t gx = cdiv(m, BC), gy = cdiv(n, DU_BR);

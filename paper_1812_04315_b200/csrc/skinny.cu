@@ -16,6 +16,7 @@
 #include "skinny.cuh"
 
 #include <cstdlib>
+#include <utility>
 
 namespace nenmf {
 
@@ -412,6 +413,205 @@ k_xv(const float* __restrict__ X, int64_t nx, int64_t mx, int64_t ldx, const flo
   }
 }
 
+// ---------------------------------------------------------------------------
+// FP64 V = A^T B on the FP64 tensor pipe (DMMA m8n8k4: exact fp64 products),
+// the same unit structure as k_ux / k_xv with 64 x 64 tiles of X.
+//   k_ux64: warp w owns columns 8w..8w+7 of the band and all 64 rows of each
+//           tile (16 k-steps): acc = 4 m-tiles of p x 8 columns
+//   k_xv64: warp w owns rows 8w..8w+7 of the band: acc = 8 rows x p
+__device__ __forceinline__ void dmma_r(double (&d)[2], double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+      : "+d"(d[0]), "+d"(d[1])
+      : "d"(a), "d"(b));
+}
+constexpr int VD_NS = 3, VD_XS = 68, VD_OS = 68;  // row strides (doubles)
+
+__global__ void __launch_bounds__(256, 1)
+k_ux64(const double* __restrict__ X, int64_t nx, int64_t mx, int64_t ldx, const double* __restrict__ U, int p,
+       int64_t nbands, int64_t rchunk, int64_t nunits, double* __restrict__ slab) {
+  constexpr int XB = 64 * VD_XS, UB = 32 * VD_OS, SF = XB + UB;
+  extern __shared__ __align__(16) double dsm[];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, gq = lane >> 2, tq = lane & 3;
+  for (int64_t u = blockIdx.x; u < nunits; u += gridDim.x) {
+    const int64_t cb = u % nbands, rc = u / nbands;
+    const int64_t j0 = cb * 64, r0 = rc * rchunk, r1 = imin(nx, r0 + rchunk);
+    const int ntl = (int)((r1 - r0 + 63) / 64);
+    auto issue = [&](int t, int stg) {
+      double* xs = dsm + stg * SF;
+      double* us = xs + XB;
+      const int64_t i0 = r0 + (int64_t)t * 64;
+      for (int c = tid; c < 64 * 32; c += 256) {  // 64 rows x 32 chunks of 2 doubles
+        const int r = c >> 5, ch = c & 31;
+        const int64_t i = i0 + r, j = j0 + 2 * ch;
+        const int valid = (i < r1) ? (int)imax(0, imin(2, mx - j)) : 0;
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(
+                         (uint32_t)__cvta_generic_to_shared(xs + r * VD_XS + 2 * ch)),
+                     "l"(X + (valid ? i * ldx + j : 0)), "r"(8 * valid)
+                     : "memory");
+      }
+      for (int c = tid; c < 32 * 32; c += 256) {  // U slice: 32 rows (a) x 64 (i)
+        const int a = c >> 5, ch = c & 31;
+        const int64_t i = i0 + 2 * ch;
+        const int valid = a < p ? (int)imax(0, imin(2, r1 - i)) : 0;
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(
+                         (uint32_t)__cvta_generic_to_shared(us + a * VD_OS + 2 * ch)),
+                     "l"(U + (valid ? (int64_t)a * nx + i : 0)), "r"(8 * valid)
+                     : "memory");
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    double acc[4][2];
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt) acc[mt][0] = acc[mt][1] = 0.0;
+    __syncthreads();
+    for (int i = 0; i < VD_NS - 1; ++i) {
+      if (i < ntl) issue(i, i);
+      else asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+    for (int t = 0; t < ntl; ++t) {
+      asm volatile("cp.async.wait_group %0;" ::"n"(VD_NS - 2) : "memory");
+      __syncthreads();
+      const double* xs = dsm + (t % VD_NS) * SF;
+      const double* us = xs + XB;
+#pragma unroll
+      for (int ks = 0; ks < 16; ++ks) {
+        const double b = xs[(4 * ks + tq) * VD_XS + 8 * wid + gq];  // B (k = row, n = column)
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt)
+          if (8 * mt < p) dmma_r(acc[mt], us[(8 * mt + gq) * VD_OS + 4 * ks + tq], b);
+      }
+      __syncthreads();
+      if (t + VD_NS - 1 < ntl) issue(t + VD_NS - 1, (t + VD_NS - 1) % VD_NS);
+      else asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    // C (a, j): a = 8 mt + gq, j = 8 w + 2 tq (+1)
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int a = 8 * mt + gq;
+        const int64_t j = j0 + 8 * wid + 2 * tq + h;
+        if (a < p && j < mx) slab[(rc * p + a) * mx + j] = acc[mt][h];
+      }
+  }
+}
+
+__global__ void __launch_bounds__(256, 1)
+k_xv64(const double* __restrict__ X, int64_t nx, int64_t mx, int64_t ldx, const double* __restrict__ V, int p,
+       int64_t nbands, int64_t cchunk, int64_t nunits, double* __restrict__ slab) {
+  constexpr int XB = 64 * VD_XS, VB = 32 * VD_OS, SF = XB + VB;
+  extern __shared__ __align__(16) double dsm[];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, gq = lane >> 2, tq = lane & 3;
+  for (int64_t u = blockIdx.x; u < nunits; u += gridDim.x) {
+    const int64_t rb = u % nbands, cc = u / nbands;
+    const int64_t i0 = rb * 64, c0 = cc * cchunk, c1 = imin(mx, c0 + cchunk);
+    const int ntl = (int)((c1 - c0 + 63) / 64);
+    auto issue = [&](int t, int stg) {
+      double* xs = dsm + stg * SF;
+      double* vs = xs + XB;
+      const int64_t j0 = c0 + (int64_t)t * 64;
+      for (int c = tid; c < 64 * 32; c += 256) {
+        const int r = c >> 5, ch = c & 31;
+        const int64_t i = i0 + r, j = j0 + 2 * ch;
+        const int valid = (i < nx) ? (int)imax(0, imin(2, c1 - j)) : 0;
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(
+                         (uint32_t)__cvta_generic_to_shared(xs + r * VD_XS + 2 * ch)),
+                     "l"(X + (valid ? i * ldx + j : 0)), "r"(8 * valid)
+                     : "memory");
+      }
+      for (int c = tid; c < 32 * 32; c += 256) {
+        const int a = c >> 5, ch = c & 31;
+        const int64_t j = j0 + 2 * ch;
+        const int valid = a < p ? (int)imax(0, imin(2, c1 - j)) : 0;
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(
+                         (uint32_t)__cvta_generic_to_shared(vs + a * VD_OS + 2 * ch)),
+                     "l"(V + (valid ? (int64_t)a * mx + j : 0)), "r"(8 * valid)
+                     : "memory");
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    double acc[4][2];
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) acc[nt][0] = acc[nt][1] = 0.0;
+    __syncthreads();
+    for (int i = 0; i < VD_NS - 1; ++i) {
+      if (i < ntl) issue(i, i);
+      else asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+    for (int t = 0; t < ntl; ++t) {
+      asm volatile("cp.async.wait_group %0;" ::"n"(VD_NS - 2) : "memory");
+      __syncthreads();
+      const double* xs = dsm + (t % VD_NS) * SF;
+      const double* vs = xs + XB;
+#pragma unroll
+      for (int ks = 0; ks < 16; ++ks) {
+        const double a = xs[(8 * wid + gq) * VD_XS + 4 * ks + tq];  // A (m = row, k = column)
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt)
+          if (8 * nt < p) dmma_r(acc[nt], a, vs[(8 * nt + gq) * VD_OS + 4 * ks + tq]);
+      }
+      __syncthreads();
+      if (t + VD_NS - 1 < ntl) issue(t + VD_NS - 1, (t + VD_NS - 1) % VD_NS);
+      else asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    // C (row, a): row = 8 w + gq, a = 8 nt + 2 tq (+1)
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int a = 8 * nt + 2 * tq + h;
+        const int64_t i = i0 + 8 * wid + gq;
+        if (a < p && i < nx) slab[(cc * p + a) * nx + i] = acc[nt][h];
+      }
+  }
+}
+
+static int ab_dmma(Arena& ws, const double* At, int64_t p, int64_t r, const double* B, int64_t c, int64_t ldb,
+                   bool trans, double* V, cudaStream_t st) {
+  if (p > 32 || getenv("NENMF_AB_SIMT") != nullptr) return NENMF_ERR_UNSUPPORTED;
+  const int64_t nx = trans ? c : r, mx = trans ? r : c;
+  auto al16 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
+  if (((nx | mx | ldb) & 1) != 0 || (ws.base != nullptr && (!al16(B) || !al16(At)))) return NENMF_ERR_UNSUPPORTED;
+  int sms = sm_count();
+  if (sms <= 0) sms = 148;
+  auto chunks = [&](int64_t along, int64_t bands) {  // (count, length) of 64-aligned chunks
+    int64_t k = imax(1, imin(cdiv(along, 64), cdiv(4 * sms, bands)));
+    const int64_t len = cdiv(cdiv(along, k), 64) * 64;
+    return std::make_pair(cdiv(along, len), len);
+  };
+  auto zneed = [&](int64_t zx, int64_t zm) { return chunks(zx, cdiv(zm, 64)).first * p * zm; };
+  auto yneed = [&](int64_t yx, int64_t ym) { return chunks(ym, cdiv(yx, 64)).first * p * yx; };
+  const int64_t need = imax(imax(zneed(r, c), zneed(c, r)), imax(yneed(c, r), yneed(r, c)));
+  double* slab = ws.take<double>((size_t)need);
+  if (ws.base == nullptr) return NENMF_OK;
+  if (!ws.ok) return NENMF_ERR_WORKSPACE;
+  const size_t smem = (size_t)VD_NS * (64 * VD_XS + 32 * VD_OS) * sizeof(double);
+  if (!trans) {  // V (p x mx) = At (p x nx) X
+    const int64_t nbands = cdiv(mx, 64);
+    const auto ch = chunks(nx, nbands);
+    const int64_t nunits = nbands * ch.first;
+    NENMF_CUDA_TRY(set_smem(k_ux64, smem));
+    k_ux64<<<(unsigned)imin(nunits, (int64_t)sms), 256, smem, st>>>(B, nx, mx, ldb, At, (int)p, nbands, ch.second,
+                                                                     nunits, slab);
+    NENMF_LAUNCH_CHECK();
+    k_chunk_reduce<double><<<(unsigned)cdiv(p * mx, 256), 256, 0, st>>>(slab, (int)ch.first, p * mx, V);
+    NENMF_LAUNCH_CHECK();
+  } else {  // V (p x nx) = At (p x mx) X^T
+    const int64_t nbands = cdiv(nx, 64);
+    const auto ch = chunks(mx, nbands);
+    const int64_t nunits = nbands * ch.first;
+    NENMF_CUDA_TRY(set_smem(k_xv64, smem));
+    k_xv64<<<(unsigned)imin(nunits, (int64_t)sms), 256, smem, st>>>(B, nx, mx, ldb, At, (int)p, nbands, ch.second,
+                                                                     nunits, slab);
+    NENMF_LAUNCH_CHECK();
+    k_chunk_reduce<double><<<(unsigned)cdiv(p * nx, 256), 256, 0, st>>>(slab, (int)ch.first, p * nx, V);
+    NENMF_LAUNCH_CHECK();
+  }
+  return NENMF_OK;
+}
+
 // FP32 tensor-core V = A^T B; NENMF_ERR_UNSUPPORTED outside p <= 32 or
 // unaligned operands (the caller then uses the CUDA-core kernel)
 static int ab_mma(Arena& ws, const float* At, int64_t p, int64_t r, const float* B, int64_t c, int64_t ldb,
@@ -420,7 +620,8 @@ static int ab_mma(Arena& ws, const float* At, int64_t p, int64_t r, const float*
   // X is B (r x c) or, transposed, the c x r matrix whose transpose B is
   const int64_t nx = trans ? c : r, mx = trans ? r : c;
   auto al16 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
-  if (((nx | mx | ldb) & 3) != 0 || !al16(B) || !al16(At)) return NENMF_ERR_UNSUPPORTED;
+  // (dry runs size the scratch without seeing the pointers: assume aligned)
+  if (((nx | mx | ldb) & 3) != 0 || (ws.base != nullptr && (!al16(B) || !al16(At)))) return NENMF_ERR_UNSUPPORTED;
   int sms = sm_count();
   if (sms <= 0) sms = 148;
   // scratch sized for either orientation of (r, c), so that sizing dry runs
@@ -485,14 +686,42 @@ static int ab_mma(Arena& ws, const float* At, int64_t p, int64_t r, const float*
 }
 
 template <typename T>
+static int ab_simt(Arena& ws, const T* At, int64_t p, int64_t r, const T* B, int64_t c, int64_t ldb, bool trans,
+                   T* V, cudaStream_t st);
+
+template <typename T>
 int ab(Arena& ws, const T* At, int64_t p, int64_t r, const T* B, int64_t c, int64_t ldb, bool trans,
        T* V, cudaStream_t st) {
   if (p < 1 || r < 1 || c < 1) return NENMF_ERR_DIM;
-  if constexpr (sizeof(T) == 4) {
-    const int rc = ab_mma(ws, reinterpret_cast<const float*>(At), p, r, reinterpret_cast<const float*>(B), c, ldb,
-                          trans, reinterpret_cast<float*>(V), st);
-    if (rc != NENMF_ERR_UNSUPPORTED) return rc;
+  {
+    // tensor-core path; a dry run sizes it AND the CUDA-core fallback below
+    // (the live call may fall back on unaligned operands)
+    Arena fast = ws;
+    int rc;
+    if constexpr (sizeof(T) == 4)
+      rc = ab_mma(fast, reinterpret_cast<const float*>(At), p, r, reinterpret_cast<const float*>(B), c, ldb, trans,
+                  reinterpret_cast<float*>(V), st);
+    else
+      rc = ab_dmma(fast, reinterpret_cast<const double*>(At), p, r, reinterpret_cast<const double*>(B), c, ldb,
+                   trans, reinterpret_cast<double*>(V), st);
+    if (rc != NENMF_ERR_UNSUPPORTED) {
+      if (ws.base != nullptr) {
+        ws = fast;
+        return rc;
+      }
+      Arena slow = ws;
+      const size_t fast_used = fast.used;
+      ab_simt<T>(slow, At, p, r, B, c, ldb, trans, V, st);
+      ws.used = fast_used > slow.used ? fast_used : slow.used;
+      return NENMF_OK;
+    }
   }
+  return ab_simt<T>(ws, At, p, r, B, c, ldb, trans, V, st);
+}
+
+template <typename T>
+static int ab_simt(Arena& ws, const T* At, int64_t p, int64_t r, const T* B, int64_t c, int64_t ldb, bool trans,
+                   T* V, cudaStream_t st) {
   if (p > 4 * AB_MAXA) return NENMF_ERR_UNSUPPORTED;
   const int64_t nchunk = cdiv(r, AB_RCHUNK);
   T* part = nchunk > 1 ? ws.take<T>((size_t)nchunk * p * c) : nullptr;
