@@ -19,6 +19,14 @@
  *   nenmf_dual_pass         compression.py:134-139 X @ A and X.T @ B in one pass
  *   nenmf_orthonormalize    compression.py:88-106 _orthonormal_columns (CholeskyQR2;
  *                           Householder TSQR for k > 32)
+ *   nenmf_power_iteration   compression.py:144-176 power_iteration_pair
+ *   nenmf_sketch_draws      compression.py:130-132 default_rng(seed).standard_normal
+ *   nenmf_panel_gram/_factor/_trsm  compression.py:88-106 split for row shards
+ *   nenmf_prepare_x + *_prepared    one X preparation shared by the sketch,
+ *                           the compression and the vanilla V products
+ *   nenmf_solve_nnls_prepared  nnls.py:119-227 with V = X F^T / X^T G from Xp
+ *   nenmf_solve_nnls_next   nnls.py:119-227 + factorize.py:110,113 (the solve
+ *                           also forms the next half-step operand)
  *
  * Conventions
  *  - All array pointers are DEVICE pointers, row-major, allocated by the
