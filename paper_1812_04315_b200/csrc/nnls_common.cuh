@@ -184,6 +184,7 @@ static __device__ void resolver_warp(SolverShared& sh, const double* pp, int ncw
           __syncwarp();
           if (trace && blockIdx.x == 0 && lane == 0 && pubw + 1 < NN_TRACE_LEN)
             g_nnls_trace(1)[pubw + 1] = gtimer_ns();
+          if (trace && lane == 0 && pubw == nwin - 1 && blockIdx.x < 512) g_nnls_trace(0)[512 + blockIdx.x] = gtimer_ns();
           ++pubw;
           progress = true;
         }
@@ -243,31 +244,56 @@ static __device__ void resolver_warp(SolverShared& sh, const double* pp, int ncw
           const double r1 = __ldcg(&res->v[lane][1]);
           const double r2 = __ldcg(&res->v[lane][2]);
           const int first = win_first(resw), last = win_last(resw);
-          for (int j = first; j <= last && !halt; ++j) {
-            const int t = j - (resw < 0 ? -1 : first);
-            const double pg = sqrt(__shfl_sync(0xffffffffu, r0, t));
-            const double partial = 0.5 * (__shfl_sync(0xffffffffu, r1, t) - __shfl_sync(0xffffffffu, r2, t));
-            if (j < 0) {
-              pg_ref = pg;
-              best_part = partial;
-              if (!(isfinite(partial) && isfinite(pg) && isfinite(L))) {
-                fail_at = 0;
-                halt = true;
-              }
-            } else if (!(isfinite(pg) && isfinite(partial))) {
-              fail_at = j;
+          if (resw < 0) {
+            // the start point (nnls.py:178-181)
+            pg_ref = sqrt(r0);
+            best_part = 0.5 * (r1 - r2);
+            pg_ref = __shfl_sync(0xffffffffu, pg_ref, 0);
+            best_part = __shfl_sync(0xffffffffu, best_part, 0);
+            if (!(isfinite(best_part) && isfinite(pg_ref) && isfinite(L))) {
+              fail_at = 0;
               halt = true;
-            } else {
-              if (partial < best_part) {  // nnls.py:198-201
-                best_part = partial;
-                best_j = j;
-              }
-              if (pg <= grad_tol * pg_ref) {  // nnls.py:202-203
-                stop_at = j;
-                halt = true;
+            }
+          } else {
+            // the window's iterations in parallel, one per lane; the same
+            // decisions as the sequential scan of nnls.py:196-203: the first
+            // non-finite iteration fails, the first with pg <= tol * pg_ref
+            // stops (after the best-update of its own iteration), and best is
+            // the earliest strict minimum of the partial objective before that
+            const int j = first + lane;
+            const bool valid = j <= last;
+            const double pg = sqrt(r0), partial = 0.5 * (r1 - r2);
+            const bool bad = valid && !(isfinite(pg) && isfinite(partial));
+            const bool stp = valid && !bad && pg <= grad_tol * pg_ref;
+            const unsigned ev = __ballot_sync(0xffffffffu, bad || stp);
+            const int e = ev ? __ffs(ev) - 1 : 32;
+            const bool e_bad = ev ? ((__ballot_sync(0xffffffffu, bad) >> e) & 1u) != 0 : false;
+            // candidates for best: valid lanes before the event, and the event itself when it is a stop
+            const bool cand = valid && !bad && (lane < e || (lane == e && !e_bad));
+            double mv = cand ? partial : __longlong_as_double(0x7ff0000000000000ll);  // +inf
+            int mi = cand ? lane : 32;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+              const double ov = __shfl_xor_sync(0xffffffffu, mv, o);
+              const int oi = __shfl_xor_sync(0xffffffffu, mi, o);
+              if (ov < mv || (ov == mv && oi < mi)) {
+                mv = ov;
+                mi = oi;
               }
             }
-            if (trace && blockIdx.x == 0 && lane == 0 && j + 1 < NN_TRACE_LEN) g_nnls_trace(2)[j + 1] = gtimer_ns();
+            if (mi < 32 && mv < best_part) {
+              best_part = mv;
+              best_j = first + mi;
+            }
+            if (e < 32) {
+              if (e_bad) {
+                fail_at = first + e;
+              } else {
+                stop_at = first + e;
+              }
+              halt = true;
+            }
+            if (trace && blockIdx.x == 0 && valid && j + 1 < NN_TRACE_LEN) g_nnls_trace(2)[j + 1] = gtimer_ns();
           }
           if (lane == 0) {
             sh.best_j = best_j;
@@ -290,6 +316,7 @@ static __device__ void resolver_warp(SolverShared& sh, const double* pp, int ncw
         }
       }
     }
+    if (trace && lane == 0 && blockIdx.x < 512) g_nnls_trace(0)[1024 + blockIdx.x] = gtimer_ns();
     if (lane == 0) {
       sh.best_j = best_j;
       sh.stop_at = stop_at;

@@ -113,6 +113,7 @@ k_nnls_mma(const __grid_constant__ MmaArgs<T> A) {
   solver_shared_init(sh);
   __syncthreads();
   if (tracebuf != nullptr && blockIdx.x == 0 && tid == 0) tracebuf[NN_TRACE_LEN + 60 + 0] = gtimer_ns();
+  if (tracebuf != nullptr && tid == 0 && blockIdx.x < 512) tracebuf[blockIdx.x] = gtimer_ns();  // per-CTA start
   if (st->code != 0) return;
 
   // element e of this thread: solver row / CTA-local column
@@ -243,6 +244,63 @@ k_nnls_mma(const __grid_constant__ MmaArgs<T> A) {
   if (tracebuf != nullptr && blockIdx.x == 0 && tid == 0) tracebuf[NN_TRACE_LEN + 60 + 3] = gtimer_ns();
   const T rnegL = (T)(-1.0 / L);
   const T* __restrict__ W = A.W;
+
+  // the final iterate is the best one (the common case: the objective still
+  // falls at max_iter) when every warp's last iteration is the decided best
+  auto spec_hit = [&](int bj_) -> bool {
+    if (!fused || bj_ < 0 || sh.fail_at != -1) return false;
+    for (int w = 0; w < ncw; ++w)
+      if (sh.kdone[w] - 1 != bj_) return false;
+    return true;
+  };
+  // partials of the next product Pout = F Pt^T (factorize.py:110,113) over this
+  // CTA's columns for one candidate (0: the best iterate, staged in ftile; 1:
+  // the start point), by threads [0, nthr); sync() orders the smem staging
+  auto stage_pt = [&](int nthr) {
+    T* Ps = Bs + (size_t)r * cpb + (size_t)p * cpb;  // [nup][cpb]
+    for (int i = tid; i < (int)A.nup * ncols; i += nthr) {
+      const int b = i / ncols, jl = i % ncols;
+      Ps[(size_t)b * cpb + jl] = A.Pt[(int64_t)b * c + j0 + jl];
+    }
+  };
+  auto next_partials = [&](int cand, int nthr, auto&& sync) {
+    const int nup = (int)A.nup, no = p * nup;
+    T* Fs = Bs + (size_t)r * cpb;  // [p][cpb]
+    T* Ps = Fs + (size_t)p * cpb;  // [nup][cpb]
+    sync();
+    for (int i = tid; i < p * ncols; i += nthr) {
+      const int a2 = i / ncols, jl = i % ncols;
+      Fs[(size_t)a2 * cpb + jl] = cand == 0 ? ftile_all[(size_t)(jl / S::CB) * 2 * 32 * S::CB + a2 * S::CB + jl % S::CB]
+                                            : F0[(int64_t)a2 * c + j0 + jl];
+    }
+    sync();
+    // 2 x 2 output blocks per thread: four independent fp64 chains, each
+    // summed over the columns in order
+    const int nba = (p + 1) / 2, nbb = (nup + 1) / 2;
+    double* dst = A.npart + ((size_t)blockIdx.x * 2 + cand) * no;
+    for (int blk = tid; blk < nba * nbb; blk += nthr) {
+      const int a0 = 2 * (blk / nbb), b0 = 2 * (blk % nbb);
+      const int a1 = imin(a0 + 1, p - 1), b1 = imin(b0 + 1, nup - 1);
+      const T* f0 = Fs + (size_t)a0 * cpb;
+      const T* f1 = Fs + (size_t)a1 * cpb;
+      const T* q0 = Ps + (size_t)b0 * cpb;
+      const T* q1 = Ps + (size_t)b1 * cpb;
+      double c00 = 0.0, c01 = 0.0, c10 = 0.0, c11 = 0.0;
+      for (int jl = 0; jl < ncols; ++jl) {
+        const double x0 = (double)f0[jl], x1 = (double)f1[jl], y0 = (double)q0[jl], y1 = (double)q1[jl];
+        c00 = fma(x0, y0, c00);
+        c01 = fma(x0, y1, c01);
+        c10 = fma(x1, y0, c10);
+        c11 = fma(x1, y1, c11);
+      }
+      dst[a0 * nup + b0] = c00;
+      if (b0 + 1 < nup) dst[a0 * nup + b0 + 1] = c01;
+      if (a0 + 1 < p) {
+        dst[(a0 + 1) * nup + b0] = c10;
+        if (b0 + 1 < nup) dst[(a0 + 1) * nup + b0 + 1] = c11;
+      }
+    }
+  };
 
   if (!resolver) {
     auto wval = [&](int i, int l) -> T {
@@ -460,11 +518,13 @@ k_nnls_mma(const __grid_constant__ MmaArgs<T> A) {
       const int i = base - 1 + lane;
       return (i >= 0 && i < max_iter) ? wtab[i] : 0.0;
     };
+    if (tracebuf != nullptr && lane == 0 && wid == 0 && blockIdx.x < 512)
+      tracebuf[3 * NN_TRACE_LEN + blockIdx.x] = gtimer_ns();  // per-CTA loop start
     if (tracebuf != nullptr && lane == 0 && wid == 0 && blockIdx.x == 0) {
       tracebuf[NN_TRACE_LEN + 52] = clock64();
       tracebuf[NN_TRACE_LEN + 53] = gtimer_ns();
     }
-    double wwin = 0.0, wnext = wload(0);
+    T wwin = T(0), wnext = (T)wload(0);
     int k = 0;
     bool go = true;
     const bool has_cols = cblk < ncols;
@@ -473,13 +533,16 @@ k_nnls_mma(const __grid_constant__ MmaArgs<T> A) {
     // iterations run in pairs (A: even k, B: odd k); B posts the sums of the
     // previous B (k - 2, in ps) and of A (k - 1, in pa) while its MMAs run
     T pa0 = T(0), pa1 = T(0);
+    // momentum weights of the current pair (wA: k, wB: k + 1), fetched one
+    // pair ahead so the shuffles are off the iteration's critical path
+    T wA = T(0), wB = T(0);
     auto half = [&](T (&u1)[NE], T (&u2)[NE], T (&fo)[NE], bool b_half) {
-      const T w = __shfl_sync(0xffffffffu, wwin, k % NW_WIN);
-      extrapolate(u1, u2, w, fo);
+      extrapolate(u1, u2, b_half ? wB : wA, fo);
       T g[NE];
       grad(fo, g);
       if (b_half) {
-        if (!(dbg & 4)) post2(k - 2, ps0, ps1, k - 1, pa0, pa1);
+        // no branch around the butterfly: its shuffles schedule between the MMAs
+        post2(k - 2, ps0, ps1, k - 1, pa0, pa1);
         finish(fo, g, u2, ps0, ps1);
       } else {
         finish(fo, g, u2, pa0, pa1);
@@ -491,7 +554,11 @@ k_nnls_mma(const __grid_constant__ MmaArgs<T> A) {
       if (k % NW_WIN == 0) {
         const int w = k / NW_WIN;
         wwin = wnext;
-        wnext = wload(k + NW_WIN);
+        wnext = (T)wload(k + NW_WIN);
+        if (k == 0) {
+          wA = __shfl_sync(0xffffffffu, wwin, 0);
+          wB = __shfl_sync(0xffffffffu, wwin, 1);
+        }
         const bool tr = tracebuf != nullptr && lane == 0 && wid == 0 && blockIdx.x == 0 && w < 200;
         if (tr) tracebuf[NN_TRACE_LEN + 100 + 4 * w] = gtimer_ns();
         int ok = 1;
@@ -529,10 +596,16 @@ k_nnls_mma(const __grid_constant__ MmaArgs<T> A) {
         if (tr) tracebuf[NN_TRACE_LEN + 100 + 4 * w + 2] = gtimer_ns();
       }
       go = sh.halt == 0;  // one LDS per warp: every lane sees the same value
+      // the next pair's weights (k + 2 starts the next window when k % 32 == 30)
+      const T wsrc = (k + 2) % NW_WIN == 0 ? wnext : wwin;
+      const T wA_n = __shfl_sync(0xffffffffu, wsrc, (k + 2) % NW_WIN);
+      const T wB_n = __shfl_sync(0xffffffffu, wsrc, (k + 3) % NW_WIN);
       // k is even here (windows have even length): u_{k-1} in ua, F_{k-1} in fa;
       // the pair leaves the roles canonical again, so the loop has no moves
       half(ua, ub, fb, false);
       half(ub, ua, fa, true);
+      wA = wA_n;
+      wB = wB_n;
       if (k > 2 && (k - 2) % NW_WIN == 0) post_flag(k - 2);  // covers the last iteration of the previous window
       if (k == max_iter || !go) break;
     }
@@ -542,6 +615,7 @@ k_nnls_mma(const __grid_constant__ MmaArgs<T> A) {
       // (a snapshot is not needed: a best iterate in this window is F_k itself)
       if (k % NW_WIN == 0) {
         wwin = wnext;
+        wA = __shfl_sync(0xffffffffu, wwin, 0);
         if (lane == 0) {
           const int need = (k / NW_WIN - NW_FLIGHT) * NW_WIN - 1;
           while (!(dbg & 1) && sh.resolved < need && !sh.halt) __nanosleep(64);
@@ -560,6 +634,8 @@ k_nnls_mma(const __grid_constant__ MmaArgs<T> A) {
         fb[e] = t;
       }
     }
+    if (tracebuf != nullptr && lane == 0 && blockIdx.x < 512 && wid < 5)
+      tracebuf[3 * NN_TRACE_LEN + 512 * (1 + wid) + blockIdx.x] = gtimer_ns();  // per-CTA, per-warp loop end
     if (tracebuf != nullptr && lane == 0 && wid == 0 && blockIdx.x == 0) {
       tracebuf[NN_TRACE_LEN + 50] = clock64();
       tracebuf[NN_TRACE_LEN + 51] = gtimer_ns();
@@ -576,6 +652,80 @@ k_nnls_mma(const __grid_constant__ MmaArgs<T> A) {
     }
     if (lane == 0) sh.kdone[wid] = k;
     __syncwarp();
+    // explicit residuals of fa (the best candidate) and the start point
+    auto resid_pair = [&]() {
+      // explicit residuals 1/2||A F - B||^2 of best and start over this warp's
+      // columns (k_resid arithmetic: T products summed over rows in order,
+      // double squares); each lane owns one column and a stride of rows t
+      double acc[2] = {0.0, 0.0};
+      if (has_cols) {
+        T* ft = ftile_all + (size_t)wid * 2 * 32 * S::CB;  // [2][32][CB]
+        const int nloc = imin(S::CB, ncols - cblk);
+#pragma unroll
+        for (int e = 0; e < NE; ++e)
+          if (evalid(e)) {
+            const int o = erow(e) * S::CB + (ecol(e) - cblk);
+            ft[o] = fa[e];
+            ft[32 * S::CB + o] = F0[eoff(e)];
+          }
+        __syncwarp();
+        const int jl = lane % S::CB;
+        constexpr int TSTEP = 32 / S::CB;
+        if (jl < nloc) {
+          // operands from shared memory in a plain counted loop (rows a2 in
+          // ascending order, as k_resid): no per-row predicates or branches
+          const T* fb0 = ft + jl;
+          const T* fb1 = ft + 32 * S::CB + jl;
+          for (int t = lane / S::CB; t < r; t += TSTEP) {
+            T s0 = T(0), s1 = T(0);
+            const T* at = At_s + t;
+#pragma unroll 4
+            for (int a2 = 0; a2 < p; ++a2) {
+              const T w = at[a2 * r];
+              s0 = fma_acc(w, fb0[a2 * S::CB], s0);
+              s1 = fma_acc(w, fb1[a2 * S::CB], s1);
+            }
+            const T b = bval(t, cblk + jl);
+            const double d0 = (double)(s0 - b), d1 = (double)(s1 - b);
+            acc[0] += d0 * d0;
+            acc[1] += d1 * d1;
+          }
+        }
+        __syncwarp();
+      }
+      const double r0 = warp_sum(acc[0]), r1 = warp_sum(acc[1]);
+      if (tracebuf != nullptr && blockIdx.x == 0 && tid == 0) tracebuf[NN_TRACE_LEN + 60 + 7] = gtimer_ns();
+      if (lane == 0) {
+        s_red[wid][0] = r0;
+        s_red[wid][1] = r1;
+      }
+    };
+
+    // speculative tie-break work while the resolver decides (nnls.py:219-227):
+    // the output, residuals and next-product partials of the final iterate,
+    // and those of the start point, which are needed in any case
+    if (fused) {
+      if (has_cols) {
+#pragma unroll
+        for (int e = 0; e < NE; ++e)
+          if (evalid(e)) Fout[eoff(e)] = fa[e];
+      }
+      auto tr = [&](int i) {
+        if (tracebuf != nullptr && blockIdx.x == 0 && tid == 0) tracebuf[NN_TRACE_LEN + 90 + i] = gtimer_ns();
+      };
+      tr(0);
+      resid_pair();
+      tr(1);
+      if (A.Pt != nullptr) {
+        auto csync = [&]() { asm volatile("bar.sync 2, %0;" ::"r"(ncw * 32) : "memory"); };
+        stage_pt(ncw * 32);
+        tr(2);
+        next_partials(0, ncw * 32, csync);
+        tr(3);
+        next_partials(1, ncw * 32, csync);
+        tr(4);
+      }
+    }
 
     // -------------------------------------------------------------- output
     // (waits for the resolver's final decision through the block barrier below)
@@ -583,8 +733,13 @@ k_nnls_mma(const __grid_constant__ MmaArgs<T> A) {
   if (tracebuf != nullptr && blockIdx.x == 0 && tid == 0) tracebuf[NN_TRACE_LEN + 60 + 6] = gtimer_ns();
     const int bj = sh.best_j;
     const bool ok_best = bj >= 0 && sh.fail_at == -1;
+    if (tracebuf != nullptr && blockIdx.x < 512 && lane == 0 && wid < 5) {
+      tracebuf[512 * (3 + wid) + blockIdx.x] = gtimer_ns();  // per-warp time past the output barrier
+      tracebuf[2 * NN_TRACE_LEN + 512 * (1 + wid) + blockIdx.x] = (unsigned long long)(bj + 1);
+    }
     if (tracebuf != nullptr && blockIdx.x == 0 && tid == 0) tracebuf[NN_TRACE_LEN + 60 + 12] = gtimer_ns();
-    if (ok_best && has_cols) {
+    const bool spec_ok = spec_hit(bj);
+    if (ok_best && has_cols && !spec_ok) {
       const int kd = sh.kdone[wid];
       if (tracebuf != nullptr && blockIdx.x == 0 && tid == 0) tracebuf[NN_TRACE_LEN + 60 + 13] = gtimer_ns();
       if (bj == kd - 2) {
@@ -626,55 +781,7 @@ k_nnls_mma(const __grid_constant__ MmaArgs<T> A) {
       for (int e = 0; e < NE; ++e)
         if (evalid(e)) Fout[eoff(e)] = fa[e];
     }
-    if (fused && ok_best) {
-      // explicit residuals 1/2||A F - B||^2 of best and start over this warp's
-      // columns (k_resid arithmetic: T products summed over rows in order,
-      // double squares); each lane owns one column and a stride of rows t
-      double acc[2] = {0.0, 0.0};
-      if (has_cols) {
-        T* ft = ftile_all + (size_t)wid * 2 * 32 * S::CB;  // [2][32][CB]
-        const int nloc = imin(S::CB, ncols - cblk);
-#pragma unroll
-        for (int e = 0; e < NE; ++e)
-          if (evalid(e)) {
-            const int o = erow(e) * S::CB + (ecol(e) - cblk);
-            ft[o] = fa[e];
-            ft[32 * S::CB + o] = F0[eoff(e)];
-          }
-        __syncwarp();
-        const int jl = lane % S::CB;
-        constexpr int TSTEP = 32 / S::CB;
-        if (jl < nloc) {
-          T f0[8 * NT], f1[8 * NT];  // p <= 8 NT
-#pragma unroll
-          for (int a2 = 0; a2 < 8 * NT; ++a2) {
-            f0[a2] = a2 < p ? ft[a2 * S::CB + jl] : T(0);
-            f1[a2] = a2 < p ? ft[32 * S::CB + a2 * S::CB + jl] : T(0);
-          }
-          for (int t = lane / S::CB; t < r; t += TSTEP) {
-            T s0 = T(0), s1 = T(0);
-#pragma unroll
-            for (int a2 = 0; a2 < 8 * NT; ++a2)
-              if (a2 < p) {
-                const T w = At_s[a2 * r + t];
-                s0 = fma_acc(w, f0[a2], s0);
-                s1 = fma_acc(w, f1[a2], s1);
-              }
-            const T b = bval(t, cblk + jl);
-            const double d0 = (double)(s0 - b), d1 = (double)(s1 - b);
-            acc[0] += d0 * d0;
-            acc[1] += d1 * d1;
-          }
-        }
-        __syncwarp();
-      }
-      const double r0 = warp_sum(acc[0]), r1 = warp_sum(acc[1]);
-  if (tracebuf != nullptr && blockIdx.x == 0 && tid == 0) tracebuf[NN_TRACE_LEN + 60 + 7] = gtimer_ns();
-      if (lane == 0) {
-        s_red[wid][0] = r0;
-        s_red[wid][1] = r1;
-      }
-    }
+    if (fused && ok_best && !spec_ok) resid_pair();
   } else {
     if (!(dbg & 1)) resolver_warp(sh, pp, ncw, max_iter, A.grad_tol, L, A.recs, A.results, tracebuf);
     if (tracebuf != nullptr && blockIdx.x == 0 && lane == 0) tracebuf[NN_TRACE_LEN + 60 + 14] = gtimer_ns();
@@ -683,6 +790,7 @@ k_nnls_mma(const __grid_constant__ MmaArgs<T> A) {
   __syncthreads();
   const int bj = sh.best_j;
   const bool ok_best = bj >= 0 && sh.fail_at == -1;
+  if (tracebuf != nullptr && blockIdx.x < 512 && tid == 0) tracebuf[2 * NN_TRACE_LEN + 3072 + blockIdx.x] = (unsigned long long)(bj + 1);
   int start_wins = 0;
   if (tracebuf != nullptr && blockIdx.x == 0 && tid == 0) tracebuf[NN_TRACE_LEN + 60 + 8] = gtimer_ns();
   if (fused && sh.fail_at == -1) {
@@ -693,30 +801,10 @@ k_nnls_mma(const __grid_constant__ MmaArgs<T> A) {
     // same decision (fixed-order sums) and reduces the chosen candidate's slice
     const bool next = A.Pt != nullptr;
     const int nup = next ? (int)A.nup : 0, no = p * nup;
-    if (next) {
-      T* Fs = Bs + (size_t)r * cpb;  // [p][cpb]
-      T* Ps = Fs + (size_t)p * cpb;  // [nup][cpb]
-      for (int i = tid; i < nup * ncols; i += blockDim.x) {
-        const int b = i / ncols, jl = i % ncols;
-        Ps[(size_t)b * cpb + jl] = A.Pt[(int64_t)b * c + j0 + jl];
-      }
-      for (int cand = ok_best ? 0 : 1; cand < 2; ++cand) {  // 0: best, 1: start
-        __syncthreads();
-        for (int i = tid; i < p * ncols; i += blockDim.x) {
-          const int a2 = i / ncols, jl = i % ncols;
-          Fs[(size_t)a2 * cpb + jl] =
-              cand == 0 ? ftile_all[(size_t)(jl / S::CB) * 2 * 32 * S::CB + a2 * S::CB + jl % S::CB]
-                        : F0[(int64_t)a2 * c + j0 + jl];
-        }
-        __syncthreads();
-        for (int o = tid; o < no; o += blockDim.x) {
-          const int a2 = o / nup, b = o % nup;
-          double acc2 = 0.0;
-          for (int jl = 0; jl < ncols; ++jl)
-            acc2 = fma((double)Fs[(size_t)a2 * cpb + jl], (double)Ps[(size_t)b * cpb + jl], acc2);
-          A.npart[((size_t)blockIdx.x * 2 + cand) * no + o] = acc2;
-        }
-      }
+    if (next && ok_best && !spec_hit(bj)) {
+      // the speculation missed: the best iterate's partials (the start's are done)
+      auto bsync = [&]() { __syncthreads(); };
+      next_partials(0, (int)blockDim.x, bsync);
     }
     start_wins = 1;
     if (ok_best || next) {

@@ -40,3 +40,20 @@ for wdw in range(0, 16):
     sm = t[3, 3072 + wdw + 1]
     print("win %2d: start %.1f waited %.1f | published %.1f | summarized(j0) %.1f | resolved %.1f" %
           (wdw, us(a), (int(b2) - int(a)) / 1e3, us(pub) if pub else -1, us(sm) if sm else -1, us(res) if res else -1))
+G = 148
+def stats(name, v):
+    v = np.array([us(x) for x in v])
+    print("%-28s min %.1f  med %.1f  max %.1f  (argmax CTA %d)" % (name, v.min(), np.median(v), v.max(), int(v.argmax())))
+stats("CTA start", t[0, :G])
+stats("loop start (warp 0)", t[3, :G])
+for wd in range(5):
+    stats("loop end warp %d" % wd, t[3, 512 * (1 + wd): 512 * (1 + wd) + G])
+stats("last window published", t[0, 512:512 + G])
+stats("resolver exit", t[0, 1024:1024 + G])
+for wd in range(5):
+    stats("past output barrier warp %d" % wd, t[0, 512 * (3 + wd): 512 * (3 + wd) + G])
+fin = t[2, 3072:3072 + G].astype(np.int64) - 1
+for wd in range(5):
+    seen = t[2, 512 * (1 + wd): 512 * (1 + wd) + G].astype(np.int64) - 1
+    print("warp %d: best_j seen past the barrier != final in %d CTAs (final %s)" % (wd, int((seen != fin).sum()), np.unique(fin)))
+print("spec path (CTA 0 warp 0): start %.1f resid %.1f stage %.1f cand0 %.1f cand1 %.1f" % tuple(us(t[1, 90 + i]) for i in range(5)))
