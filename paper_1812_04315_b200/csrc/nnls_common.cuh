@@ -107,6 +107,7 @@ static NnlsPlan plan_nnls(int64_t p, int64_t c) {
 
 struct SolverShared {
   volatile int resolved, best_j, halt;
+  volatile int prep_done;  // fused: the resolver staged the start point's tie-break inputs
   volatile int posted[NW_MAXW];
   int kdone[NW_MAXW], bsw[NW_MAXW];  // per warp: iterations done, window held in the best slot
   int stop_at, fail_at;
@@ -123,6 +124,7 @@ __device__ __forceinline__ void solver_shared_init(SolverShared& sh) {
     sh.resolved = -2;
     sh.best_j = -1;
     sh.halt = 0;
+    sh.prep_done = 0;
     sh.stop_at = -1;
     sh.fail_at = -1;
     sh.best_part = 0.0;

@@ -138,6 +138,70 @@ k_nnls_mma(const __grid_constant__ MmaArgs<T> A) {
   // B(t, global column j) of the reference's V = A^T B (B may be a transposed view)
   // B(t, CTA-local column jl) of the reference's V = A^T B, staged in smem
   auto bval = [&](int t, int jl) -> T { return Bs[(size_t)t * cpb + jl]; };
+  // explicit residual 1/2||A F - B||^2 of one candidate (0: best, 1: start)
+  // over the 16 columns of compute warp w, staged in its ftile slot, into
+  // s_red[w][which] (k_resid arithmetic: T products summed over rows in
+  // order, double squares); each lane owns one column and a stride of rows t
+  auto resid_rows = [&](int w, int which) {
+    double acc = 0.0;
+    const int cb0 = S::CB * w;
+    if (cb0 < ncols) {
+      const T* ft = ftile_all + (size_t)w * 2 * 32 * S::CB + (size_t)which * 32 * S::CB;  // [32][CB]
+      const int nloc = imin(S::CB, ncols - cb0);
+      const int jl = lane % S::CB;
+      constexpr int TSTEP = 32 / S::CB;
+      if (jl < nloc) {
+        const T* fb = ft + jl;
+        for (int t = lane / S::CB; t < r; t += TSTEP) {
+          T s0 = T(0);
+          const T* at = At_s + t;
+#pragma unroll 4
+          for (int a2 = 0; a2 < p; ++a2) s0 = fma_acc(at[a2 * r], fb[a2 * S::CB], s0);
+          const double d0 = (double)(s0 - bval(t, cb0 + jl));
+          acc += d0 * d0;
+        }
+      }
+    }
+    acc = warp_sum(acc);
+    if (lane == 0) s_red[w][which] = acc;
+  };
+  // compute warps: a candidate held in registers (accumulator layout)
+  auto resid_one = [&](const T (&fv)[NE], int which) {
+    if (cblk < ncols) {
+      T* ft = ftile_all + (size_t)wid * 2 * 32 * S::CB + (size_t)which * 32 * S::CB;
+#pragma unroll
+      for (int e = 0; e < NE; ++e)
+        if (evalid(e)) ft[erow(e) * S::CB + (ecol(e) - cblk)] = fv[e];
+    }
+    __syncwarp();
+    resid_rows(wid, which);
+    __syncwarp();
+  };
+  // resolver warp: the start point of every compute warp's columns, from F0
+  auto resid_start_all = [&](int ncw_) {
+    for (int w = 0; w < ncw_; ++w) {
+      const int cb0 = S::CB * w;
+      if (cb0 >= ncols) {
+        if (lane == 0) s_red[w][1] = 0.0;
+        continue;
+      }
+      T* ft = ftile_all + (size_t)w * 2 * 32 * S::CB + 32 * S::CB;
+      for (int i = lane; i < p * S::CB; i += 32) {
+        const int a2 = i / S::CB, jl = i % S::CB;
+        ft[a2 * S::CB + jl] = cb0 + jl < ncols ? F0[(int64_t)a2 * c + j0 + cb0 + jl] : T(0);
+      }
+      __syncwarp();
+      resid_rows(w, 1);
+      __syncwarp();
+    }
+  };
+  auto stage_pt = [&](int i0, int nthr) {
+    T* Ps = Bs + (size_t)r * cpb + (size_t)p * cpb;  // [nup][cpb]
+    for (int i = i0; i < (int)A.nup * ncols; i += nthr) {
+      const int b = i / ncols, jl = i % ncols;
+      Ps[(size_t)b * cpb + jl] = A.Pt[(int64_t)b * c + j0 + jl];
+    }
+  };
 
   T nv[NE];  // -V in the accumulator layout (compute warps)
   if (fused) {
@@ -176,7 +240,9 @@ k_nnls_mma(const __grid_constant__ MmaArgs<T> A) {
       int draw = 1;
       double est = 0.0;
       bool conv_any = false;
+      int pits = 0;
       for (int it = 0; it < A.pmax; ++it) {
+        ++pits;
         double wi = 0.0;
         if (lane < k) {
 #pragma unroll
@@ -201,6 +267,7 @@ k_nnls_mma(const __grid_constant__ MmaArgs<T> A) {
         }
       }
       if (!conv_any) est = est * 1.01;
+      if (tracebuf != nullptr && blockIdx.x == 0 && lane == 0) tracebuf[NN_TRACE_LEN + 60 + 15] = (unsigned long long)pits;
       if (tracebuf != nullptr && blockIdx.x == 0 && lane == 0) tracebuf[NN_TRACE_LEN + 60 + 11] = gtimer_ns();
       if (lane == 0) {
         s_L = A.safety * est;
@@ -256,13 +323,6 @@ k_nnls_mma(const __grid_constant__ MmaArgs<T> A) {
   // partials of the next product Pout = F Pt^T (factorize.py:110,113) over this
   // CTA's columns for one candidate (0: the best iterate, staged in ftile; 1:
   // the start point), by threads [0, nthr); sync() orders the smem staging
-  auto stage_pt = [&](int nthr) {
-    T* Ps = Bs + (size_t)r * cpb + (size_t)p * cpb;  // [nup][cpb]
-    for (int i = tid; i < (int)A.nup * ncols; i += nthr) {
-      const int b = i / ncols, jl = i % ncols;
-      Ps[(size_t)b * cpb + jl] = A.Pt[(int64_t)b * c + j0 + jl];
-    }
-  };
   auto next_partials = [&](int cand, int nthr, auto&& sync) {
     const int nup = (int)A.nup, no = p * nup;
     T* Fs = Bs + (size_t)r * cpb;  // [p][cpb]
@@ -652,79 +712,30 @@ k_nnls_mma(const __grid_constant__ MmaArgs<T> A) {
     }
     if (lane == 0) sh.kdone[wid] = k;
     __syncwarp();
-    // explicit residuals of fa (the best candidate) and the start point
-    auto resid_pair = [&]() {
-      // explicit residuals 1/2||A F - B||^2 of best and start over this warp's
-      // columns (k_resid arithmetic: T products summed over rows in order,
-      // double squares); each lane owns one column and a stride of rows t
-      double acc[2] = {0.0, 0.0};
-      if (has_cols) {
-        T* ft = ftile_all + (size_t)wid * 2 * 32 * S::CB;  // [2][32][CB]
-        const int nloc = imin(S::CB, ncols - cblk);
-#pragma unroll
-        for (int e = 0; e < NE; ++e)
-          if (evalid(e)) {
-            const int o = erow(e) * S::CB + (ecol(e) - cblk);
-            ft[o] = fa[e];
-            ft[32 * S::CB + o] = F0[eoff(e)];
-          }
-        __syncwarp();
-        const int jl = lane % S::CB;
-        constexpr int TSTEP = 32 / S::CB;
-        if (jl < nloc) {
-          // operands from shared memory in a plain counted loop (rows a2 in
-          // ascending order, as k_resid): no per-row predicates or branches
-          const T* fb0 = ft + jl;
-          const T* fb1 = ft + 32 * S::CB + jl;
-          for (int t = lane / S::CB; t < r; t += TSTEP) {
-            T s0 = T(0), s1 = T(0);
-            const T* at = At_s + t;
-#pragma unroll 4
-            for (int a2 = 0; a2 < p; ++a2) {
-              const T w = at[a2 * r];
-              s0 = fma_acc(w, fb0[a2 * S::CB], s0);
-              s1 = fma_acc(w, fb1[a2 * S::CB], s1);
-            }
-            const T b = bval(t, cblk + jl);
-            const double d0 = (double)(s0 - b), d1 = (double)(s1 - b);
-            acc[0] += d0 * d0;
-            acc[1] += d1 * d1;
-          }
-        }
-        __syncwarp();
-      }
-      const double r0 = warp_sum(acc[0]), r1 = warp_sum(acc[1]);
-      if (tracebuf != nullptr && blockIdx.x == 0 && tid == 0) tracebuf[NN_TRACE_LEN + 60 + 7] = gtimer_ns();
-      if (lane == 0) {
-        s_red[wid][0] = r0;
-        s_red[wid][1] = r1;
-      }
-    };
-
     // speculative tie-break work while the resolver decides (nnls.py:219-227):
-    // the output, residuals and next-product partials of the final iterate,
-    // and those of the start point, which are needed in any case
+    // the output, residual and next-product partials of the final iterate
+    // (the start point's residual was formed in the prologue)
     if (fused) {
+      auto tr = [&](int i) {
+        if (tracebuf != nullptr && blockIdx.x == 0 && tid == 0) tracebuf[NN_TRACE_LEN + 90 + i] = gtimer_ns();
+      };
+      tr(0);
       if (has_cols) {
 #pragma unroll
         for (int e = 0; e < NE; ++e)
           if (evalid(e)) Fout[eoff(e)] = fa[e];
       }
-      auto tr = [&](int i) {
-        if (tracebuf != nullptr && blockIdx.x == 0 && tid == 0) tracebuf[NN_TRACE_LEN + 90 + i] = gtimer_ns();
-      };
-      tr(0);
-      resid_pair();
+      resid_one(fa, 0);
       tr(1);
+      if (lane == 0)
+        while (!sh.prep_done) __nanosleep(32);
+      __syncwarp();
+      __threadfence_block();
       if (A.Pt != nullptr) {
         auto csync = [&]() { asm volatile("bar.sync 2, %0;" ::"r"(ncw * 32) : "memory"); };
-        stage_pt(ncw * 32);
-        tr(2);
         next_partials(0, ncw * 32, csync);
-        tr(3);
-        next_partials(1, ncw * 32, csync);
-        tr(4);
       }
+      tr(2);
     }
 
     // -------------------------------------------------------------- output
@@ -781,8 +792,21 @@ k_nnls_mma(const __grid_constant__ MmaArgs<T> A) {
       for (int e = 0; e < NE; ++e)
         if (evalid(e)) Fout[eoff(e)] = fa[e];
     }
-    if (fused && ok_best && !spec_ok) resid_pair();
+    if (fused && ok_best && !spec_ok) resid_one(fa, 0);
   } else {
+    if (fused) {
+      // while the first windows run: the start point's tie-break residual and
+      // Pt staged for the next product (the compute warps wait for prep_done
+      // before their end-of-solve use)
+      resid_start_all(ncw);
+      if (A.Pt != nullptr) stage_pt(lane, 32);
+      __syncwarp();
+      if (lane == 0) {
+        __threadfence_block();
+        sh.prep_done = 1;
+      }
+      __syncwarp();
+    }
     if (!(dbg & 1)) resolver_warp(sh, pp, ncw, max_iter, A.grad_tol, L, A.recs, A.results, tracebuf);
     if (tracebuf != nullptr && blockIdx.x == 0 && lane == 0) tracebuf[NN_TRACE_LEN + 60 + 14] = gtimer_ns();
     asm volatile("bar.sync 1, %0;" ::"r"(blockDim.x) : "memory");
@@ -795,14 +819,15 @@ k_nnls_mma(const __grid_constant__ MmaArgs<T> A) {
   if (tracebuf != nullptr && blockIdx.x == 0 && tid == 0) tracebuf[NN_TRACE_LEN + 60 + 8] = gtimer_ns();
   if (fused && sh.fail_at == -1) {
     // tie-break (nnls.py:219-227) and the next product Pout = F_out Pt^T
-    // (factorize.py:110,113) behind ONE grid barrier: each CTA posts its
+    // (factorize.py:110,113) behind one grid barrier: each CTA posts its
     // residual partials of best and start and, for the next product, its
-    // partials for both candidates; after the barrier every CTA reaches the
-    // same decision (fixed-order sums) and reduces the chosen candidate's slice
+    // partials of the best iterate; after the barrier every CTA reaches the
+    // same decision (fixed-order sums) and reduces the chosen candidate's
+    // slice (a start-point win adds its partials and a second barrier)
     const bool next = A.Pt != nullptr;
     const int nup = next ? (int)A.nup : 0, no = p * nup;
     if (next && ok_best && !spec_hit(bj)) {
-      // the speculation missed: the best iterate's partials (the start's are done)
+      // the speculation missed: the best iterate's partials
       auto bsync = [&]() { __syncthreads(); };
       next_partials(0, (int)blockDim.x, bsync);
     }
@@ -850,6 +875,19 @@ k_nnls_mma(const __grid_constant__ MmaArgs<T> A) {
       }
       __syncthreads();
       start_wins = s_start_wins;
+    }
+    if (next && start_wins) {
+      // the start point won (rare; always without a best iterate): its
+      // partials of the next product, then a second grid barrier
+      auto bsync = [&]() { __syncthreads(); };
+      next_partials(1, (int)blockDim.x, bsync);
+      __syncthreads();
+      if (tid == 0) {
+        __threadfence();
+        atomicAdd(A.bar, 1u);
+        while (ld_acquire_u32(A.bar) < 2 * gridDim.x) __nanosleep(32);
+      }
+      __syncthreads();
     }
     if (start_wins && !resolver && cblk < ncols) {
 #pragma unroll

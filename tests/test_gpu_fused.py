@@ -123,3 +123,39 @@ def test_next_product(monkeypatch, unfused, dtype, tol, shape):
     _ops.solve(At, Bd, F0d, Fo2, trans_b=False, max_iter=60, grad_tol=1e-6, lipschitz_safety=1.0,
                status=_lib.new_status())
     assert torch.equal(Fo, Fo2)
+
+
+@pytest.mark.parametrize("case", ["start_wins", "early_stop", "full"])
+def test_next_product_decision_paths(case):
+    """The fused launch forms the next product from the final iterate before
+    the stopping decision is known; check the product against F_out when that
+    guess holds (full run), when the solve stops early (best != final
+    iterate) and when the start point wins (second grid barrier)."""
+    import torch
+    from paper_1812_04315_b200 import _lib, _ops
+    rng = np.random.default_rng({"start_wins": 1, "early_stop": 2, "full": 3}[case])
+    r, p, c, k = 30, 20, 5000, 30
+    A = rng.random((r, p))
+    if case == "start_wins":
+        F0 = rng.random((p, c))
+        B = A @ F0
+    else:
+        B = A @ rng.random((p, c)) + 0.05 * rng.standard_normal((r, c))
+        F0 = rng.random((p, c))
+    P = rng.standard_normal((k, c))
+    dev = lambda a: torch.as_tensor(np.ascontiguousarray(a), dtype=torch.float64, device="cuda")
+    At, Bd, F0d, Pd = dev(A.T), dev(B), dev(F0), dev(P)
+    Fo = torch.empty_like(F0d)
+    out = torch.empty((p, k), dtype=torch.float64, device="cuda")
+    st = _lib.new_status()
+    tol = {"start_wins": 1e-6, "early_stop": 1e-2, "full": 1e-12}[case]
+    _ops.solve(At, Bd, F0d, Fo, trans_b=False, max_iter=80, grad_tol=tol, lipschitz_safety=1.0, status=st,
+               next_bt=Pd, next_out=out)
+    rep = _lib.read_status(st)[0]
+    F = Fo.cpu().numpy()
+    if case == "start_wins":
+        assert np.abs(F - F0).max() <= 1e-12
+    if case == "early_stop":
+        assert int(rep["inner_iters"]) < 80
+    ref = F @ P.T
+    assert np.abs(out.cpu().numpy() - ref).max() <= 1e-12 * np.abs(ref).max()

@@ -22,7 +22,13 @@ N = 4 * 4096
 buf = (ctypes.c_ulonglong * N)()
 for rep in range(3):
     status.zero_()
-    _ops.solve(FR, XRt, Gt, Gout, trans_b=False, max_iter=w.inner, grad_tol=1e-4, lipschitz_safety=1.0, status=status)
+    if "next" in sys.argv:
+        GLt = torch.empty((w.p, w.nu), dtype=Xd.dtype, device="cuda")
+        _ops.solve(FR, XRt, Gt, Gout, trans_b=False, max_iter=w.inner, grad_tol=1e-4, lipschitz_safety=1.0,
+                   status=status, next_bt=L, next_out=GLt)
+    else:
+        _ops.solve(FR, XRt, Gt, Gout, trans_b=False, max_iter=w.inner, grad_tol=1e-4, lipschitz_safety=1.0,
+                   status=status)
     torch.cuda.synchronize()
 lib.nenmf_debug_nnls_trace(ctypes.addressof(buf), N)
 t = np.array(buf[:], dtype=np.int64).reshape(4, 4096)
@@ -56,4 +62,4 @@ fin = t[2, 3072:3072 + G].astype(np.int64) - 1
 for wd in range(5):
     seen = t[2, 512 * (1 + wd): 512 * (1 + wd) + G].astype(np.int64) - 1
     print("warp %d: best_j seen past the barrier != final in %d CTAs (final %s)" % (wd, int((seen != fin).sum()), np.unique(fin)))
-print("spec path (CTA 0 warp 0): start %.1f resid %.1f stage %.1f cand0 %.1f cand1 %.1f" % tuple(us(t[1, 90 + i]) for i in range(5)))
+print("spec path (CTA 0 warp 0): start %.1f resid %.1f partials %.1f" % tuple(us(t[1, 90 + i]) for i in range(3)))
