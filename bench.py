@@ -75,6 +75,12 @@ class ClockSampler:
             return
         self.thread = threading.Thread(target=self._read, daemon=True)
         self.thread.start()
+        # nvidia-smi needs a moment before its first line: wait for it so the
+        # periodic samples fall inside the timed region, then drop it
+        t0 = time.time()
+        while not self.rows and time.time() - t0 < 3.0 and self.proc.poll() is None:
+            time.sleep(0.01)
+        self.rows.clear()
 
     def _read(self):
         for line in self.proc.stdout:
@@ -92,6 +98,17 @@ class ClockSampler:
             self.proc.kill()
         if self.thread is not None:
             self.thread.join(timeout=2)
+        if not self.rows:
+            # a timed region shorter than the sampling period: one sample at its end
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=10)
+                for line in out.stdout.splitlines():
+                    parts = [p.strip() for p in line.split(",")]
+                    if len(parts) == 4:
+                        self.rows.append(parts)
+            except (OSError, subprocess.TimeoutExpired):
+                pass
         sm, mx, reasons = [], None, set()
         names = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
                  0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
