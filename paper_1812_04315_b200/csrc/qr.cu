@@ -356,7 +356,11 @@ inline void split_ctas(PanelSet& P) {
   for (int i = 0; i < P.npan; ++i) tot += P.rows[i];
   int c0 = 0;
   for (int i = 0; i < P.npan; ++i) {
-    const int64_t want = imax(1, imin(cdiv(P.rows[i], 256), (int64_t)sms * P.rows[i] / imax(tot, 1)));
+    static const int64_t min_rows = [] {
+      const char* e = getenv("NENMF_QR_ROWS");  // development knob (timing experiments)
+      return (int64_t)(e != nullptr ? atoi(e) : 256);
+    }();
+    const int64_t want = imax(1, imin(cdiv(P.rows[i], min_rows), (int64_t)sms * P.rows[i] / imax(tot, 1)));
     P.ncta[i] = (int)imax(1, want);
     P.cta0[i] = c0;
     c0 += P.ncta[i];
