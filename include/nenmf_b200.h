@@ -27,6 +27,7 @@
  *   nenmf_solve_nnls_prepared  nnls.py:119-227 with V = X F^T / X^T G from Xp
  *   nenmf_solve_nnls_next   nnls.py:119-227 + factorize.py:110,113 (the solve
  *                           also forms the next half-step operand)
+ *   nenmf_convert_f64       matrix.py:194-214 read_nmfb payload -> device dtype
  *
  * Conventions
  *  - All array pointers are DEVICE pointers, row-major, allocated by the
@@ -288,6 +289,13 @@ int nenmf_power_iteration(int dtype, const void* X, const void* Xp, int64_t n, i
 int nenmf_compress_prepared(int dtype, const void* X, const void* Xp, int64_t n, int64_t m,
                             int64_t ldx, const void* L, const void* Rt, int64_t nu,
                             void* XL, void* XRt, void* ws, size_t ws_bytes, void* stream);
+
+/* ---- NMFB payload conversion (matrix.py:180-214) -------------------------
+ * dst[i] = (dtype) src[i] for count float64 values already on the device (a
+ * chunk of an NMFB file's little-endian payload; src 16-byte aligned); sets
+ * *nonfinite (device int) to 1 if any value is NaN/Inf (read_nmfb's
+ * require_finite, matrix.py:39-42).  dtype NENMF_F64 copies. */
+int nenmf_convert_f64(int dtype, const double* src, int64_t count, void* dst, int* nonfinite, void* stream);
 
 /* ---- measurement hooks (not part of the reference interface) ------------
  * While enabled, every tensor-core X-pass kernel launch is bracketed by CUDA

@@ -10,14 +10,16 @@ the L-chain and the R-chain from one read of X; TSQR in shared memory).
 
 from __future__ import annotations
 
+import json
 import math
 from dataclasses import dataclass, field
+from pathlib import Path
 
 import numpy as np
 
 from . import _lib, _ops
 from .errors import DimensionError, ZeroMatrixError, raise_for_status
-from .matrix import DenseMatrix, as_matrix, check_seed
+from .matrix import DenseMatrix, as_matrix, check_seed, read_nmfb, write_nmfb
 
 GAUSSIAN = "gaussian"
 POWER_ITERATION = "power_iteration"
@@ -303,3 +305,21 @@ def compress_problem(X, sketch: SketchPair, *, dtype: str = "fp64") -> Compresse
     L, Rt = sketch_on_device(sketch, dtype)
     XL, XRt = compress_device(Xd, L, Rt)
     return CompressedProblem(X_L=_lib.to_host(XL), X_R=np.ascontiguousarray(_lib.to_host(XRt).T))
+
+
+def save_sketch(sketch: SketchPair, directory) -> None:
+    """L and R as NMFB matrices plus a JSON provenance header (compression.py:191-198)."""
+    directory = Path(directory)
+    directory.mkdir(parents=True, exist_ok=True)
+    write_nmfb(directory / "L.nmfb", sketch.L)
+    write_nmfb(directory / "R.nmfb", sketch.R)
+    meta = {"nu": sketch.nu, "scheme": sketch.scheme, "q": sketch.q, "seed": sketch.seed}
+    (directory / "sketch.json").write_text(json.dumps(meta, sort_keys=True, indent=2) + "\n")
+
+
+def load_sketch(directory) -> SketchPair:
+    """Inverse of :func:`save_sketch` (compression.py:201-210)."""
+    directory = Path(directory)
+    meta = json.loads((directory / "sketch.json").read_text())
+    return SketchPair(L=read_nmfb(directory / "L.nmfb"), R=read_nmfb(directory / "R.nmfb"), nu=int(meta["nu"]),
+                      scheme=str(meta["scheme"]), q=int(meta["q"]), seed=int(meta["seed"]))

@@ -8,12 +8,21 @@ through ``libnenmf_b200`` (no CPU fallback).
 
 from __future__ import annotations
 
+import struct
+from pathlib import Path
+
 import numpy as np
 
 from . import _lib, _ops
 from .errors import DimensionError, ZeroMatrixError
 
 DenseMatrix = np.ndarray
+
+# NMFB binary format (matrix.py:26-28): magic, u32 version, u64 rows, u64 cols,
+# then rows*cols little-endian float64, row-major
+NMFB_MAGIC = b"NMFB"
+NMFB_VERSION = 1
+_NMFB_HEADER = struct.Struct("<4sIQQ")
 
 
 def as_matrix(value, name: str = "matrix") -> DenseMatrix:
@@ -24,6 +33,12 @@ def as_matrix(value, name: str = "matrix") -> DenseMatrix:
     if M.ndim != 2:
         raise DimensionError(f"{name} must be 2-D, got shape {M.shape}")
     return M
+
+
+def require_finite(M: DenseMatrix, source: str) -> None:
+    """Reject NaN/Inf entries of matrices read from files (matrix.py:39-42)."""
+    if not np.isfinite(M).all():
+        raise ValueError(f"non-finite entries in matrix from {source}")
 
 
 def check_seed(seed: int) -> int:
@@ -94,3 +109,91 @@ def frobenius_norm(M, *, dtype: str = "fp64") -> float:
     out = _device_scalar()
     _ops.sumsq(Md, out)
     return float(np.sqrt(out[0].item()))
+
+
+# ------------------------------------------------------------------ NMFB IO
+def write_nmfb(path, M) -> None:
+    """Write ``M`` in the NMFB format (matrix.py:180-191)."""
+    M = as_matrix(M)
+    require_finite(M, f"write_nmfb({path})")
+    rows, cols = M.shape
+    header = _NMFB_HEADER.pack(NMFB_MAGIC, NMFB_VERSION, rows, cols)
+    Path(path).write_bytes(header + np.ascontiguousarray(M, dtype="<f8").tobytes())
+
+
+def _nmfb_header(path, size: int):
+    """Validated (rows, cols) of an NMFB file of ``size`` bytes (matrix.py:196-208)."""
+    with open(path, "rb") as fh:
+        head = fh.read(_NMFB_HEADER.size)
+    if len(head) < _NMFB_HEADER.size:
+        raise ValueError(f"{path}: truncated NMFB file ({size} bytes)")
+    magic, version, rows, cols = _NMFB_HEADER.unpack(head)
+    if magic != NMFB_MAGIC:
+        raise ValueError(f"{path}: bad magic {magic!r}, expected {NMFB_MAGIC!r}")
+    if version != NMFB_VERSION:
+        raise ValueError(f"{path}: unsupported NMFB version {version}")
+    if rows < 1 or cols < 1:
+        raise DimensionError(f"{path}: degenerate dimensions {rows}x{cols}")
+    expected = _NMFB_HEADER.size + 8 * rows * cols
+    if size != expected:
+        raise ValueError(f"{path}: expected {expected} bytes, found {size}")
+    return int(rows), int(cols)
+
+
+def read_nmfb(path) -> DenseMatrix:
+    """Read a matrix written by :func:`write_nmfb`; bit-exact (matrix.py:194-214)."""
+    size = Path(path).stat().st_size
+    rows, cols = _nmfb_header(path, size)
+    data = np.fromfile(path, dtype="<f8", offset=_NMFB_HEADER.size, count=rows * cols)
+    M = np.array(data, dtype=np.float64).reshape(rows, cols)
+    require_finite(M, str(path))
+    return M
+
+
+def read_nmfb_device(path, *, dtype: str = "fp32", row0: int = 0, rows: int | None = None,
+                     chunk_bytes: int = 64 << 20):
+    """Rows [row0, row0 + rows) of an NMFB file straight into a CUDA tensor of
+    ``dtype`` (feeding large X, e.g. one rank's row shard).
+
+    The payload is read in chunks into two pinned host buffers; while one
+    chunk is copied to the device and converted there (``nenmf_convert_f64``,
+    which also flags NaN/Inf as read_nmfb's require_finite does), the host
+    reads the next.  Header validation and errors follow read_nmfb."""
+    lib, torch = _lib.require_device()
+    size = Path(path).stat().st_size
+    n, m = _nmfb_header(path, size)
+    rows = n - row0 if rows is None else int(rows)
+    if row0 < 0 or rows < 1 or row0 + rows > n:
+        raise DimensionError(f"{path}: rows [{row0}, {row0 + rows}) outside the file's {n} rows")
+    out = torch.empty((rows, m), dtype=_lib.torch_dtype(dtype), device="cuda")
+    total = rows * m
+    per = max(2, (int(chunk_bytes) // 8) & ~1)  # even: the device loads pairs
+    per = min(per, total + (total & 1))
+    stream = torch.cuda.current_stream()
+    host = [torch.empty(per, dtype=torch.float64).pin_memory() for _ in range(2)]
+    dev = [torch.empty(per, dtype=torch.float64, device="cuda") for _ in range(2)]
+    done = [torch.cuda.Event(), torch.cuda.Event()]
+    flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+    code = _lib.code_of(dtype)
+    flat = out.view(-1)
+    with open(path, "rb") as fh:
+        fh.seek(_NMFB_HEADER.size + 8 * row0 * m)
+        off, i = 0, 0
+        while off < total:
+            cnt = min(per, total - off)
+            b = i & 1
+            done[b].synchronize()  # the pinned buffer's previous copy has left
+            hv = host[b].numpy()
+            got = fh.readinto(memoryview(hv[:cnt]).cast("B"))
+            if got != 8 * cnt:
+                raise ValueError(f"{path}: truncated NMFB file")
+            dev[b][:cnt].copy_(host[b][:cnt], non_blocking=True)
+            rc = lib.nenmf_convert_f64(code, dev[b].data_ptr(), cnt, flat[off:].data_ptr(), flag.data_ptr(),
+                                       stream.cuda_stream)
+            _lib.check(rc, "read_nmfb_device")
+            done[b].record(stream)
+            off += cnt
+            i += 1
+    if int(flag.item()) != 0:
+        raise ValueError(f"non-finite entries in matrix from {path}")
+    return out

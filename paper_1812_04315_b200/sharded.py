@@ -45,6 +45,18 @@ def row_block(n: int, world: int, rank: int) -> tuple[int, int]:
     return r0, r1 - r0
 
 
+def load_row_shard(path, world: int, rank: int, *, dtype: str = "fp32"):
+    """This rank's row block of an NMFB file as a CUDA tensor, streamed from
+    disk through pinned chunks; returns (X_local, n, row0)."""
+    from pathlib import Path
+
+    from .matrix import _nmfb_header, read_nmfb_device
+
+    n, _ = _nmfb_header(path, Path(path).stat().st_size)
+    row0, rows = row_block(n, world, rank)
+    return read_nmfb_device(path, dtype=dtype, row0=row0, rows=rows), n, row0
+
+
 class Comm:
     """The collectives of the sharded path over a torch.distributed group."""
 
