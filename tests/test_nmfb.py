@@ -122,3 +122,17 @@ def test_same_bytes_as_reference_writer(tmp_path):
     assert a.read_bytes() == b.read_bytes()
     assert ref.read_nmfb(a).tobytes() == M.tobytes()
 
+
+
+def test_trace_csv_round_trip_and_header(tmp_path):
+    """tracing.py:85-119: 17 significant digits round-trip every double."""
+    recs = [nm.TraceRecord(outer_iter=i, solver_elapsed_s=0.1 * i + 1e-17, wall_elapsed_s=np.pi * i,
+                           rre=1.0 / (i + 3), objective=2.0 ** -40 * i) for i in range(5)]
+    path = tmp_path / "t.csv"
+    nm.write_trace_csv(recs, path)
+    assert nm.read_trace_csv(path) == recs
+    assert path.read_text().splitlines()[0] == ",".join(nm.TRACE_CSV_HEADER)
+    bad = tmp_path / "bad.csv"
+    bad.write_text("a,b,c\n1,2,3\n")
+    with pytest.raises(ValueError, match="header"):
+        nm.read_trace_csv(bad)
