@@ -20,7 +20,8 @@ from pathlib import Path
 REPO = Path(__file__).resolve().parents[1]
 REF = Path("/root/reference/pkg")
 DST = REPO / "baseline" / "_ref" / "suite"
-TESTS = ["test_nnls.py", "test_compression.py", "test_factorize.py", "test_matrix.py", "test_tracing.py"]
+TESTS = ["test_nnls.py", "test_compression.py", "test_factorize.py", "test_matrix.py", "test_tracing.py",
+         "test_synthetic.py", "test_cli.py", "test_acceptance.py"]
 HOT = ["errors", "matrix", "nnls", "compression", "factorize", "tracing"]
 # names a reference module exposes that live elsewhere in this package
 EXTRA = {
@@ -50,16 +51,23 @@ def main():
     (comp / "__init__.py").write_text(
         "# composite: hot path from paper_1812_04315_b200, the rest from the reference copy;\n"
         "# the reference copy raises this package's exception classes\n"
+        "import importlib\n"
         "import sys\n"
-        "import paper_1812_04315_b200.errors as _errors\n"
-        "sys.modules['nenmf_ref.errors'] = _errors\n"
-        "from paper_1812_04315_b200 import *  # noqa: F401,F403\n")
+        "# the reference copy's hot-path submodules ARE this package's: its CLI and\n"
+        "# generator then run on the GPU path (its host matrix helpers stay)\n"
+        "for _m in ('errors', 'nnls', 'compression', 'factorize', 'tracing'):\n"
+        "    sys.modules['nenmf_ref.' + _m] = importlib.import_module('paper_1812_04315_b200.' + _m)\n"
+        "from paper_1812_04315_b200 import *  # noqa: F401,F403\n"
+        "from nenmf_ref.matrix import orthonormal_basis, read_csv_matrix, write_csv_matrix  # noqa: F401\n"
+        "from nenmf_ref.synthetic import ProblemInstance, generate_problem, load_instance, save_instance  # noqa\n")
     for m in HOT:
         (comp / f"{m}.py").write_text(f"from paper_1812_04315_b200.{m} import *  # noqa: F401,F403\n"
                                       + EXTRA.get(m, ""))
     (comp / "synthetic.py").write_text("from nenmf_ref.synthetic import *  # noqa: F401,F403\n"
                                        "from nenmf_ref.synthetic import generate_problem, load_instance, "
                                        "save_instance, ProblemInstance\n")
+    (comp / "cli.py").write_text("from nenmf_ref.cli import *  # noqa: F401,F403\n"
+                                 "from nenmf_ref.cli import derive_seed, main  # noqa: F401\n")
     (DST / "conftest.py").write_text(
         "# evidence that the suite ran through this package's CUDA library\n"
         "def pytest_sessionfinish(session, exitstatus):\n"
