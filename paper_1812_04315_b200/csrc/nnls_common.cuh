@@ -395,9 +395,11 @@ struct StreamArgs {
   WinRec* recs;
   WinRec* results;
   nenmf_device_status* st;
+  int resident;     // 1: u_k and V of the CTA's columns stay in shared memory (set by the launcher)
 };
 
-int launch_nnls_stream(const StreamArgs& a, int grid, cudaStream_t s);
+// 1 when the launch keeps its state in shared memory (the CTA's columns fit)
+int launch_nnls_stream(StreamArgs& a, int grid, cudaStream_t s);
 
 template <typename T>
 int nnls_mma_max_cols(int p);  // columns one CTA of the tensor-core solver can hold

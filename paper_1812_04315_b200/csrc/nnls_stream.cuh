@@ -16,26 +16,37 @@
 
 namespace nenmf {
 
-// 4 compute warps + the resolver; each compute warp streams its tiles through
-// a shared-memory ring (stage: u_{k-1}, u_{k-2}, V tiles of 8 NT x 16);
+// 8 (NT <= 3) or 4 compute warps + the resolver.  When the CTA's columns fit
+// (BASELINE cfg5) u_{k-1}, u_{k-2} and V stay in shared memory for the whole
+// solve; otherwise each compute warp streams its tiles from HBM through a
+// shared-memory ring (stage: u_{k-1}, u_{k-2}, V tiles of 8 NT x 16);
 // NT <= 4 (p <= 32): 3 stages, W^T fragments in registers; NT 5..8
 // (p <= 64, BASELINE cfg3's p = 50): 2 stages, W^T fragments in shared memory.
-template <int NT>
-__host__ __device__ constexpr int stream_threads() {
-  return 5 * 32;
-}
-constexpr int SS_ROW = 20, SS_PPW = 8;  // ring row stride (floats); pp ring stride (warps)
+constexpr int SS_ROW = 20;  // ring / resident tile row stride (floats): conflict-free accumulator reads
 template <int NT>
 struct SS {
   static constexpr bool WSM = NT > 4;
+  // compute warps: 8 (two per SMSP, interleaving their per-tile latency
+  // chains) while the rings fit, 4 otherwise; the sum ring has one row per warp
+  static constexpr int NCW = NT <= 3 ? 8 : 4;
+  static constexpr int PPW = NCW;
   static constexpr int STAGES = WSM ? 2 : 3;
   static constexpr int ARR_F = 8 * NT * SS_ROW;
   static constexpr int STAGE_F = 3 * ARR_F;
-  static constexpr size_t smem() {
-    return (size_t)NW_PPD * SS_PPW * 3 * sizeof(double) + (size_t)4 * STAGES * STAGE_F * sizeof(float) +
+  // dynamic shared memory: sum ring, then the per-warp cp.async rings or (resident)
+  // [ntiles][3][ARR_F] tiles of U slot 0, U slot 1, V; then the W^T fragments (WSM)
+  __host__ __device__ static constexpr size_t state_bytes(bool resident, int ntiles) {
+    return resident ? (size_t)ntiles * STAGE_F * sizeof(float) : (size_t)NCW * STAGES * STAGE_F * sizeof(float);
+  }
+  __host__ __device__ static constexpr size_t smem(bool resident = false, int ntiles = 0) {
+    return (size_t)NW_PPD * PPW * 3 * sizeof(double) + state_bytes(resident, ntiles) +
            (WSM ? (size_t)NT * NT * 32 * 16 : 0);
   }
 };
+template <int NT>
+__host__ __device__ constexpr int stream_threads() {
+  return (SS<NT>::NCW + 1) * 32;
+}
 
 template <int NT>
 __global__ void __launch_bounds__(stream_threads<NT>(), 1) k_nnls_stream(const __grid_constant__ StreamArgs A) {
@@ -67,8 +78,10 @@ __global__ void __launch_bounds__(stream_threads<NT>(), 1) k_nnls_stream(const _
     constexpr bool WSM = SS<NT>::WSM;
     constexpr int NTR = WSM ? 1 : NT;  // register array extent
     uint32_t bhi[NTR][NTR][2], bco[NTR][NTR][2];
-    uint4* wf = reinterpret_cast<uint4*>(reinterpret_cast<float*>(smem_d + (size_t)NW_PPD * SS_PPW * 3) +
-                                         (size_t)4 * SS<NT>::STAGES * SS<NT>::STAGE_F);  // [NT][NT][32]
+    const bool resident = A.resident != 0;
+    const int ntiles_cta = (int)((A.cpb + CB - 1) / CB);
+    uint4* wf = reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(smem_d + (size_t)NW_PPD * SS<NT>::PPW * 3) +
+                                         SS<NT>::state_bytes(resident, ntiles_cta));  // [NT][NT][32]
 #pragma unroll
     for (int kt = 0; kt < NT; ++kt)
 #pragma unroll
@@ -149,7 +162,7 @@ __global__ void __launch_bounds__(stream_threads<NT>(), 1) k_nnls_stream(const _
         s1 += __shfl_xor_sync(0xffffffffu, s1, o);
       }
       if (lane == 0) {
-        double* q = pp + ((size_t)((j + NW_PPD) % NW_PPD) * SS_PPW + wid) * 3;
+        double* q = pp + ((size_t)((j + NW_PPD) % NW_PPD) * SS<NT>::PPW + wid) * 3;
         q[0] = s0;
         q[1] = s1;
         q[2] = 0.0;
@@ -180,7 +193,7 @@ __global__ void __launch_bounds__(stream_threads<NT>(), 1) k_nnls_stream(const _
     // the accumulator-layout reads are bank-conflict free), two tiles ahead
     // of the one being computed.
     constexpr int SS_STAGES = SS<NT>::STAGES, SS_ARR_F = SS<NT>::ARR_F, SS_STAGE_F = SS<NT>::STAGE_F;
-    float* ring = reinterpret_cast<float*>(smem_d + (size_t)NW_PPD * SS_PPW * 3) +
+    float* ring = reinterpret_cast<float*>(smem_d + (size_t)NW_PPD * SS<NT>::PPW * 3) +
                   (size_t)wid * SS_STAGES * SS_STAGE_F;
     const bool vec = (c & 3) == 0;  // 16-byte rows: cp.async; otherwise plain loads
     auto issue = [&](int tile, int k, int stg) {
@@ -212,16 +225,19 @@ __global__ void __launch_bounds__(stream_threads<NT>(), 1) k_nnls_stream(const _
       }
       asm volatile("cp.async.commit_group;" ::: "memory");
     };
-    auto tcompute = [&](int tile, int k, float w, bool snap, int slot, bool save, const float* st, float& s0,
-                        float& s1) {
+    // su1 / su2 / sv: this tile's u_{k-1}, u_{k-2} and V in shared memory (a
+    // ring stage, or the resident copy); su_out: where u_k goes in shared
+    // memory (resident), else u_k is written to U in HBM
+    auto tcompute = [&](int tile, int k, float w, bool snap, int slot, bool save, const float* su1,
+                        const float* su2, const float* sv, float* su_out, float& s0, float& s1) {
       const int64_t cb = j0 + (int64_t)tile * CB;
       float u1[NE], u2[NE], nv[NE], fe[NE], g[NE];
 #pragma unroll
       for (int e = 0; e < NE; ++e) {
         const int sidx = erow(e) * SS_ROW + ecol(e);
-        u1[e] = st[sidx];
-        u2[e] = k <= 0 ? u1[e] : st[SS_ARR_F + sidx];
-        nv[e] = -st[2 * SS_ARR_F + sidx];
+        u1[e] = su1[sidx];
+        u2[e] = k <= 0 ? u1[e] : su2[sidx];
+        nv[e] = -sv[sidx];
       }
       if (k >= 0) {
         if (snap) {
@@ -251,16 +267,32 @@ __global__ void __launch_bounds__(stream_threads<NT>(), 1) k_nnls_stream(const _
       for (int e = 0; e < NE; ++e) {
         const bool ok = eok(cb, e);
         const float u = fmaf(g[e], rnegL, fe[e]);
-        if (ok) Uo[eoff(cb, e)] = u;
+        if (su_out != nullptr) {
+          su_out[erow(e) * SS_ROW + ecol(e)] = ok ? u : 0.f;
+        } else if (ok) {
+          Uo[eoff(cb, e)] = u;
+        }
         const float pgv = ok ? (fe[e] > 0.f ? g[e] : min0_nan(g[e])) : 0.f;
         s0 = fmaf(pgv, pgv, s0);
         s1 = ok ? fmaf(fe[e], g[e] + nv[e], s1) : s1;
       }
     };
     // all of this warp's tiles for iteration k through the ring
+    float* res = reinterpret_cast<float*>(smem_d + (size_t)NW_PPD * SS<NT>::PPW * 3);  // resident tiles
     auto sweep = [&](int k, float w, bool snap, int slot, bool save, float& s0, float& s1) {
-      __syncwarp();  // this warp's u stores of iteration k - 1 are visible to its cp.async reads
+      __syncwarp();  // this warp's u stores of iteration k - 1 are visible to its reads
       const int nmine = wid < ntiles ? (ntiles - 1 - wid) / ncw + 1 : 0;
+      if (resident) {
+        // every element is read and rewritten by the same lane: no hazards
+        for (int i = 0; i < nmine; ++i) {
+          const int t = wid + i * ncw;
+          float* base = res + (size_t)t * SS_STAGE_F;
+          const int s1i = k < 0 ? 0 : ((k + 1) & 1), s2i = k & 1, so = k < 0 ? 1 : (k & 1);
+          tcompute(t, k, w, snap, slot, save, base + s1i * SS_ARR_F, base + s2i * SS_ARR_F, base + 2 * SS_ARR_F,
+                   base + so * SS_ARR_F, s0, s1);
+        }
+        return;
+      }
       for (int i = 0; i < SS_STAGES - 1; ++i) {
         if (i < nmine) issue(wid + i * ncw, k, i);
         else asm volatile("cp.async.commit_group;" ::: "memory");
@@ -268,13 +300,30 @@ __global__ void __launch_bounds__(stream_threads<NT>(), 1) k_nnls_stream(const _
       for (int i = 0; i < nmine; ++i) {
         asm volatile("cp.async.wait_group %0;" ::"n"(SS_STAGES - 2) : "memory");
         __syncwarp();
-        tcompute(wid + i * ncw, k, w, snap, slot, save, ring + (i % SS_STAGES) * SS_STAGE_F, s0, s1);
+        const float* st = ring + (i % SS_STAGES) * SS_STAGE_F;
+        tcompute(wid + i * ncw, k, w, snap, slot, save, st, st + SS_ARR_F, st + 2 * SS_ARR_F, nullptr, s0, s1);
         __syncwarp();  // the stage is refilled below
         if (i + SS_STAGES - 1 < nmine) issue(wid + (i + SS_STAGES - 1) * ncw, k, (i + SS_STAGES - 1) % SS_STAGES);
         else asm volatile("cp.async.commit_group;" ::: "memory");
       }
       asm volatile("cp.async.wait_group 0;" ::: "memory");
     };
+    if (resident) {
+      // this warp's tiles of F0 (-> U slot 0, the start point's input) and V,
+      // zero-padded past the problem, once
+      for (int t = wid; t < ntiles; t += ncw) {
+        const int64_t cb = j0 + (int64_t)t * CB;
+        float* base = res + (size_t)t * SS_STAGE_F;
+        for (int q = lane; q < 8 * NT * CB; q += 32) {
+          const int r = q / CB, cc = q % CB;
+          const bool ok = r < p && cb + cc < jend;
+          const int64_t o = (int64_t)r * c + cb + cc;
+          base[r * SS_ROW + cc] = ok ? A.F0[o] : 0.f;
+          base[2 * SS_ARR_F + r * SS_ROW + cc] = ok ? V[o] : 0.f;
+        }
+      }
+      __syncwarp();
+    }
     // start point (nnls.py:163-178)
     {
       float s0 = 0.f, s1 = 0.f;
@@ -359,7 +408,7 @@ __global__ void __launch_bounds__(stream_threads<NT>(), 1) k_nnls_stream(const _
       }
     }
   } else {
-    resolver_warp(sh, pp, ncw, max_iter, A.grad_tol, L, A.recs, A.results, nullptr, SS_PPW);
+    resolver_warp(sh, pp, ncw, max_iter, A.grad_tol, L, A.recs, A.results, nullptr, SS<NT>::PPW);
     asm volatile("bar.sync 1, %0;" ::"r"(blockDim.x) : "memory");
   }
   __syncthreads();
@@ -375,15 +424,21 @@ __global__ void __launch_bounds__(stream_threads<NT>(), 1) k_nnls_stream(const _
 }
 
 // grid: one CTA per SM (cooperative); returns NENMF_ERR_UNSUPPORTED outside FP32, p <= 32
-int launch_nnls_stream(const StreamArgs& a, int grid, cudaStream_t s) {
+int launch_nnls_stream(StreamArgs& a, int grid, cudaStream_t s) {
   const int nt = (a.p + 7) / 8;
+  const int ntiles = (int)((a.cpb + 15) / 16);
+  // the CTA's state stays on chip when its tiles fit (cfg5: 43 tiles of 16 x 16)
+  constexpr size_t kSmemCap = 227 * 1024 - 2048;  // leave room for the static shared memory
   void* args[] = {(void*)&a};
   switch (nt) {
 #define NENMF_STREAM_CASE(N)                                                                               \
   case N: {                                                                                                \
-    NENMF_CUDA_TRY(set_smem(k_nnls_stream<N>, SS<N>::smem()));                                             \
+    const char* env = getenv("NENMF_STREAM_RING");  /* development knob: force the HBM ring */             \
+    a.resident = (env == nullptr && SS<N>::smem(true, ntiles) <= kSmemCap) ? 1 : 0;                       \
+    const size_t sm = SS<N>::smem(a.resident != 0, ntiles);                                               \
+    NENMF_CUDA_TRY(set_smem(k_nnls_stream<N>, sm));                                                        \
     NENMF_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k_nnls_stream<N>, dim3(grid),                  \
-                                               dim3(stream_threads<N>()), args, SS<N>::smem(), s));        \
+                                               dim3(stream_threads<N>()), args, sm, s));                   \
     break;                                                                                                 \
   }
     NENMF_STREAM_CASE(1)

@@ -198,3 +198,22 @@ def test_streamed_solver_many_columns(monkeypatch, p, c, max_iter):
     assert rep_s[0].inner_iters == rep_simt[0].inner_iters
     assert np.linalg.norm(Fs - Fr) <= 1e-3 * np.linalg.norm(Fr)
     assert np.linalg.norm(Fs - Fsimt) <= 1e-3 * np.linalg.norm(Fsimt)
+
+
+@pytest.mark.parametrize("p,c,max_iter", [(16, 30000, 80), (20, 20000, 64), (30, 17000, 45), (50, 3000, 40)])
+def test_streamed_resident_matches_ring(monkeypatch, p, c, max_iter):
+    """The streamed solver keeps a CTA's state in shared memory when its
+    columns fit (BASELINE cfg5) and streams it through the cp.async ring from
+    HBM otherwise: same arithmetic, bit-identical results."""
+    rng = np.random.default_rng(p * 7 + c)
+    r = max(30, p + 10)
+    A = rng.random((r, p))
+    B = A @ rng.random((p, c)) + 0.05 * rng.standard_normal((r, c))
+    F0 = rng.random((p, c))
+    cfg = nm.InnerSolverConfig(max_iter=max_iter, grad_tol=1e-9)
+    rep_a, rep_b = [], []
+    Fa = nm.solve_nnls(A, B, F0, cfg, dtype="fp32", report=rep_a)
+    monkeypatch.setenv("NENMF_STREAM_RING", "1")
+    Fb = nm.solve_nnls(A, B, F0, cfg, dtype="fp32", report=rep_b)
+    assert rep_a[0].inner_iters == rep_b[0].inner_iters
+    assert np.array_equal(Fa, Fb)
