@@ -272,9 +272,11 @@ __global__ void __launch_bounds__(stream_threads<NT>(), 1) k_nnls_stream(const _
         } else if (ok) {
           Uo[eoff(cb, e)] = u;
         }
-        const float pgv = ok ? (fe[e] > 0.f ? g[e] : min0_nan(g[e])) : 0.f;
+        // padded elements are exact zeros (zero-filled loads, zero W rows / V
+        // entries): they add nothing to the sums
+        const float pgv = fe[e] > 0.f ? g[e] : min0_nan(g[e]);
         s0 = fmaf(pgv, pgv, s0);
-        s1 = ok ? fmaf(fe[e], g[e] + nv[e], s1) : s1;
+        s1 = fmaf(fe[e], g[e] + nv[e], s1);
       }
     };
     // all of this warp's tiles for iteration k through the ring
@@ -283,13 +285,53 @@ __global__ void __launch_bounds__(stream_threads<NT>(), 1) k_nnls_stream(const _
       __syncwarp();  // this warp's u stores of iteration k - 1 are visible to its reads
       const int nmine = wid < ntiles ? (ntiles - 1 - wid) / ncw + 1 : 0;
       if (resident) {
-        // every element is read and rewritten by the same lane: no hazards
+        // every element is read and rewritten by the same lane: no hazards.
+        // Padding (rows >= p, columns past the block) holds exact zeros that
+        // stay zero (W's padded rows and V's padded entries are zero), so the
+        // sums and stores need no validity tests: same values as the ring path
+        const int s1i = k < 0 ? 0 : ((k + 1) & 1), s2i = k & 1, so = k < 0 ? 1 : (k & 1);
         for (int i = 0; i < nmine; ++i) {
           const int t = wid + i * ncw;
-          float* base = res + (size_t)t * SS_STAGE_F;
-          const int s1i = k < 0 ? 0 : ((k + 1) & 1), s2i = k & 1, so = k < 0 ? 1 : (k & 1);
-          tcompute(t, k, w, snap, slot, save, base + s1i * SS_ARR_F, base + s2i * SS_ARR_F, base + 2 * SS_ARR_F,
-                   base + so * SS_ARR_F, s0, s1);
+          const int ob = t * SS_STAGE_F;
+          float u1[NE], u2[NE], nv[NE], fe[NE], g[NE];
+#pragma unroll
+          for (int e = 0; e < NE; ++e) {
+            const int sidx = ob + erow(e) * SS_ROW + ecol(e);
+            u1[e] = res[sidx + s1i * SS_ARR_F];
+            u2[e] = k <= 0 ? u1[e] : res[sidx + s2i * SS_ARR_F];
+            nv[e] = -res[sidx + 2 * SS_ARR_F];
+          }
+          if (k >= 0) {
+            if (snap) {
+              const int64_t cb = j0 + (int64_t)t * CB;
+              float* sp = A.snaps + (int64_t)(slot * 2) * pc;
+              float* bp = A.snaps + (int64_t)(NW_SNAP * 2) * pc;
+#pragma unroll
+              for (int e = 0; e < NE; ++e)
+                if (eok(cb, e)) {
+                  const int64_t o = eoff(cb, e);
+                  if (save) {
+                    bp[o] = sp[o];
+                    bp[pc + o] = sp[pc + o];
+                  }
+                  sp[o] = u1[e];
+                  sp[pc + o] = u2[e];
+                }
+            }
+#pragma unroll
+            for (int e = 0; e < NE; ++e) fe[e] = relu_nan_fast(fmaf(u1[e] - u2[e], w, u1[e]));
+          } else {
+#pragma unroll
+            for (int e = 0; e < NE; ++e) fe[e] = u1[e];  // F0
+          }
+          grad(fe, nv, g);
+#pragma unroll
+          for (int e = 0; e < NE; ++e) {
+            res[ob + erow(e) * SS_ROW + ecol(e) + so * SS_ARR_F] = fmaf(g[e], rnegL, fe[e]);
+            const float pgv = fe[e] > 0.f ? g[e] : min0_nan(g[e]);
+            s0 = fmaf(pgv, pgv, s0);
+            s1 = fmaf(fe[e], g[e] + nv[e], s1);
+          }
         }
         return;
       }
