@@ -18,5 +18,5 @@ done
 ncu --set full --clock-control none --import-source on -k regex:k_nnls_stream -c 1 \
     -o gpurun_out/prof/full_k_nnls_stream python tools/probe_cfg4_solve.py 40 > gpurun_out/prof/ncu_full_k_nnls_stream.log 2>&1
 { python tools/probe_cfg.py 3 2; python tools/probe_cfg.py 4 2; python tools/probe_vanilla.py fp32 10;
-  python tools/probe_vanilla.py fp32 10 tv; python tools/probe_solve.py | head -1; } > gpurun_out/prof/probes.txt 2>&1
+  python tools/probe_vanilla.py fp32 10 tv; python tools/probe_solve.py fp32 0; } > gpurun_out/prof/probes.txt 2>&1
 ls -la gpurun_out/prof

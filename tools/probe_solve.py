@@ -21,7 +21,7 @@ status = _lib.new_status()
 def solve():
     status.zero_()
     _ops.solve(FR, XRt, Gt, Gout, trans_b=False, max_iter=w.inner, grad_tol=1e-4, lipschitz_safety=1.0, status=status)
-for dbg in ["0", "1", "2", "4", "3", "7"]:
+for dbg in (sys.argv[2].split(",") if len(sys.argv) > 2 else ["0", "1", "2", "4", "3", "7"]):
     os.environ["NENMF_NNLS_DBG"] = dbg
     solve(); torch.cuda.synchronize()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
