@@ -28,6 +28,7 @@
  *   nenmf_solve_nnls_next   nnls.py:119-227 + factorize.py:110,113 (the solve
  *                           also forms the next half-step operand)
  *   nenmf_convert_f64       matrix.py:194-214 read_nmfb payload -> device dtype
+ *   nenmf_uniform_draws     synthetic.py:62-64 / matrix.py:73-82 G, F draws of generate_problem
  *
  * Conventions
  *  - All array pointers are DEVICE pointers, row-major, allocated by the
@@ -231,6 +232,13 @@ int nenmf_sketch_draws(int dtype, const void* tables, uint64_t state_lo, uint64_
                        uint64_t inc_lo, uint64_t inc_hi, int64_t n, int64_t m, int64_t nu,
                        void* omega_l_t, void* omega_r, int* ok, unsigned long long* tails,
                        void* ws, size_t ws_bytes, void* stream);
+
+/* NumPy Generator.random (float64) draws from the PCG64 state/increment
+ * (128-bit halves): out[i] = (next64 >> 11) 2^-53 for count values, as the
+ * reference's open_uniform (matrix.py:73-82) takes them; *zero (device int)
+ * = 1 if a draw is exactly 0 (the caller then redraws like open_uniform). */
+int nenmf_uniform_draws(uint64_t state_lo, uint64_t state_hi, uint64_t inc_lo, uint64_t inc_hi, int64_t count,
+                        double* out, int* zero, void* stream);
 
 /* ---- stages of the orthonormalisation, for row-sharded panels ----------
  * nenmf_orthonormalize is CholeskyQR2 (rank-revealing first pass).  When a

@@ -132,6 +132,14 @@ def sketch_draws_device(n: int, m: int, nu: int, seed: int, dtype: str):
     """The draws of ``sketch_draws`` generated on the device (nenmf_sketch_draws,
     bit-identical to NumPy): (Omega_L^T (nu x m), Omega_R (nu x n), ok flag),
     or None when NumPy's ziggurat tables are not available."""
+    st = np.random.PCG64(check_seed(seed)).state["state"]
+    return normal_draws_device(int(st["state"]), int(st["inc"]), n, m, nu, dtype)
+
+
+def normal_draws_device(s: int, inc: int, n: int, m: int, nu: int, dtype: str):
+    """NumPy's standard_normal stream from PCG64 state ``s`` / increment ``inc``
+    on the device: m*nu draws into (nu x m) transposed, then nu*n into (nu x n)
+    (the Omega_L^T / Omega_R layout of sketch_draws); see sketch_draws_device."""
     lib, torch = _lib.require_device()
     tabs = _numpy_ziggurat_tables()
     if tabs is None:
@@ -140,8 +148,6 @@ def sketch_draws_device(n: int, m: int, nu: int, seed: int, dtype: str):
     dt = _ZIG_TABLES.get(dev)
     if dt is None:
         dt = _ZIG_TABLES[dev] = torch.from_numpy(tabs.view(np.int64).copy()).to("cuda")
-    st = np.random.PCG64(check_seed(seed)).state["state"]
-    s, inc = int(st["state"]), int(st["inc"])
     M64 = (1 << 64) - 1
     tdt = _lib.torch_dtype(dtype)
     olt = torch.empty((nu, m), dtype=tdt, device="cuda")

@@ -294,9 +294,40 @@ int sketch_draws_device(int dtype, const void* tables, uint64_t s_lo, uint64_t s
   return NENMF_OK;
 }
 
+// NumPy's Generator.random (float64): one raw value per draw, (r >> 11) 2^-53.
+// Thread t owns draws [t CH, (t + 1) CH): one jump-ahead, then sequential.
+constexpr int UNI_CH = 32;
+__global__ void k_uniform(uint64_t s_lo, uint64_t s_hi, uint64_t i_lo, uint64_t i_hi, int64_t count,
+                          double* __restrict__ out, int* __restrict__ zero) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t i0 = t * UNI_CH;
+  if (i0 >= count) return;
+  const zig::u128 inc = ((zig::u128)i_hi << 64) | i_lo;
+  zig::Stream g{zig::advance(((zig::u128)s_hi << 64) | s_lo, inc, (uint64_t)i0), inc};
+  const int64_t i1 = i0 + UNI_CH < count ? i0 + UNI_CH : count;
+  bool z = false;
+  for (int64_t i = i0; i < i1; ++i) {
+    const double v = g.next_double();
+    z |= v == 0.0;
+    out[i] = v;
+  }
+  if (z) *zero = 1;
+}
+
 }  // namespace nenmf
 
 extern "C" {
+
+int nenmf_uniform_draws(uint64_t state_lo, uint64_t state_hi, uint64_t inc_lo, uint64_t inc_hi, int64_t count,
+                        double* out, int* zero, void* stream) {
+  if (count < 0 || (count > 0 && (out == nullptr || zero == nullptr))) return NENMF_ERR_VALUE;
+  if (count == 0) return NENMF_OK;
+  const int64_t threads = (count + nenmf::UNI_CH - 1) / nenmf::UNI_CH;
+  nenmf::k_uniform<<<(unsigned)((threads + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      state_lo, state_hi, inc_lo, inc_hi, count, out, zero);
+  NENMF_LAUNCH_CHECK();
+  return NENMF_OK;
+}
 
 size_t nenmf_sketch_draws_workspace_bytes(int64_t n, int64_t m, int64_t nu) {
   nenmf::Arena a(nullptr, 0);
