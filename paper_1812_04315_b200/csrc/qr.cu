@@ -283,7 +283,8 @@ __global__ void __launch_bounds__(256) k_gram_part(PanelSet P, int k) {
 // one CTA per panel: G = sum of partials in CTA order (then written to P.G),
 // or G read from P.G when the partials were reduced elsewhere (gin);
 // factorisation into P.R / P.meta
-__global__ void __launch_bounds__(256) k_gram_factor(PanelSet P, int k, int pivot, double tol, int gin,
+constexpr int GF_THREADS = 1024;  // more loads in flight for the partial reduction
+__global__ void __launch_bounds__(GF_THREADS) k_gram_factor(PanelSet P, int k, int pivot, double tol, int gin,
                                                      nenmf_device_status* st) {
   extern __shared__ double qsm[];
   double* S = qsm;
@@ -385,7 +386,7 @@ int launch_gram_part(PanelSet& P, int k, cudaStream_t s) {
 int launch_gram_factor(PanelSet& P, int k, int pivot, double tol, int gin, nenmf_device_status* st,
                        cudaStream_t s) {
   NENMF_CUDA_TRY(set_smem(k_gram_factor, factor_smem(k)));
-  k_gram_factor<<<P.npan, 256, factor_smem(k), s>>>(P, k, pivot, tol, gin, st);
+  k_gram_factor<<<P.npan, GF_THREADS, factor_smem(k), s>>>(P, k, pivot, tol, gin, st);
   NENMF_LAUNCH_CHECK();
   return NENMF_OK;
 }
@@ -461,7 +462,7 @@ int panel_gram(Arena& ws, const T* Pt, int64_t rows, int64_t k, double* G, cudaS
   // reduce only (the factorisation runs after the cross-rank all-reduce):
   // k_gram_factor with pivot = -1 stops after writing G
   NENMF_CUDA_TRY(set_smem(k_gram_factor, factor_smem((int)k)));
-  k_gram_factor<<<1, 256, factor_smem((int)k), s>>>(P, (int)k, -1, 0.0, 0, nullptr);
+  k_gram_factor<<<1, GF_THREADS, factor_smem((int)k), s>>>(P, (int)k, -1, 0.0, 0, nullptr);
   NENMF_LAUNCH_CHECK();
   return NENMF_OK;
 }
