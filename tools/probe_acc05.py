@@ -1,3 +1,4 @@
+"""Acceptance criterion 5 of the reference (vanilla noiseless recovery, 15 s budget) per seed on the GPU; development aid."""
 import math, sys, time
 sys.path.insert(0, "baseline/_ref/suite"); sys.path.insert(0, ".")
 import nenmf as nm
