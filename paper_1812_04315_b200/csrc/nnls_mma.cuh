@@ -48,7 +48,7 @@ __device__ __forceinline__ uint32_t tf32_lo(float x, uint32_t hi) { return __flo
 // address/bookkeeping registers); chosen so that ptxas reports no spills.
 template <typename T>
 __host__ __device__ constexpr int mma_threads(int nt) {
-  return sizeof(T) == 4 ? (nt <= 2 ? 512 : 256) : (nt <= 1 ? 512 : (nt == 2 ? 384 : 256));
+  return sizeof(T) == 4 ? (nt <= 2 ? 512 : 256) : (nt <= 1 ? 512 : (nt == 2 ? 384 : (nt == 3 ? 320 : 256)));
 }
 
 __device__ __forceinline__ void mma_tf32(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {

@@ -159,3 +159,16 @@ def test_next_product_decision_paths(case):
         assert int(rep["inner_iters"]) < 80
     ref = F @ P.T
     assert np.abs(out.cpu().numpy() - ref).max() <= 1e-12 * np.abs(ref).max()
+
+
+def test_fp64_mma_solver_cfg2_shape():
+    """FP64 at the cfg2 compressed shape (p = 20, r = 30, 10 000 columns: 68
+    per CTA, 9 DMMA compute warps) against the fp64 oracle."""
+    A, B, F0 = _case(30, 20, 10000, seed=2024)
+    cfg = nm.InnerSolverConfig(max_iter=120, grad_tol=1e-7)
+    rep = []
+    F = nm.solve_nnls(A, B, F0, cfg, report=rep)
+    info = orc.SolveInfo()
+    ref = orc.nesterov_nnls(A, B, F0, 120, 1e-7, 1.0, info)
+    assert abs(rep[0].inner_iters - info.iterations) <= 1
+    assert np.abs(F - ref).max() <= 1e-9 * np.abs(ref).max()

@@ -7,14 +7,15 @@ import numpy as np
 import torch
 from paper_1812_04315_b200 import workloads, _lib, _ops
 from paper_1812_04315_b200.compression import rsi_device, compress_device
-w = workloads.make_workload(2, dtype="fp32")
-Xd = _lib.to_device(w.X, "fp32")
+DT = "fp64" if "fp64" in sys.argv else "fp32"
+w = workloads.make_workload(2, dtype=DT)
+Xd = _lib.to_device(w.X, DT)
 L, Rt, st = rsi_device(Xd, w.nu, w.q, w.sketch_seed)
 XL, XRt = compress_device(Xd, L, Rt)
-Fd = _lib.to_device(w.F0, "fp32")
+Fd = _lib.to_device(w.F0, DT)
 FR = torch.empty((w.p, w.nu), dtype=Xd.dtype, device="cuda")
 _ops.abt(Fd, Rt, FR)
-Gt = _lib.to_device(w.G0.T.copy(), "fp32")
+Gt = _lib.to_device(w.G0.T.copy(), DT)
 Gout = torch.empty_like(Gt)
 status = _lib.new_status()
 lib = _lib.load_library()
