@@ -850,6 +850,21 @@ k_nnls_mma(const __grid_constant__ MmaArgs<T> A) {
       }
       __syncthreads();
     }
+    // the best candidate's slice of the next product, reduced by warps 1..
+    // while warp 0 reduces the tie-break residuals (same order as below)
+    __shared__ double s_pout[32];
+    const int nwarps_all = (int)(blockDim.x >> 5);
+    const int per_s = next ? (no + (int)gridDim.x - 1) / (int)gridDim.x : 0;
+    const int os0 = (int)blockIdx.x * per_s, os1 = min(no, os0 + per_s);
+    const bool pre = next && ok_best && per_s <= 32 && nwarps_all > 1;
+    if (pre && wid >= 1) {
+      for (int o = os0 + wid - 1; o < os1; o += nwarps_all - 1) {
+        double sacc = 0.0;
+        for (int g = lane; g < (int)gridDim.x; g += 32) sacc += __ldcg(&A.npart[((size_t)g * 2) * no + o]);
+        sacc = warp_sum(sacc);
+        if (lane == 0) s_pout[o - os0] = sacc;
+      }
+    }
     if (ok_best) {
       if (wid == 0) {
         // CTA partials summed lane-strided then by a fixed butterfly: the same
@@ -894,7 +909,9 @@ k_nnls_mma(const __grid_constant__ MmaArgs<T> A) {
       for (int e = 0; e < NE; ++e)
         if (evalid(e)) Fout[eoff(e)] = F0[eoff(e)];
     }
-    if (next) {
+    if (next && pre && !start_wins) {
+      for (int i = tid; i < os1 - os0; i += (int)blockDim.x) A.Pout[os0 + i] = (T)s_pout[i];
+    } else if (next) {
       const int cand = (ok_best && !start_wins) ? 0 : 1;
       const int per = (no + (int)gridDim.x - 1) / (int)gridDim.x;
       const int o0 = (int)blockIdx.x * per, o1 = min(no, o0 + per);
