@@ -207,6 +207,8 @@ k_nnls_mma(const __grid_constant__ MmaArgs<T> A) {
   if (fused) {
     // ---- prologue: At -> smem, W = A^T A (k_abt order: double, t ascending)
     for (int i = tid; i < p * r; i += blockDim.x) At_s[i] = A.At[i];
+    // the power iteration's start vector, loaded while At is staged
+    if (resolver && lane < (p <= r ? p : r)) pv[lane] = A.pvec[lane];
     __syncthreads();
     for (int o = tid; o < p * p; o += blockDim.x) {
       const int a = o / p, b = o % p;
@@ -229,8 +231,7 @@ k_nnls_mma(const __grid_constant__ MmaArgs<T> A) {
       } else {
         for (int o = lane; o < k * k; o += 32) gram[o] = (double)W_s[(o / k) * 32 + (o % k)];
       }
-      double* v = pv;
-      if (lane < k) v[lane] = A.pvec[lane];
+      double* v = pv;  // start vector loaded with At above
       __syncwarp();
       // this lane's Gram row in registers (the row reads from shared memory
       // would conflict: rows are k doubles apart); same arithmetic as k_power
