@@ -284,9 +284,19 @@ k_nnls_mma(const __grid_constant__ MmaArgs<T> A) {
         for (int jl = wid; jl < ncols; jl += ncw)
           for (int t = lane; t < r; t += 32) Bs[(size_t)t * cpb + jl] = A.B[(j0 + jl) * A.ldb + t];
       } else {
+        // asynchronous element copies: every element of the block in flight at once
         for (int t = wid; t < r; t += ncw)
-          for (int jl = lane; jl < ncols; jl += 32) Bs[(size_t)t * cpb + jl] = A.B[(int64_t)t * A.ldb + j0 + jl];
+          for (int jl = lane; jl < ncols; jl += 32)
+            asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(
+                             (uint32_t)__cvta_generic_to_shared(Bs + (size_t)t * cpb + jl)),
+                         "l"(A.B + (int64_t)t * A.ldb + j0 + jl), "n"((int)sizeof(T))
+                         : "memory");
+        asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
       }
+      // the start point is read right after the prologue: pull it into L1 now
+#pragma unroll
+      for (int e = 0; e < NE; ++e)
+        if (evalid(e)) asm volatile("prefetch.global.L1 [%0];" ::"l"(F0 + eoff(e)));
       asm volatile("bar.sync 2, %0;" ::"r"(ncw * 32) : "memory");
       // this warp's columns of V = A^T B (k_ab order: T precision, t ascending)
 #pragma unroll
