@@ -206,9 +206,14 @@ k_nnls_mma(const __grid_constant__ MmaArgs<T> A) {
   T nv[NE];  // -V in the accumulator layout (compute warps)
   if (fused) {
     // ---- prologue: At -> smem, W = A^T A (k_abt order: double, t ascending)
-    for (int i = tid; i < p * r; i += blockDim.x) At_s[i] = A.At[i];
+    for (int i = tid; i < p * r; i += blockDim.x)
+      asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"((uint32_t)__cvta_generic_to_shared(At_s + i)),
+                   "l"(A.At + i), "n"((int)sizeof(T))
+                   : "memory");
+    asm volatile("cp.async.commit_group;" ::: "memory");
     // the power iteration's start vector, loaded while At is staged
     if (resolver && lane < (p <= r ? p : r)) pv[lane] = A.pvec[lane];
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
     __syncthreads();
     for (int o = tid; o < p * p; o += blockDim.x) {
       const int a = o / p, b = o % p;
