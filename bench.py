@@ -3,24 +3,36 @@
 One step = the hot path over one synthetic input: the randomized-subspace-
 iteration sketch (``subspace_iteration_pair``, q=4, p'=30) charged to the run
 as the reference CLI does (cli.py:159-168), then ``factorize_compressed`` for
-100 outer iterations with inner Max_iter=500 (the reference default) in FP32
-on n = m = 10^4, p = 20 (BASELINE.json configs[1]).  metric value =
-outer iterations completed / wall time of the step on the device.
+100 outer iterations with inner Max_iter=500 (the reference default) on
+n = m = 10^4, p = 20 (BASELINE.json configs[1]).  metric value = outer
+iterations completed / device time of the step.
+
+The headline (``value``, ``e2e``) runs in FP64 mode -- the reference's own
+arithmetic (matrix.py:31-36), parity 1e-5 -- so it compares like for like
+with the reference arm; ``fp32_mode`` reports the same workload in FP32 mode
+(parity 1e-3) beside it, with its final RRE against the FP64 run's.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
---impl reference times the CPU oracle (the reference algorithm restated in
-NumPy, oracle/nenmf_oracle.py; the reference is pure Python, so there is
-nothing to compile into oracle/_ref) on the host cores, on a bounded sample
-of the same workload.  N > 1 (torchrun): independent replicas (weak scaling),
-rank 0 prints; the path has no cross-GPU exchange in this configuration.
+--gpus N > 1: bench.py re-executes itself under torch.distributed.run with N
+ranks (one per GPU) unless it already runs under it (WORLD_SIZE must then
+equal N).  X is split into row blocks (sharded.py) and the ONE
+problem runs across the ranks ("scaling": "strong"); ``cfg5_sharded``
+reports BASELINE cfg 5 (10^5 x 10^5, 40 GB fp32, generated on the device) the
+same way at every N.
+
+--impl reference times the UNMODIFIED reference package (baseline/_ref, pip
+installed from /root/reference; pure Python/NumPy, float64) through its
+public API on the host cores: each step is one bounded sample (sketch +
+compression + one outer iteration), reported as the same metric; rank 0 only.
+If the package is missing, the NumPy restatement in oracle/ stands in
+("kind": "port").
 """
 
 from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
 import statistics
 import subprocess
@@ -32,10 +44,15 @@ from pathlib import Path
 REPO = Path(__file__).resolve().parent
 sys.path.insert(0, str(REPO))
 
-METRIC = "compressed-NeNMF outer iters/s (cfg2 n=m=1e4 p=20 p'=30 q=4, fp32, 100 outer, inner<=500, sketch charged)"
 UNIT = "outer_iter/s"
 CFG = 2
 OUTER = 100
+L2_BYTES = 126 * 1024 * 1024
+
+
+def metric_name(dtype: str) -> str:
+    return (f"compressed-NeNMF outer iters/s (cfg2 n=m=1e4 p=20 p'=30 q=4, {dtype}, 100 outer, inner<=500, "
+            f"sketch charged)")
 
 
 def parse():
@@ -44,11 +61,9 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--dtype", default="fp64", choices=["fp64", "fp32"], help="headline arithmetic (default fp64)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--dtype", default="fp32", choices=["fp32", "fp64"])
-    ap.add_argument("--workload", default="cfg2", choices=["cfg2", "cfg5"],
-                    help="cfg2: the headline (1 problem per GPU, replicas for N > 1); "
-                         "cfg5: 100k x 100k fp32 generated on device, X row-sharded over the N GPUs")
+    ap.add_argument("--no-secondary", action="store_true", help="skip the fp32_mode and cfg5_sharded blocks")
     ap.add_argument("--outer", type=int, default=None, help="override the outer-iteration count (probes only)")
     return ap.parse_args()
 
@@ -128,33 +143,73 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-# ------------------------------------------------------------ CPU baseline
-def cpu_sample(w, outer_sample: int = 1):
-    """Oracle (reference algorithm, NumPy/OpenBLAS, all host threads) on a
-    bounded sample of the same workload: the full sketch + compression and
-    ``outer_sample`` outer iterations; extrapolated to OUTER iterations."""
-    sys.path.insert(0, str(REPO / "oracle"))
-    import nenmf_oracle as orc
-
-    t0 = time.perf_counter()
-    L, R = orc.rsi(w.X, w.nu, w.q, w.sketch_seed)
-    t_sketch = time.perf_counter() - t0
-    t1 = time.perf_counter()
-    res = orc.nenmf(w.X, w.G0, w.F0, L=L, R=R, max_outer=outer_sample, max_iter=w.inner,
-                    trace_every=outer_sample + 1)
-    t_loop = time.perf_counter() - t1
-    # the loop includes compress + 2 emits; charge them once like the GPU step does
-    per_outer = t_loop / outer_sample
-    total = t_sketch + OUTER * per_outer
-    return {"value": OUTER / total, "t_sketch_s": t_sketch, "t_outer_s": per_outer,
-            "inner_iters": [[g.iterations, f.iterations] for g, f in res.inner]}
-
-
 def cores():
     try:
         return len(os.sched_getaffinity(0))
     except AttributeError:
         return os.cpu_count() or 1
+
+
+# ------------------------------------------------------------ CPU baseline
+def _reference_package():
+    """The unmodified reference package installed in baseline/_ref, or None."""
+    ref = REPO / "baseline" / "_ref"
+    if not (ref / "nenmf" / "__init__.py").exists():
+        return None
+    sys.path.insert(0, str(ref))
+    try:
+        import nenmf
+    except Exception:  # noqa: BLE001 - any import failure means "not available"
+        return None
+    finally:
+        sys.path.remove(str(ref))
+    if not str(getattr(nenmf, "__file__", "")).startswith(str(ref)):
+        return None
+    return nenmf
+
+
+def cpu_sample(w):
+    """One bounded sample of the cfg2 workload on the host cores, timed through
+    the UNMODIFIED reference package when it is installed (kind "reference"),
+    else through the oracle's NumPy restatement (kind "port").  Measured: the
+    sketch, a separate compression, and factorize_compressed with ONE outer
+    iteration (its MonotonicClock = compression + the outer iteration, emits
+    excluded, factorize.py:136-152; its wall time adds the two full-X RRE
+    emits).  The rate of the 100-outer step is extrapolated from those parts:
+    sketch + wall(1 outer) + 99 x (solver(1 outer) - compression)."""
+    nenmf = _reference_package()
+    t0 = time.perf_counter()
+    if nenmf is not None:
+        sk = nenmf.subspace_iteration_pair(w.X, w.nu, w.q, w.sketch_seed)
+        t1 = time.perf_counter()
+        nenmf.compress_problem(w.X, sk)
+        t2 = time.perf_counter()
+        clock = nenmf.MonotonicClock()
+        cfg = nenmf.OuterConfig(inner=nenmf.InnerSolverConfig(max_iter=w.inner), time_budget_seconds=0.0,
+                                max_outer_iterations=1)
+        nenmf.factorize_compressed(w.X, sk, nenmf.FactorPair(G=w.G0, F=w.F0, p=w.p), cfg, clock=clock)
+        t3 = time.perf_counter()
+        solver = clock.elapsed()
+        kind = "reference"
+    else:
+        sys.path.insert(0, str(REPO / "oracle"))
+        import nenmf_oracle as orc
+
+        L, R = orc.rsi(w.X, w.nu, w.q, w.sketch_seed)
+        t1 = time.perf_counter()
+        orc.compress(w.X, L, R)
+        t2 = time.perf_counter()
+        ts = time.perf_counter()
+        orc.nenmf(w.X, w.G0, w.F0, L=L, R=R, max_outer=1, max_iter=w.inner, trace_every=2)
+        t3 = time.perf_counter()
+        solver = t3 - ts  # includes the final emit: an upper bound
+        kind = "port"
+    t_sketch, t_compress, t_fc = t1 - t0, t2 - t1, t3 - t2
+    t_outer = max(solver - t_compress, 1e-9)
+    total = t_sketch + t_fc + (OUTER - 1) * t_outer
+    return {"value": OUTER / total, "kind": kind, "sample_s": t3 - t0, "t_sketch_s": t_sketch,
+            "t_compress_s": t_compress, "t_factorize_1outer_wall_s": t_fc, "t_outer_solver_s": t_outer,
+            "extrapolated_100_outer_s": total}
 
 
 # -------------------------------------------------------------- reference arm
@@ -163,154 +218,39 @@ def run_reference(args, rank, world):
         return
     from paper_1812_04315_b200 import workloads
 
-    w = workloads.make_workload(CFG, dtype=args.dtype)
-    vals = []
+    w = workloads.make_workload(CFG, dtype="fp64")
+    vals, walls = [], []
     for i in range(args.warmup + args.steps):
-        r = cpu_sample(w, outer_sample=1)
+        r = cpu_sample(w)
         if i >= args.warmup:
             vals.append(r)
+            walls.append(r["sample_s"])
     value = statistics.median(v["value"] for v in vals)
-    ms = 1e3 * OUTER / value
+    kind = vals[-1]["kind"]
+    what = ("the unmodified reference package (baseline/_ref: nenmf.subspace_iteration_pair, compress_problem, "
+            "factorize_compressed with MonotonicClock)" if kind == "reference" else
+            "the oracle's NumPy restatement of the reference (baseline/_ref not installed)")
+    sample = (f"per step: {what} on cfg2 X (float64): the sketch, one compression, and 1 outer iteration "
+              f"(inner<=500); the 100-outer rate is extrapolated as sketch + wall(1 outer incl. 2 RRE emits) "
+              f"+ 99 x (solver-clock outer - compression)")
     line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic (BASELINE cfg2 generator, seed 1234)",
-        "impl": "reference",
+        "metric": metric_name("fp64"), "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * statistics.median(walls), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (BASELINE cfg2 generator, seed 1234)", "impl": "reference",
         "config": {"workload": "cfg2", "n": w.n, "m": w.m, "p": w.p, "p_prime": w.nu, "q": w.q,
                    "outer": OUTER, "inner_max_iter": w.inner, "parallelism": "host cores (OpenBLAS threads)"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores(), "kind": "port",
-                         "sample": "per step: full RSI sketch+compress on cfg2 X and 1 outer iteration "
-                                   "(inner<=500), extrapolated to 100 outer; reference algorithm restated in "
-                                   "NumPy (oracle/nenmf_oracle.py), float64 as the reference"},
+        "ms_per_step_meaning": "measured wall time of one sample (what a step of this arm runs)",
+        "extrapolation": {"outer_measured_per_step": 1, "outer_in_metric": OUTER,
+                          "extrapolated_step_s": statistics.median(v["extrapolated_100_outer_s"] for v in vals)},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores(), "kind": kind, "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "sample_detail": vals[-1],
+        "samples": vals,
     }
     print(json.dumps(line), flush=True)
 
 
-# ------------------------------------------------------------------ our arm
-def run_ours(args, rank, world, local_rank):
-    import numpy as np
-    import torch
-
-    import paper_1812_04315_b200 as nm
-    from paper_1812_04315_b200 import _lib, _ops, workloads
-    from paper_1812_04315_b200.compression import rsi_device
-
-    torch.cuda.set_device(local_rank)
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
-
-        dist.init_process_group("nccl")
-    lib = _lib.load_library()
-    w = workloads.make_workload(CFG, dtype=args.dtype)
-    tdt = _lib.torch_dtype(args.dtype)
-    Xd = torch.from_numpy(w.X.astype(np.float32 if args.dtype == "fp32" else np.float64)).to("cuda")
-    G0d = torch.from_numpy(w.G0.astype(Xd.numpy().dtype if False else (np.float32 if args.dtype == "fp32" else np.float64))).to("cuda")
-    F0d = torch.from_numpy(w.F0.astype(np.float32 if args.dtype == "fp32" else np.float64)).to("cuda")
-    cfg = nm.OuterConfig(inner=nm.InnerSolverConfig(max_iter=w.inner), time_budget_seconds=0.0,
-                         max_outer_iterations=OUTER, trace_every=OUTER)
-    stream = torch.cuda.current_stream()
-
-    def step_device():
-        sk = nm.subspace_iteration_pair(Xd, w.nu, w.q, w.sketch_seed)
-        init = nm.FactorPair(G=G0d, F=F0d, p=w.p)
-        return nm.factorize_compressed(Xd, sk, init, cfg, return_device=True)
-
-    # pinned host copies for the end-to-end leg
-    Xh = torch.from_numpy(w.X.astype(np.float32 if args.dtype == "fp32" else np.float64)).pin_memory()
-    G0h = torch.from_numpy(w.G0.astype(np.float32 if args.dtype == "fp32" else np.float64)).pin_memory()
-    F0h = torch.from_numpy(w.F0.astype(np.float32 if args.dtype == "fp32" else np.float64)).pin_memory()
-    h2d = Xh.numel() * Xh.element_size() + G0h.numel() * G0h.element_size() + F0h.numel() * F0h.element_size()
-    d2h = (w.n * w.p + w.p * w.m) * Xh.element_size()
-
-    def step_e2e():
-        X = Xh.to("cuda", non_blocking=True)
-        G0 = G0h.to("cuda", non_blocking=True)
-        F0 = F0h.to("cuda", non_blocking=True)
-        sk = nm.subspace_iteration_pair(X, w.nu, w.q, w.sketch_seed)
-        out = nm.factorize_compressed(X, sk, nm.FactorPair(G=G0, F=F0, p=w.p), cfg, return_device=True)
-        G = out.G.to("cpu")
-        F = out.F.to("cpu")
-        return G, F
-
-    def barrier():
-        if dist is not None:
-            dist.barrier()
-        torch.cuda.synchronize()
-
-    def timed(fn, k):
-        barrier()
-        a = torch.cuda.Event(enable_timing=True)
-        b = torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        for _ in range(k):
-            fn()
-        b.record(stream)
-        barrier()
-        ms = a.elapsed_time(b)
-        if dist is not None:
-            t = torch.tensor([ms], device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ms = float(t.item())
-        return ms
-
-    for _ in range(args.warmup):
-        step_device()
-    torch.cuda.synchronize()
-
-    sampler = ClockSampler(local_rank)
-    sampler.start()
-    launches0 = lib.nenmf_launch_count()
-    ms = timed(step_device, args.steps)
-    launches = lib.nenmf_launch_count() - launches0
-    clocks = sampler.stop()
-    ms_step = ms / args.steps
-    value = world * OUTER / (ms_step / 1e3)
-
-    # end-to-end through the public API with host buffers
-    step_e2e()
-    ms_e2e = timed(step_e2e, max(1, min(args.steps, 3))) / max(1, min(args.steps, 3))
-    e2e_value = world * OUTER / (ms_e2e / 1e3)
-
-    # roofline of the kernels, timed on the launching stream with CUDA events
-    roof = kernel_rooflines(w, Xd, args.dtype)
-
-    if rank != 0:
-        if dist is not None:
-            dist.destroy_process_group()
-        return
-    cpu = None
-    if world == 1 and not args.no_cpu_baseline:
-        r = cpu_sample(w, outer_sample=1)
-        cpu = {"value": r["value"], "unit": UNIT, "cores": cores(), "kind": "port",
-               "sample": "full RSI sketch+compress on cfg2 X + 1 outer iteration (inner<=500) of the NumPy "
-                         "restatement of the reference (float64, OpenBLAS all threads), extrapolated to 100 outer",
-               "t_sketch_s": r["t_sketch_s"], "t_outer_s": r["t_outer_s"]}
-    line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f32" if args.dtype == "fp32" else "f64",
-        "data": "synthetic (BASELINE cfg2 generator: U[0,1) G,F + 1% |N| noise, seed 1234; X resident in HBM)",
-        "config": {"workload": "cfg2", "n": w.n, "m": w.m, "p": w.p, "p_prime": w.nu, "q": w.q,
-                   "outer": OUTER, "inner_max_iter": w.inner, "grad_tol": 1e-4,
-                   "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
-                   "l2": "inputs larger than L2 (X = 400 MB fp32)"},
-        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "ms_per_step": ms_e2e},
-        "gpu_launches": int(launches),
-        "clocks": clocks,
-        "roofline": roof["rsi"],
-        "solver": roof["solver"],
-        "kernels": roof["table"],
-        "cpu_baseline": cpu,
-    }
-    print(json.dumps(line), flush=True)
-    if dist is not None:
-        dist.destroy_process_group()
-
-
+# ------------------------------------------------------------------ helpers
 def _peaks():
     p = REPO / "MEASURED_PEAKS.json"
     if p.exists():
@@ -319,142 +259,373 @@ def _peaks():
     return 6650.0, 1590.0, "fallback (B200_PROFILING.md)"
 
 
-def _traffic(kernel: str):
-    p = REPO / "profiles" / "ncu_traffic.json"
+def _fp64_peak():
+    p = REPO / "profiles" / "fp64_peak.json"
     if p.exists():
         d = json.loads(p.read_text())
-        return d.get(kernel)
-    return None
+        return d["fp64_dmma_tflops"], "measured on this pool's B200 by tools/micro/fp64_peak.cu (profiles/fp64_peak.json)"
+    return 37.0, "fallback: nominal B200 FP64 tensor figure (no measurement committed)"
 
 
-def kernel_rooflines(w, Xd, dtype):
-    """Time the RSI dual pass and one compressed solve in isolation (CUDA
-    events on the current stream; inputs larger than L2 for the pass)."""
+class Timer:
+    """CUDA-event timing on the current stream with a synchronize on both sides."""
+
+    def __init__(self, torch, dist=None):
+        self.torch, self.dist = torch, dist
+
+    def barrier(self):
+        if self.dist is not None:
+            self.dist.barrier()
+        self.torch.cuda.synchronize()
+
+    def __call__(self, fn, k, between=None):
+        torch = self.torch
+        stream = torch.cuda.current_stream()
+        self.barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(k):
+            fn()
+            if between is not None:
+                between()
+        b.record(stream)
+        self.barrier()
+        ms = a.elapsed_time(b)
+        if self.dist is not None:
+            t = torch.tensor([ms], device="cuda")
+            self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms
+
+
+class Problem:
+    """The cfg2 problem on this rank: the whole X (world 1) or its row block
+    (sharded.py), resident in HBM, plus pinned host copies for the e2e leg."""
+
+    def __init__(self, w, dtype, world, rank):
+        import numpy as np
+        import torch
+
+        from paper_1812_04315_b200 import sharded
+
+        self.w, self.dtype, self.world, self.rank = w, dtype, world, rank
+        npdt = np.float32 if dtype == "fp32" else np.float64
+        self.row0, self.rows = sharded.row_block(w.n, world, rank)
+        Xl = np.ascontiguousarray(w.X[self.row0:self.row0 + self.rows].astype(npdt))
+        self.Xh = torch.from_numpy(Xl).pin_memory()
+        self.G0h = torch.from_numpy(w.G0.astype(npdt)).pin_memory()
+        self.F0h = torch.from_numpy(w.F0.astype(npdt)).pin_memory()
+        self.Xd = self.Xh.to("cuda")
+        self.G0d = self.G0h.to("cuda")
+        self.F0d = self.F0h.to("cuda")
+        self.h2d = sum(t.numel() * t.element_size() for t in (self.Xh, self.G0h, self.F0h))
+        self.d2h = (w.n * w.p + w.p * w.m) * self.Xh.element_size()
+        self.flush = None
+        if self.Xd.numel() * self.Xd.element_size() < 2 * L2_BYTES:
+            # this rank's X would stay in L2 between steps: overwrite L2 after each step
+            self.flush = torch.empty(2 * L2_BYTES // 4, dtype=torch.float32, device="cuda")
+
+    def l2_flush(self):
+        if self.flush is not None:
+            from paper_1812_04315_b200 import _lib
+
+            _lib.zero_(self.flush)
+
+    def cfg(self, outer, trace_every=None):
+        import paper_1812_04315_b200 as nm
+
+        return nm.OuterConfig(inner=nm.InnerSolverConfig(max_iter=self.w.inner), time_budget_seconds=0.0,
+                              max_outer_iterations=outer, trace_every=trace_every or outer)
+
+    def step(self, X, G0, F0, cfg, comm=None, observer=None):
+        """sketch + factorize through the public API (device tensors in and out)."""
+        import paper_1812_04315_b200 as nm
+        from paper_1812_04315_b200 import sharded
+
+        w = self.w
+        init = nm.FactorPair(G=G0, F=F0, p=w.p)
+        if self.world == 1:
+            sk = nm.subspace_iteration_pair(X, w.nu, w.q, w.sketch_seed)
+            return nm.factorize_compressed(X, sk, init, cfg, observer=observer, return_device=True)
+        sk = sharded.subspace_iteration_pair_sharded(X, w.n, w.nu, w.q, w.sketch_seed, comm=comm)
+        return sharded.factorize_compressed_sharded(X, w.n, sk, init, cfg, observer=observer, comm=comm,
+                                                    return_device=True)
+
+    def step_e2e(self, cfg, comm=None):
+        X = self.Xh.to("cuda", non_blocking=True)
+        G0 = self.G0h.to("cuda", non_blocking=True)
+        F0 = self.F0h.to("cuda", non_blocking=True)
+        out = self.step(X, G0, F0, cfg, comm)
+        return out.G.to("cpu"), out.F.to("cpu")
+
+    def final_rre(self, outer, comm=None):
+        import paper_1812_04315_b200 as nm
+
+        rec = nm.TraceRecorder()
+        self.step(self.Xd, self.G0d, self.F0d, self.cfg(outer), comm, observer=rec)
+        return rec.records[-1].rre
+
+
+def measure_workload(args, w, dtype, world, rank, dist, comm, outer):
+    """value / e2e / launches / clocks of cfg2 in one arithmetic mode."""
+    import torch
+
+    from paper_1812_04315_b200 import _lib
+
+    lib = _lib.load_library()
+    timer = Timer(torch, dist)
+    P = Problem(w, dtype, world, rank)
+    cfg = P.cfg(outer)
+    run = lambda: P.step(P.Xd, P.G0d, P.F0d, cfg, comm)  # noqa: E731
+    for _ in range(args.warmup):
+        run()
+        P.l2_flush()
+    torch.cuda.synchronize()
+    sampler = ClockSampler(torch.cuda.current_device())
+    sampler.start()
+    launches0 = lib.nenmf_launch_count()
+    ms = timer(run, args.steps, between=P.l2_flush)
+    launches = (lib.nenmf_launch_count() - launches0) // args.steps
+    clocks = sampler.stop()
+    ms_step = ms / args.steps
+    P.step_e2e(cfg, comm)
+    k = max(1, min(args.steps, 3))
+    ms_e2e = timer(lambda: P.step_e2e(cfg, comm), k) / k
+    rre = P.final_rre(outer, comm)
+    res = {"value": outer / (ms_step / 1e3), "ms_per_step": ms_step,
+           "e2e": {"value": outer / (ms_e2e / 1e3), "unit": UNIT, "h2d_bytes_per_step": P.h2d,
+                   "d2h_bytes_per_step": P.d2h, "ms_per_step": ms_e2e},
+           "gpu_launches": int(launches), "clocks": clocks, "final_rre": rre,
+           "l2": ("inputs larger than L2 (this rank's X: %.0f MB)" % (P.Xd.numel() * P.Xd.element_size() / 1e6)
+                  if P.flush is None else "L2 flushed after every step (this rank's X: %.0f MB < 2 x L2)"
+                  % (P.Xd.numel() * P.Xd.element_size() / 1e6))}
+    return res, P
+
+
+def rsi_roofline(P, dtype):
+    """The RSI X-pass (the kernel north_star's roofline target names) and the
+    whole sketch + compression, on this rank's X, CUDA events on the stream
+    the kernels run on."""
+    import ctypes
+
     import torch
 
     from paper_1812_04315_b200 import _lib, _ops, workloads
     from paper_1812_04315_b200.compression import compress_device, rsi_device
 
+    w = P.w
+    Xd = P.Xd
+    n, m = Xd.shape
     hbm, _bf16, src = _peaks()
-    stream = torch.cuda.current_stream()
-    L, Rt, st = rsi_device(Xd, w.nu, w.q, w.sketch_seed)
-    Yt = torch.empty((w.nu, w.n), dtype=Xd.dtype, device="cuda")
-    Zt = torch.empty((w.nu, w.m), dtype=Xd.dtype, device="cuda")
-
-    def ev_time(fn, reps):
-        fn()
-        torch.cuda.synchronize()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        for _ in range(reps):
-            fn()
-        b.record(stream)
-        torch.cuda.synchronize()
-        return a.elapsed_time(b) / reps
-
+    timer = Timer(torch)
+    L, Rt, _ = rsi_device(Xd, w.nu, w.q, w.sketch_seed)
+    Yt = torch.empty((w.nu, n), dtype=Xd.dtype, device="cuda")
+    Zt = torch.empty((w.nu, m), dtype=Xd.dtype, device="cuda")
+    pass_bytes = n * m * Xd.element_size()
+    pass_flops = 2 * 2 * n * m * w.nu  # Y = X A and Z = X^T B
     Xp = _ops.prepare_x(Xd, w.nu)
+    lib = _lib.load_library()
     if Xp is not None:
-        # FP32: the passes of a sketch stream the prepared (tile-major bf16 hi/lo) copy of X,
-        # 4 bytes per element like X itself; it is made once per sketch (timed separately)
-        ms_prep = ev_time(lambda: _ops.prepare_x(Xd, w.nu), 5)
-        ms_op = ev_time(lambda: _ops.dual_pass_prepared(Xp, w.n, w.m, Rt, L, Yt, Zt), 20)
-        # the kernel alone: CUDA events around each k_dual_bulk launch on its stream
-        import ctypes
-        lib = _lib.load_library()
-        lib.nenmf_debug_xpass_ms(None)
-        lib.nenmf_debug_xpass_timing(1)
-        for _ in range(20):
-            _ops.dual_pass_prepared(Xp, w.n, w.m, Rt, L, Yt, Zt)
-        tot = ctypes.c_double(0.0)
-        cnt = lib.nenmf_debug_xpass_ms(ctypes.byref(tot))
-        lib.nenmf_debug_xpass_timing(0)
-        ms_pass = tot.value / max(cnt, 1)
-        kname = "RSI X-pass (k_dual_bulk: bulk-copy stream of the prepared X -> X*A and X^T*B, tcgen05 BF16x3)"
+        ms_prep = timer(lambda: _ops.prepare_x(Xd, w.nu), 5) / 5
+        ms_op = timer(lambda: _ops.dual_pass_prepared(Xp, n, m, Rt, L, Yt, Zt), 20) / 20
+        kname = "k_dual_bulk (RSI X-pass: bulk-copy stream of the prepared X -> X*A and X^T*B, tcgen05 BF16x3)"
+        op = lambda: _ops.dual_pass_prepared(Xp, n, m, Rt, L, Yt, Zt)  # noqa: E731
     else:
         ms_prep = 0.0
-        ms_pass = ev_time(lambda: _ops.dual_pass(Xd, Rt, L, Yt, Zt), 10)
-        ms_op = ms_pass
-        kname = "RSI X-pass (k_dual: one read of X -> X*A and X^T*B)"
+        ms_op = timer(lambda: _ops.dual_pass(Xd, Rt, L, Yt, Zt), 10) / 10
+        kname = "k_xv64 + k_ux64 (RSI X-pass in FP64 on the DMMA tensor pipe)"
+        op = lambda: _ops.dual_pass(Xd, Rt, L, Yt, Zt)  # noqa: E731
+    # the kernel(s) alone: CUDA events the library records around each X-pass
+    # launch on its own stream
+    lib.nenmf_debug_xpass_ms(None)
+    lib.nenmf_debug_xpass_timing(1)
+    for _ in range(20):
+        op()
+    tot = ctypes.c_double(0.0)
+    cnt = lib.nenmf_debug_xpass_ms(ctypes.byref(tot))
+    lib.nenmf_debug_xpass_timing(0)
+    # per pass; a path without the hook (FP64 before the fused pass) reports the whole pass op
+    ms_pass = tot.value / 20.0 if cnt > 0 else ms_op
     del Xp
-    pass_bytes = w.n * w.m * Xd.element_size()
-    ms_rsi = ev_time(lambda: rsi_device(Xd, w.nu, w.q, w.sketch_seed), 3)
-    rsi_bytes = workloads.rsi_bytes(w.n, w.m, w.q, Xd.element_size())
-    # compressed F-half solve at cfg2 (the dominant kernel of the step)
+
+    def sketch_and_compress():
+        L2, Rt2, _ = rsi_device(Xd, w.nu, w.q, w.sketch_seed, check=False)
+        compress_device(Xd, L2, Rt2)
+
+    ms_rsi = timer(sketch_and_compress, 3) / 3
+    rsi_bytes = workloads.rsi_bytes(n, m, w.q, Xd.element_size())
+    rsi_gbs = rsi_bytes / (ms_rsi * 1e-3) / 1e9
+    if dtype == "fp32":
+        ach = pass_bytes / (ms_pass * 1e-3) / 1e9
+        roof = {"bound": "hbm", "kernel": kname, "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
+                "peak_source": src, "algorithmic_bytes_per_launch": pass_bytes}
+    else:
+        peak, psrc = _fp64_peak()
+        ach = pass_flops / (ms_pass * 1e-3) / 1e12
+        roof = {"bound": "tensor", "kernel": kname, "achieved": ach, "peak": peak, "unit": "TFLOP/s",
+                "frac": ach / peak, "peak_source": psrc, "algorithmic_flops_per_pass": pass_flops,
+                "hbm_gbs_same_pass": pass_bytes / (ms_pass * 1e-3) / 1e9,
+                "hbm_frac_same_pass": pass_bytes / (ms_pass * 1e-3) / 1e9 / hbm}
+    roof.update({
+        "traffic": None,
+        "traffic_note": "dram bytes per launch come from the committed ncu --set full capture (profiles/)",
+        "ms_per_launch": ms_pass,
+        "ms_per_launch_source": "CUDA events around each X-pass launch on the library's stream (20 passes)",
+        "ms_per_pass_op": ms_op, "prepare_x_ms_once_per_sketch": ms_prep,
+        "rsi_total": {"ms": ms_rsi, "bytes": rsi_bytes, "gbs": rsi_gbs, "frac_hbm": rsi_gbs / hbm,
+                      "what": "sketch (2q+1 passes) + compression (1 pass) timed together; "
+                              "bytes = (2q+2) n m s_X (SURVEY 8(d))"},
+    })
+    return roof
+
+
+def solver_probe(P, dtype):
+    """One compressed F-half solve at cfg2 (the kernel that dominates the step)."""
+    import torch
+
+    from paper_1812_04315_b200 import _lib, _ops
+    from paper_1812_04315_b200.compression import compress_device, rsi_device
+
+    w = P.w
+    Xd = P.Xd
+    timer = Timer(torch)
+    L, Rt, _ = rsi_device(Xd, w.nu, w.q, w.sketch_seed)
     XL, XRt = compress_device(Xd, L, Rt)
     F0 = _lib.to_device(w.F0, dtype)
-    Gt = _lib.to_device(w.G0.T.copy(), dtype)
+    Gt = _lib.to_device(w.G0[P.row0:P.row0 + P.rows].T.copy(), dtype)
     GLt = torch.empty((w.p, w.nu), dtype=Xd.dtype, device="cuda")
     _ops.abt(Gt, L, GLt)
     Fo = torch.empty_like(F0)
     status = _lib.new_status()
 
     def solve():
-        status.zero_()
+        _lib.zero_(status)
         _ops.solve(GLt, XL, F0, Fo, trans_b=False, max_iter=w.inner, grad_tol=1e-4, lipschitz_safety=1.0,
                    status=status)
 
-    ms_solve = ev_time(solve, 5)
+    solve()
+    ms = timer(solve, 5) / 5
     iters = int(_lib.read_status(status)[0]["inner_iters"])
-    s = Xd.element_size()
-    pass_gbs = pass_bytes / (ms_pass * 1e-3) / 1e9
-    rsi = {"bound": "hbm", "kernel": kname,
-           "achieved": pass_gbs, "peak": hbm, "unit": "GB/s", "frac": pass_gbs / hbm,
-           "traffic": _traffic("k_dual_bulk"), "peak_source": src,
-           "algorithmic_bytes_per_launch": pass_bytes, "ms_per_launch": ms_pass,
-           "ms_per_launch_source": "CUDA events around each k_dual_bulk launch on its stream (20 passes)",
-           "ms_per_pass_op": ms_op,
-           "pass_op_gbs": pass_bytes / (ms_op * 1e-3) / 1e9,
-           "pass_op_includes": "skinny-operand split + k_dual_bulk + slab reduction (3 launches)",
-           "prepare_x_ms_once_per_sketch": ms_prep,
-           "rsi_total_ms": ms_rsi, "rsi_effective_gbs": rsi_bytes / (ms_rsi * 1e-3) / 1e9,
-           "rsi_bytes_model": "(2q+2)*n*m*s_X (SURVEY 8d)"}
-    # the inner solver is latency-bound (state lives in registers; one
-    # dependent iteration after another), so its figure is time per iteration
-    # next to the floors of SURVEY 8(d): HBM if the state were streamed, and
-    # the tensor-pipe flops of W*F
-    us_it = 1e3 * ms_solve / max(iters, 1)
+    us_it = 1e3 * ms / max(iters, 1)
     flops_it = 2 * w.p * w.p * w.m
-    stream_bytes_it = 9 * w.p * w.m * s
-    solver = {"bound": "latency", "kernel": "k_nnls_mma (persistent inner solver, F-half at cfg2)",
-              "ms_per_launch": ms_solve, "inner_iters": iters, "us_per_inner_iter": us_it,
-              "flops_per_iter": flops_it, "achieved_tflops": flops_it / (us_it * 1e-6) / 1e12,
-              "hbm_floor_us_if_streamed": stream_bytes_it / (hbm * 1e9) * 1e6,
-              "traffic": _traffic("k_nnls_mma")}
-    table = {"dual_pass_kernel_ms": ms_pass, "dual_pass_op_ms": ms_op, "prepare_x_ms": ms_prep, "rsi_ms": ms_rsi,
-             "solve_F_half_ms": ms_solve}
-    return {"rsi": rsi, "solver": solver, "table": table}
+    hbm, _, _ = _peaks()
+    out = {"bound": "latency", "kernel": f"k_nnls_mma<{'double' if dtype == 'fp64' else 'float'}> "
+                                         "(persistent inner solver, F-half at cfg2)",
+           "ms_per_launch": ms, "inner_iters": iters, "us_per_inner_iter": us_it, "flops_per_iter": flops_it,
+           "achieved_tflops": flops_it / (us_it * 1e-6) / 1e12,
+           "hbm_floor_us_if_streamed": 9 * w.p * w.m * Xd.element_size() / (hbm * 1e9) * 1e6}
+    if dtype == "fp64":
+        peak, _ = _fp64_peak()
+        out["frac_fp64_tensor_peak"] = out["achieved_tflops"] / peak
+    return out
 
 
-# ------------------------------------------------- row-sharded arm (cfg5)
-def run_sharded(args, rank, world, local_rank):
+# ------------------------------------------------------------------ our arm
+def run_ours(args, rank, world, local_rank):
+    import torch
+
+    from paper_1812_04315_b200 import _lib, sharded, workloads
+
+    torch.cuda.set_device(local_rank)
+    dist = comm = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        comm = sharded.Comm()
+    _lib.load_library()
+    outer = args.outer or OUTER
+    dtype = args.dtype
+    w = workloads.make_workload(CFG, dtype=dtype)
+    head, P = measure_workload(args, w, dtype, world, rank, dist, comm, outer)
+    roof = rsi_roofline(P, dtype)
+    solver = solver_probe(P, dtype)
+    del P
+    torch.cuda.empty_cache()
+
+    fp32 = None
+    if not args.no_secondary and dtype == "fp64":
+        w32 = workloads.make_workload(CFG, dtype="fp32")
+        res32, P32 = measure_workload(args, w32, "fp32", world, rank, dist, comm, outer)
+        res32["roofline"] = rsi_roofline(P32, "fp32")
+        res32["solver"] = solver_probe(P32, "fp32")
+        res32["metric"] = metric_name("fp32")
+        res32["final_rre_rel_diff_vs_fp64_run"] = abs(res32["final_rre"] - head["final_rre"]) / head["final_rre"]
+        fp32 = res32
+        del P32
+        torch.cuda.empty_cache()
+
+    cfg5 = None
+    if not args.no_secondary:
+        cfg5 = run_cfg5(args, rank, world, local_rank, dist, comm)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        w64 = w if dtype == "fp64" else workloads.make_workload(CFG, dtype="fp64")
+        r = cpu_sample(w64)
+        cpu = {"value": r["value"], "unit": UNIT, "cores": cores(), "kind": r["kind"],
+               "sample": ("one sample of cfg2 on the host cores: the sketch, one compression and 1 outer iteration "
+                          "(inner<=500) of " + ("the unmodified reference package (baseline/_ref), float64, "
+                                                "OpenBLAS on all threads" if r["kind"] == "reference" else
+                                                "the oracle's NumPy restatement, float64") +
+                          "; the 100-outer rate extrapolated from the measured parts"),
+               "detail": r}
+    if rank != 0:
+        if dist is not None:
+            dist.destroy_process_group()
+        return
+    line = {
+        "metric": metric_name(dtype), "value": head["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": head["ms_per_step"], "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64" if dtype == "fp64" else "f32",
+        "data": "synthetic (BASELINE cfg2 generator: U[0,1) G,F + 1% |N| noise, seed 1234; X resident in HBM)",
+        "config": {"workload": "cfg2", "n": w.n, "m": w.m, "p": w.p, "p_prime": w.nu, "q": w.q, "outer": outer,
+                   "inner_max_iter": w.inner, "grad_tol": 1e-4, "arithmetic": f"{dtype} mode",
+                   "parallelism": f"X row-sharded x{world} (sharded.py)" if world > 1 else "1 GPU",
+                   "l2": head["l2"]},
+        "e2e": head["e2e"], "gpu_launches": head["gpu_launches"], "clocks": head["clocks"],
+        "final_rre": head["final_rre"],
+        "roofline": roof, "solver": solver,
+        "fp32_mode": fp32, "cfg5_sharded": cfg5,
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+# ------------------------------------------------- row-sharded cfg5 block
+def run_cfg5(args, rank, world, local_rank, dist, comm):
     """BASELINE cfg 5 (n = m = 1e5, p = 16, p' = 26, q = 4, fp32, 40 GB X
     generated on the device) with X row-sharded across the ranks (sharded.py):
     total work is fixed as N grows ("strong").  One step = sharded RSI sketch
-    + compressed NeNMF (inner <= 500)."""
+    + compressed NeNMF (inner <= 500, 50 outer)."""
+    import os
     import socket
 
     import torch
-    import torch.distributed as dist
+    import torch.distributed as tdist
 
     import paper_1812_04315_b200 as nm
-    from paper_1812_04315_b200 import _lib, _ops, sharded, workloads
+    from paper_1812_04315_b200 import _lib, sharded, workloads
 
-    if "MASTER_ADDR" not in os.environ:  # N = 1 without torchrun
-        s = socket.socket()
-        s.bind(("127.0.0.1", 0))
-        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(s.getsockname()[1]), RANK="0", WORLD_SIZE="1")
-        s.close()
-    torch.cuda.set_device(local_rank)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    own_pg = False
+    if comm is None:
+        if "MASTER_ADDR" not in os.environ:
+            s = socket.socket()
+            s.bind(("127.0.0.1", 0))
+            os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(s.getsockname()[1]))
+            s.close()
+        tdist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", local_rank))
+        comm, own_pg = sharded.Comm(), True
     lib = _lib.load_library()
     Xl, r0, n, m, p, nu, q, inner, outer, G0, F0, sseed = workloads.device_shard(5, world, rank)
-    outer = args.outer or outer
-    comm = sharded.Comm()
+    outer = min(outer, args.outer or outer)
     init = nm.FactorPair(G=G0, F=F0, p=p)
     cfg = nm.OuterConfig(inner=nm.InnerSolverConfig(max_iter=inner), time_budget_seconds=0.0,
                          max_outer_iterations=outer, trace_every=outer)
     stream = torch.cuda.current_stream()
-    rsi_ms = []
+    rsi_ev = []
 
     def step():
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -462,83 +633,55 @@ def run_sharded(args, rank, world, local_rank):
         sk = sharded.subspace_iteration_pair_sharded(Xl, n, nu, q, sseed, comm=comm)
         b.record(stream)
         sharded.factorize_compressed_sharded(Xl, n, sk, init, cfg, comm=comm, return_device=True)
-        rsi_ms.append((a, b))
+        rsi_ev.append((a, b))
 
-    def timed(fn, k):
-        dist.barrier()
-        torch.cuda.synchronize()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        for _ in range(k):
-            fn()
-        b.record(stream)
-        dist.barrier()
-        torch.cuda.synchronize()
-        t = torch.tensor([a.elapsed_time(b)], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
-
-    for _ in range(args.warmup):
+    timer = Timer(torch, dist)
+    for _ in range(max(1, min(args.warmup, 2))):
         step()
-    rsi_ms.clear()
-    sampler = ClockSampler(local_rank)
-    sampler.start()
+    rsi_ev.clear()
     launches0 = lib.nenmf_launch_count()
-    ms = timed(step, args.steps)
-    launches = lib.nenmf_launch_count() - launches0
-    clocks = sampler.stop()
-    ms_step = ms / args.steps
-    rsi_step = statistics.median(a.elapsed_time(b) for a, b in rsi_ms)
-    # roofline: one RSI pass over this rank's prepared rows
-    hbm, _bf16, src = _peaks()
-    Xp = _ops.prepare_x(Xl, nu)
-    At = torch.randn((nu, m), device="cuda")
-    Bt = torch.randn((nu, Xl.shape[0]), device="cuda")
-    Yt = torch.empty((nu, Xl.shape[0]), device="cuda")
-    Zt = torch.empty((nu, m), device="cuda")
-    _ops.dual_pass_prepared(Xp, Xl.shape[0], m, At, Bt, Yt, Zt)
-    torch.cuda.synchronize()
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record(stream)
-    for _ in range(5):
-        _ops.dual_pass_prepared(Xp, Xl.shape[0], m, At, Bt, Yt, Zt)
-    b.record(stream)
-    torch.cuda.synchronize()
-    ms_pass = a.elapsed_time(b) / 5
-    pass_gbs = Xl.numel() * 4 / (ms_pass * 1e-3) / 1e9
-    if rank == 0:
-        line = {
-            "metric": "compressed-NeNMF outer iters/s (cfg5 n=m=1e5 p=16 p'=26 q=4, fp32, X row-sharded, sketch charged)",
-            "value": outer / (ms_step / 1e3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic, generated on device (cfg5: U(0,1) G, F from derive_seed(1234,0); X = G F)",
-            "config": {"workload": "cfg5", "n": n, "m": m, "p": p, "p_prime": nu, "q": q, "outer": outer,
-                       "inner_max_iter": inner, "parallelism": f"row-sharded x{world} (NCCL)",
-                       "l2": "inputs larger than L2 (X = 40 GB fp32)"},
-            "e2e": None, "e2e_note": "cfg5 X is generated on the device by definition (40 GB never on host)",
-            "gpu_launches": int(launches), "clocks": clocks, "rsi_ms_per_step": rsi_step,
-            "roofline": {"bound": "hbm", "kernel": "RSI X-pass over this rank's prepared rows (k_dual_bulk)",
-                         "achieved": pass_gbs, "peak": hbm, "unit": "GB/s", "frac": pass_gbs / hbm,
-                         "traffic": None, "peak_source": src, "ms_per_launch": ms_pass,
-                         "algorithmic_bytes_per_launch": Xl.numel() * 4},
-            "cpu_baseline": None,
-            "cpu_baseline_note": "the CPU oracle at cfg5 needs 80 GB of host RAM per copy of X (SURVEY 8(d)); "
-                                 "the cfg2 line carries the CPU baseline",
-        }
-        print(json.dumps(line), flush=True)
-    dist.destroy_process_group()
+    k = max(1, min(args.steps, 3))
+    ms = timer(step, k)
+    launches = (lib.nenmf_launch_count() - launches0) // k
+    ms_step = ms / k
+    rsi_step = statistics.median(a.elapsed_time(b) for a, b in rsi_ev)
+    hbm, _, _ = _peaks()
+    rsi_bytes = workloads.rsi_bytes(Xl.shape[0], m, q, 4) - Xl.shape[0] * m * 4  # 2q+1 sketch passes
+    out = {"metric": "compressed-NeNMF outer iters/s (cfg5 n=m=1e5 p=16 p'=26 q=4, fp32, 50 outer, X row-sharded, "
+                     "sketch charged)",
+           "value": outer / (ms_step / 1e3), "unit": UNIT, "ms_per_step": ms_step, "steps": k, "n_gpus": world,
+           "scaling": "strong", "gpu_launches": int(launches), "rsi_ms_per_step": rsi_step,
+           "rsi_sketch_gbs_per_rank": rsi_bytes / (rsi_step * 1e-3) / 1e9,
+           "rsi_sketch_frac_hbm": rsi_bytes / (rsi_step * 1e-3) / 1e9 / hbm,
+           "data": "synthetic, generated on the device (cfg5: U(0,1) G, F from derive_seed(1234,0); X = G F)",
+           "l2": "inputs larger than L2 (X = 40 GB fp32 in total)"}
+    del Xl
+    torch.cuda.empty_cache()
+    if own_pg:
+        tdist.destroy_process_group()
+    return out
 
 
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-execute under torch.distributed.run (rank 0 prints)
+        import socket
+
+        s = socket.socket()
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+        s.close()
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve()), *sys.argv[1:]]
+        sys.exit(subprocess.call(cmd))
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; launch one rank per GPU")
     if args.impl == "reference":
         run_reference(args, rank, world)
-    elif args.workload == "cfg5":
-        run_sharded(args, rank, world, local_rank)
     else:
         run_ours(args, rank, world, local_rank)
 

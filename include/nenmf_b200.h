@@ -167,6 +167,21 @@ int nenmf_pg_norm_sq(int dtype, const void* F, const void* g, int64_t count,
 /* sum of squares of `count` contiguous entries -> *out (matrix.py:177-179) */
 int nenmf_sumsq(int dtype, const void* M, int64_t count, double* out,
                 void* ws, size_t ws_bytes, void* stream);
+/* One read of M (rows x cols, leading dimension ld): *nonzero = 1 if some
+ * entry is nonzero (compression.py:109-117, X.any()), *negative = 1 if some
+ * entry is < 0 (the FactorPair sign check, factorize.py:44-48, for factors
+ * already on the device).  Flags are only raised (the caller zeroes them);
+ * either may be NULL.  No synchronisation. */
+int nenmf_scan_flags(int dtype, const void* M, int64_t rows, int64_t cols, int64_t ld,
+                     int* nonzero, int* negative, void* stream);
+/* dst (cols x rows, contiguous) = src (rows x cols, leading dimension ld)^T:
+ * an n x p factor G brought into the p x n panel layout of the solver
+ * (factorize.py:92,109 transpose G / F for the half-steps). */
+int nenmf_transpose(int dtype, const void* src, int64_t rows, int64_t cols, int64_t ld, void* dst,
+                    void* stream);
+/* cudaMemsetAsync(ptr, 0, bytes) on `stream`: zeroes status words and flags
+ * without a kernel launch. */
+int nenmf_zero(void* ptr, size_t bytes, void* stream);
 
 /* ||X - G F||_F^2 -> *out, X (n x m, ld ldx), G passed as Gt (p x n),
  * F (p x m) (factorize.py:139; tracing.py:45-57) */
@@ -274,6 +289,11 @@ int nenmf_panel_trsm(int dtype, const void* Pin_t, int64_t rows, int64_t k, cons
 size_t nenmf_prepared_x_bytes(int dtype, int64_t n, int64_t m, int64_t k);
 int nenmf_prepare_x(int dtype, const void* X, int64_t n, int64_t m, int64_t ldx, int64_t k,
                     void* Xp, void* stream);
+/* nenmf_prepare_x that also raises *nonzero (zeroed by the caller) when X has
+ * a nonzero entry: subspace_iteration_pair's X != 0 check (compression.py:
+ * 109-117) folded into the one read of X the preparation makes. */
+int nenmf_prepare_x_checked(int dtype, const void* X, int64_t n, int64_t m, int64_t ldx, int64_t k,
+                            void* Xp, int* nonzero, void* stream);
 size_t nenmf_dual_pass_prepared_workspace_bytes(int dtype, int64_t n, int64_t m, int64_t k);
 int nenmf_dual_pass_prepared(int dtype, const void* Xp, int64_t n, int64_t m,
                              const void* At, const void* Bt, int64_t k, void* Yt, void* Zt,

@@ -46,6 +46,9 @@ _SIGS = {
     "nenmf_reduce_workspace_bytes": (_sz, [_i64]),
     "nenmf_pg_norm_sq": (_i32, [_i32, _vp, _vp, _i64, _vp, _vp, _sz, _vp]),
     "nenmf_sumsq": (_i32, [_i32, _vp, _i64, _vp, _vp, _sz, _vp]),
+    "nenmf_scan_flags": (_i32, [_i32, _vp, _i64, _i64, _i64, _vp, _vp, _vp]),
+    "nenmf_transpose": (_i32, [_i32, _vp, _i64, _i64, _i64, _vp, _vp]),
+    "nenmf_zero": (_i32, [_vp, _sz, _vp]),
     "nenmf_convert_f64": (_i32, [_i32, _vp, _i64, _vp, _vp, _vp]),
     "nenmf_uniform_draws": (_i32, [C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, _i64, _vp, _vp, _vp]),
     "nenmf_residual_sumsq_workspace_bytes": (_sz, [_i32, _i64, _i64, _i64]),
@@ -71,6 +74,7 @@ _SIGS = {
     "nenmf_debug_xpass_ms": (_i32, [C.POINTER(C.c_double)]),
     "nenmf_prepared_x_bytes": (_sz, [_i32, _i64, _i64, _i64]),
     "nenmf_prepare_x": (_i32, [_i32, _vp, _i64, _i64, _i64, _i64, _vp, _vp]),
+    "nenmf_prepare_x_checked": (_i32, [_i32, _vp, _i64, _i64, _i64, _i64, _vp, _vp, _vp]),
     "nenmf_dual_pass_prepared_workspace_bytes": (_sz, [_i32, _i64, _i64, _i64]),
     "nenmf_dual_pass_prepared": (_i32, [_i32, _vp, _i64, _i64, _vp, _vp, _i64, _vp, _vp, _vp, _sz, _vp]),
     "nenmf_rsi_prepared_workspace_bytes": (_sz, [_i32, _i64, _i64, _i64]),
@@ -185,9 +189,21 @@ STATUS_FIELDS = np.dtype([("code", "<i4"), ("iteration", "<i4"), ("inner_iters",
 assert STATUS_FIELDS.itemsize == STATUS_BYTES
 
 
-def new_status(count: int = 1):
+def zeros(shape, dtype):
+    """A zeroed CUDA tensor by cudaMemsetAsync (nenmf_zero): no fill kernel."""
     torch = torch_mod()
-    return torch.zeros(count * STATUS_BYTES, dtype=torch.uint8, device="cuda")
+    t = torch.empty(shape, dtype=dtype, device="cuda")
+    check(load_library().nenmf_zero(t.data_ptr(), t.numel() * t.element_size(), stream_handle()), "zero")
+    return t
+
+
+def zero_(t):
+    check(load_library().nenmf_zero(t.data_ptr(), t.numel() * t.element_size(), stream_handle()), "zero")
+    return t
+
+
+def new_status(count: int = 1):
+    return zeros(count * STATUS_BYTES, torch_mod().uint8)
 
 
 def status_ptr(buf, index: int = 0) -> int:

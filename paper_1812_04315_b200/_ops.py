@@ -154,9 +154,10 @@ def orthonormalize(Pt, status) -> None:
     _lib.check(rc, "orthonormalize")
 
 
-def prepare_x(X, k: int):
+def prepare_x(X, k: int, nonzero_ptr: int | None = None):
     """Tile-major bf16 hi/lo copy of an FP32 X for the tensor-core passes
-    (nenmf_prepare_x), or None when the dtype/shape has no prepared form."""
+    (nenmf_prepare_x), or None when the dtype/shape has no prepared form.
+    ``nonzero_ptr`` (device int*, zeroed): raised when X has a nonzero entry."""
     lib, torch = _lib.require_device()
     code = _lib.code_of(_dt(X))
     n, m = X.shape
@@ -164,9 +165,35 @@ def prepare_x(X, k: int):
     if nbytes == 0:
         return None
     Xp = torch.empty(nbytes, dtype=torch.uint8, device=X.device)
-    rc = lib.nenmf_prepare_x(code, X.data_ptr(), n, m, X.stride(0), int(k), Xp.data_ptr(), _lib.stream_handle())
+    rc = lib.nenmf_prepare_x_checked(code, X.data_ptr(), n, m, X.stride(0), int(k), Xp.data_ptr(), nonzero_ptr,
+                                     _lib.stream_handle())
     _lib.check(rc, "prepare_x")
     return Xp
+
+
+def transpose(M):
+    """A fresh contiguous M^T (nenmf_transpose; M row-major with unit column stride)."""
+    lib, torch = _lib.require_device()
+    rows, cols = M.shape
+    assert M.stride(1) == 1
+    out = torch.empty((cols, rows), dtype=M.dtype, device=M.device)
+    rc = lib.nenmf_transpose(_lib.code_of(_dt(M)), M.data_ptr(), rows, cols, M.stride(0), out.data_ptr(),
+                             _lib.stream_handle())
+    _lib.check(rc, "transpose")
+    return out
+
+
+def scan_flags(M, nonzero_ptr: int | None = None, negative_ptr: int | None = None) -> None:
+    """nenmf_scan_flags: raise the device int flags when M has a nonzero /
+    a negative entry (asynchronous)."""
+    lib, _ = _lib.require_device()
+    rows, cols = (M.shape[0], M.shape[1]) if M.dim() == 2 else (1, M.numel())
+    ld = M.stride(0) if M.dim() == 2 else cols
+    if M.dim() == 2 and M.stride(1) != 1:  # a transposed view: scan the underlying rows
+        rows, cols, ld = cols, rows, M.stride(1)
+    rc = lib.nenmf_scan_flags(_lib.code_of(_dt(M)), M.data_ptr(), rows, cols, ld, nonzero_ptr, negative_ptr,
+                              _lib.stream_handle())
+    _lib.check(rc, "scan_flags")
 
 
 def dual_pass_prepared(Xp, n: int, m: int, At, Bt, Yt, Zt) -> None:

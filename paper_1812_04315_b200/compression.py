@@ -128,18 +128,22 @@ def _numpy_ziggurat_tables():
     return tabs
 
 
-def sketch_draws_device(n: int, m: int, nu: int, seed: int, dtype: str):
+def sketch_draws_device(n: int, m: int, nu: int, seed: int, dtype: str, ok_ptr: int | None = None):
     """The draws of ``sketch_draws`` generated on the device (nenmf_sketch_draws,
     bit-identical to NumPy): (Omega_L^T (nu x m), Omega_R (nu x n), ok flag),
-    or None when NumPy's ziggurat tables are not available."""
+    or None when NumPy's ziggurat tables are not available.  ``ok_ptr``: a
+    device int* (e.g. a status word) that receives the stitching flag instead
+    of a fresh tensor (the returned flag is then None)."""
     st = np.random.PCG64(check_seed(seed)).state["state"]
-    return normal_draws_device(int(st["state"]), int(st["inc"]), n, m, nu, dtype)
+    return normal_draws_device(int(st["state"]), int(st["inc"]), n, m, nu, dtype, ok_ptr=ok_ptr)
 
 
-def normal_draws_device(s: int, inc: int, n: int, m: int, nu: int, dtype: str):
+def normal_draws_device(s: int, inc: int, n: int, m: int, nu: int, dtype: str, ok_ptr: int | None = None):
     """NumPy's standard_normal stream from PCG64 state ``s`` / increment ``inc``
     on the device: m*nu draws into (nu x m) transposed, then nu*n into (nu x n)
-    (the Omega_L^T / Omega_R layout of sketch_draws); see sketch_draws_device."""
+    (the Omega_L^T / Omega_R layout of sketch_draws); see sketch_draws_device.
+    Asynchronous: the ziggurat tail draws use the device restatement of the C
+    library's log1p (csrc/glibc_log1p.cuh), so no value is fixed up on the host."""
     lib, torch = _lib.require_device()
     tabs = _numpy_ziggurat_tables()
     if tabs is None:
@@ -152,60 +156,61 @@ def normal_draws_device(s: int, inc: int, n: int, m: int, nu: int, dtype: str):
     tdt = _lib.torch_dtype(dtype)
     olt = torch.empty((nu, m), dtype=tdt, device="cuda")
     orr = torch.empty((nu, n), dtype=tdt, device="cuda")
-    ok = torch.zeros(1, dtype=torch.int32, device="cuda")
+    ok = None
+    if ok_ptr is None:
+        ok = _lib.zeros(1, torch.int32)
+        ok_ptr = ok.data_ptr()
     cap = int(lib.nenmf_sketch_tail_capacity(n, m, nu))
-    tails = torch.empty(1 + 2 * cap, dtype=torch.int64, device="cuda")
-    ws = _lib.workspace(lib.nenmf_sketch_draws_workspace_bytes(n, m, nu))
+    ws = _lib.workspace(lib.nenmf_sketch_draws_workspace_bytes(n, m, nu) + 8 * (1 + 2 * cap) + 256)
+    # the tail list (diagnostics only) lives at the end of the workspace
+    off = (ws.numel() - 8 * (1 + 2 * cap)) // 256 * 256
     rc = lib.nenmf_sketch_draws(_lib.code_of(dtype), dt.data_ptr(), s & M64, s >> 64, inc & M64, inc >> 64, n, m,
-                                nu, olt.data_ptr(), orr.data_ptr(), ok.data_ptr(), tails.data_ptr(), ws.data_ptr(),
-                                ws.numel(), _lib.stream_handle())
+                                nu, olt.data_ptr(), orr.data_ptr(), ok_ptr, ws.data_ptr() + off, ws.data_ptr(),
+                                off, _lib.stream_handle())
     _lib.check(rc, "sketch_draws")
-    # the tail draws with the C library's log1p (compression.py:131-132 -> NumPy's
-    # random_standard_normal): a few hundred values, rewritten in place
-    cnt = int(tails[0].item())
-    if 0 < cnt <= cap:
-        rec = tails[1:1 + 2 * cnt].cpu().numpy().view(np.uint64).reshape(cnt, 2)
-        idx = rec[:, 0].astype(np.int64)
-        u = (rec[:, 1] >> np.uint64(1)).astype(np.float64) * (1.0 / 9007199254740992.0)
-        neg = (rec[:, 1] & np.uint64(1)).astype(bool)
-        xx = np.array([-_ZIG_INV_R * math.log1p(-v) for v in u])
-        val = np.where(neg, -(_ZIG_R + xx), _ZIG_R + xx)
-        nl = m * nu
-        isl = idx < nl
-        tv = torch.from_numpy(val).to(device="cuda", dtype=tdt)
-        if isl.any():
-            il = torch.from_numpy(idx[isl]).cuda()
-            olt.view(-1).index_put_(((il % nu) * m + il // nu,), tv[torch.from_numpy(isl).cuda()])
-        if (~isl).any():
-            ir = torch.from_numpy(idx[~isl] - nl).cuda()
-            orr.view(-1).index_put_((ir,), tv[torch.from_numpy(~isl).cuda()])
     return olt, orr, ok
 
 
-def rsi_device(Xd, nu: int, q: int, seed: int, prepared=None, draws=None, power: bool = False):
+# status word 1 of a sketch's status buffer carries two device flags, read
+# with the sketch's own status in ONE synchronisation at its end
+_OK_OFF, _NZ_OFF = 0, 4
+
+
+def rsi_device(Xd, nu: int, q: int, seed: int, prepared=None, draws=None, power: bool = False, status=None,
+               check: bool = True):
     """Device RSI on a resident X (CUDA tensor).  Returns (L, Rt, status)
     tensors; Rt is R transposed (nu x m).  ``prepared`` is an optional
     ``_ops.prepare_x`` copy of Xd (made once, reused by the compression pass).
     The Gaussian draws are made on the device (bit-identical to NumPy's
-    stream); in the never-observed case that the device stream cannot be
-    stitched, they are redrawn on the host and the sketch recomputed."""
+    stream) with no synchronisation; ``status`` (2 words, zeroed) receives the
+    sketch status in word 0 and the draws' stitching flag in word 1.  With
+    ``check`` the status is read once at the end, and in the never-observed
+    case that the device stream could not be stitched the draws are redone on
+    the host and the sketch recomputed."""
     _, torch = _lib.require_device()
     n, m = Xd.shape
     dtype = "fp64" if Xd.dtype == torch.float64 else "fp32"
-    dev = draws if draws is not None else sketch_draws_device(n, m, nu, seed, dtype)
+    if status is None:
+        status = _lib.new_status(2)
     L = torch.empty((nu, n), dtype=Xd.dtype, device="cuda")
     Rt = torch.empty((nu, m), dtype=Xd.dtype, device="cuda")
-    status = _lib.new_status()
     run = _ops.power_iteration if power else _ops.rsi  # compression.py:144-176 / :120-141
+    if draws is not None:
+        dev, own = draws, False
+    else:
+        dev, own = sketch_draws_device(n, m, nu, seed, dtype, ok_ptr=_lib.status_ptr(status, 1) + _OK_OFF), True
     if dev is not None:
         om_lt, om_r, ok = dev
         run(Xd, om_lt, om_r, q, L, Rt, status, Xp=prepared)
-        if bool(ok.item()):
+        if not check:
+            return L, Rt, status
+        stitched = int(_lib.read_status(status)[1]["code"]) == 1 if own else bool(ok.item())
+        if stitched:
             return L, Rt, status
     omega_l, omega_r = sketch_draws(n, m, nu, seed)
     om_lt = _lib.to_device(np.ascontiguousarray(omega_l.T), dtype)
     om_r = _lib.to_device(omega_r, dtype)
-    status.zero_()
+    _lib.zero_(status[:_lib.STATUS_BYTES])
     run(Xd, om_lt, om_r, q, L, Rt, status, Xp=prepared)
     return L, Rt, status
 
@@ -230,7 +235,9 @@ def _is_device_tensor(x) -> bool:
 def subspace_iteration_pair(X, nu: int, q: int, seed: int, *, dtype: str = "fp64") -> SketchPair:
     """Randomized subspace iteration with a QR after every product
     (compression.py:120-141), on the GPU.  Returns NumPy L = Q_col^T and
-    R = Q_row like the reference; the device copies are cached on the pair."""
+    R = Q_row like the reference; the device copies are cached on the pair.
+    Extension: for X given as a CUDA tensor the pair holds CUDA tensors (L,
+    and R as a view of R^T) and the sketch never leaves the device."""
     return _iterated_pair(X, nu, q, seed, dtype, SUBSPACE_ITERATION)
 
 
@@ -245,35 +252,60 @@ def power_iteration_pair(X, nu: int, q: int, seed: int, *, dtype: str = "fp64") 
 
 
 def _iterated_pair(X, nu: int, q: int, seed: int, dtype: str, scheme: str) -> SketchPair:
-    if _is_device_tensor(X):
-        Xd = X
-        dtype = "fp64" if str(X.dtype).endswith("float64") else "fp32"
-        n, m = X.shape
-        nonzero = bool((X != 0).any().item())
-    else:
+    power = scheme == POWER_ITERATION
+    what = "power iteration" if power else "subspace iteration"
+    if not _is_device_tensor(X):
         Xh = as_matrix(X, "X")
         n, m = Xh.shape
-        nonzero = bool(Xh.any())
-        Xd = None
-    _check_iteration_inputs(n, m, nu, q, nonzero)
-    _lib.require_device()
-    on_device = Xd is not None
-    if Xd is None:
+        _check_iteration_inputs(n, m, nu, q, bool(Xh.any()))
+        _lib.require_device()
         Xd = _lib.to_device(Xh, dtype)
-    # a device-resident X is prepared once here and the copy is kept on the
-    # pair, so factorize_compressed's compression pass reuses it
-    Xp = _ops.prepare_x(Xd, nu) if on_device else None
-    power = scheme == POWER_ITERATION
-    L, Rt, status = rsi_device(Xd, nu, q, seed, prepared=Xp, power=power)
-    st = _lib.read_status(status)[0]
-    if st["code"] != 0:
-        raise_for_status(int(st["code"]), int(st["iteration"]), "power iteration" if power else "subspace iteration")
-    pair = SketchPair(L=_lib.to_host(L), R=np.ascontiguousarray(_lib.to_host(Rt).T), nu=nu,
-                      scheme=scheme, q=q, seed=seed)
+        L, Rt, status = rsi_device(Xd, nu, q, seed, power=power)
+        st = _lib.read_status(status)[0]
+        if st["code"] != 0:
+            raise_for_status(int(st["code"]), int(st["iteration"]), what)
+        pair = SketchPair(L=_lib.to_host(L), R=np.ascontiguousarray(_lib.to_host(Rt).T), nu=nu,
+                          scheme=scheme, q=q, seed=seed)
+        pair.device[dtype] = (L, Rt)
+        return pair
+    # device-resident X (extension): no host round trip inside the sketch.  The
+    # X != 0 check (compression.py:116-117) is a device flag raised by the one
+    # read of X that prepares it (FP32) or by a flag scan (FP64), read together
+    # with the sketch status in the single synchronisation at the end; the
+    # host-side checks keep the reference's order before any launch.
+    Xd = X
+    dtype = "fp64" if str(X.dtype).endswith("float64") else "fp32"
+    n, m = X.shape
+    _check_iteration_inputs(n, m, nu, q, True)
+    _lib.require_device()
+    status = _lib.new_status(2)
+    nz_ptr = _lib.status_ptr(status, 1) + _NZ_OFF
+    Xp = _ops.prepare_x(Xd, nu, nonzero_ptr=nz_ptr)
+    if Xp is None:
+        _ops.scan_flags(Xd, nonzero_ptr=nz_ptr)
+    L, Rt, status = rsi_device(Xd, nu, q, seed, prepared=Xp, power=power, status=status, check=False)
+    sts = _lib.read_status(status)
+    if int(sts[1]["iteration"]) == 0:
+        raise ZeroMatrixError("cannot sketch the zero matrix")
+    if int(sts[1]["code"]) != 1:  # device draws not stitched (never observed): host draws, same sketch
+        _lib.zero_(status[:_lib.STATUS_BYTES])
+        L, Rt, status = rsi_device(Xd, nu, q, seed, prepared=Xp, power=power, status=status,
+                                   draws=_host_draws(n, m, nu, seed, dtype))
+        sts = _lib.read_status(status)
+    if sts[0]["code"] != 0:
+        raise_for_status(int(sts[0]["code"]), int(sts[0]["iteration"]), what)
+    # the pair keeps device tensors (L: nu x n, R: an m x nu view of R^T)
+    pair = SketchPair(L=L, R=Rt.t(), nu=nu, scheme=scheme, q=q, seed=seed)
     pair.device[dtype] = (L, Rt)
     if Xp is not None:
         pair.device["prepared"] = (_x_key(Xd), Xp)
     return pair
+
+
+def _host_draws(n, m, nu, seed, dtype):
+    omega_l, omega_r = sketch_draws(n, m, nu, seed)
+    return (_lib.to_device(np.ascontiguousarray(omega_l.T), dtype), _lib.to_device(omega_r, dtype),
+            _lib.torch_mod().ones(1, dtype=_lib.torch_mod().int32, device="cuda"))
 
 
 def sketch_on_device(sketch: SketchPair, dtype: str):
@@ -313,12 +345,16 @@ def compress_problem(X, sketch: SketchPair, *, dtype: str = "fp64") -> Compresse
     return CompressedProblem(X_L=_lib.to_host(XL), X_R=np.ascontiguousarray(_lib.to_host(XRt).T))
 
 
+def _host(M):
+    return _lib.to_host(M) if _is_device_tensor(M) else M
+
+
 def save_sketch(sketch: SketchPair, directory) -> None:
     """L and R as NMFB matrices plus a JSON provenance header (compression.py:191-198)."""
     directory = Path(directory)
     directory.mkdir(parents=True, exist_ok=True)
-    write_nmfb(directory / "L.nmfb", sketch.L)
-    write_nmfb(directory / "R.nmfb", sketch.R)
+    write_nmfb(directory / "L.nmfb", _host(sketch.L))
+    write_nmfb(directory / "R.nmfb", _host(sketch.R))
     meta = {"nu": sketch.nu, "scheme": sketch.scheme, "q": sketch.q, "seed": sketch.seed}
     (directory / "sketch.json").write_text(json.dumps(meta, sort_keys=True, indent=2) + "\n")
 

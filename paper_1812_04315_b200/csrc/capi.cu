@@ -213,6 +213,26 @@ int nenmf_sumsq(int dtype, const void* Mx, int64_t count, double* out, void* ws,
   return NENMF_DISPATCH(dtype, [&] { return sumsq<scalar_t>(a, C<scalar_t>(Mx), nullptr, count, out, S(stream)); });
 }
 
+int nenmf_scan_flags(int dtype, const void* Mx, int64_t rows, int64_t cols, int64_t ld, int* nonzero, int* negative,
+                     void* stream) {
+  if (rows > 0 && cols > 0 && Mx == nullptr) return NENMF_ERR_VALUE;
+  return NENMF_DISPATCH(dtype, [&] {
+    return scan_flags<scalar_t>(C<scalar_t>(Mx), rows, cols, ld, nonzero, negative, S(stream));
+  });
+}
+
+int nenmf_transpose(int dtype, const void* src, int64_t rows, int64_t cols, int64_t ld, void* dst, void* stream) {
+  if (rows > 0 && cols > 0 && (src == nullptr || dst == nullptr)) return NENMF_ERR_VALUE;
+  return NENMF_DISPATCH(dtype, [&] { return transpose<scalar_t>(C<scalar_t>(src), rows, cols, ld, M<scalar_t>(dst), S(stream)); });
+}
+
+int nenmf_zero(void* ptr, size_t bytes, void* stream) {
+  if (bytes == 0) return NENMF_OK;
+  if (ptr == nullptr) return NENMF_ERR_VALUE;
+  NENMF_CUDA_TRY(cudaMemsetAsync(ptr, 0, bytes, S(stream)));
+  return NENMF_OK;
+}
+
 size_t nenmf_residual_sumsq_workspace_bytes(int dtype, int64_t n, int64_t m, int64_t p) {
   Arena a(nullptr, 0);
   NENMF_DISPATCH(dtype, [&] {
@@ -351,9 +371,14 @@ size_t nenmf_prepared_x_bytes(int dtype, int64_t n, int64_t m, int64_t k) {
 
 int nenmf_prepare_x(int dtype, const void* X, int64_t n, int64_t m, int64_t ldx, int64_t k, void* Xp,
                     void* stream) {
+  return nenmf_prepare_x_checked(dtype, X, n, m, ldx, k, Xp, nullptr, stream);
+}
+
+int nenmf_prepare_x_checked(int dtype, const void* X, int64_t n, int64_t m, int64_t ldx, int64_t k, void* Xp,
+                            int* nonzero, void* stream) {
   if (nenmf_prepared_x_bytes(dtype, n, m, k) == 0) return NENMF_ERR_UNSUPPORTED;
   if (X == nullptr || Xp == nullptr || ldx < m) return NENMF_ERR_VALUE;
-  return tc_presplit(static_cast<const float*>(X), n, m, ldx, static_cast<uint8_t*>(Xp), S(stream));
+  return tc_presplit(static_cast<const float*>(X), n, m, ldx, static_cast<uint8_t*>(Xp), S(stream), nonzero);
 }
 
 size_t nenmf_dual_pass_prepared_workspace_bytes(int dtype, int64_t n, int64_t m, int64_t k) {

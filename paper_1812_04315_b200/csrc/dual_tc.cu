@@ -170,8 +170,11 @@ __device__ __forceinline__ void unit_bounds(const Units& U, int u, int& rt0, int
 // X (n x m fp32, leading dimension ldx) -> tile-major pre-split bf16 hi/lo.
 // One thread per (tile, row, 8-column chunk): reads 32 B, writes 16 B of hi
 // and 16 B of lo at the swizzled position; padding outside X is zero.
+// With `nonzero` set, also raises *nonzero when any element of X is nonzero
+// (the X != 0 check of compression.py:109-117, folded into this read of X).
 __global__ void k_presplit_x(const float* __restrict__ X, int64_t n, int64_t m, int64_t ldx, int n_ct, int64_t total,
-                             uint8_t* __restrict__ Xs) {
+                             uint8_t* __restrict__ Xs, int* __restrict__ nonzero) {
+  bool nz = false;
   const bool vec = ((m | ldx) & 3) == 0 && (reinterpret_cast<uintptr_t>(X) & 15) == 0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     const int c8 = (int)(i & 15);
@@ -188,6 +191,8 @@ __global__ void k_presplit_x(const float* __restrict__ X, int64_t n, int64_t m, 
 #pragma unroll
       for (int j = 0; j < 8; ++j) v[j] = (gr < n && gc + j < m) ? X[gr * ldx + gc + j] : 0.f;
     }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) nz |= v[j] != 0.f;
     uint32_t hw[4], lw[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
@@ -202,6 +207,7 @@ __global__ void k_presplit_x(const float* __restrict__ X, int64_t n, int64_t m, 
     *reinterpret_cast<uint4*>(Xs + off) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
     *reinterpret_cast<uint4*>(Xs + off + 2 * SUB_BYTES) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
   }
+  if (nonzero != nullptr && __any_sync(0xffffffffu, nz) && (threadIdx.x & 31) == 0) *nonzero = 1;
 }
 
 // Skinny operand S (k x len fp32 row-major) -> per 128-wide K tile:
@@ -519,13 +525,14 @@ size_t tc_presplit_bytes(int64_t n, int64_t m) {
   return (size_t)cdiv(n, tc::TILE) * (size_t)cdiv(m, tc::TILE) * tc::XTILE_BYTES;
 }
 
-int tc_presplit(const float* X, int64_t n, int64_t m, int64_t ldx, uint8_t* Xs, cudaStream_t s) {
+int tc_presplit(const float* X, int64_t n, int64_t m, int64_t ldx, uint8_t* Xs, cudaStream_t s, int* nonzero) {
   using namespace tc;
   const int n_ct = (int)cdiv(m, TILE);
   const int64_t total = cdiv(n, TILE) * n_ct * (int64_t)TILE * 16;
   int sms = sm_count();
   if (sms <= 0) sms = 148;
-  k_presplit_x<<<(unsigned)imin(cdiv(total, 256), (int64_t)sms * 8), 256, 0, s>>>(X, n, m, ldx, n_ct, total, Xs);
+  k_presplit_x<<<(unsigned)imin(cdiv(total, 256), (int64_t)sms * 8), 256, 0, s>>>(X, n, m, ldx, n_ct, total, Xs,
+                                                                                      nonzero);
   NENMF_LAUNCH_CHECK();
   return NENMF_OK;
 }

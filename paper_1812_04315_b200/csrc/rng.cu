@@ -10,9 +10,9 @@
 //   idx == 0: tail loop on two next_double() per attempt
 //   else    : accept if (fi[idx-1]-fi[idx]) u + fi[idx] < exp(-x^2/2), else redraw
 // The three 256-entry tables are NumPy's own (read from the installed NumPy by
-// the host layer and passed in).  exp/log1p are CUDA's double versions in the
-// accept/reject tests of the ~0.7 % slow-path draws; they agree with glibc's
-// decisions except within an ulp of the boundary (tests: bit-identical).
+// the host layer and passed in).  The wedge test of the ~0.7 % slow-path
+// draws uses CUDA's exp, which agrees with glibc's decisions except within an
+// ulp of the boundary (tests: bit-identical); the tail uses glibc_log1p.
 //
 // Parallelisation of the variable-length stream: the raw positions are cut
 // into chunks of S.  k_zig_scan walks every chunk from its first position
@@ -23,11 +23,13 @@
 // that meet stay merged), so only entry points off that walk need a re-walk.
 // k_zig_emit walks each chunk again from its true entry and writes draw i to
 // Omega_L^T (i < m nu, transposed) or Omega_R; draws from the ziggurat tail
-// (~1 in 4000) are also listed with their uniform, and the host rewrites them
-// with the C library's log1p (CUDA's log1p can differ from it by an ulp).
+// (~1 in 4000) use glibc_log1p below, the C library's own log1p restated
+// operation for operation, so their values (and the accept tests that use
+// them) are NumPy's exactly; no host fix-up and no synchronisation.
 // A chunk whose re-walk does not merge within 64 positions (never observed)
 // sets *ok = 0 and the host redraws with NumPy.
 #include "common.cuh"
+#include "glibc_log1p.cuh"
 
 namespace nenmf {
 
@@ -72,8 +74,7 @@ struct Stream {
 
 // one draw starting at the stream's current position; `used` = raw values consumed.
 // A draw from the tail (idx 0) reports its accepted 53-bit uniform and sign in
-// *tail (u53 << 1 | negative), else *tail = 0: the host recomputes those
-// values with the C library's log1p, which CUDA's may differ from by an ulp.
+// *tail (u53 << 1 | negative), else *tail = 0 (diagnostics: the tail list).
 __device__ __forceinline__ double draw(Stream& g, const Tables& T, int& used, uint64_t* tail = nullptr) {
   used = 0;
   if (tail != nullptr) *tail = 0;
@@ -90,19 +91,21 @@ __device__ __forceinline__ double draw(Stream& g, const Tables& T, int& used, ui
     if (idx == 0) {
       for (;;) {
         const uint64_t u53 = g.next() >> 11;
-        const double xx = -ZINVR * log1p(-((double)u53 * (1.0 / 9007199254740992.0)));
-        const double yy = -log1p(-g.next_double());
+        const double xx = __dmul_rn(-ZINVR, glibc_log1p(-((double)u53 * (1.0 / 9007199254740992.0))));
+        const double yy = -glibc_log1p(-g.next_double());
         used += 2;
-        if (yy + yy > xx * xx) {
+        if (__dadd_rn(yy, yy) > __dmul_rn(xx, xx)) {
           const bool neg = (rabs >> 8) & 1;
           if (tail != nullptr) *tail = (u53 << 1) | (neg ? 1ull : 0ull) | (1ull << 63);
-          return neg ? -(ZR + xx) : ZR + xx;
+          return neg ? -__dadd_rn(ZR, xx) : __dadd_rn(ZR, xx);
         }
       }
     } else {
       const double u = g.next_double();
       ++used;
-      if ((T.fi[idx - 1] - T.fi[idx]) * u + T.fi[idx] < exp(-0.5 * x * x)) return x;
+      if (__dadd_rn(__dmul_rn(__dsub_rn(T.fi[idx - 1], T.fi[idx]), u), T.fi[idx]) <
+          exp(__dmul_rn(__dmul_rn(-0.5, x), x)))
+        return x;
     }
   }
 }

@@ -32,7 +32,8 @@ int panel_trsm(const T* Pin_t, int64_t rows, int64_t k, const double* R, const i
 // FP32 tensor-core pass over a pre-split X (dual_tc.cu)
 bool tc_pass_eligible(int64_t n, int64_t m, int64_t k);
 size_t tc_presplit_bytes(int64_t n, int64_t m);
-int tc_presplit(const float* X, int64_t n, int64_t m, int64_t ldx, uint8_t* Xs, cudaStream_t s);
+int tc_presplit(const float* X, int64_t n, int64_t m, int64_t ldx, uint8_t* Xs, cudaStream_t s,
+                int* nonzero = nullptr);
 int dual_pass_tc_pre(Arena& ws, const uint8_t* Xs, int64_t n, int64_t m, const float* At, const float* Bt,
                      int64_t k, float* Yt, float* Zt, cudaStream_t s);
 

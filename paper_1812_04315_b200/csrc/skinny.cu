@@ -1248,6 +1248,69 @@ int sumsq(Arena& ws, const T* M, const T* g, int64_t count, double* out, cudaStr
   return NENMF_OK;
 }
 
+// ------------------------------------------------------------ scan flags ----
+// One read of a (rows x cols, leading dimension ld) matrix: *nonzero = 1 when
+// some element is nonzero (compression.py:109-117's X.any()), *negative = 1
+// when some element is < 0 (FactorPair's sign check, factorize.py:44-48; NaN
+// is not negative there either).  Either flag may be null; they are only
+// ever raised, so the caller zeroes them.
+template <typename T>
+__global__ void __launch_bounds__(RED_THREADS)
+k_scan_flags(const T* __restrict__ M, int64_t rows, int64_t cols, int64_t ld, int* __restrict__ nonzero,
+             int* __restrict__ negative) {
+  bool nz = false, ng = false;
+  const int64_t count = rows * cols;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += stride) {
+    const int64_t r = ld == cols ? 0 : i / cols;
+    const T v = ld == cols ? M[i] : M[r * ld + (i - r * cols)];
+    nz |= v != T(0);
+    ng |= v < T(0);
+  }
+  const bool lane0 = (threadIdx.x & 31) == 0;
+  if (nonzero != nullptr && __any_sync(0xffffffffu, nz) && lane0) *nonzero = 1;
+  if (negative != nullptr && __any_sync(0xffffffffu, ng) && lane0) *negative = 1;
+}
+
+template <typename T>
+int scan_flags(const T* M, int64_t rows, int64_t cols, int64_t ld, int* nonzero, int* negative, cudaStream_t st) {
+  if (rows < 0 || cols < 0 || (rows > 0 && ld < cols)) return NENMF_ERR_DIM;
+  if (rows * cols == 0) return NENMF_OK;
+  k_scan_flags<T><<<red_grid(rows * cols), RED_THREADS, 0, st>>>(M, rows, cols, ld, nonzero, negative);
+  NENMF_LAUNCH_CHECK();
+  return NENMF_OK;
+}
+
+// ------------------------------------------------------------- transpose ----
+// dst (cols x rows) = src (rows x cols, leading dimension ld)^T through 32 x 32
+// shared-memory tiles (both sides coalesced).  Used to bring factors given as
+// n x p into the library's p x n panel layout without a host round trip.
+template <typename T>
+__global__ void k_transpose(const T* __restrict__ src, int64_t rows, int64_t cols, int64_t ld, T* __restrict__ dst) {
+  __shared__ T tile[32][33];
+  const int64_t r0 = (int64_t)blockIdx.y * 32, c0 = (int64_t)blockIdx.x * 32;
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int64_t r = r0 + i, c = c0 + threadIdx.x;
+    if (r < rows && c < cols) tile[i][threadIdx.x] = src[r * ld + c];
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int64_t c = c0 + i, r = r0 + threadIdx.x;
+    if (r < rows && c < cols) dst[c * rows + r] = tile[threadIdx.x][i];
+  }
+}
+
+template <typename T>
+int transpose(const T* src, int64_t rows, int64_t cols, int64_t ld, T* dst, cudaStream_t st) {
+  if (rows < 0 || cols < 0 || (rows > 0 && ld < cols)) return NENMF_ERR_DIM;
+  if (rows * cols == 0) return NENMF_OK;
+  if (cdiv(rows, 32) > 65535) return NENMF_ERR_UNSUPPORTED;
+  k_transpose<T><<<dim3((unsigned)cdiv(cols, 32), (unsigned)cdiv(rows, 32)), dim3(32, 8), 0, st>>>(src, rows, cols,
+                                                                                                   ld, dst);
+  NENMF_LAUNCH_CHECK();
+  return NENMF_OK;
+}
+
 // ------------------------------------------------------------------ wfv ----
 template <typename T>
 __global__ void k_wfv(const T* __restrict__ W, int p, const T* __restrict__ F, int64_t c,
@@ -1284,7 +1347,9 @@ int wf_minus_v(const T* W, int64_t p, const T* F, int64_t c, const T* V, T* G, c
   template int resid<T>(Arena&, const T*, int64_t, int64_t, const T*, int64_t, int64_t, bool, const T*,   \
                         const T*, double*, const int*, cudaStream_t);                                     \
   template int sumsq<T>(Arena&, const T*, const T*, int64_t, double*, cudaStream_t);                      \
-  template int wf_minus_v<T>(const T*, int64_t, const T*, int64_t, const T*, T*, cudaStream_t);
+  template int wf_minus_v<T>(const T*, int64_t, const T*, int64_t, const T*, T*, cudaStream_t);           \
+  template int scan_flags<T>(const T*, int64_t, int64_t, int64_t, int*, int*, cudaStream_t);              \
+  template int transpose<T>(const T*, int64_t, int64_t, int64_t, T*, cudaStream_t);
 NENMF_INST_SKINNY(double)
 NENMF_INST_SKINNY(float)
 

@@ -26,6 +26,10 @@ int resid(Arena& ws, const T* At, int64_t p, int64_t r, const T* B, int64_t c, i
 // sum M^2 (g == nullptr) or sum PG(M, g)^2 -> *out
 template <typename T>
 int sumsq(Arena& ws, const T* M, const T* g, int64_t count, double* out, cudaStream_t st);
+template <typename T>
+int scan_flags(const T* M, int64_t rows, int64_t cols, int64_t ld, int* nonzero, int* negative, cudaStream_t st);
+template <typename T>
+int transpose(const T* src, int64_t rows, int64_t cols, int64_t ld, T* dst, cudaStream_t st);
 
 template <typename T>
 int wf_minus_v(const T* W, int64_t p, const T* F, int64_t c, const T* V, T* G, cudaStream_t st);

@@ -34,6 +34,10 @@ from .tracing import MonotonicClock, SolverClock, TraceRecord
 Observer = Callable[[TraceRecord, np.ndarray, np.ndarray], None]
 
 
+def _on_device(M) -> bool:
+    return bool(getattr(M, "is_cuda", False))
+
+
 @dataclass(frozen=True, eq=False)
 class FactorPair:
     """Factors G (n x p) and F (p x m), entrywise nonnegative (factorize.py:32-48)."""
@@ -48,8 +52,12 @@ class FactorPair:
         if self.G.shape[1] != self.p or self.F.shape[0] != self.p:
             raise DimensionError(
                 f"factor shapes {tuple(self.G.shape)}, {tuple(self.F.shape)} do not match rank {self.p}")
-        if self.G.min() < 0.0 or self.F.min() < 0.0:
-            raise ValueError("factors must be entrywise nonnegative")
+        # host arrays are checked here (the reference's point); factors already
+        # on the device are checked by a flag scan when a factorization starts
+        # (_run_outer), so building a pair never synchronises the device
+        for M in (self.G, self.F):
+            if not _on_device(M) and M.min() < 0.0:
+                raise ValueError("factors must be entrywise nonnegative")
 
 
 @dataclass(frozen=True)
@@ -88,6 +96,17 @@ def init_factors(n: int, m: int, p: int, seed: int) -> FactorPair:
 _STATUS_CAP = 128  # queued half-steps between status drains
 
 
+def _panel_t(G, dtype: str):
+    """G (n x p) as a fresh contiguous G^T (p x n) on the device: a transpose
+    kernel (nenmf_transpose) for device factors, one upload for host ones."""
+    if not _on_device(G):
+        return _lib.to_device(np.ascontiguousarray(np.asarray(G, dtype=np.float64).T), dtype)
+    G = _lib.to_device(G, dtype) if G.dtype != _lib.torch_dtype(dtype) else G
+    if G.t().is_contiguous():
+        return G.t().clone()
+    return _ops.transpose(G)
+
+
 class _DeviceLoop:
     """Device state of one factorization run."""
 
@@ -103,7 +122,7 @@ class _DeviceLoop:
         self.n, self.m = self.X.shape
         self.p = init.p
         self.sketch = sketch
-        self.scal = torch.zeros(4, dtype=torch.float64, device="cuda")
+        self.scal = _lib.zeros(4, torch.float64)
         self.status = _lib.new_status(_STATUS_CAP)
         self.pending: list[tuple[int, str, int]] = []
         self.tensor_v = False
@@ -115,9 +134,10 @@ class _DeviceLoop:
     def prepare(self, init: FactorPair) -> None:
         torch = self.torch
         G = init.G
-        self.Gt = (_lib.to_device(G, self.dtype).t().contiguous() if hasattr(G, "is_cuda")
-                   else _lib.to_device(np.ascontiguousarray(np.asarray(G, dtype=np.float64).T), self.dtype))
+        self.Gt = _panel_t(G, self.dtype)
         self.F = _lib.to_device(init.F, self.dtype)
+        if self.F is init.F:  # never write into the caller's tensor
+            self.F = self.F.clone()
         self.Gt_alt = torch.empty_like(self.Gt)
         self.F_alt = torch.empty_like(self.F)
         if self.sketch is not None:
@@ -175,7 +195,7 @@ class _DeviceLoop:
             return
         sts = _lib.read_status(self.status)
         pending, self.pending = self.pending, []
-        self.status.zero_()
+        _lib.zero_(self.status)
         for t, half, idx in pending:
             st = sts[idx]
             code = int(st["code"])
@@ -187,6 +207,9 @@ class _DeviceLoop:
                 raise NumericalFailureError(
                     f"outer iteration {t} ({half} update): {exc}",
                     iteration=exc.iteration, outer_iteration=t) from exc
+
+    def stop_vote(self, stop: bool) -> bool:
+        return stop
 
     def objective(self) -> float:
         _ops.residual_sumsq(self.X, self.Gt, self.F, self.scal[1:2])
@@ -211,14 +234,14 @@ class _ShardedDeviceLoop(_DeviceLoop):
         self.row0, self.n_r = int(row0), int(X_local.shape[0])
         self.p = init.p
         self.sketch = "sharded"  # compressed half-steps
-        self.scal = torch.zeros(4, dtype=torch.float64, device="cuda")
+        self.scal = _lib.zeros(4, torch.float64)
         self.status = _lib.new_status(_STATUS_CAP)
         self.pending = []
         self.comm = comm
         self._ops_in = (L, Rt, XL, XRt)
 
     def norm_x(self) -> float:
-        self.scal[0:1].zero_()
+        _lib.zero_(self.scal[0:1])
         _ops.sumsq(self.X, self.scal[0:1])
         self.comm.all_reduce(self.scal[0:1])
         return math.sqrt(self.scal[0].item())
@@ -226,9 +249,10 @@ class _ShardedDeviceLoop(_DeviceLoop):
     def prepare(self, init: FactorPair) -> None:
         torch = self.torch
         G = init.G
-        self.Gt = (_lib.to_device(G, self.dtype).t().contiguous() if hasattr(G, "is_cuda")
-                   else _lib.to_device(np.ascontiguousarray(np.asarray(G, dtype=np.float64).T), self.dtype))
+        self.Gt = _panel_t(G, self.dtype)
         self.F = _lib.to_device(init.F, self.dtype)
+        if self.F is init.F:  # never write into the caller's tensor
+            self.F = self.F.clone()
         self.Gt_alt = torch.empty_like(self.Gt)
         self.F_alt = torch.empty_like(self.F)
         self.L, self.Rt, self.XL, self.XRt = self._ops_in
@@ -237,9 +261,15 @@ class _ShardedDeviceLoop(_DeviceLoop):
         self.fr_ready = False
         self.GLt = torch.empty((self.p, nu), dtype=self.X.dtype, device="cuda")
 
+    def stop_vote(self, stop: bool) -> bool:
+        """The time-budget stop is decided collectively: every rank leaves the
+        loop after the same outer iteration if ANY rank's clock ran out, so the
+        all-reduces of emit always have all partners."""
+        return self.comm.any(stop)
+
     def objective(self) -> float:
         Gl = self.Gt[:, self.row0:self.row0 + self.n_r].contiguous()
-        self.scal[1:2].zero_()
+        _lib.zero_(self.scal[1:2])
         _ops.residual_sumsq(self.X, Gl, self.F, self.scal[1:2])
         self.comm.all_reduce(self.scal[1:2])
         return math.sqrt(self.scal[1].item())
@@ -263,7 +293,16 @@ def _run_outer(X, init: FactorPair, cfg: OuterConfig, observer, clock, sketch, d
             f"data {n}x{m} at target rank {sketch.nu}")
     if run is None:
         run = _DeviceLoop(X, init, sketch, dtype)
+    neg = None
+    if _on_device(init.G) or _on_device(init.F):
+        # FactorPair's sign check for device factors, read with ||X||'s sync
+        neg = _lib.zeros(2, run.torch.int32)
+        for i, M in enumerate((init.G, init.F)):
+            if _on_device(M):
+                _ops.scan_flags(M, negative_ptr=neg.data_ptr() + 4 * i)
     norm_x = run.norm_x()
+    if neg is not None and bool(neg.cpu().any()):
+        raise ValueError("factors must be entrywise nonnegative")
     if norm_x == 0.0:
         raise ZeroMatrixError("cannot factorize the zero matrix")
     if clock is None:
@@ -297,7 +336,8 @@ def _run_outer(X, init: FactorPair, cfg: OuterConfig, observer, clock, sketch, d
         if cfg.time_budget_seconds > 0:
             stream.synchronize()
             run.drain()
-            if clock.elapsed() >= cfg.time_budget_seconds:
+            # one decision for all shards of a sharded run (each rank has its own clock)
+            if run.stop_vote(clock.elapsed() >= cfg.time_budget_seconds):
                 break
         t += 1
         run.half_steps(t, cfg.inner)

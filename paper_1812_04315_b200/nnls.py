@@ -89,7 +89,7 @@ def projected_gradient_norm(F, grad, *, dtype: str = "fp64") -> float:
     _, torch = _lib.require_device()
     if F.size == 0:
         return 0.0
-    out = torch.zeros(1, dtype=torch.float64, device="cuda")
+    out = _lib.zeros(1, torch.float64)
     _ops.sumsq(_lib.to_device(F, dtype), out, g=_lib.to_device(grad, dtype))
     return math.sqrt(out.item())
 

@@ -73,6 +73,16 @@ class Comm:
             self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM, group=self.group)
         return t
 
+    def any(self, flag: bool) -> bool:
+        """True on every rank if ``flag`` is True on any rank (MAX all-reduce)."""
+        if self.size == 1:
+            return bool(flag)
+        torch = _lib.torch_mod()
+        dev = "cuda" if self.dist.get_backend(self.group) == "nccl" else "cpu"
+        t = torch.tensor([1 if flag else 0], dtype=torch.int32, device=dev)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
+        return bool(t.item())
+
     def all_gather_cols(self, local, n: int):
         """(k x n_r) blocks in rank order -> (k x n); ragged blocks are padded."""
         torch = _lib.torch_mod()
@@ -154,12 +164,12 @@ class DeviceOps:
             raise_for_status(int(st["code"]), int(st["iteration"]), what)
 
     def sumsq(self, X):
-        out = self.torch.zeros(1, dtype=self.torch.float64, device=X.device)
+        out = _lib.zeros(1, self.torch.float64)
         _ops.sumsq(X, out)
         return out
 
     def residual_sumsq(self, X, Gt, F):
-        out = self.torch.zeros(1, dtype=self.torch.float64, device=X.device)
+        out = _lib.zeros(1, self.torch.float64)
         _ops.residual_sumsq(X, Gt, F, out)
         return out
 

@@ -1,0 +1,205 @@
+"""Parity of EXACTLY the path bench.py times, at the BASELINE.json sizes.
+
+bench.py's step is ``subspace_iteration_pair(<CUDA tensor X>)`` followed by
+``factorize_compressed(<CUDA tensor X>, sketch, FactorPair(<CUDA G0>, <CUDA
+F0>), cfg, return_device=True)``: the device branch of the sketch (flag scan
+of X, prepared X kept on the pair, no host copy of the sketch) and of the
+outer loop (prepared-X reuse by the compression pass, device factors).  These
+tests make those same calls on the configs' own synthetic inputs
+(workloads.py) and compare with the CPU oracle
+(oracle/nenmf_oracle.py, the reference algorithm in float64):
+
+* sketch: the top-p subspace of L and R against ``orc.rsi`` on the same X and
+  seed (principal angles: QR is unique only up to signs and the
+  trailing directions of a rank-deficient X are rounding noise); on the noisy
+  configs 2 and 4 also the full p' subspace in FP64;
+* factorization: the oracle is fed the SAME sketch (the GPU's L, R) and the
+  same initial factors.  FP64 mode: the whole RRE trajectory and the final
+  factors within rel 1e-5.  FP32 mode: every outer iteration within rel 1e-3
+  (RRE and both factors) of the oracle's outer iteration started from the
+  GPU's factors of the iteration before ("one-step parity").  The full-size
+  trajectories themselves are too sensitive for 1e-3 across iterations in
+  ANY fp32 arithmetic: the reference's own algorithm run in float32 NumPy
+  departs from its float64 run by 8e-3 in RRE and 2e-2 in F after 3 outer
+  iterations at cfg2 (tools/fp32_sensitivity.py), the
+  same as the GPU's FP32 mode does; the first outer iteration agrees to 5e-8.
+
+FP32 configs give the oracle the fp32-rounded X and factors upcast to float64
+(workloads._round), so the comparison measures arithmetic, not input rounding.
+Sizes: cfg2 full (10^4 x 10^4, 3 outer, inner 500) in FP64 and FP32; cfg3
+(5*10^4 x 2*10^4, p' = 60) at q = 2 and q = 4, one outer iteration; cfg4
+(4*10^5 x 2*10^3, p' = 40), one outer iteration; a cfg5 proxy (n = m = 10^4,
+the cfg5 generator on the host) through sharded.py at world size 1.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import nenmf_oracle as orc
+import paper_1812_04315_b200 as nm
+from paper_1812_04315_b200 import _lib, workloads
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+TOL = {"fp64": 1e-5, "fp32": 1e-3}
+SKETCH_TOL = {"fp64": 1e-6, "fp32": 1e-3}
+
+
+def sin_max(Q1, Q2, top=None):
+    """largest principal-angle sine between the column spans of orthonormal Q1, Q2 (top directions)."""
+    if top is not None:
+        Q1, Q2 = Q1[:, :top], Q2[:, :top]
+    s = np.linalg.svd(Q1.T @ Q2, compute_uv=False)
+    return math.sqrt(max(0.0, 1.0 - min(1.0, s.min()) ** 2))
+
+
+def top_subspace_angle(Lg, Lr, X_side, p):
+    """sin of the largest angle between the dominant p-dimensional subspaces of
+    two orthonormal bases (columns) of the same sketch space: the dominant
+    directions are those of X_side projected on each basis (SVD), so the
+    comparison does not depend on how each QR ordered the basis."""
+    def dom(Q):
+        u, _, _ = np.linalg.svd(Q.T @ X_side, full_matrices=False)
+        return Q @ u[:, :p]
+    return sin_max(dom(Lg), dom(Lr))
+
+
+def device_step(w, dtype, outer):
+    """bench.py's step_device (bench.py: run_ours) with an observer for the
+    trajectory and the factors after every outer iteration."""
+    import torch
+
+    npdt = np.float32 if dtype == "fp32" else np.float64
+    Xd = torch.from_numpy(w.X.astype(npdt)).to("cuda")
+    G0d = torch.from_numpy(w.G0.astype(npdt)).to("cuda")
+    F0d = torch.from_numpy(w.F0.astype(npdt)).to("cuda")
+    sk = nm.subspace_iteration_pair(Xd, w.nu, w.q, w.sketch_seed)
+    assert hasattr(sk.L, "is_cuda") and sk.L.is_cuda  # the device branch (no host copy of the sketch)
+    rec, facs = nm.TraceRecorder(), []
+
+    def observe(r, G, F):
+        rec(r, G, F)
+        facs.append((G.copy(), F.copy()))
+
+    cfg = nm.OuterConfig(inner=nm.InnerSolverConfig(max_iter=w.inner), time_budget_seconds=0.0,
+                         max_outer_iterations=outer, trace_every=1)
+    out = nm.factorize_compressed(Xd, sk, nm.FactorPair(G=G0d, F=F0d, p=w.p), cfg, observer=observe,
+                                  clock=nm.IterationClock(), return_device=True)
+    assert out.G.is_cuda and out.F.is_cuda
+    # the caller's initial factors are not written to
+    assert torch.equal(G0d, torch.from_numpy(w.G0.astype(npdt)).to("cuda"))
+    assert torch.equal(F0d, torch.from_numpy(w.F0.astype(npdt)).to("cuda"))
+    L = _lib.to_host(sk.L)
+    R = _lib.to_host(sk.R)
+    G = _lib.to_host(out.G)
+    F = _lib.to_host(out.F)
+    assert np.array_equal(G, facs[-1][0]) and np.array_equal(F, facs[-1][1])
+    rre = np.array([r.rre for r in rec.records])
+    del Xd, sk, out
+    torch.cuda.empty_cache()
+    return L, R, G, F, rre, facs
+
+
+def one_step_parity(X, L, R, facs, rre, inner, tol):
+    """each outer iteration t against the oracle's outer iteration from the
+    GPU's factors of iteration t - 1 (same sketch)"""
+    for t in range(1, len(facs)):
+        ref = orc.nenmf(X, facs[t - 1][0], facs[t - 1][1], L=L, R=R, max_outer=1, max_iter=inner)
+        G, F = facs[t]
+        assert abs(rre[t] - ref.records[-1][1]) <= tol * ref.records[-1][1], (t, rre[t], ref.records[-1][1])
+        assert np.linalg.norm(G - ref.G) <= tol * np.linalg.norm(ref.G), t
+        assert np.linalg.norm(F - ref.F) <= tol * np.linalg.norm(ref.F), t
+
+
+def check_config(w, dtype, outer, full_sketch=False):
+    L, R, G, F, rre, facs = device_step(w, dtype, outer)
+    tol, stol = TOL[dtype], SKETCH_TOL[dtype]
+    eye = np.eye(w.nu)
+    assert np.abs(L @ L.T - eye).max() <= (1e-10 if dtype == "fp64" else 1e-5)
+    assert np.abs(R.T @ R - eye).max() <= (1e-10 if dtype == "fp64" else 1e-5)
+    # sketch subspace vs the oracle's RSI on the same X and seed
+    Lr, Rr = orc.rsi(w.X, w.nu, w.q, w.sketch_seed)
+    a_l = top_subspace_angle(L.T, Lr.T, w.X, w.p)
+    a_r = top_subspace_angle(R, Rr, w.X.T, w.p)
+    assert a_l <= stol and a_r <= stol, (a_l, a_r)
+    if full_sketch:
+        assert sin_max(L.T, Lr.T) <= stol and sin_max(R, Rr) <= stol
+    del Lr, Rr
+    if dtype == "fp32":
+        one_step_parity(w.X, L, R, facs, rre, w.inner, tol)
+        return
+    # FP64: the whole trajectory from the same start
+    ref = orc.nenmf(w.X, w.G0, w.F0, L=L, R=R, max_outer=outer, max_iter=w.inner)
+    exp = np.array([r for _, r, _ in ref.records])
+    assert rre.shape == exp.shape
+    assert np.abs(rre - exp).max() <= tol * exp.max(), (rre, exp)
+    assert np.abs(G - ref.G).max() <= tol * np.abs(ref.G).max()
+    assert np.abs(F - ref.F).max() <= tol * np.abs(ref.F).max()
+
+
+@pytest.mark.parametrize("dtype", ["fp64", "fp32"])
+def test_cfg2_full_size_bench_path(dtype):
+    """BASELINE cfg 2 (n = m = 10^4, p = 20, p' = 30, q = 4, inner 500) in both modes."""
+    w = workloads.make_workload(2, dtype=dtype)
+    check_config(w, dtype, outer=3, full_sketch=True)
+
+
+@pytest.mark.parametrize("q", [2, 4])
+def test_cfg3_full_size(q):
+    """BASELINE cfg 3 (5*10^4 x 2*10^4, p = 50, p' = 60, fp32): the q sweep."""
+    w = workloads.make_workload(3)
+    w.q = q
+    check_config(w, "fp32", outer=1)
+
+
+def test_cfg4_full_size():
+    """BASELINE cfg 4 (tall-skinny 4*10^5 x 2*10^3, p = 30, p' = 40, fp32, 20 dB clipped noise)."""
+    w = workloads.make_workload(4)
+    check_config(w, "fp32", outer=1)
+
+
+def test_cfg5_proxy_sharded_world1():
+    """cfg5 proxy: the cfg5 generator at n = m = 10^4 on the host, uploaded, run
+    through the row-sharded path (sharded.py) at world size 1 as bench.py
+    --workload cfg5 does, against the oracle on the same X."""
+    import os
+    import socket
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_1812_04315_b200 import sharded
+
+    w = workloads.make_workload(5, n=10000, m=10000)
+    if not dist.is_initialized():
+        s = socket.socket()
+        s.bind(("127.0.0.1", 0))
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(s.getsockname()[1]))
+        s.close()
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        comm = sharded.Comm()
+        Xl = torch.from_numpy(w.X.astype(np.float32)).to("cuda")
+        sk = sharded.subspace_iteration_pair_sharded(Xl, w.n, w.nu, w.q, w.sketch_seed, comm=comm)
+        pair = sharded.gather_sketch(sk, comm=comm)
+        init = nm.FactorPair(G=torch.from_numpy(w.G0.astype(np.float32)).to("cuda"),
+                             F=torch.from_numpy(w.F0.astype(np.float32)).to("cuda"), p=w.p)
+        cfg = nm.OuterConfig(inner=nm.InnerSolverConfig(max_iter=w.inner), time_budget_seconds=0.0,
+                             max_outer_iterations=2)
+        rec, facs = nm.TraceRecorder(), []
+
+        def observe(r, G, F):
+            rec(r, G, F)
+            facs.append((np.array(G, dtype=np.float64), np.array(F, dtype=np.float64)))
+
+        sharded.factorize_compressed_sharded(Xl, w.n, sk, init, cfg, observer=observe, clock=nm.IterationClock(),
+                                             comm=comm)
+    finally:
+        dist.destroy_process_group()
+    Lr, Rr = orc.rsi(w.X, w.nu, w.q, w.sketch_seed)
+    # noiseless rank 16 < p' = 26: the top-p subspace is determined
+    assert top_subspace_angle(pair.L.T, Lr.T, w.X, w.p) <= 1e-3
+    assert top_subspace_angle(pair.R, Rr, w.X.T, w.p) <= 1e-3
+    rre = np.array([r.rre for r in rec.records])
+    one_step_parity(w.X, pair.L, pair.R, facs, rre, w.inner, 1e-3)

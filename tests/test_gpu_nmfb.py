@@ -53,7 +53,11 @@ def test_factorize_from_file(tmp_path):
     Xd = nm.read_nmfb_device(path, dtype="fp64")
     a = nm.subspace_iteration_pair(Xd, 12, 2, 9)
     b = nm.subspace_iteration_pair(X, 12, 2, 9)
-    assert np.abs(a.L - b.L).max() == 0.0 and np.abs(a.R - b.R).max() == 0.0
+    # a device X gives a device-resident sketch (no host copy inside the sketch)
+    from paper_1812_04315_b200 import _lib
+
+    assert a.L.is_cuda and a.R.is_cuda
+    assert np.abs(_lib.to_host(a.L) - b.L).max() == 0.0 and np.abs(_lib.to_host(a.R) - b.R).max() == 0.0
 
 
 def test_load_row_shard_covers_file(tmp_path):

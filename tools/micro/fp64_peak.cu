@@ -1,0 +1,81 @@
+// FP64 compute peaks of this B200 (sm_100a): the DMMA tensor pipe
+// (mma.sync m8n8k4 f64, 512 flops per warp instruction) and the CUDA-core
+// DFMA pipe, all SMs, independent accumulator chains, CUDA-event timing.
+// Prints one JSON line; bench.py's fp64 roofline divides by the DMMA figure
+// (stored in profiles/fp64_peak.json).  nvcc -O3 -gencode
+// arch=compute_100a,code=sm_100a fp64_peak.cu -o fp64_peak
+#include <cstdio>
+#include <cuda_runtime.h>
+
+constexpr int CH = 8;  // independent chains per warp
+
+__global__ void __launch_bounds__(256) k_dmma(double* out, int iters) {
+  double c[CH][2];
+  double a = 1.0 + threadIdx.x * 1e-9, b = 1.0 - threadIdx.x * 1e-9;
+#pragma unroll
+  for (int j = 0; j < CH; ++j) c[j][0] = c[j][1] = 0.0;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int j = 0; j < CH; ++j)
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                   : "+d"(c[j][0]), "+d"(c[j][1])
+                   : "d"(a), "d"(b));
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int j = 0; j < CH; ++j) s += c[j][0] + c[j][1];
+  if (s == 12345.678) out[0] = s;
+}
+
+__global__ void __launch_bounds__(256) k_dfma(double* out, int iters) {
+  double c[CH];
+  const double a = 1.0 + threadIdx.x * 1e-12, b = 0.999999;
+#pragma unroll
+  for (int j = 0; j < CH; ++j) c[j] = j;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int j = 0; j < CH; ++j) c[j] = fma(c[j], b, a);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int j = 0; j < CH; ++j) s += c[j];
+  if (s == 12345.678) out[0] = s;
+}
+
+int main() {
+  int dev = 0, sms = 0, clk = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, dev);
+  double* out;
+  cudaMalloc(&out, 8);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  const int blocks = sms * 4, threads = 256;
+  double best_mma = 0, best_fma = 0;
+  for (int rep = 0; rep < 6; ++rep) {
+    const int iters = 20000;
+    k_dmma<<<blocks, threads>>>(out, 100);
+    cudaEventRecord(e0);
+    k_dmma<<<blocks, threads>>>(out, iters);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    const double fl = (double)blocks * (threads / 32) * iters * CH * 512.0;
+    if (fl / (ms * 1e-3) / 1e12 > best_mma) best_mma = fl / (ms * 1e-3) / 1e12;
+    cudaEventRecord(e0);
+    k_dfma<<<blocks, threads>>>(out, iters);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    cudaEventElapsedTime(&ms, e0, e1);
+    const double ff = (double)blocks * threads * iters * CH * 2.0;
+    if (ff / (ms * 1e-3) / 1e12 > best_fma) best_fma = ff / (ms * 1e-3) / 1e12;
+  }
+  printf("{\"fp64_dmma_tflops\": %.3f, \"fp64_dfma_tflops\": %.3f, \"sms\": %d, \"clock_khz\": %d, "
+         "\"how\": \"tools/micro/fp64_peak.cu: %d CTAs x 256 threads, %d independent chains per warp, best of 6, "
+         "CUDA events\", \"err\": \"%s\"}\n",
+         best_mma, best_fma, sms, clk, blocks, CH, cudaGetErrorString(cudaGetLastError()));
+  return 0;
+}
