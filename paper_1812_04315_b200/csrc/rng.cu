@@ -20,7 +20,8 @@
 // positions start a draw, how many draws start inside the chunk and where the
 // walk leaves it.  k_zig_link (one thread) chains the chunks: a chunk entered
 // at a position its own walk also starts a draw at has the same tail (walks
-// that meet stay merged), so only entry points off that walk need a re-walk.
+// that meet stay merged), so only entry points off that walk need a re-walk;
+// k_zig_link_par does the common case as a parallel scan.
 // k_zig_emit walks each chunk again from its true entry and writes draw i to
 // Omega_L^T (i < m nu, transposed) or Omega_R; draws from the ziggurat tail
 // (~1 in 4000) use glibc_log1p below, the C library's own log1p restated
@@ -151,7 +152,9 @@ constexpr int LINK_TILE = 2048;
 __global__ void __launch_bounds__(256) k_zig_link(const Tables* __restrict__ T, uint64_t s_lo, uint64_t s_hi,
                                                   uint64_t i_lo, uint64_t i_hi, const ChunkScan* __restrict__ sc,
                                                   int64_t nchunks, int S, int64_t need, int* __restrict__ entry,
-                                                  int64_t* __restrict__ base, int* __restrict__ ok) {
+                                                  int64_t* __restrict__ base, int* __restrict__ ok,
+                                                  const int* __restrict__ seq_needed) {
+  if (seq_needed != nullptr && *seq_needed == 0) return;  // k_zig_link_par chained every chunk
   __shared__ ChunkScan tile[LINK_TILE];
   __shared__ int s_e, s_good;
   __shared__ long long s_b;
@@ -215,6 +218,99 @@ __global__ void __launch_bounds__(256) k_zig_link(const Tables* __restrict__ T, 
   if (threadIdx.x == 0) *ok = (s_good && s_b >= need) ? 1 : 0;
 }
 
+// The chaining above is a scan in disguise: a chunk entered at an offset
+// its own walk also starts a draw at contributes count - (draws of its walk
+// before the entry) and leaves at its own exit, whatever happened before; a
+// chunk entered off its walk is re-walked from the entry until the two walks
+// meet (about one chunk boundary in 10^4) and then leaves at its own exit
+// too.  So with every chunk's entry taken as its predecessor's own exit, all
+// chunks are counted in parallel (one block, a prefix sum for the first draw
+// indices).  Only a re-walk that leaves the chunk before meeting its walk
+// (never observed) changes an exit; then the sequential k_zig_link redoes
+// the chaining after this kernel.
+constexpr int LINKP_THREADS = 1024;
+__device__ __forceinline__ int chunk_contribution(const Tables& T, uint64_t s_lo, uint64_t s_hi, uint64_t i_lo,
+                                                  uint64_t i_hi, int64_t c, int S, int e, const ChunkScan& s,
+                                                  bool& exit_changed) {
+  if (e == 0) return s.count;
+  if (e < 64 && ((s.mask >> e) & 1ull)) return s.count - __popcll(s.mask & ((1ull << e) - 1ull));
+  Stream g;
+  g.inc = ((u128)i_hi << 64) | i_lo;
+  g.s = advance(((u128)s_hi << 64) | s_lo, g.inc, (uint64_t)c * (uint64_t)S + (uint64_t)e);
+  int pos = e, extra = 0;
+  while (pos < S && pos < 64 && !((s.mask >> pos) & 1ull)) {
+    int used;
+    draw(g, T, used);
+    pos += used;
+    ++extra;
+  }
+  if (pos < 64 && pos < S && ((s.mask >> pos) & 1ull)) return extra + s.count - __popcll(s.mask & ((1ull << pos) - 1ull));
+  exit_changed = true;
+  return 0;
+}
+
+__global__ void __launch_bounds__(LINKP_THREADS) k_zig_link_par(const Tables* __restrict__ T, uint64_t s_lo,
+                                                                uint64_t s_hi, uint64_t i_lo, uint64_t i_hi,
+                                                                const ChunkScan* __restrict__ sc, int64_t nchunks,
+                                                                int S, int64_t need, int* __restrict__ entry,
+                                                                int64_t* __restrict__ base, int* __restrict__ ok,
+                                                                int* __restrict__ seq_needed) {
+  __shared__ Tables tb;
+  __shared__ long long wsum[LINKP_THREADS / 32];
+  __shared__ int s_bad;
+  const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  for (int i = t; i < 256; i += blockDim.x) {
+    tb.fi[i] = T->fi[i];
+    tb.wi[i] = T->wi[i];
+    tb.ki[i] = T->ki[i];
+  }
+  if (t == 0) s_bad = 0;
+  __syncthreads();
+  const int64_t per = (nchunks + LINKP_THREADS - 1) / LINKP_THREADS;
+  const int64_t c0 = min(nchunks, (int64_t)t * per), c1 = min(nchunks, c0 + per);
+  long long mine = 0;
+  bool bad = false;
+  for (int64_t c = c0; c < c1; ++c) {
+    const int e = c == 0 ? 0 : sc[c - 1].exit;
+    mine += chunk_contribution(tb, s_lo, s_hi, i_lo, i_hi, c, S, e, sc[c], bad);
+  }
+  if (bad) s_bad = 1;
+  // block-wide exclusive scan of the per-thread counts (thread order = chunk order)
+  long long incl = mine;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const long long v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  if (lane == 31) wsum[wid] = incl;
+  __syncthreads();
+  if (wid == 0) {
+    long long v = wsum[lane], w = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const long long u = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += u;
+    }
+    wsum[lane] = w - v;  // exclusive
+  }
+  __syncthreads();
+  long long b = wsum[wid] + incl - mine;
+  if (s_bad) {
+    if (t == 0) *seq_needed = 1;
+    return;
+  }
+  for (int64_t c = c0; c < c1; ++c) {
+    const int e = c == 0 ? 0 : sc[c - 1].exit;
+    entry[c] = e;
+    base[c] = b;
+    b += chunk_contribution(tb, s_lo, s_hi, i_lo, i_hi, c, S, e, sc[c], bad);
+  }
+  if (t == LINKP_THREADS - 1) {
+    *seq_needed = 0;
+    *ok = b >= need ? 1 : 0;
+  }
+}
+
 template <typename TO>
 __global__ void k_zig_emit(const Tables* __restrict__ T, uint64_t s_lo, uint64_t s_hi, uint64_t i_lo, uint64_t i_hi,
                            int64_t nchunks, int S, const int* __restrict__ entry, const int64_t* __restrict__ base,
@@ -270,13 +366,16 @@ int sketch_draws_device(int dtype, const void* tables, uint64_t s_lo, uint64_t s
   using namespace zig;
   if (n < 1 || m < 1 || nu < 1) return NENMF_ERR_DIM;
   const int64_t need = (m + n) * nu;
-  // chunk length: ~4096 chunks (the link pass is sequential over chunks)
-  int S = 256;
-  while (S < 4096 && need / S > 4096) S *= 2;
+  // chunk length: short walks (latency of the scan and emit passes), at
+  // most ~64 K chunks for the parallel link; >= 64 so that an entry offset
+  // (a few positions) always lies inside the chunk's start mask
+  int S = 64;
+  while (S < 4096 && need / S > 65536) S *= 2;
   const int64_t nchunks = (int64_t)((double)need * 1.03 / S) + 8;
   ChunkScan* sc = ws.take<ChunkScan>((size_t)nchunks);
   int* entry = ws.take<int>((size_t)nchunks);
   int64_t* base = ws.take<int64_t>((size_t)nchunks);
+  int* seq = ws.take<int>(4);
   if (ws.base == nullptr) return NENMF_OK;
   if (!ws.ok) return NENMF_ERR_WORKSPACE;
   const Tables* T = static_cast<const Tables*>(tables);
@@ -285,7 +384,10 @@ int sketch_draws_device(int dtype, const void* tables, uint64_t s_lo, uint64_t s
   const unsigned blocks = (unsigned)cdiv(nchunks, 64);
   k_zig_scan<<<blocks, 64, 0, s>>>(T, s_lo, s_hi, i_lo, i_hi, nchunks, S, sc);
   NENMF_LAUNCH_CHECK();
-  k_zig_link<<<1, 256, 0, s>>>(T, s_lo, s_hi, i_lo, i_hi, sc, nchunks, S, need, entry, base, ok);
+  k_zig_link_par<<<1, LINKP_THREADS, 0, s>>>(T, s_lo, s_hi, i_lo, i_hi, sc, nchunks, S, need, entry, base, ok,
+                                              seq);
+  NENMF_LAUNCH_CHECK();
+  k_zig_link<<<1, 256, 0, s>>>(T, s_lo, s_hi, i_lo, i_hi, sc, nchunks, S, need, entry, base, ok, seq);
   NENMF_LAUNCH_CHECK();
   if (dtype == NENMF_F64)
     k_zig_emit<double><<<blocks, 64, 0, s>>>(T, s_lo, s_hi, i_lo, i_hi, nchunks, S, entry, base, ok, n, m, nu,
