@@ -129,13 +129,26 @@ __device__ void block_factor(double* S_in, int k, int pivot, double rel_tol, dou
       s_rank = rank;
       if (bad) s_bad = 1;
     }
-  } else if (tid < 32) {
-    const int a0 = lane, a1 = lane + 32;
-    bool live0 = a0 < k, live1 = a1 < k;
-    double dg0 = live0 ? S[a0 * LD + a0] : 0.0, dg1 = live1 ? S[a1 * LD + a1] : 0.0;
-    double mx = fmax(dg0, dg1);
+  } else if (k > 32 && tid < 64) {
+    // 32 < k <= 64: two warps, lane l of warp w holds row 32 w + l in
+    // registers (64 doubles); per step the warps exchange their pivot
+    // candidates and their pivot-column entries through shared memory
+    // (named barrier 1, 64 threads)
+    __shared__ unsigned s_key[2];
+    __shared__ int s_idx[2];
+    __shared__ double rcv[64];
+    const int w = tid >> 5, a = tid;
+    double row[64];
+#pragma unroll
+    for (int bcol = 0; bcol < 64; ++bcol) row[bcol] = S[a * LD + bcol];
+    bool live = a < k;
+    double dg = live ? S[a * LD + a] : 0.0;
+    double mx = dg;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(FULL, mx, o));
+    if (lane == 0) rcv[w] = mx;
+    asm volatile("bar.sync 1, 64;" ::: "memory");
+    mx = fmax(rcv[0], rcv[1]);
     const bool bad = s_bad || !(mx > 0.0);
     const double tau = rel_tol * mx;
     int rank = k;
@@ -145,44 +158,57 @@ __device__ void block_factor(double* S_in, int k, int pivot, double rel_tol, dou
       for (int j = 0; j < k; ++j) {
         int pj;
         if (pivot) {
-          // positive doubles order like their bit patterns: compare the top 32 bits
-          const unsigned k0 = live0 && dg0 > 0.0 ? (unsigned)(__double_as_longlong(dg0) >> 32) : 0u;
-          const unsigned k1 = live1 && dg1 > 0.0 ? (unsigned)(__double_as_longlong(dg1) >> 32) : 0u;
-          const unsigned best = __reduce_max_sync(FULL, k0 > k1 ? k0 : k1);
-          const unsigned c0 = __ballot_sync(FULL, live0 && k0 == best);
-          const unsigned c1 = __ballot_sync(FULL, live1 && k1 == best);
-          pj = c0 ? __ffs(c0) - 1 : (c1 ? 32 + __ffs(c1) - 1 : j);
+          const unsigned kk0 = live && dg > 0.0 ? (unsigned)(__double_as_longlong(dg) >> 32) : 0u;
+          const unsigned best = __reduce_max_sync(FULL, kk0);
+          const unsigned c0 = __ballot_sync(FULL, live && kk0 == best);
+          asm volatile("bar.sync 1, 64;" ::: "memory");  // previous step's readers are done
+          if (lane == 0) {
+            s_key[w] = best;
+            s_idx[w] = c0 ? 32 * w + __ffs(c0) - 1 : 1 << 30;
+          }
+          asm volatile("bar.sync 1, 64;" ::: "memory");
+          // larger key wins; equal keys: the lower index (warp 0 first)
+          pj = s_key[1] > s_key[0] ? s_idx[1] : (s_key[0] > s_key[1] ? s_idx[0] : min(s_idx[0], s_idx[1]));
+          if (pj >= (1 << 30)) pj = j;
         } else {
           pj = j;
         }
-        const double bv = pj < 32 ? __shfl_sync(FULL, dg0, pj) : __shfl_sync(FULL, dg1, pj - 32);
+        // the pivot's diagonal, from its owner
+        asm volatile("bar.sync 1, 64;" ::: "memory");
+        if (a == pj) rcv[0] = dg;
+        asm volatile("bar.sync 1, 64;" ::: "memory");
+        const double bv = rcv[0];
         if (!(bv > tau)) {
           rank = j;
           break;
         }
-        const double rjj = sqrt(bv), inv = 1.0 / rjj;
-        // R[j][a] = S[a][pj] / rjj for the remaining rows, rjj at the pivot
-        const double ra0 = live0 ? (a0 == pj ? rjj : S[a0 * LD + pj] * inv) : 0.0;
-        const double ra1 = live1 ? (a1 == pj ? rjj : S[a1 * LD + pj] * inv) : 0.0;
-        if (a0 < k) Rout[j * k + a0] = ra0;
-        if (a1 < k) Rout[j * k + a1] = ra1;
-        if (lane == 0) perm[j] = pj;
-        if (a0 == pj) live0 = false;
-        if (a1 == pj) live1 = false;
-        const double rc0 = live0 ? ra0 : 0.0, rc1 = live1 ? ra1 : 0.0;
-        // rank-1 update of the remaining block (rc is 0 outside it)
-        for (int bcol = 0; bcol < k; ++bcol) {
-          const double rb = bcol < 32 ? __shfl_sync(FULL, rc0, bcol) : __shfl_sync(FULL, rc1, bcol - 32);
-          if (rb != 0.0) {
-            if (rc0 != 0.0) S[a0 * LD + bcol] = fma(-rc0, rb, S[a0 * LD + bcol]);
-            if (rc1 != 0.0) S[a1 * LD + bcol] = fma(-rc1, rb, S[a1 * LD + bcol]);
-          }
-        }
-        if (rc0 != 0.0) dg0 = fma(-rc0, rc0, dg0);
-        if (rc1 != 0.0) dg1 = fma(-rc1, rc1, dg1);
+        const double inv = rsqrt(bv), rjj = bv * inv;
+        double v32[32], v16[16], v8[8], v4[4], v2[2];
+#pragma unroll
+        for (int u = 0; u < 32; ++u) v32[u] = (pj & 1) ? row[2 * u + 1] : row[2 * u];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) v16[u] = (pj & 2) ? v32[2 * u + 1] : v32[2 * u];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v8[u] = (pj & 4) ? v16[2 * u + 1] : v16[2 * u];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v4[u] = (pj & 8) ? v8[2 * u + 1] : v8[2 * u];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) v2[u] = (pj & 16) ? v4[2 * u + 1] : v4[2 * u];
+        const double sp = (pj & 32) ? v2[1] : v2[0];
+        const double ra = live ? (a == pj ? rjj : sp * inv) : 0.0;
+        if (a < k) Rout[j * k + a] = ra;
+        if (tid == 0) perm[j] = pj;
+        if (a == pj) live = false;
+        const double rc = live ? ra : 0.0;
+        asm volatile("bar.sync 1, 64;" ::: "memory");  // everyone has read rcv[0]
+        rcv[a] = rc;
+        asm volatile("bar.sync 1, 64;" ::: "memory");
+#pragma unroll
+        for (int bcol = 0; bcol < 64; ++bcol) row[bcol] = fma(-rc, rcv[bcol], row[bcol]);
+        dg = fma(-rc, rc, dg);
       }
     }
-    if (lane == 0) {
+    if (tid == 0) {
       s_rank = rank;
       if (bad) s_bad = 1;
     }
@@ -227,7 +253,16 @@ __device__ void solve_rows(const T* __restrict__ in_t, int64_t rows, int k, cons
   if (t >= TPR) return;
   double* __restrict__ z = zs + t;
   for (int64_t i = r0 + t; i < r1; i += TPR) {
-    for (int l = 0; l < r; ++l) z[l * TPR] = (double)in_t[(int64_t)perm[l] * rows + i];
+    // all loads of the row in flight at once (a load-convert-store loop
+    // waited one memory latency per entry)
+    {
+      T v[KM];
+#pragma unroll
+      for (int l = 0; l < KM; ++l) v[l] = l < r ? in_t[(int64_t)perm[l] * rows + i] : T(0);
+#pragma unroll
+      for (int l = 0; l < KM; ++l)
+        if (l < r) z[l * TPR] = (double)v[l];
+    }
     for (int c0 = 0; c0 < r; c0 += 8) {
       double acc[8];
 #pragma unroll
@@ -331,27 +366,37 @@ __device__ __forceinline__ void gram_partial_block(const T* __restrict__ Pt, int
   double acc[NT][2];
 #pragma unroll
   for (int t = 0; t < NT; ++t) acc[t][0] = acc[t][1] = 0.0;
-  auto load = [&](int64_t r, double (&f)[NB]) {
+  // raw values stay in their storage type until used, so no conversion makes
+  // the warp wait for a load issued ahead of time
+  auto load = [&](int64_t r, T (&f)[NB]) {
     const int64_t row = r + tq;
 #pragma unroll
     for (int b = 0; b < NB; ++b) {
       const int col = 8 * b + gq;
-      f[b] = (b < nb && col < k && row < r1) ? (double)__ldcg(&Pt[(int64_t)col * rows + row]) : 0.0;
+      f[b] = (b < nb && col < k && row < r1) ? __ldcg(&Pt[(int64_t)col * rows + row]) : T(0);
     }
   };
-  double fn[NB];
-  load(r0 + 4 * wid, fn);  // software pipelined: the next step's loads are in flight during the DMMAs
-  for (int64_t r = r0 + 4 * wid; r < r1; r += 32) {
-    double f[NB];
+  // software pipeline PD steps deep: the loads of the next PD - 1 row steps
+  // are in flight during a step's DMMAs (one step ahead left every step
+  // waiting a memory latency)
+  constexpr int PD = NB <= 4 ? 4 : 2;
+  T fn[PD][NB];
 #pragma unroll
-    for (int b = 0; b < NB; ++b) f[b] = fn[b];
-    if (r + 32 < r1) load(r + 32, fn);
-    int t = 0;
+  for (int d = 0; d < PD; ++d) load(r0 + 4 * wid + 32 * d, fn[d]);
+  for (int64_t r = r0 + 4 * wid; r < r1; r += 32 * PD) {
 #pragma unroll
-    for (int ma = 0; ma < NB; ++ma)
+    for (int d = 0; d < PD; ++d) {
+      double f[NB];
 #pragma unroll
-      for (int na = ma; na < NB; ++na, ++t)
-        if (na < nb) dmma(acc[t], f[ma], f[na]);
+      for (int b = 0; b < NB; ++b) f[b] = (double)fn[d][b];
+      load(r + 32 * (d + PD), fn[d]);
+      int t = 0;
+#pragma unroll
+      for (int ma = 0; ma < NB; ++ma)
+#pragma unroll
+        for (int na = ma; na < NB; ++na, ++t)
+          if (na < nb) dmma(acc[t], f[ma], f[na]);
+    }
   }
   // cross-warp sum in fixed warp order (0 + w0 + w1 + ... + w7): every warp
   // stores its fragments (no read-modify-write chains in shared memory), then
