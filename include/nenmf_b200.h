@@ -70,7 +70,8 @@ typedef enum {
   NENMF_ERR_VALUE = 5,               /* ValueError                            */
   NENMF_ERR_CUDA = 6,
   NENMF_ERR_WORKSPACE = 7,
-  NENMF_ERR_UNSUPPORTED = 8
+  NENMF_ERR_UNSUPPORTED = 8,
+  NENMF_ERR_WATCHDOG = 9             /* a persistent solve made no progress for NENMF_WATCHDOG_S seconds */
 } nenmf_status_code;
 
 /* Written by the kernels (device memory, 64 bytes).  Zero it before use. */
@@ -147,6 +148,47 @@ int nenmf_solve_nnls_next(int dtype, const void* At, int64_t r, int64_t p,
 
 /* sigma_max(A)^2 by power iteration on the smaller Gram (matrix.py:158-174).
  * A (r x p) passed as At (p x r).  Result (double) -> *out (device). */
+/* ---- rank groups ------------------------------------------
+ * A compressed half-step whose columns are split over R ranks (X row-sharded
+ * across GPUs: the G-half owns this rank's rows of G, the F-half a slice of
+ * F's columns).  Each rank launches the same persistent solver on its own
+ * columns; the per-iteration sums of the stopping/best decisions (nnls.py:
+ * 177,196-203) and the tie-break residuals (nnls.py:219-227) are exchanged
+ * inside the kernel through an exchange buffer on every rank (peer memory
+ * over NVLink, epoch-tagged, summed in rank order), so all ranks take the
+ * same decisions.  next_out receives nvr partial next products (p x next_k
+ * each, this launch's virtual ranks in order); the caller all-reduces them.
+ * With nvr = R one launch emulates the whole group on one GPU (its CTAs split
+ * into R virtual ranks), which is how the exchange is tested on one device.
+ * Replaces nnls.py:119-227 for the sharded compressed loop (factorize.py:
+ * 197-213 run on row blocks). */
+typedef struct nenmf_group {
+  int ranks;        /* R, 2..8 */
+  int rank0;        /* rank of this launch's first virtual rank */
+  int nvr;          /* virtual ranks in this launch: 1 per GPU, or R to emulate the group */
+  int reserved;
+  int64_t col0[9];  /* virtual rank v owns columns [col0[v], col0[v+1]) of this launch's arrays; col0[nvr] = c */
+  void* xch[8];     /* every rank's exchange buffer (nenmf_group_xch_bytes() each, zeroed once) */
+  uint64_t epoch;   /* the same on every rank, unique per solve over the buffers' lifetime, 0 < epoch < 2^40 */
+} nenmf_group;
+size_t nenmf_group_xch_bytes(void);
+/* NENMF_OK when a solve of this shape runs as a group solve (ranks, nvr
+ * virtual ranks in one launch), NENMF_ERR_UNSUPPORTED when the caller must
+ * replicate it instead (columns beyond the register-resident solver). */
+int nenmf_solve_nnls_group_check(int dtype, int64_t r, int64_t p, int64_t c, int64_t next_k, int ranks,
+                                 int nvr, int max_iter);
+int nenmf_solve_nnls_group(int dtype, const void* At, int64_t r, int64_t p, const void* B, int64_t c,
+                           int64_t ldb, int trans_b, const void* F0, void* F_out, int max_iter,
+                           double grad_tol, double lipschitz_safety, const double* power_vectors,
+                           int power_count, int power_max_iters, double power_tol, const void* next_bt,
+                           int64_t next_k, void* next_out, const nenmf_group* group,
+                           nenmf_device_status* status, void* ws, size_t ws_bytes, void* stream);
+/* CUDA IPC of the exchange buffers: a 64-byte handle of a device allocation,
+ * and the peer mapping of a handle from another process. */
+int nenmf_ipc_handle(const void* dev_ptr, void* handle64);
+int nenmf_ipc_open(const void* handle64, void** dev_ptr);
+int nenmf_ipc_close(void* dev_ptr);
+
 size_t nenmf_spectral_norm_sq_workspace_bytes(int dtype, int64_t r, int64_t p);
 int nenmf_spectral_norm_sq(int dtype, const void* At, int64_t r, int64_t p,
                            const double* power_vectors, int power_count, int max_iters, double tol,

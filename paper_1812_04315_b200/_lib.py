@@ -37,6 +37,13 @@ _SIGS = {
     "nenmf_solve_nnls_next": (_i32, [_i32, _vp, _i64, _i64, _vp, _i64, _i64, _i32, _vp, _vp, _i32, _dbl, _dbl,
                                      _vp, _i32, _i32, _dbl, _vp, _i64, _vp, _vp, _vp, _sz, _vp]),
     "nenmf_solve_nnls_prepared_workspace_bytes": (_sz, [_i32, _i64, _i64, _i64]),
+    "nenmf_group_xch_bytes": (_sz, []),
+    "nenmf_solve_nnls_group_check": (_i32, [_i32, _i64, _i64, _i64, _i64, _i32, _i32, _i32]),
+    "nenmf_solve_nnls_group": (_i32, [_i32, _vp, _i64, _i64, _vp, _i64, _i64, _i32, _vp, _vp, _i32, _dbl, _dbl,
+                                      _vp, _i32, _i32, _dbl, _vp, _i64, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "nenmf_ipc_handle": (_i32, [_vp, _vp]),
+    "nenmf_ipc_open": (_i32, [_vp, _vp]),
+    "nenmf_ipc_close": (_i32, [_vp]),
     "nenmf_solve_nnls_prepared": (_i32, [_i32, _vp, _i64, _i64, _vp, _i64, _i64, _i32, _vp, _vp, _vp, _i32, _dbl,
                                          _dbl, _vp, _i32, _i32, _dbl, _vp, _vp, _sz, _vp]),
     "nenmf_spectral_norm_sq_workspace_bytes": (_sz, [_i32, _i64, _i64]),
@@ -179,6 +186,14 @@ def workspace(nbytes: int):
         buf = torch.empty(int(nbytes * 1.25) + 4096, dtype=torch.uint8, device="cuda")
         cache[dev] = buf
     return buf
+
+
+# ------------------------------------------------------------- rank groups
+class GroupStruct(C.Structure):
+    """nenmf_group (include/nenmf_b200.h): one solve split over R ranks."""
+
+    _fields_ = [("ranks", C.c_int), ("rank0", C.c_int), ("nvr", C.c_int), ("reserved", C.c_int),
+                ("col0", C.c_int64 * 9), ("xch", C.c_void_p * 8), ("epoch", C.c_uint64)]
 
 
 # -------------------------------------------------------------- status words

@@ -70,6 +70,30 @@ def solve(At, B, F0, Fout, *, trans_b: bool, max_iter: int, grad_tol: float, lip
     _lib.check(rc, "solve_nnls")
 
 
+def solve_group(At, B, F0, Fout, *, max_iter: int, grad_tol: float, lipschitz_safety: float, status, group,
+                status_index: int = 0, next_bt=None, next_out=None) -> None:
+    """nenmf_solve_nnls_group: one half-step whose columns are split over the
+    ranks of ``group`` (a _lib.GroupStruct); B (r x c) this launch's columns,
+    next_out (nvr x p x k) one partial next product per virtual rank."""
+    lib, _ = _lib.require_device()
+    dt = _dt(At)
+    p, r = At.shape
+    c = F0.shape[1]
+    assert B.shape == (r, c)
+    k = min(r, p)
+    pv = _lib.power_vectors(k)
+    code = _lib.code_of(dt)
+    nk = next_bt.shape[0] if next_bt is not None else 0
+    ws = _lib.workspace(lib.nenmf_solve_nnls_next_workspace_bytes(code, r, p, c, nk))
+    rc = lib.nenmf_solve_nnls_group(code, At.data_ptr(), r, p, B.data_ptr(), c, B.shape[1], 0, F0.data_ptr(),
+                                    Fout.data_ptr(), int(max_iter), float(grad_tol), float(lipschitz_safety),
+                                    pv.data_ptr(), pv.shape[0], POWER_MAX_ITERS, POWER_TOL,
+                                    _lib.ptr(next_bt), nk, _lib.ptr(next_out), _lib.C.byref(group),
+                                    _lib.status_ptr(status, status_index), ws.data_ptr(), ws.numel(),
+                                    _lib.stream_handle())
+    _lib.check(rc, "solve_nnls_group")
+
+
 def spectral_norm_sq(At, tol: float, max_iters: int, out, status) -> None:
     lib, _ = _lib.require_device()
     dt = _dt(At)

@@ -2,6 +2,8 @@
 // Plain pointers and sizes only; dtype-dispatches into the templated kernels.
 #include "common.cuh"
 #include "nnls.cuh"
+#include "nnls_common.cuh"
+#include <cstring>
 #include "rsi.cuh"
 #include "skinny.cuh"
 
@@ -89,6 +91,72 @@ size_t nenmf_solve_nnls_next_workspace_bytes(int dtype, int64_t r, int64_t p, in
     best = a.used > best ? a.used : best;
   }
   return best + 256;
+}
+
+size_t nenmf_group_xch_bytes(void) { return sizeof(XchBuf); }
+
+int nenmf_solve_nnls_group_check(int dtype, int64_t r, int64_t p, int64_t c, int64_t next_k, int ranks, int nvr,
+                                 int max_iter) {
+  // the planning of nenmf_solve_nnls_group without a launch: OK when this
+  // shape runs as a group solve (the fused tensor-core path), else UNSUPPORTED
+  GroupHost g{};
+  g.ranks = ranks;
+  g.rank0 = 0;
+  g.nvr = nvr;
+  for (int v = 0; v <= nvr && v <= NG_MAXR; ++v) g.col0[v] = c * v / nvr;
+  for (int d = 0; d < NG_MAXR; ++d) g.xch[d] = reinterpret_cast<void*>(256);
+  g.epoch = 1;
+  Arena a(nullptr, 0);
+  return NENMF_DISPATCH(dtype, [&] {
+    const scalar_t* sent = reinterpret_cast<const scalar_t*>(256);
+    return solve_nnls<scalar_t>(a, sent, r, p, sent, c, c, false, sent, nullptr, max_iter, 1e-4, 1.0, nullptr, 1,
+                                100, 1e-9, nullptr, nullptr, next_k > 0 ? sent : nullptr, next_k,
+                                next_k > 0 ? const_cast<scalar_t*>(sent) : nullptr, nullptr, &g);
+  });
+}
+
+int nenmf_solve_nnls_group(int dtype, const void* At, int64_t r, int64_t p, const void* B, int64_t c, int64_t ldb,
+                           int trans_b, const void* F0, void* F_out, int max_iter, double grad_tol,
+                           double lipschitz_safety, const double* power_vectors, int power_count,
+                           int power_max_iters, double power_tol, const void* next_bt, int64_t next_k,
+                           void* next_out, const nenmf_group* group, nenmf_device_status* status, void* ws,
+                           size_t ws_bytes, void* stream) {
+  if (ws == nullptr || status == nullptr || group == nullptr) return NENMF_ERR_VALUE;
+  static_assert(sizeof(nenmf_group) == sizeof(GroupHost), "nenmf_group layout");
+  GroupHost g;
+  memcpy(&g, group, sizeof(g));
+  for (int d = 0; d < g.ranks && d < NG_MAXR; ++d)
+    if (g.xch[d] == nullptr) return NENMF_ERR_VALUE;
+  Arena a(ws, ws_bytes);
+  return NENMF_DISPATCH(dtype, [&] {
+    return solve_nnls<scalar_t>(a, C<scalar_t>(At), r, p, C<scalar_t>(B), c, ldb, trans_b != 0, C<scalar_t>(F0),
+                                M<scalar_t>(F_out), max_iter, grad_tol, lipschitz_safety, power_vectors,
+                                power_count, power_max_iters, power_tol, status, S(stream), C<scalar_t>(next_bt),
+                                next_k, M<scalar_t>(next_out), nullptr, &g);
+  });
+}
+
+int nenmf_ipc_handle(const void* dev_ptr, void* handle64) {
+  if (dev_ptr == nullptr || handle64 == nullptr) return NENMF_ERR_VALUE;
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "ipc handle size");
+  cudaIpcMemHandle_t h;
+  NENMF_CUDA_TRY(cudaIpcGetMemHandle(&h, const_cast<void*>(dev_ptr)));
+  memcpy(handle64, &h, 64);
+  return NENMF_OK;
+}
+
+int nenmf_ipc_open(const void* handle64, void** dev_ptr) {
+  if (handle64 == nullptr || dev_ptr == nullptr) return NENMF_ERR_VALUE;
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle64, 64);
+  NENMF_CUDA_TRY(cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return NENMF_OK;
+}
+
+int nenmf_ipc_close(void* dev_ptr) {
+  if (dev_ptr == nullptr) return NENMF_ERR_VALUE;
+  NENMF_CUDA_TRY(cudaIpcCloseMemHandle(dev_ptr));
+  return NENMF_OK;
 }
 
 size_t nenmf_solve_nnls_prepared_workspace_bytes(int dtype, int64_t r, int64_t p, int64_t c) {

@@ -192,11 +192,20 @@ static int launch_nnls(const NnlsPlan& pl, const T* W, const T* V, const T* F0, 
   return NENMF_ERR_UNSUPPORTED;
 }
 
+unsigned long long nn_watchdog_ns() {
+  static const unsigned long long ns = [] {
+    const char* e = getenv("NENMF_WATCHDOG_S");
+    const double sec = e != nullptr ? atof(e) : 0.0;
+    return sec > 0.0 ? (unsigned long long)(sec * 1e9) : NN_WATCHDOG_NS_DEFAULT;
+  }();
+  return ns;
+}
+
 template <typename T>
 int solve_nnls(Arena& ws, const T* At, int64_t r, int64_t p, const T* B, int64_t c, int64_t ldb, bool trans,
                const T* F0, T* Fout, int max_iter, double grad_tol, double safety, const double* pvec,
                int pcount, int pmax, double ptol, nenmf_device_status* st, cudaStream_t s, const T* Pt,
-               int64_t nup, T* Pout, const uint8_t* Xpre) {
+               int64_t nup, T* Pout, const uint8_t* Xpre, const GroupHost* grp) {
   if (r < 1 || p < 1 || c < 1) return NENMF_ERR_DIM;
   if (Pt != nullptr && (nup < 1 || Pout == nullptr)) return NENMF_ERR_VALUE;
   if (p > 64) return NENMF_ERR_UNSUPPORTED;
@@ -207,8 +216,27 @@ int solve_nnls(Arena& ws, const T* At, int64_t r, int64_t p, const T* B, int64_t
   // tensor-core solver: p <= 32 and at most 15 blocks of 8 columns per CTA
   int sms = sm_count();
   if (sms <= 0) sms = 148;
-  const int mgrid = (int)imax(1, imin(sms, cdiv(c, nnls_mma_col_block<T>())));
-  const int64_t mcpb = cdiv(c, mgrid);
+  const bool grouped = grp != nullptr && grp->ranks > 1;
+  int mgrid = (int)imax(1, imin(sms, cdiv(c, nnls_mma_col_block<T>())));
+  int64_t mcpb = cdiv(c, mgrid);
+  int grid_r = mgrid;
+  if (grouped) {
+    // a rank group: nvr virtual ranks of grid_r CTAs each in this
+    // launch (nvr = 1 on a real multi-GPU run); columns per CTA = the largest
+    // rank's share
+    if (grp->ranks > NG_MAXR || grp->nvr < 1 || grp->nvr > grp->ranks || grp->rank0 < 0 ||
+        grp->rank0 + grp->nvr > grp->ranks || grp->col0[0] != 0 || grp->col0[grp->nvr] != c || grp->epoch == 0 ||
+        grp->epoch >= (1ull << 40))
+      return NENMF_ERR_VALUE;
+    int64_t cmax = 1;
+    for (int v = 0; v < grp->nvr; ++v) {
+      if (grp->col0[v + 1] < grp->col0[v]) return NENMF_ERR_VALUE;
+      cmax = imax(cmax, grp->col0[v + 1] - grp->col0[v]);
+    }
+    grid_r = (int)imax(1, imin(sms / grp->nvr, cdiv(cmax, nnls_mma_col_block<T>())));
+    mgrid = grid_r * grp->nvr;
+    mcpb = cdiv(cmax, grid_r);
+  }
   const bool use_mma = p <= 32 && mcpb <= nnls_mma_max_cols<T>((int)p) && max_iter <= NN_WTAB_LEN &&
                        getenv("NENMF_NNLS_SIMT") == nullptr;
   // FP32, p <= 32, too many columns for the register-resident solver: the
@@ -232,6 +260,9 @@ int solve_nnls(Arena& ws, const T* At, int64_t r, int64_t p, const T* B, int64_t
                                   fused_smem_bytes(sizeof(T), (int)p, r, (int)cdiv(mcpb, cbm), cbm, mcpb) +
                                   (size_t)(p + nup) * mcpb * sizeof(T) <=
                               227 * 1024;
+  // a group solve runs only on the fused tensor-core path (its exchange lives
+  // in that kernel): other shapes are the caller's to replicate
+  if (grouped && !(fused && (Pt == nullptr || fused_next))) return NENMF_ERR_UNSUPPORTED;
   T* W = fused ? nullptr : ws.take<T>((size_t)p * p);
   T* V = fused ? nullptr : ws.take<T>((size_t)pc);
   double* Lbuf = ws.take<double>(4);
@@ -315,6 +346,17 @@ int solve_nnls(Arena& ws, const T* At, int64_t r, int64_t p, const T* B, int64_t
       a.nup = fused_next ? nup : 0;
       a.Pout = fused_next ? Pout : nullptr;
       a.npart = npart;
+      a.watchdog_ns = nn_watchdog_ns();
+      a.grp.ranks = 1;
+      if (grouped) {
+        a.grp.ranks = grp->ranks;
+        a.grp.rank0 = grp->rank0;
+        a.grp.nvr = grp->nvr;
+        a.grp.grid_r = grid_r;
+        for (int v = 0; v <= grp->nvr; ++v) a.grp.col0[v] = grp->col0[v];
+        for (int d = 0; d < grp->ranks; ++d) a.grp.xch[d] = static_cast<XchBuf*>(grp->xch[d]);
+        a.grp.epoch = grp->epoch;
+      }
       NENMF_TRY(launch_nnls_mma<T>(a, mgrid, s));
       if (fused) {
         if (Pt != nullptr && !fused_next) NENMF_TRY(abt<T>(ws, Fout, p, Pt, nup, c, Pout, s));
@@ -341,6 +383,7 @@ int solve_nnls(Arena& ws, const T* At, int64_t r, int64_t p, const T* B, int64_t
         a.recs = recs;
         a.results = results;
         a.st = st;
+        a.watchdog_ns = nn_watchdog_ns();
         NENMF_TRY(launch_nnls_stream(a, sgrid, s));
       }
     } else {
@@ -396,7 +439,7 @@ namespace nenmf {
 #define NENMF_INST_NNLS(T)                                                                                    \
   template int solve_nnls<T>(Arena&, const T*, int64_t, int64_t, const T*, int64_t, int64_t, bool, const T*,  \
                              T*, int, double, double, const double*, int, int, double, nenmf_device_status*,   \
-                             cudaStream_t, const T*, int64_t, T*, const uint8_t*);                           \
+                             cudaStream_t, const T*, int64_t, T*, const uint8_t*, const GroupHost*);         \
   template int spectral_norm_sq<T>(Arena&, const T*, int64_t, int64_t, const double*, int, int, double, double*, \
                                    nenmf_device_status*, cudaStream_t);                                      \
   template int gradient<T>(Arena&, const T*, int64_t, int64_t, const T*, int64_t, int64_t, bool, const T*,    \

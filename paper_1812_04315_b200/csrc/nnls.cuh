@@ -4,6 +4,15 @@
 
 namespace nenmf {
 
+struct GroupDev;
+// Host view of a rank group (C ABI nenmf_group, include/nenmf_b200.h).
+struct GroupHost {
+  int ranks, rank0, nvr, reserved;
+  int64_t col0[9];
+  void* xch[8];
+  unsigned long long epoch;
+};
+
 // Whole solve_nnls (nnls.py:119-227).  F_out receives the returned iterate;
 // F0 and F_out must not alias.  The caller zeroes *st before the first use.
 // Optional next product (Pt != nullptr): Pout (p x nup) = F_out Pt^T with Pt
@@ -16,7 +25,8 @@ template <typename T>
 int solve_nnls(Arena& ws, const T* At, int64_t r, int64_t p, const T* B, int64_t c, int64_t ldb, bool trans,
                const T* F0, T* Fout, int max_iter, double grad_tol, double safety, const double* pvec,
                int pcount, int pmax, double ptol, nenmf_device_status* st, cudaStream_t s,
-               const T* Pt = nullptr, int64_t nup = 0, T* Pout = nullptr, const uint8_t* Xpre = nullptr);
+               const T* Pt = nullptr, int64_t nup = 0, T* Pout = nullptr, const uint8_t* Xpre = nullptr,
+               const GroupHost* grp = nullptr);
 
 template <typename T>
 int spectral_norm_sq(Arena& ws, const T* At, int64_t r, int64_t p, const double* pvec, int pcount, int pmax,

@@ -19,9 +19,12 @@ __device__ __forceinline__ unsigned long long gtimer_ns() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
-// a grid that stops making progress for this long aborts with NENMF_ERR_CUDA
-// (iteration -2) instead of hanging the device
-constexpr unsigned long long NN_WATCHDOG_NS = 5000000000ull;
+// a grid that stops making progress for this long aborts with
+// NENMF_ERR_WATCHDOG instead of hanging the device; the host passes the limit
+// (NENMF_WATCHDOG_S, default 60 s: long enough for preemption, a debugger or
+// compute-sanitizer, and for the ranks of a group to reach the same solve)
+constexpr unsigned long long NN_WATCHDOG_NS_DEFAULT = 60000000000ull;
+unsigned long long nn_watchdog_ns();
 
 // optional per-iteration timeline (NENMF_NNLS_TRACE=1): [0] CTA 0 compute
 // warp 0 posts, [1] CTA 0 publishes, [2] CTA 0 resolves, [3] last CTA posts
@@ -39,6 +42,51 @@ struct __align__(16) WinRec {
   unsigned long long tag;  // window index + 1 once v is valid
   unsigned long long pad;
 };
+
+// ------------------------------------------------ rank groups
+// A solve whose columns are split over R ranks (one process per GPU, or R
+// "virtual ranks" emulated by one launch on one GPU for tests).  Every rank
+// runs the same persistent solver on its own columns; the per-iteration sums
+// of the decision protocol and the tie-break residuals are exchanged through
+// an exchange buffer on every rank (peer-mapped over NVLink; st.sys + release
+// tags), summed in rank order, so every rank takes the same decisions and the
+// same result as one GPU up to the summation order.
+constexpr int NG_MAXR = 8;
+constexpr int NG_XSLOTS = 2 * NW_FLIGHT + 4;  // window ring: a rank can run 2 x NW_FLIGHT windows ahead of a peer's reads
+struct __align__(16) XWin {
+  double v[NW_WIN][3];
+  unsigned long long tag[NW_WIN];  // (epoch << 20) | (window + 2) per iteration entry
+};
+struct __align__(16) XTie {
+  double b0, b1;
+  unsigned long long tag;  // epoch
+  unsigned long long pad;
+};
+struct __align__(16) XchBuf {
+  XWin win[NG_XSLOTS][NG_MAXR];  // [slot][source rank]
+  XTie tie[NG_MAXR];             // [source rank]
+};
+struct GroupDev {
+  int ranks;     // R (1: no group)
+  int rank0;     // rank of this launch's first virtual rank
+  int nvr;       // virtual ranks in this launch (1 per GPU; R when emulated)
+  int grid_r;    // CTAs per virtual rank
+  int64_t col0[NG_MAXR + 1];  // first column of each virtual rank in this launch's arrays
+  XchBuf* xch[NG_MAXR];       // every rank's exchange buffer
+  unsigned long long epoch;   // identical on all ranks, unique per solve
+};
+__device__ __forceinline__ void st_relaxed_sys_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_relaxed_sys_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void fence_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
+__device__ __forceinline__ unsigned long long xwin_tag(unsigned long long epoch, int w) {
+  return (epoch << 20) | (unsigned long long)(w + 2);
+}
 
 __device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
   unsigned long long v;
@@ -138,15 +186,25 @@ __device__ __forceinline__ void solver_shared_init(SolverShared& sh) {
 // order.  `pp` holds the compute warps' per-iteration sums [PPD][MAXW][3].
 static __device__ void resolver_warp(SolverShared& sh, const double* pp, int ncw, int max_iter, double grad_tol, double L,
                               WinRec* __restrict__ recs, WinRec* __restrict__ results,
-                              unsigned long long* __restrict__ tracebuf, int ppw = NW_MAXW) {
+                              unsigned long long* __restrict__ tracebuf, int ppw = NW_MAXW,
+                              const GroupDev* grp = nullptr, unsigned long long watchdog_ns = NN_WATCHDOG_NS_DEFAULT) {
   const int lane = threadIdx.x & 31;
   const int G = gridDim.x;
+  // group: this CTA's virtual rank and its CTA range; summarised windows go to
+  // every rank's exchange buffer instead of `results`
+  const bool grouped = grp != nullptr && grp->ranks > 1;
+  const int Gr = grouped ? grp->grid_r : G;
+  const int vr = grouped ? (int)blockIdx.x / Gr : 0;
+  const int lb = grouped ? (int)blockIdx.x % Gr : (int)blockIdx.x;
+  const int b_lo = vr * Gr, b_hi = b_lo + Gr;
+  const int myrank = grouped ? grp->rank0 + vr : 0;
+  auto xslot = [&](int w) { return (w + 1 + NG_XSLOTS) % NG_XSLOTS; };
   const bool trace = tracebuf != nullptr;
   auto g_nnls_trace = [&](int row) { return tracebuf + (size_t)row * NN_TRACE_LEN; };
     const int nwin = (max_iter + NW_WIN - 1) / NW_WIN;
     const int nq = (nwin + 1) * NW_WIN;  // pairs of windows -1 .. nwin-1
     int pubw = -1;                       // next window to publish (-1: the start point)
-    int sumq = (int)blockIdx.x;          // next owned (window, iteration) pair to summarize
+    int sumq = lb;                       // next owned (window, iteration) pair to summarize
     int ready_w = -2;                    // window whose records were all seen published
     int resw = -1;                       // next window to resolve
     int best_j = -1, stop_at = -1, fail_at = -1;
@@ -201,7 +259,7 @@ static __device__ void resolver_warp(SolverShared& sh, const double* pp, int ncw
         bool ok = w == ready_w;
         if (!ok) {
           ok = true;
-          for (int b = lane; b < G; b += 32) ok &= ld_relaxed_u64(&row[b].tag) == want;
+          for (int b = b_lo + lane; b < b_hi; b += 32) ok &= ld_relaxed_u64(&row[b].tag) == want;
           ok = __all_sync(0xffffffffu, ok);
           if (ok) ready_w = w;
         }
@@ -210,7 +268,7 @@ static __device__ void resolver_warp(SolverShared& sh, const double* pp, int ncw
           double v0 = 0.0, v1 = 0.0, v2 = 0.0;
           const int it = w < 0 ? (j == 0 ? -1 : INT_MAX) : w * NW_WIN + j;
           if (it <= win_last(w)) {
-            for (int b = lane; b < G; b += 32) {
+            for (int b = b_lo + lane; b < b_hi; b += 32) {
               v0 += __ldcg(&row[b].v[j][0]);
               v1 += __ldcg(&row[b].v[j][1]);
               v2 += __ldcg(&row[b].v[j][2]);
@@ -219,32 +277,67 @@ static __device__ void resolver_warp(SolverShared& sh, const double* pp, int ncw
             v1 = warp_sum(v1);
             v2 = warp_sum(v2);
           }
-          if (lane == 0) {
-            WinRec* res = results + rec_idx(w);
-            res->v[j][0] = v0;
-            res->v[j][1] = v1;
-            res->v[j][2] = v2;
-            __threadfence();
-            atomicAdd(&res->tag, 1ull);
-            if (trace && w + 1 < 1024 && j == 0) g_nnls_trace(3)[3072 + w + 1] = gtimer_ns();
+          if (!grouped) {
+            if (lane == 0) {
+              WinRec* res = results + rec_idx(w);
+              res->v[j][0] = v0;
+              res->v[j][1] = v1;
+              res->v[j][2] = v2;
+              __threadfence();
+              atomicAdd(&res->tag, 1ull);
+              if (trace && w + 1 < 1024 && j == 0) g_nnls_trace(3)[3072 + w + 1] = gtimer_ns();
+            }
+          } else if (lane < grp->ranks) {
+            // this rank's sums of (w, j) into every rank's exchange buffer (lane d -> rank d)
+            XWin* xw = &grp->xch[lane]->win[xslot(w)][myrank];
+            xw->v[j][0] = v0;
+            xw->v[j][1] = v1;
+            xw->v[j][2] = v2;
+            fence_sys();
+            st_relaxed_sys_u64(&xw->tag[j], xwin_tag(grp->epoch, w));
           }
           __syncwarp();
-          sumq += G;
+          sumq += Gr;
           progress = true;
         }
       }
       // C. resolve window resw
       {
         const WinRec* res = results + rec_idx(resw);
-        // results of a ring slot count 32 per use: window resw is the
-        // ((resw + 1) / NW_SLOTS)-th use of its slot
-        const unsigned long long want = (unsigned long long)NW_WIN * ((resw + 1) / NW_SLOTS + 1);
-        const bool ready = ld_relaxed_u64(&res->tag) >= want;  // same address in all lanes
+        bool ready;
+        if (!grouped) {
+          // results of a ring slot count 32 per use: window resw is the
+          // ((resw + 1) / NW_SLOTS)-th use of its slot
+          const unsigned long long want = (unsigned long long)NW_WIN * ((resw + 1) / NW_SLOTS + 1);
+          ready = ld_relaxed_u64(&res->tag) >= want;  // same address in all lanes
+        } else {
+          // every source rank's entry of this lane's iteration
+          const XWin* xr = grp->xch[myrank]->win[xslot(resw)];
+          const unsigned long long want = xwin_tag(grp->epoch, resw);
+          bool mine = true;
+          for (int src = 0; src < grp->ranks; ++src) mine &= ld_relaxed_sys_u64(&xr[src].tag[lane]) == want;
+          ready = __all_sync(0xffffffffu, mine);
+        }
         if (ready) {
-          fence_gpu();
-          const double r0 = __ldcg(&res->v[lane][0]);
-          const double r1 = __ldcg(&res->v[lane][1]);
-          const double r2 = __ldcg(&res->v[lane][2]);
+          double r0, r1, r2;
+          if (!grouped) {
+            fence_gpu();
+            r0 = __ldcg(&res->v[lane][0]);
+            r1 = __ldcg(&res->v[lane][1]);
+            r2 = __ldcg(&res->v[lane][2]);
+          } else {
+            fence_sys();
+            // summed in rank order: the same value on every rank
+            const XWin* xr = grp->xch[myrank]->win[xslot(resw)];
+            r0 = __ldcv(&xr[0].v[lane][0]);
+            r1 = __ldcv(&xr[0].v[lane][1]);
+            r2 = __ldcv(&xr[0].v[lane][2]);
+            for (int src = 1; src < grp->ranks; ++src) {
+              r0 += __ldcv(&xr[src].v[lane][0]);
+              r1 += __ldcv(&xr[src].v[lane][1]);
+              r2 += __ldcv(&xr[src].v[lane][2]);
+            }
+          }
           const int first = win_first(resw), last = win_last(resw);
           if (resw < 0) {
             // the start point (nnls.py:178-181)
@@ -312,7 +405,7 @@ static __device__ void resolver_warp(SolverShared& sh, const double* pp, int ncw
         t_prog = gtimer_ns();
       } else {
         __nanosleep(32);
-        if (gtimer_ns() - t_prog > NN_WATCHDOG_NS) {
+        if (gtimer_ns() - t_prog > watchdog_ns) {
           fail_at = -2;
           halt = true;
         }
@@ -374,6 +467,8 @@ struct MmaArgs {
   int64_t nup;
   T* Pout;
   double* npart;      // [grid][p][nup] per-CTA partials
+  GroupDev grp;       // rank group (grp.ranks == 1: a single-GPU solve)
+  unsigned long long watchdog_ns;
 };
 template <typename T>
 int launch_nnls_mma(const MmaArgs<T>& a, int grid, cudaStream_t s);
@@ -396,6 +491,7 @@ struct StreamArgs {
   WinRec* results;
   nenmf_device_status* st;
   int resident;     // 1: u_k and V of the CTA's columns stay in shared memory (set by the launcher)
+  unsigned long long watchdog_ns;
 };
 
 // 1 when the launch keeps its state in shared memory (the CTA's columns fit)

@@ -332,7 +332,7 @@ k_nnls(const T* __restrict__ W, const T* __restrict__ V, const T* __restrict__ F
     }
     if (lane == 0) sh.kdone[wid] = k;  // warps may stop at different k; each keeps its own columns
   } else {
-    resolver_warp(sh, pp, ncw, max_iter, grad_tol, L, recs, results, tracebuf);
+    resolver_warp(sh, pp, ncw, max_iter, grad_tol, L, recs, results, tracebuf, NW_MAXW, nullptr, NN_WATCHDOG_NS_DEFAULT);
   }
   __syncthreads();  // compute warps done; decisions final
 
@@ -407,7 +407,7 @@ k_nnls(const T* __restrict__ W, const T* __restrict__ V, const T* __restrict__ F
   }
   if (blockIdx.x == 0 && tid == 0) {
     if (sh.fail_at >= 0) status_fail(st, NENMF_ERR_NUMERICAL_FAILURE, sh.fail_at);
-    if (sh.fail_at == -2) status_fail(st, NENMF_ERR_CUDA, -2);
+    if (sh.fail_at == -2) status_fail(st, NENMF_ERR_WATCHDOG, -2);
     st->inner_iters = sh.stop_at >= 0 ? sh.stop_at + 1 : (sh.fail_at >= 0 ? sh.fail_at : max_iter);
     st->returned_best = sh.best_j >= 0 ? 1 : 0;
     st->best_partial = sh.best_part;

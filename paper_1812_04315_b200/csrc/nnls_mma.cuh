@@ -19,10 +19,12 @@ namespace nenmf {
 // accumulator fragment of n-tile t IS the A fragment of k-tile t, so an
 // iteration never leaves registers: elementwise update on the accumulator
 // layout -> A fragments -> MMAs -> next accumulator.
-//   FP32: 16 columns per warp, split precision: hi*hi on m16n8k8 TF32 and
-//         the two correction terms lo*hi + hi*lo as ONE m16n8k16 BF16 MMA per
-//         k-tile (K = [F_lo | F_hi] against [W_hi ; W_lo]); 18 instead of 27
-//         MMAs per iteration at p <= 24, W^T fragments resident
+//   FP32: 16 columns per warp, 3xTF32: hi*hi, lo*hi and hi*lo on m16n8k8
+//         TF32 (relative error ~2^-21 per product; an earlier variant folded
+//         the corrections into one BF16 m16n8k16 MMA -- 18 instead of 27 MMAs
+//         -- but its 8-bit operands left one-step factors ~1.3e-3 from the
+//         fp64 reference, outside the FP32 mode's 1e-3); 27 MMAs per
+//         iteration at p <= 24, W^T fragments resident
 //   FP64: m8n8k4 F64, 8 columns per warp, exact products
 template <typename T>
 struct MmaShape;
@@ -35,13 +37,17 @@ struct MmaShape<double> {
   static constexpr int CB = 8, EPT = 2;
 };
 
-// 3xTF32 split by truncation: hi keeps the top 10 mantissa bits (exactly
-// representable), lo = x - hi is exact in fp32 and is handed to the MMA raw
-// (the tensor core ignores its low 13 bits).  Two instructions per value
-// instead of the cvt.rna sequence; the dropped lo*lo term and lo's truncation
-// leave a relative error ~2^-20 per product, fp32-class.
+// 3xTF32 split: hi keeps the top 10 mantissa bits by truncation (exactly
+// representable), lo = x - hi is exact in fp32 and rounded to nearest TF32;
+// the dropped lo*lo term and lo's rounding leave a relative error ~2^-22 per
+// product.
 __device__ __forceinline__ uint32_t tf32_hi(float x) { return __float_as_uint(x) & 0xffffe000u; }
-__device__ __forceinline__ uint32_t tf32_lo(float x, uint32_t hi) { return __float_as_uint(x - __uint_as_float(hi)); }
+// the residual rounded to nearest TF32 (the tensor core would truncate it)
+__device__ __forceinline__ uint32_t tf32_lo(float x, uint32_t hi) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x - __uint_as_float(hi)));
+  return r;
+}
 
 // CTA size each instantiation is compiled for (register budget per thread:
 // 5 state arrays of 4*NT (fp32) / 2*NT doubles, resident W fragments, the
@@ -107,8 +113,17 @@ k_nnls_mma(const __grid_constant__ MmaArgs<T> A) {
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int ncw = (blockDim.x >> 5) - 1;
   const bool resolver = wid == ncw;
-  const int64_t j0 = (int64_t)blockIdx.x * cpb;
-  const int ncols = (int)(imin(c, j0 + cpb) - j0);
+  // rank group: the launch's CTAs split into virtual ranks of
+  // grid_r CTAs; each virtual rank owns the columns [col0[vr], col0[vr + 1])
+  const bool grouped = A.grp.ranks > 1;
+  const int Gr = grouped ? A.grp.grid_r : (int)gridDim.x;
+  const int vr = grouped ? (int)blockIdx.x / Gr : 0;
+  const int lb = grouped ? (int)blockIdx.x % Gr : (int)blockIdx.x;
+  const int g_lo = vr * Gr, g_hi = g_lo + Gr;
+  const int64_t vc0 = grouped ? A.grp.col0[vr] : 0, vc1 = grouped ? A.grp.col0[vr + 1] : c;
+  const int64_t vcpb = grouped ? (vc1 - vc0 + Gr - 1) / Gr : cpb;
+  const int64_t j0 = vc0 + (int64_t)lb * vcpb;
+  const int ncols = (int)imax(0, imin(vc1, j0 + vcpb) - j0);
   const int gq = lane >> 2, tq = lane & 3;
   solver_shared_init(sh);
   __syncthreads();
@@ -383,24 +398,20 @@ k_nnls_mma(const __grid_constant__ MmaArgs<T> A) {
       return (i < p && l < p) ? (fused ? W_s[i * 32 + l] : W[i * p + l]) : T(0);
     };
     // W^T fragments (B operand), resident for the whole solve; b[kt][nt]:
-    // bhi = TF32 hi (m16n8k8), bco = BF16 [W_hi ; W_lo] of the correction MMA
-    uint32_t bhi[NT][NT][2], bco[NT][NT][2];
+    // bhi = TF32 hi (m16n8k8), blo = the residual W - W_hi (TF32 correction MMAs)
+    uint32_t bhi[NT][NT][2], blo[NT][NT][2];
     double bd[2 * NT][NT];
     if constexpr (S::EPT == 4) {
 #pragma unroll
       for (int kt = 0; kt < NT; ++kt)
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) {
-          float wh[2], wl[2];
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             const float w = (float)wval(8 * nt + gq, 8 * kt + 2 * tq + h);
             bhi[kt][nt][h] = tf32_hi(w);
-            wh[h] = __uint_as_float(bhi[kt][nt][h]);
-            wl[h] = w - wh[h];
+            blo[kt][nt][h] = tf32_lo(w, bhi[kt][nt][h]);
           }
-          bco[kt][nt][0] = pack_bf16(wh[0], wh[1]);  // K 2tq, 2tq+1   <-> F_lo rows
-          bco[kt][nt][1] = pack_bf16(wl[0], wl[1]);  // K 2tq+8, 2tq+9 <-> F_hi rows
         }
     } else {
 #pragma unroll
@@ -416,7 +427,7 @@ k_nnls_mma(const __grid_constant__ MmaArgs<T> A) {
     auto grad = [&](const T (&fe)[NE], T (&g)[NE]) {
       if constexpr (S::EPT == 4) {
         // accumulator element (col, row): c0 (gq, 2tq), c1 (gq, 2tq+1), c2 (gq+8, 2tq), c3 (gq+8, 2tq+1)
-        uint32_t ahi[NT][4], aco[NT][4];
+        uint32_t ahi[NT][4], alo[NT][4];
 #pragma unroll
         for (int t = 0; t < NT; ++t) {
           const float c0 = (float)fe[4 * t + 0], c1 = (float)fe[4 * t + 1], c2 = (float)fe[4 * t + 2],
@@ -426,12 +437,10 @@ k_nnls_mma(const __grid_constant__ MmaArgs<T> A) {
           ahi[t][1] = h2;  // (gq+8, K slot tq)
           ahi[t][2] = h1;  // (gq,   K slot tq+4 -> row 2tq+1)
           ahi[t][3] = h3;
-          const float f0 = __uint_as_float(h0), f1 = __uint_as_float(h1), f2 = __uint_as_float(h2),
-                      f3 = __uint_as_float(h3);
-          aco[t][0] = pack_bf16(c0 - f0, c1 - f1);  // (gq,   K 2tq, 2tq+1): F_lo
-          aco[t][1] = pack_bf16(c2 - f2, c3 - f3);  // (gq+8, K 2tq, 2tq+1)
-          aco[t][2] = pack_bf16(f0, f1);            // (gq,   K 2tq+8, 2tq+9): F_hi
-          aco[t][3] = pack_bf16(f2, f3);
+          alo[t][0] = tf32_lo(c0, h0);
+          alo[t][1] = tf32_lo(c2, h2);
+          alo[t][2] = tf32_lo(c1, h1);
+          alo[t][3] = tf32_lo(c3, h3);
         }
         // n-tiles innermost: consecutive MMAs are independent, so the NT
         // accumulation chains overlap in the tensor pipe
@@ -443,7 +452,10 @@ k_nnls_mma(const __grid_constant__ MmaArgs<T> A) {
 #pragma unroll
         for (int kt = 0; kt < NT; ++kt)  // correction terms F_lo W_hi + F_hi W_lo first (small)
 #pragma unroll
-          for (int nt = 0; nt < NT; ++nt) mma_bf16(cc[nt], aco[kt], bco[kt][nt][0], bco[kt][nt][1]);
+          for (int nt = 0; nt < NT; ++nt) {
+            mma_tf32(cc[nt], alo[kt], bhi[kt][nt][0], bhi[kt][nt][1]);
+            mma_tf32(cc[nt], ahi[kt], blo[kt][nt][0], blo[kt][nt][1]);
+          }
 #pragma unroll
         for (int kt = 0; kt < NT; ++kt)
 #pragma unroll
@@ -823,7 +835,9 @@ k_nnls_mma(const __grid_constant__ MmaArgs<T> A) {
       }
       __syncwarp();
     }
-    if (!(dbg & 1)) resolver_warp(sh, pp, ncw, max_iter, A.grad_tol, L, A.recs, A.results, tracebuf);
+    if (!(dbg & 1))
+      resolver_warp(sh, pp, ncw, max_iter, A.grad_tol, L, A.recs, A.results, tracebuf, NW_MAXW, &A.grp,
+                    A.watchdog_ns);
     if (tracebuf != nullptr && blockIdx.x == 0 && lane == 0) tracebuf[NN_TRACE_LEN + 60 + 14] = gtimer_ns();
     asm volatile("bar.sync 1, %0;" ::"r"(blockDim.x) : "memory");
   }
@@ -861,8 +875,8 @@ k_nnls_mma(const __grid_constant__ MmaArgs<T> A) {
           A.rpart[2 * blockIdx.x + 1] = a1;
         }
         __threadfence();
-        atomicAdd(A.bar, 1u);
-        while (ld_acquire_u32(A.bar) < gridDim.x) __nanosleep(32);
+        atomicAdd(A.bar + vr, 1u);
+        while (ld_acquire_u32(A.bar + vr) < (unsigned)Gr) __nanosleep(32);
       }
       __syncthreads();
     }
@@ -870,13 +884,13 @@ k_nnls_mma(const __grid_constant__ MmaArgs<T> A) {
     // while warp 0 reduces the tie-break residuals (same order as below)
     __shared__ double s_pout[32];
     const int nwarps_all = (int)(blockDim.x >> 5);
-    const int per_s = next ? (no + (int)gridDim.x - 1) / (int)gridDim.x : 0;
-    const int os0 = (int)blockIdx.x * per_s, os1 = min(no, os0 + per_s);
+    const int per_s = next ? (no + Gr - 1) / Gr : 0;
+    const int os0 = lb * per_s, os1 = min(no, os0 + per_s);
     const bool pre = next && ok_best && per_s <= 32 && nwarps_all > 1;
     if (pre && wid >= 1) {
       for (int o = os0 + wid - 1; o < os1; o += nwarps_all - 1) {
         double sacc = 0.0;
-        for (int g = lane; g < (int)gridDim.x; g += 32) sacc += __ldcg(&A.npart[((size_t)g * 2) * no + o]);
+        for (int g = g_lo + lane; g < g_hi; g += 32) sacc += __ldcg(&A.npart[((size_t)g * 2) * no + o]);
         sacc = warp_sum(sacc);
         if (lane == 0) s_pout[o - os0] = sacc;
       }
@@ -886,12 +900,42 @@ k_nnls_mma(const __grid_constant__ MmaArgs<T> A) {
         // CTA partials summed lane-strided then by a fixed butterfly: the same
         // order (and value) in every CTA
         double b0 = 0.0, b1 = 0.0;
-        for (int g = lane; g < (int)gridDim.x; g += 32) {
+        for (int g = g_lo + lane; g < g_hi; g += 32) {
           b0 += __ldcg(&A.rpart[2 * g]);
           b1 += __ldcg(&A.rpart[2 * g + 1]);
         }
         b0 = warp_sum(b0);
         b1 = warp_sum(b1);
+        if (grouped) {
+          // this rank's residual sums to every rank (the rank's first CTA),
+          // then every CTA sums all ranks' in rank order
+          const int myrank = A.grp.rank0 + vr;
+          if (lb == 0 && lane < A.grp.ranks) {
+            XTie* xt = &A.grp.xch[lane]->tie[myrank];
+            xt->b0 = b0;
+            xt->b1 = b1;
+            fence_sys();
+            st_relaxed_sys_u64(&xt->tag, A.grp.epoch);
+          }
+          const XTie* xt = A.grp.xch[myrank]->tie;
+          const unsigned long long t0 = gtimer_ns();
+          for (;;) {
+            const bool mine = lane >= A.grp.ranks || ld_relaxed_sys_u64(&xt[lane].tag) == A.grp.epoch;
+            if (__all_sync(0xffffffffu, mine)) break;
+            __nanosleep(64);
+            if (gtimer_ns() - t0 > A.watchdog_ns) {
+              if (lane == 0) status_fail(st, NENMF_ERR_WATCHDOG, -2);
+              break;
+            }
+          }
+          fence_sys();
+          b0 = __ldcv(&xt[0].b0);
+          b1 = __ldcv(&xt[0].b1);
+          for (int src = 1; src < A.grp.ranks; ++src) {
+            b0 += __ldcv(&xt[src].b0);
+            b1 += __ldcv(&xt[src].b1);
+          }
+        }
         if (lane == 0) {
           const double nb = sqrt(b0), ns = sqrt(b1);
           const double tb = 0.5 * (nb * nb), ts = 0.5 * (ns * ns);
@@ -915,8 +959,8 @@ k_nnls_mma(const __grid_constant__ MmaArgs<T> A) {
       __syncthreads();
       if (tid == 0) {
         __threadfence();
-        atomicAdd(A.bar, 1u);
-        while (ld_acquire_u32(A.bar) < 2 * gridDim.x) __nanosleep(32);
+        atomicAdd(A.bar + vr, 1u);
+        while (ld_acquire_u32(A.bar + vr) < 2u * (unsigned)Gr) __nanosleep(32);
       }
       __syncthreads();
     }
@@ -925,25 +969,28 @@ k_nnls_mma(const __grid_constant__ MmaArgs<T> A) {
       for (int e = 0; e < NE; ++e)
         if (evalid(e)) Fout[eoff(e)] = F0[eoff(e)];
     }
+    // the next product: this (virtual) rank's partial sum over its columns
+    // (a group's ranks add theirs with one all-reduce of p x nup afterwards)
+    T* Pout_r = next ? A.Pout + (size_t)vr * no : nullptr;
     if (next && pre && !start_wins) {
-      for (int i = tid; i < os1 - os0; i += (int)blockDim.x) A.Pout[os0 + i] = (T)s_pout[i];
+      for (int i = tid; i < os1 - os0; i += (int)blockDim.x) Pout_r[os0 + i] = (T)s_pout[i];
     } else if (next) {
       const int cand = (ok_best && !start_wins) ? 0 : 1;
-      const int per = (no + (int)gridDim.x - 1) / (int)gridDim.x;
-      const int o0 = (int)blockIdx.x * per, o1 = min(no, o0 + per);
+      const int per = (no + Gr - 1) / Gr;
+      const int o0 = lb * per, o1 = min(no, o0 + per);
       const int nwarps = blockDim.x >> 5;
       for (int o = o0 + wid; o < o1; o += nwarps) {
         double sacc = 0.0;
-        for (int g = lane; g < (int)gridDim.x; g += 32) sacc += __ldcg(&A.npart[((size_t)g * 2 + cand) * no + o]);
+        for (int g = g_lo + lane; g < g_hi; g += 32) sacc += __ldcg(&A.npart[((size_t)g * 2 + cand) * no + o]);
         sacc = warp_sum(sacc);
-        if (lane == 0) A.Pout[o] = (T)sacc;
+        if (lane == 0) Pout_r[o] = (T)sacc;
       }
     }
   }
   if (tracebuf != nullptr && blockIdx.x == 0 && tid == 0) tracebuf[NN_TRACE_LEN + 60 + 10] = gtimer_ns();
   if (blockIdx.x == 0 && tid == 0) {
     if (sh.fail_at >= 0) status_fail(st, NENMF_ERR_NUMERICAL_FAILURE, sh.fail_at);
-    if (sh.fail_at == -2) status_fail(st, NENMF_ERR_CUDA, -2);
+    if (sh.fail_at == -2) status_fail(st, NENMF_ERR_WATCHDOG, -2);
     st->inner_iters = sh.stop_at >= 0 ? sh.stop_at + 1 : (sh.fail_at >= 0 ? sh.fail_at : max_iter);
     st->returned_best = (bj >= 0 && !start_wins) ? 1 : 0;
     st->best_partial = sh.best_part;

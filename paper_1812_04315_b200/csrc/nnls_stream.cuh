@@ -2,8 +2,9 @@
 // register-resident solver holds (BASELINE cfg4's G-half: 400 000 columns,
 // cfg5's: 100 000; nnls.py:160-227).
 //
-// Same arithmetic per 16-column tile as k_nnls_mma (TF32 hi x hi + one BF16
-// correction MMA per k-tile, accumulators reused as the next A operand) and
+// Same arithmetic per 16-column tile as k_nnls_mma (3xTF32: hi x hi plus the
+// two TF32 correction MMAs per k-tile, accumulators reused as the next A
+// operand) and
 // the same windowed decision protocol (resolver warp, window records, fixed
 // order sums), but the iterate state lives in HBM: per iteration every warp
 // sweeps its tiles, reading u_{k-1}, u_{k-2} and V and writing u_k (16 bytes
@@ -87,17 +88,15 @@ __global__ void __launch_bounds__(stream_threads<NT>(), 1) k_nnls_stream(const _
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) {
         if (WSM && (kt * NT + nt) % ncw != wid) continue;  // fill the shared copy cooperatively
-        float wh[2], wl[2];
-        uint32_t h2[2];
+        uint32_t h2[2], l2[2];
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int i = 8 * nt + gq, l = 8 * kt + 2 * tq + h;
           const float w = (i < p && l < p) ? A.W[i * p + l] : 0.f;
           h2[h] = tf32_hi(w);
-          wh[h] = __uint_as_float(h2[h]);
-          wl[h] = w - wh[h];
+          l2[h] = tf32_lo(w, h2[h]);
         }
-        const uint32_t c0 = pack_bf16(wh[0], wh[1]), c1 = pack_bf16(wl[0], wl[1]);
+        const uint32_t c0 = l2[0], c1 = l2[1];  // the W residual (3xTF32 corrections)
         if constexpr (WSM) {
           wf[(kt * NT + nt) * 32 + lane] = make_uint4(h2[0], h2[1], c0, c1);
         } else {
@@ -118,12 +117,10 @@ __global__ void __launch_bounds__(stream_threads<NT>(), 1) k_nnls_stream(const _
         ahi[t][1] = h2;
         ahi[t][2] = h1;
         ahi[t][3] = h3;
-        const float f0 = __uint_as_float(h0), f1 = __uint_as_float(h1), f2 = __uint_as_float(h2),
-                    f3 = __uint_as_float(h3);
-        aco[t][0] = pack_bf16(c0 - f0, c1 - f1);
-        aco[t][1] = pack_bf16(c2 - f2, c3 - f3);
-        aco[t][2] = pack_bf16(f0, f1);
-        aco[t][3] = pack_bf16(f2, f3);
+        aco[t][0] = tf32_lo(c0, h0);  // F residual, same slots as ahi
+        aco[t][1] = tf32_lo(c2, h2);
+        aco[t][2] = tf32_lo(c1, h1);
+        aco[t][3] = tf32_lo(c3, h3);
       }
       float cc[NT][4];
 #pragma unroll
@@ -136,15 +133,18 @@ __global__ void __launch_bounds__(stream_threads<NT>(), 1) k_nnls_stream(const _
 #pragma unroll
           for (int nt = 0; nt < NT; ++nt) {
             const uint4 b = wf[(kt * NT + nt) * 32 + lane];
-            mma_bf16(cc[nt], aco[kt], b.z, b.w);
+            mma_tf32(cc[nt], aco[kt], b.x, b.y);  // F_lo W_hi
+            mma_tf32(cc[nt], ahi[kt], b.z, b.w);  // F_hi W_lo
             mma_tf32(cc[nt], ahi[kt], b.x, b.y);
           }
       } else {
 #pragma unroll
         for (int kt = 0; kt < NT; ++kt)
 #pragma unroll
-          for (int nt = 0; nt < NT; ++nt)
-            mma_bf16(cc[nt], aco[kt], bco[kt % NTR][nt % NTR][0], bco[kt % NTR][nt % NTR][1]);
+          for (int nt = 0; nt < NT; ++nt) {
+            mma_tf32(cc[nt], aco[kt], bhi[kt % NTR][nt % NTR][0], bhi[kt % NTR][nt % NTR][1]);
+            mma_tf32(cc[nt], ahi[kt], bco[kt % NTR][nt % NTR][0], bco[kt % NTR][nt % NTR][1]);
+          }
 #pragma unroll
         for (int kt = 0; kt < NT; ++kt)
 #pragma unroll
@@ -450,14 +450,15 @@ __global__ void __launch_bounds__(stream_threads<NT>(), 1) k_nnls_stream(const _
       }
     }
   } else {
-    resolver_warp(sh, pp, ncw, max_iter, A.grad_tol, L, A.recs, A.results, nullptr, SS<NT>::PPW);
+    resolver_warp(sh, pp, ncw, max_iter, A.grad_tol, L, A.recs, A.results, nullptr, SS<NT>::PPW, nullptr,
+                  A.watchdog_ns);
     asm volatile("bar.sync 1, %0;" ::"r"(blockDim.x) : "memory");
   }
   __syncthreads();
   if (blockIdx.x == 0 && tid == 0) {
     nenmf_device_status* st = A.st;
     if (sh.fail_at >= 0) status_fail(st, NENMF_ERR_NUMERICAL_FAILURE, sh.fail_at);
-    if (sh.fail_at == -2) status_fail(st, NENMF_ERR_CUDA, -2);
+    if (sh.fail_at == -2) status_fail(st, NENMF_ERR_WATCHDOG, -2);
     st->inner_iters = sh.stop_at >= 0 ? sh.stop_at + 1 : (sh.fail_at >= 0 ? sh.fail_at : max_iter);
     st->returned_best = sh.best_j >= 0 ? 1 : 0;
     st->best_partial = sh.best_part;

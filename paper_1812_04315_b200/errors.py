@@ -69,6 +69,7 @@ ST_VALUE = 5
 ST_CUDA = 6
 ST_WORKSPACE = 7
 ST_UNSUPPORTED = 8
+ST_WATCHDOG = 9  # a persistent solve made no progress for NENMF_WATCHDOG_S seconds (default 60)
 
 
 def raise_for_status(code: int, iteration: int = -1, what: str = "") -> None:
@@ -89,4 +90,7 @@ def raise_for_status(code: int, iteration: int = -1, what: str = "") -> None:
         raise ValueError(f"invalid value{where}")
     if code == ST_UNSUPPORTED:
         raise BackendError(f"shape outside the kernels' supported range{where}")
+    if code == ST_WATCHDOG:
+        raise BackendError(f"solver made no progress within NENMF_WATCHDOG_S (a stalled peer rank or a "
+                           f"preempted device){where}")
     raise BackendError(f"libnenmf_b200 status {code}{where}")

@@ -275,6 +275,120 @@ class _ShardedDeviceLoop(_DeviceLoop):
         return math.sqrt(self.scal[1].item())
 
 
+class _GroupDeviceLoop(_DeviceLoop):
+    """Compressed NeNMF with every inner solve split by columns over the ranks
+    of a SolveGroup (group.py).
+
+    Real group (one process per GPU, group.nvr == 1): this rank holds rows
+    [row0, row0 + n_r) of X, its columns of X_R^T and L (from the sharded
+    compression), the replicated X_L and R^T; it solves its n_r columns of
+    G^T and its slice [m0, m0 + m_r) of F's columns; the partial next products
+    (L_r G_r and F_r R_r) are all-reduced, F is all-gathered at emits.
+
+    Emulated group (group.nvr == R, one GPU): the whole problem in this
+    process, each solve ONE launch whose CTAs form R virtual ranks over the
+    same column split; the per-rank partial next products are summed here."""
+
+    def __init__(self, X_local, n: int, row0: int, init: FactorPair, L_local, Rt, XL, XRt_local, group, comm=None):
+        _, torch = _lib.require_device()
+        self.torch = torch
+        self.X = X_local if X_local.is_contiguous() else X_local.contiguous()
+        self.dtype = "fp64" if X_local.dtype == torch.float64 else "fp32"
+        self.n, self.m = int(n), int(X_local.shape[1])
+        self.row0, self.n_r = int(row0), int(X_local.shape[0])
+        self.p = init.p
+        self.sketch = "group"
+        self.scal = _lib.zeros(4, torch.float64)
+        self.status = _lib.new_status(_STATUS_CAP)
+        self.pending = []
+        self.group, self.comm = group, comm
+        self.emulated = group.nvr > 1
+        self._ops_in = (L_local, Rt, XL, XRt_local)
+
+    def norm_x(self) -> float:
+        _lib.zero_(self.scal[0:1])
+        _ops.sumsq(self.X, self.scal[0:1])
+        if not self.emulated:
+            self.comm.all_reduce(self.scal[0:1])
+        return math.sqrt(self.scal[0].item())
+
+    def prepare(self, init: FactorPair) -> None:
+        from .group import partition
+        from .sharded import row_block
+
+        torch = self.torch
+        L, Rt, XL, XRt = self._ops_in
+        nu = Rt.shape[0]
+        G = init.G
+        Gt_full = _panel_t(G, self.dtype)
+        F_full = _lib.to_device(init.F, self.dtype)
+        R = self.group.ranks
+        # the first G-half's F R from the (replicated) initial F
+        self.FR = torch.empty((self.p, nu), dtype=self.X.dtype, device="cuda")
+        _ops.abt(F_full, Rt, self.FR)
+        self.GLt = torch.empty((self.p, nu), dtype=self.X.dtype, device="cuda")
+        self.L, self.Rt_full = L, Rt
+        if self.emulated:
+            self.Gt = Gt_full
+            self.F = F_full if F_full is not init.F else F_full.clone()
+            self.XRt, self.XL_s, self.Rt_s = XRt, XL, Rt
+            self.g_cols, self.f_cols = partition(self.n, R), partition(self.m, R)
+        else:
+            self.Gt = Gt_full[:, self.row0:self.row0 + self.n_r].contiguous()
+            self.m0, self.m_r = row_block(self.m, R, self.group.rank)
+            self.F = F_full[:, self.m0:self.m0 + self.m_r].contiguous()
+            self.XRt = XRt
+            self.XL_s = XL[:, self.m0:self.m0 + self.m_r].contiguous()
+            self.Rt_s = Rt[:, self.m0:self.m0 + self.m_r].contiguous()
+            self.g_cols, self.f_cols = [0, self.n_r], [0, self.m_r]
+        self.Gt_alt = torch.empty_like(self.Gt)
+        self.F_alt = torch.empty_like(self.F)
+        self.part = torch.empty((self.group.nvr, self.p, nu), dtype=self.X.dtype, device="cuda")
+
+    def _reduce_next(self, out) -> None:
+        if self.emulated:
+            self.torch.sum(self.part, dim=0, out=out)
+        else:
+            out.copy_(self.part[0])
+            self.comm.all_reduce(out)
+
+    def half_steps(self, t: int, icfg: InnerSolverConfig) -> None:
+        kw = dict(max_iter=icfg.max_iter, grad_tol=icfg.grad_tol, lipschitz_safety=icfg.lipschitz_safety,
+                  status=self.status)
+        # G-half: A = (F R)^T, B = X_R^T (factorize.py:109-110), columns = G's rows
+        _ops.solve_group(self.FR, self.XRt, self.Gt, self.Gt_alt, group=self.group.struct(self.g_cols),
+                         status_index=self._slot(t, "G"), next_bt=self.L, next_out=self.part, **kw)
+        self.Gt, self.Gt_alt = self.Gt_alt, self.Gt
+        self._reduce_next(self.GLt)
+        # F-half: A = L G, B = X_L (factorize.py:112-113), columns = F's columns
+        _ops.solve_group(self.GLt, self.XL_s, self.F, self.F_alt, group=self.group.struct(self.f_cols),
+                         status_index=self._slot(t, "F"), next_bt=self.Rt_s, next_out=self.part, **kw)
+        self.F, self.F_alt = self.F_alt, self.F
+        self._reduce_next(self.FR)
+
+    def stop_vote(self, stop: bool) -> bool:
+        return stop if self.emulated else self.comm.any(stop)
+
+    def full_F(self):
+        return self.F if self.emulated else self.comm.all_gather_cols(self.F, self.m)
+
+    def objective(self) -> float:
+        _lib.zero_(self.scal[1:2])
+        _ops.residual_sumsq(self.X, self.Gt, self.full_F(), self.scal[1:2])
+        if not self.emulated:
+            self.comm.all_reduce(self.scal[1:2])
+        return math.sqrt(self.scal[1].item())
+
+    def full_Gt(self):
+        return self.Gt if self.emulated else self.comm.all_gather_cols(self.Gt, self.n)
+
+    def host_factors(self):
+        return _lib.to_host(self.full_Gt()).T.copy(), _lib.to_host(self.full_F())
+
+    def device_factors(self):
+        return self.full_Gt().t(), self.full_F()
+
+
 def _run_outer(X, init: FactorPair, cfg: OuterConfig, observer, clock, sketch, dtype: str,
                return_device: bool = False, run: _DeviceLoop | None = None) -> FactorPair:
     if run is not None:
@@ -350,6 +464,9 @@ def _run_outer(X, init: FactorPair, cfg: OuterConfig, observer, clock, sketch, d
         emit(t)
     run.drain()
     if return_device:
+        if hasattr(run, "device_factors"):
+            G, F = run.device_factors()
+            return FactorPair(G=G, F=F, p=init.p)
         return FactorPair(G=run.Gt.t(), F=run.F, p=init.p)
     G, F = run.host_factors()
     return FactorPair(G=G, F=F, p=init.p)

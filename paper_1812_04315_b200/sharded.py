@@ -272,18 +272,75 @@ def gather_sketch(sketch: ShardedSketch, *, comm: Comm | None = None) -> SketchP
     return pair
 
 
+def _group_for(comm: Comm):
+    """The SolveGroup of this communicator (created once: IPC-mapped buffers)."""
+    from .group import SolveGroup
+
+    g = getattr(comm, "_solve_group", None)
+    if g is None:
+        g = comm._solve_group = SolveGroup.over(comm)
+    return g
+
+
 def factorize_compressed_sharded(X_local, n: int, sketch: ShardedSketch, init, cfg=None, observer=None, clock=None,
-                                 *, comm: Comm | None = None, return_device: bool = False):
-    """Compressed NeNMF (factorize.py:197-213) on a row-sharded X: sharded
-    compression, one all-gather of X_R^T and of L, then the replicated outer
-    loop of ``factorize_compressed``; RRE from all-reduced shard residuals.
-    ``init`` holds the FULL initial factors (the same on every rank)."""
-    from .factorize import OuterConfig, _run_outer, _ShardedDeviceLoop
+                                 *, comm: Comm | None = None, return_device: bool = False,
+                                 split_solves: bool | None = None):
+    """Compressed NeNMF (factorize.py:197-213) on a row-sharded X.  ``init``
+    holds the FULL initial factors (the same on every rank).
+
+    With more than one rank the inner solves are split by columns over the
+    ranks (group.py: this rank's rows of G, a slice of F's columns; the
+    decision sums exchanged inside the solver over NVLink; two p x p'
+    all-reduces per outer iteration) whenever every rank's share fits the
+    register-resident solver -- the ranks agree on that first.  Otherwise
+    (or with split_solves=False) X_R^T and L are all-gathered once and the
+    outer loop is replicated on every rank.  The RRE always comes from
+    all-reduced shard residuals."""
+    from .factorize import OuterConfig, _GroupDeviceLoop, _run_outer, _ShardedDeviceLoop
 
     comm = comm or Comm()
     cfg = cfg or OuterConfig()
     XL, XRt_local = compress_problem_sharded(X_local, sketch, comm=comm)
+    if split_solves is None:
+        split_solves = comm.size > 1
+    if split_solves and comm.size > 1:
+        dt = "fp64" if str(X_local.dtype).endswith("float64") else "fp32"
+        group = _group_for(comm)
+        m = int(X_local.shape[1])
+        _, n_r = row_block(n, comm.size, comm.rank)
+        _, m_r = row_block(m, comm.size, comm.rank)
+        ok = (group.supported(dt, sketch.nu, init.p, n_r, sketch.nu, cfg.inner.max_iter) and
+              group.supported(dt, sketch.nu, init.p, m_r, sketch.nu, cfg.inner.max_iter))
+        if not comm.any(not ok):
+            run = _GroupDeviceLoop(X_local, n, sketch.row0, init, sketch.L_local, sketch.Rt, XL, XRt_local, group,
+                                   comm)
+            return _run_outer(X_local, init, cfg, observer, clock, None, run.dtype, return_device, run=run)
     XRt = comm.all_gather_cols(XRt_local, n)
     L = comm.all_gather_cols(sketch.L_local, n)
     run = _ShardedDeviceLoop(X_local, n, sketch.row0, init, L, sketch.Rt, XL, XRt, comm)
     return _run_outer(X_local, init, cfg, observer, clock, None, run.dtype, return_device, run=run)
+
+
+def factorize_compressed_emulated(X, sketch, init, cfg=None, observer=None, clock=None, *, ranks: int = 2,
+                                  return_device: bool = False):
+    """factorize_compressed with every inner solve run as an R-rank group
+    EMULATED on the current GPU (group.SolveGroup.emulated: one launch whose
+    CTAs form R virtual ranks over the same column split and exchange
+    protocol as R GPUs).  X, the sketch and the factors as in the 1-GPU API;
+    used to test the group solver on one device."""
+    from .compression import compress_device, sketch_on_device
+    from .factorize import OuterConfig, _GroupDeviceLoop, _run_outer
+    from .group import SolveGroup
+
+    cfg = cfg or OuterConfig()
+    if hasattr(X, "is_cuda") and X.is_cuda:
+        Xd = X
+        dt = "fp64" if str(X.dtype).endswith("float64") else "fp32"
+    else:
+        dt = "fp64"
+        Xd = _lib.to_device(np.asarray(X, dtype=np.float64), dt)
+    L, Rt = sketch_on_device(sketch, dt)
+    XL, XRt = compress_device(Xd, L, Rt)
+    group = SolveGroup.emulated(ranks)
+    run = _GroupDeviceLoop(Xd, Xd.shape[0], 0, init, L, Rt, XL, XRt, group)
+    return _run_outer(Xd, init, cfg, observer, clock, None, dt, return_device, run=run)
