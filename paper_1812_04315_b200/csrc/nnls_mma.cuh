@@ -42,6 +42,11 @@ struct MmaShape<double> {
 // the dropped lo*lo term and lo's rounding leave a relative error ~2^-22 per
 // product.
 __device__ __forceinline__ uint32_t tf32_hi(float x) { return __float_as_uint(x) & 0xffffe000u; }
+// FP32 correction terms: false = two TF32 MMAs (lo*hi, hi*lo) per k-tile;
+// true = one BF16 m16n8k16 MMA over [F_lo | F_hi] x [W_hi ; W_lo]
+#ifndef NN_FP32_BF16_CORR
+#define NN_FP32_BF16_CORR 0
+#endif
 // the residual rounded to nearest TF32 (the tensor core would truncate it)
 __device__ __forceinline__ uint32_t tf32_lo(float x, uint32_t hi) {
   uint32_t r;
@@ -412,6 +417,12 @@ k_nnls_mma(const __grid_constant__ MmaArgs<T> A) {
             bhi[kt][nt][h] = tf32_hi(w);
             blo[kt][nt][h] = tf32_lo(w, bhi[kt][nt][h]);
           }
+          if (NN_FP32_BF16_CORR) {
+            const float wh0 = __uint_as_float(bhi[kt][nt][0]), wh1 = __uint_as_float(bhi[kt][nt][1]);
+            const float w0 = (float)wval(8 * nt + gq, 8 * kt + 2 * tq), w1 = (float)wval(8 * nt + gq, 8 * kt + 2 * tq + 1);
+            blo[kt][nt][0] = pack_bf16(wh0, wh1);            // K 2tq, 2tq+1   <-> F_lo rows
+            blo[kt][nt][1] = pack_bf16(w0 - wh0, w1 - wh1);  // K 2tq+8, 2tq+9 <-> F_hi rows
+          }
         }
     } else {
 #pragma unroll
@@ -437,33 +448,63 @@ k_nnls_mma(const __grid_constant__ MmaArgs<T> A) {
           ahi[t][1] = h2;  // (gq+8, K slot tq)
           ahi[t][2] = h1;  // (gq,   K slot tq+4 -> row 2tq+1)
           ahi[t][3] = h3;
-          alo[t][0] = tf32_lo(c0, h0);
-          alo[t][1] = tf32_lo(c2, h2);
-          alo[t][2] = tf32_lo(c1, h1);
-          alo[t][3] = tf32_lo(c3, h3);
+          if (NN_FP32_BF16_CORR) {
+            const float f0 = __uint_as_float(h0), f1 = __uint_as_float(h1), f2 = __uint_as_float(h2),
+                        f3 = __uint_as_float(h3);
+            alo[t][0] = pack_bf16(c0 - f0, c1 - f1);  // (gq,   K 2tq, 2tq+1): F_lo
+            alo[t][1] = pack_bf16(c2 - f2, c3 - f3);  // (gq+8, K 2tq, 2tq+1)
+            alo[t][2] = pack_bf16(f0, f1);            // (gq,   K 2tq+8, 2tq+9): F_hi
+            alo[t][3] = pack_bf16(f2, f3);
+          } else {
+            alo[t][0] = tf32_lo(c0, h0);
+            alo[t][1] = tf32_lo(c2, h2);
+            alo[t][2] = tf32_lo(c1, h1);
+            alo[t][3] = tf32_lo(c3, h3);
+          }
         }
         // n-tiles innermost: consecutive MMAs are independent, so the NT
         // accumulation chains overlap in the tensor pipe
-        float cc[NT][4];
+        // The tensor core's fp32 accumulation truncates.  A chain started from
+        // -V (the large, nearly cancelling term) or summing the hi*hi products
+        // of all k-tiles carried that bias into g every iteration, and over
+        // 500 accelerated iterations the factors drifted up to ~1.4e-3 from
+        // the fp64 reference (NumPy float32: ~2e-5 on the same solve).  So
+        // every k-tile's hi*hi product starts from zero and is added with a
+        // round-to-nearest fp32 add, the corrections (2^-11 smaller) have
+        // their own accumulator, and -V comes last, also rounded to nearest:
+        // the same solve is then 1.6e-5 from fp64, like NumPy float32
+        // (tools/diag_fp32_iters.py).
+        float cc[NT][4], cl[NT][4];
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
-          for (int r = 0; r < 4; ++r) cc[nt][r] = (float)nv[4 * nt + r];
+          for (int r = 0; r < 4; ++r) cc[nt][r] = cl[nt][r] = 0.f;
 #pragma unroll
-        for (int kt = 0; kt < NT; ++kt)  // correction terms F_lo W_hi + F_hi W_lo first (small)
+        for (int kt = 0; kt < NT; ++kt)  // correction terms F_lo W_hi + F_hi W_lo
 #pragma unroll
           for (int nt = 0; nt < NT; ++nt) {
-            mma_tf32(cc[nt], alo[kt], bhi[kt][nt][0], bhi[kt][nt][1]);
-            mma_tf32(cc[nt], ahi[kt], blo[kt][nt][0], blo[kt][nt][1]);
+            if (NN_FP32_BF16_CORR) {
+              mma_bf16(cl[nt], alo[kt], blo[kt][nt][0], blo[kt][nt][1]);
+            } else {
+              mma_tf32(cl[nt], alo[kt], bhi[kt][nt][0], bhi[kt][nt][1]);
+              mma_tf32(cl[nt], ahi[kt], blo[kt][nt][0], blo[kt][nt][1]);
+            }
           }
 #pragma unroll
         for (int kt = 0; kt < NT; ++kt)
 #pragma unroll
-          for (int nt = 0; nt < NT; ++nt) mma_tf32(cc[nt], ahi[kt], bhi[kt][nt][0], bhi[kt][nt][1]);
+          for (int nt = 0; nt < NT; ++nt) {
+            // each k-tile's hi*hi product from zero, added with round-to-nearest
+            float tk[4] = {0.f, 0.f, 0.f, 0.f};
+            mma_tf32(tk, ahi[kt], bhi[kt][nt][0], bhi[kt][nt][1]);
+#pragma unroll
+            for (int r = 0; r < 4; ++r) cc[nt][r] = __fadd_rn(cc[nt][r], tk[r]);
+          }
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
-          for (int r = 0; r < 4; ++r) g[4 * nt + r] = (T)cc[nt][r];
+          for (int r = 0; r < 4; ++r)
+            g[4 * nt + r] = (T)__fadd_rn(__fadd_rn(cc[nt][r], cl[nt][r]), (float)nv[4 * nt + r]);
       } else {
         double cc[NT][2];
 #pragma unroll

@@ -122,38 +122,47 @@ __global__ void __launch_bounds__(stream_threads<NT>(), 1) k_nnls_stream(const _
         aco[t][2] = tf32_lo(c1, h1);
         aco[t][3] = tf32_lo(c3, h3);
       }
-      float cc[NT][4];
+      // zero-started accumulators, -V added with round-to-nearest (see k_nnls_mma)
+      float cc[NT][4], cl[NT][4];
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
-        for (int r = 0; r < 4; ++r) cc[nt][r] = nv[4 * nt + r];
+        for (int r = 0; r < 4; ++r) cc[nt][r] = cl[nt][r] = 0.f;
       if constexpr (WSM) {
 #pragma unroll
         for (int kt = 0; kt < NT; ++kt)
 #pragma unroll
           for (int nt = 0; nt < NT; ++nt) {
             const uint4 b = wf[(kt * NT + nt) * 32 + lane];
-            mma_tf32(cc[nt], aco[kt], b.x, b.y);  // F_lo W_hi
-            mma_tf32(cc[nt], ahi[kt], b.z, b.w);  // F_hi W_lo
-            mma_tf32(cc[nt], ahi[kt], b.x, b.y);
+            mma_tf32(cl[nt], aco[kt], b.x, b.y);  // F_lo W_hi
+            mma_tf32(cl[nt], ahi[kt], b.z, b.w);  // F_hi W_lo
+            float tk[4] = {0.f, 0.f, 0.f, 0.f};   // hi*hi per k-tile, added with round-to-nearest
+            mma_tf32(tk, ahi[kt], b.x, b.y);
+#pragma unroll
+            for (int r = 0; r < 4; ++r) cc[nt][r] = __fadd_rn(cc[nt][r], tk[r]);
           }
       } else {
 #pragma unroll
         for (int kt = 0; kt < NT; ++kt)
 #pragma unroll
           for (int nt = 0; nt < NT; ++nt) {
-            mma_tf32(cc[nt], aco[kt], bhi[kt % NTR][nt % NTR][0], bhi[kt % NTR][nt % NTR][1]);
-            mma_tf32(cc[nt], ahi[kt], bco[kt % NTR][nt % NTR][0], bco[kt % NTR][nt % NTR][1]);
+            mma_tf32(cl[nt], aco[kt], bhi[kt % NTR][nt % NTR][0], bhi[kt % NTR][nt % NTR][1]);
+            mma_tf32(cl[nt], ahi[kt], bco[kt % NTR][nt % NTR][0], bco[kt % NTR][nt % NTR][1]);
           }
 #pragma unroll
         for (int kt = 0; kt < NT; ++kt)
 #pragma unroll
-          for (int nt = 0; nt < NT; ++nt) mma_tf32(cc[nt], ahi[kt], bhi[kt % NTR][nt % NTR][0], bhi[kt % NTR][nt % NTR][1]);
+          for (int nt = 0; nt < NT; ++nt) {
+            float tk[4] = {0.f, 0.f, 0.f, 0.f};   // hi*hi per k-tile, added with round-to-nearest
+            mma_tf32(tk, ahi[kt], bhi[kt % NTR][nt % NTR][0], bhi[kt % NTR][nt % NTR][1]);
+#pragma unroll
+            for (int r = 0; r < 4; ++r) cc[nt][r] = __fadd_rn(cc[nt][r], tk[r]);
+          }
       }
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
-        for (int r = 0; r < 4; ++r) g[4 * nt + r] = cc[nt][r];
+        for (int r = 0; r < 4; ++r) g[4 * nt + r] = __fadd_rn(__fadd_rn(cc[nt][r], cl[nt][r]), nv[4 * nt + r]);
     };
     auto post = [&](int j, float s0, float s1) {
 #pragma unroll

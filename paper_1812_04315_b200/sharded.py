@@ -273,12 +273,19 @@ def gather_sketch(sketch: ShardedSketch, *, comm: Comm | None = None) -> SketchP
 
 
 def _group_for(comm: Comm):
-    """The SolveGroup of this communicator (created once: IPC-mapped buffers)."""
+    """The SolveGroup of this communicator (created once: IPC-mapped buffers),
+    or None when two ranks share a GPU: group solves wait on each other
+    inside the kernel, so every rank needs its own device."""
     from .group import SolveGroup
 
-    g = getattr(comm, "_solve_group", None)
-    if g is None:
-        g = comm._solve_group = SolveGroup.over(comm)
+    g = getattr(comm, "_solve_group", False)
+    if g is False:
+        torch = _lib.torch_mod()
+        uuid = str(torch.cuda.get_device_properties(torch.cuda.current_device()).uuid)
+        uuids = [None] * comm.size
+        comm.dist.all_gather_object(uuids, uuid, group=comm.group)
+        g = SolveGroup.over(comm) if len(set(uuids)) == comm.size else None
+        comm._solve_group = g
     return g
 
 
@@ -309,8 +316,8 @@ def factorize_compressed_sharded(X_local, n: int, sketch: ShardedSketch, init, c
         m = int(X_local.shape[1])
         _, n_r = row_block(n, comm.size, comm.rank)
         _, m_r = row_block(m, comm.size, comm.rank)
-        ok = (group.supported(dt, sketch.nu, init.p, n_r, sketch.nu, cfg.inner.max_iter) and
-              group.supported(dt, sketch.nu, init.p, m_r, sketch.nu, cfg.inner.max_iter))
+        ok = group is not None and (group.supported(dt, sketch.nu, init.p, n_r, sketch.nu, cfg.inner.max_iter) and
+                                    group.supported(dt, sketch.nu, init.p, m_r, sketch.nu, cfg.inner.max_iter))
         if not comm.any(not ok):
             run = _GroupDeviceLoop(X_local, n, sketch.row0, init, sketch.L_local, sketch.Rt, XL, XRt_local, group,
                                    comm)
