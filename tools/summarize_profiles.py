@@ -53,12 +53,15 @@ def main():
     dst.mkdir(exist_ok=True)
     if (prof / "bench.json").exists():
         (dst / f"{tag}_bench.json").write_text((prof / "bench.json").read_text())
-    if (prof / "launches.csv").exists():
-        out = subprocess.run([sys.executable, str(REPO / "tools" / "launches.py"), str(prof / "launches.csv")],
-                             capture_output=True, text=True).stdout
-        (dst / f"{tag}_launches.txt").write_text(
-            "# ncu --metrics gpu__time_duration.sum --clock-control none (cold, serialised launches) of\n"
-            "# python bench.py --steps 1 --warmup 3 --no-cpu-baseline; per-kernel totals and share\n" + out)
+    for name, cmd in (("launches", "python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-secondary (FP64)"),
+                      ("launches_fp32", "python bench.py --dtype fp32 --steps 1 --warmup 3 --no-cpu-baseline "
+                                        "--no-secondary")):
+        if (prof / f"{name}.csv").exists():
+            out = subprocess.run([sys.executable, str(REPO / "tools" / "launches.py"), str(prof / f"{name}.csv")],
+                                 capture_output=True, text=True).stdout
+            (dst / f"{tag}_{name}.txt").write_text(
+                "# ncu --metrics gpu__time_duration.sum --clock-control none (cold, serialised launches) of\n"
+                f"# {cmd}; per-kernel totals and share\n" + out)
     traffic_path = dst / "ncu_traffic.json"
     traffic = json.loads(traffic_path.read_text()) if traffic_path.exists() else {}
     for rep in sorted(prof.glob("full_*.ncu-rep")):
