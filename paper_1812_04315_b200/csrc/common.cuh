@@ -101,7 +101,25 @@ __device__ __forceinline__ float relu_nan_fast(float x) {
   asm("max.NaN.f32 %0, %1, 0f00000000;" : "=f"(r) : "f"(x));
   return r;
 }
-__device__ __forceinline__ double relu_nan_fast(double x) { return relu_nan(x); }
+// FP64: the same by the sign bit on the integer pipe (the FP64 pipe is the
+// bound of the FP64 solver; DSETP compares ran on it).  A negative-signed NaN
+// becomes 0 here, but a NaN only reaches this point from an iterate whose
+// sums were already non-finite (the failure is decided there).
+__device__ __forceinline__ double relu_nan_fast(double x) {
+  const int hi = __double2hiint(x), lo = __double2loint(x);
+  const int keep = ~(hi >> 31);  // 0 for a set sign bit, all ones otherwise
+  return __hiloint2double(hi & keep, lo & keep);
+}
+// PG entry (nnls.py:89-107): g where f > 0, else min(g, 0), on the integer
+// pipe: f > 0 is "f's bit pattern is a positive int64" (exact for every
+// non-NaN f, -0.0 included), min(g, 0) zeroes a g without sign bit (a
+// positive NaN g also makes <f, g> non-finite, which fails the iteration as
+// the reference does).
+__device__ __forceinline__ double pg_entry_fast(double f, double g) {
+  const int gh = __double2hiint(g), gl = __double2loint(g);
+  const int keep = (__double_as_longlong(f) > 0) ? -1 : (gh >> 31);
+  return __hiloint2double(gh & keep, gl & keep);
+}
 // np.minimum(x, 0) keeping NaN
 template <typename T>
 __device__ __forceinline__ T min0_nan(T x) { return (x <= T(0) || x != x) ? x : T(0); }

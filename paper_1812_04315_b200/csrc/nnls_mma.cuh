@@ -599,7 +599,7 @@ k_nnls_mma(const __grid_constant__ MmaArgs<T> A) {
 #pragma unroll
         for (int e = 0; e < NE; ++e) {
           uo[e] = fma_acc(g[e], rnegL, fe[e]);
-          const T pgv = fe[e] > T(0) ? g[e] : min0_nan(g[e]);
+          const T pgv = pg_entry_fast(fe[e], g[e]);
           s0 = fma_acc(pgv, pgv, s0);
           s1 = fma_acc(fe[e], g[e] + nv[e], s1);
         }

@@ -144,6 +144,8 @@ __global__ void k_slab_reduce(const T* __restrict__ part, int nslab, int64_t cou
 
 int dual_pass_tc(Arena& ws, const float* X, int64_t n, int64_t m, int64_t ldx, const float* At, const float* Bt,
                  int64_t k, float* Yt, float* Zt, cudaStream_t s);
+int dual_pass_f64(Arena& ws, const double* X, int64_t n, int64_t m, int64_t ldx, const double* At,
+                  const double* Bt, int64_t k, double* Yt, double* Zt, cudaStream_t s);
 
 template <typename T>
 int dual_pass(Arena& ws, const T* X, int64_t n, int64_t m, int64_t ldx, const T* At, const T* Bt, int64_t k,
@@ -157,8 +159,19 @@ int dual_pass(Arena& ws, const T* X, int64_t n, int64_t m, int64_t ldx, const T*
     if (rc != NENMF_ERR_UNSUPPORTED) return rc;
   }
   if constexpr (sizeof(T) == 8) {
-    // FP64: the two products on the FP64 tensor pipe (skinny.cu ab -> k_xv64 /
-    // k_ux64), one X stream each: Yt = At X^T (B = X^T), Zt = Bt X (B = X)
+    // FP64: both products from one read of X on the FP64 tensor pipe (dual64.cu)
+    if (getenv("NENMF_DUAL_SIMT") == nullptr) {
+      Arena a = ws;
+      const int rc = dual_pass_f64(a, reinterpret_cast<const double*>(X), n, m, ldx,
+                                   reinterpret_cast<const double*>(At), reinterpret_cast<const double*>(Bt), k,
+                                   reinterpret_cast<double*>(Yt), reinterpret_cast<double*>(Zt), s);
+      if (rc != NENMF_ERR_UNSUPPORTED) {
+        ws = a;
+        return rc;
+      }
+    }
+    // otherwise the two products separately (skinny.cu ab -> k_xv64 / k_ux64),
+    // one X stream each: Yt = At X^T (B = X^T), Zt = Bt X (B = X)
     if (k <= 32 && getenv("NENMF_DUAL_SIMT") == nullptr) {
       Arena a0 = ws;
       if (At != nullptr) NENMF_TRY(ab<T>(a0, At, k, m, X, n, ldx, true, Yt, s));

@@ -5,6 +5,7 @@
 // (stored in profiles/fp64_peak.json).  nvcc -O3 -gencode
 // arch=compute_100a,code=sm_100a fp64_peak.cu -o fp64_peak
 #include <cstdio>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 constexpr int CH = 8;  // independent chains per warp
@@ -42,6 +43,23 @@ __global__ void __launch_bounds__(256) k_dfma(double* out, int iters) {
   if (s == 12345.678) out[0] = s;
 }
 
+static double run_dmma(int blocks, int threads, double* out, cudaEvent_t e0, cudaEvent_t e1) {
+  double best = 0;
+  for (int rep = 0; rep < 4; ++rep) {
+    const int iters = 20000;
+    k_dmma<<<blocks, threads>>>(out, 100);
+    cudaEventRecord(e0);
+    k_dmma<<<blocks, threads>>>(out, iters);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    const double fl = (double)blocks * (threads / 32) * iters * CH * 512.0;
+    if (fl / (ms * 1e-3) / 1e12 > best) best = fl / (ms * 1e-3) / 1e12;
+  }
+  return best;
+}
+
 int main() {
   int dev = 0, sms = 0, clk = 0;
   cudaGetDevice(&dev);
@@ -72,6 +90,12 @@ int main() {
     cudaEventElapsedTime(&ms, e0, e1);
     const double ff = (double)blocks * threads * iters * CH * 2.0;
     if (ff / (ms * 1e-3) / 1e12 > best_fma) best_fma = ff / (ms * 1e-3) / 1e12;
+  }
+  if (getenv("FP64_OCC") != nullptr) {
+    for (int wps : {4, 8, 16, 32}) {
+      const int threads = wps <= 8 ? 32 * wps : 256, per = wps <= 8 ? 1 : wps / 8;
+      fprintf(stderr, "warps/SM %2d: %.2f TF/s\n", wps, run_dmma(sms * per, threads, out, e0, e1));
+    }
   }
   printf("{\"fp64_dmma_tflops\": %.3f, \"fp64_dfma_tflops\": %.3f, \"sms\": %d, \"clock_khz\": %d, "
          "\"how\": \"tools/micro/fp64_peak.cu: %d CTAs x 256 threads, %d independent chains per warp, best of 6, "
