@@ -1102,6 +1102,106 @@ k_resid_pipe(const float* __restrict__ X, int64_t nx, int64_t mx, int64_t ldx, i
   }
 }
 
+// FP64 residuals ||X - U^T V||^2 for one or two candidates on the FP64 tensor
+// pipe (the RRE emit, tracing.py:45-57, and the vanilla tie-break pair,
+// nnls.py:219-227): X in 64 x 64 tiles through a cp.async ring with the U
+// slice of the tile's rows and the V slice(s) of its columns; warp w forms
+// the product for rows 8w..8w+7 (DMMA m8n8k4, K = p) and accumulates
+// (x - p)^2 straight from the accumulator fragments.  One CTA per SM, tiles
+// dealt round-robin, per-CTA partials summed in fixed order.
+constexpr int RD_XS = 68;  // shared row stride (doubles)
+template <int NC>
+__global__ void __launch_bounds__(256, 1)
+k_resid64(const double* __restrict__ X, int64_t nx, int64_t mx, int64_t ldx, int p, const double* __restrict__ U1,
+          const double* __restrict__ V1, const double* __restrict__ U2, const double* __restrict__ V2,
+          double* __restrict__ part, const int* __restrict__ gate) {
+  constexpr int NS = NC == 1 ? 3 : 2;
+  constexpr int SF = 64 * RD_XS + 2 * NC * 32 * RD_XS;  // X | U1 V1 (| U2 V2), doubles
+  extern __shared__ __align__(16) double dsm[];
+  __shared__ double red[33];
+  if (gate != nullptr && *gate == 0) return;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, gq = lane >> 2, tq = lane & 3;
+  const int64_t nrt = (nx + 63) / 64, nct = (mx + 63) / 64, ntiles = nrt * nct;
+  const int nks = (p + 3) >> 2;
+  double s1 = 0.0, s2 = 0.0;
+  auto issue = [&](int64_t tile, int stg) {
+    double* xs = dsm + (size_t)stg * SF;
+    const int64_t i0 = (tile / nct) * 64, j0 = (tile % nct) * 64;
+    for (int c = tid; c < 64 * 32; c += 256) {
+      const int r = c >> 5, ch = c & 31;
+      const int64_t i = i0 + r, j = j0 + 2 * ch;
+      const int valid = i < nx ? (int)imax(0, imin(2, mx - j)) : 0;
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(
+                       (uint32_t)__cvta_generic_to_shared(xs + r * RD_XS + 2 * ch)),
+                   "l"(X + (valid ? i * ldx + j : 0)), "r"(8 * valid)
+                   : "memory");
+    }
+    for (int c = tid; c < 2 * NC * 32 * 32; c += 256) {  // [U1 | V1 | U2 | V2] slices, p x 64 each
+      const int which = c >> 10, cc = c & 1023, a = cc >> 5, ch = cc & 31;
+      const bool isU = (which & 1) == 0;
+      const double* src = which == 0 ? U1 : which == 1 ? V1 : which == 2 ? U2 : V2;
+      const int64_t len = isU ? nx : mx, base = isU ? i0 : j0, j = base + 2 * ch;
+      const int valid = a < p ? (int)imax(0, imin(2, len - j)) : 0;
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"((uint32_t)__cvta_generic_to_shared(
+                       xs + 64 * RD_XS + (size_t)which * 32 * RD_XS + a * RD_XS + 2 * ch)),
+                   "l"(src + (valid ? (int64_t)a * len + j : 0)), "r"(8 * valid)
+                   : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  int64_t t0 = blockIdx.x;
+  for (int i = 0; i < NS - 1; ++i) {
+    const int64_t tl = t0 + (int64_t)i * gridDim.x;
+    if (tl < ntiles) issue(tl, i);
+    else asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  int k = 0;
+  for (int64_t tile = t0; tile < ntiles; tile += gridDim.x, ++k) {
+    asm volatile("cp.async.wait_group %0;" ::"n"(NS - 2) : "memory");
+    __syncthreads();
+    const double* xs = dsm + (size_t)(k % NS) * SF;
+    const int64_t i0 = (tile / nct) * 64, j0 = (tile % nct) * 64;
+#pragma unroll
+    for (int cand = 0; cand < NC; ++cand) {
+      const double* us = xs + 64 * RD_XS + (size_t)(2 * cand) * 32 * RD_XS;
+      const double* vs = us + 32 * RD_XS;
+      double acc[8][2];
+#pragma unroll
+      for (int nt = 0; nt < 8; ++nt) acc[nt][0] = acc[nt][1] = 0.0;
+      for (int ks = 0; ks < nks; ++ks) {
+        const double a = us[(4 * ks + tq) * RD_XS + 8 * wid + gq];  // A (row, k) = U[k][row]
+#pragma unroll
+        for (int nt = 0; nt < 8; ++nt) dmma_r(acc[nt], a, vs[(4 * ks + tq) * RD_XS + 8 * nt + gq]);
+      }
+      const int r = 8 * wid + gq;
+      double sc = 0.0;
+#pragma unroll
+      for (int nt = 0; nt < 8; ++nt)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int col = 8 * nt + 2 * tq + h;
+          if (i0 + r < nx && j0 + col < mx) {
+            const double d = xs[r * RD_XS + col] - acc[nt][h];
+            sc = fma(d, d, sc);
+          }
+        }
+      if (cand == 0) s1 += sc;
+      else s2 += sc;
+    }
+    __syncthreads();
+    const int64_t nxt = tile + (int64_t)(NS - 1) * gridDim.x;
+    if (nxt < ntiles) issue(nxt, (k + NS - 1) % NS);
+    else asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  s1 = block_sum(s1, red);
+  s2 = block_sum(s2, red);
+  if (tid == 0) {
+    part[2 * blockIdx.x] = s1;
+    part[2 * blockIdx.x + 1] = s2;
+  }
+}
+
 // fixed-order sum of `n` pairs -> out[0..1]; optional gate
 __global__ void k_pair_final(const double* __restrict__ part, int64_t n, double* __restrict__ out,
                              const int* __restrict__ gate) {
@@ -1170,6 +1270,39 @@ int resid(Arena& ws, const T* At, int64_t p, int64_t r, const T* B, int64_t c, i
       else if (kt == 2) k_resid_mma<2><<<grid, 256, 0, st>>>(Xf, nx, mx, ldb, (int)p, U1, V1, U2, V2, part, gate);
       else if (kt == 3) k_resid_mma<3><<<grid, 256, 0, st>>>(Xf, nx, mx, ldb, (int)p, U1, V1, U2, V2, part, gate);
       else k_resid_mma<4><<<grid, 256, 0, st>>>(Xf, nx, mx, ldb, (int)p, U1, V1, U2, V2, part, gate);
+      NENMF_LAUNCH_CHECK();
+      k_pair_final<<<1, 256, 0, st>>>(part, (int64_t)grid, out2, gate);
+      NENMF_LAUNCH_CHECK();
+      return NENMF_OK;
+    }
+  }
+  if constexpr (sizeof(T) == 8) {
+    const int64_t nx = trans ? c : r, mx = trans ? r : c;
+    const double* U1 = reinterpret_cast<const double*>(trans ? F1 : At);
+    const double* U2 = F2 == nullptr ? nullptr : reinterpret_cast<const double*>(trans ? F2 : At);
+    const double* V1 = reinterpret_cast<const double*>(trans ? At : F1);
+    const double* V2 = F2 == nullptr ? nullptr : reinterpret_cast<const double*>(trans ? At : F2);
+    auto al16 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
+    const bool ok = p <= 32 && ((nx | mx | ldb) & 1) == 0 && getenv("NENMF_RESID_SIMT") == nullptr &&
+                    (ws.base == nullptr || (al16(B) && al16(U1) && al16(V1) && (U2 == nullptr || al16(U2)) &&
+                                            (V2 == nullptr || al16(V2))));
+    if (ok) {
+      int sms = sm_count();
+      if (sms <= 0) sms = 148;
+      const unsigned grid = (unsigned)imax(1, imin((int64_t)sms, cdiv(nx, 64) * cdiv(mx, 64)));
+      double* part = ws.take<double>((size_t)grid * 2);
+      if (ws.base == nullptr) return NENMF_OK;
+      if (!ws.ok) return NENMF_ERR_WORKSPACE;
+      const double* Xd = reinterpret_cast<const double*>(B);
+      if (F2 == nullptr) {
+        const size_t smem = (size_t)3 * (64 * RD_XS + 2 * 32 * RD_XS) * sizeof(double);
+        NENMF_CUDA_TRY(set_smem(k_resid64<1>, smem));
+        k_resid64<1><<<grid, 256, smem, st>>>(Xd, nx, mx, ldb, (int)p, U1, V1, nullptr, nullptr, part, gate);
+      } else {
+        const size_t smem = (size_t)2 * (64 * RD_XS + 4 * 32 * RD_XS) * sizeof(double);
+        NENMF_CUDA_TRY(set_smem(k_resid64<2>, smem));
+        k_resid64<2><<<grid, 256, smem, st>>>(Xd, nx, mx, ldb, (int)p, U1, V1, U2, V2, part, gate);
+      }
       NENMF_LAUNCH_CHECK();
       k_pair_final<<<1, 256, 0, st>>>(part, (int64_t)grid, out2, gate);
       NENMF_LAUNCH_CHECK();
