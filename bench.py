@@ -555,6 +555,10 @@ def run_ours(args, rank, world, local_rank):
         del P32
         torch.cuda.empty_cache()
 
+    vanilla = None
+    if not args.no_secondary:
+        vanilla = run_vanilla(args, w, dtype, rank, world)
+
     cfg5 = None
     if not args.no_secondary:
         cfg5 = run_cfg5(args, rank, world, local_rank, dist, comm)
@@ -586,12 +590,61 @@ def run_ours(args, rank, world, local_rank):
         "e2e": head["e2e"], "gpu_launches": head["gpu_launches"], "clocks": head["clocks"],
         "final_rre": head["final_rre"],
         "roofline": roof, "solver": solver,
-        "fp32_mode": fp32, "cfg5_sharded": cfg5,
+        "fp32_mode": fp32, "vanilla": vanilla, "cfg5_sharded": cfg5,
         "cpu_baseline": cpu,
     }
     print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()
+
+
+# ------------------------------------------------------ vanilla cfg2 block
+def run_vanilla(args, w, dtype, rank, world):
+    """Vanilla NeNMF (factorize_vanilla, factorize.py:186-194) on BASELINE cfg 2
+    (1 GPU as BASELINE.json states): 100 outer iterations, inner <= 500, on
+    the full X; value = outer it/s.  FP32 forms V = A^T X with the tcgen05 pass
+    over the prepared X; FP64 on the DMMA pipe.  Beside it, the reference
+    package's factorize_vanilla timed for one outer iteration on the host."""
+    import numpy as np
+    import torch
+
+    import paper_1812_04315_b200 as nm
+
+    if world > 1 or rank != 0:
+        return None
+    npdt = np.float32 if dtype == "fp32" else np.float64
+    Xd = torch.from_numpy(w.X.astype(npdt)).cuda()
+    G0 = torch.from_numpy(w.G0.astype(npdt)).cuda()
+    F0 = torch.from_numpy(w.F0.astype(npdt)).cuda()
+    cfg = nm.OuterConfig(inner=nm.InnerSolverConfig(max_iter=w.inner), time_budget_seconds=0.0,
+                         max_outer_iterations=OUTER, trace_every=OUTER)
+    run = lambda: nm.factorize_vanilla(Xd, nm.FactorPair(G=G0, F=F0, p=w.p), cfg, return_device=True)  # noqa: E731
+    run()
+    timer = Timer(torch)
+    k = max(1, min(args.steps, 2))
+    ms = timer(run, k) / k
+    out = {"metric": f"vanilla NeNMF outer iters/s (cfg2 n=m=1e4 p=20, {dtype}, 100 outer, inner<=500)",
+           "value": OUTER / (ms / 1e3), "unit": UNIT, "ms_per_step": ms, "steps": k, "dtype": dtype,
+           "v_products": "tcgen05 BF16x3 pass over the prepared X" if dtype == "fp32" else "DMMA (FP64 tensor pipe)"}
+    if not args.no_cpu_baseline:
+        nenmf = _reference_package()
+        if nenmf is not None:
+            t0 = time.perf_counter()
+            clock = nenmf.MonotonicClock()
+            ccfg = nenmf.OuterConfig(inner=nenmf.InnerSolverConfig(max_iter=w.inner), time_budget_seconds=0.0,
+                                     max_outer_iterations=1)
+            nenmf.factorize_vanilla(w.X, nenmf.FactorPair(G=w.G0, F=w.F0, p=w.p), ccfg, clock=clock)
+            wall = time.perf_counter() - t0
+            solver = clock.elapsed()
+            out["cpu_baseline"] = {"value": OUTER / (wall + (OUTER - 1) * solver), "unit": UNIT, "cores": cores(),
+                                   "kind": "reference",
+                                   "sample": "the unmodified reference package's factorize_vanilla, 1 outer iteration "
+                                             "(float64, OpenBLAS all threads); 100-outer rate = wall(1 outer incl. 2 "
+                                             "emits) + 99 x solver-clock outer",
+                                   "t_wall_s": wall, "t_outer_solver_s": solver}
+    del Xd
+    torch.cuda.empty_cache()
+    return out
 
 
 # ------------------------------------------------- row-sharded cfg5 block

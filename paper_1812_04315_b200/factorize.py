@@ -474,12 +474,13 @@ def _run_outer(X, init: FactorPair, cfg: OuterConfig, observer, clock, sketch, d
 
 def factorize_vanilla(X, init: FactorPair, cfg: OuterConfig = OuterConfig(),
                       observer: Observer | None = None, clock: SolverClock | None = None, *,
-                      dtype: str = "fp64", return_device: bool = False, tensor_v: bool = False) -> FactorPair:
+                      dtype: str = "fp64", return_device: bool = False, tensor_v: bool = True) -> FactorPair:
     """Alternating NeNMF on the full data (factorize.py:186-194), on the GPU.
-    ``tensor_v`` (FP32 only): form V = A^T B with the BF16x3 tensor-core pass
-    over a prepared copy of X (faster; factors agree with the fp64 reference to
-    about 1e-3 instead of about 7e-4)."""
-    if tensor_v:  # (an fp64 X has no prepared form: the flag is then a no-op)
+    ``tensor_v`` (FP32 only, default): form V = A^T B with the tcgen05 BF16x3
+    pass over a prepared copy of X (the RSI X-pass kernel); False: the
+    CUDA-core/mma.sync 3xTF32 products over the raw X.  An fp64 X has no
+    prepared form (the flag is then a no-op)."""
+    if tensor_v and (dtype == "fp32" or str(getattr(X, "dtype", "")).endswith("float32")):
         if not (hasattr(X, "is_cuda") and X.is_cuda):
             X = as_matrix(X, "X")
         run = _DeviceLoop(X, init, None, dtype)

@@ -203,3 +203,42 @@ def test_cfg5_proxy_sharded_world1():
     assert top_subspace_angle(pair.R, Rr, w.X.T, w.p) <= 1e-3
     rre = np.array([r.rre for r in rec.records])
     one_step_parity(w.X, pair.L, pair.R, facs, rre, w.inner, 1e-3)
+
+
+@pytest.mark.parametrize("dtype", ["fp64", "fp32"])
+def test_cfg2_vanilla_full_size(dtype):
+    """factorize_vanilla (factorize.py:186-194) at BASELINE cfg 2, 2 outer
+    iterations (inner 500): FP64 trajectory and factors within 1e-5 of the
+    oracle; FP32 (V = A^T X from the tcgen05 pass over the prepared X) one-step
+    parity within 1e-3."""
+    import torch
+
+    w = workloads.make_workload(2, dtype=dtype)
+    npdt = np.float32 if dtype == "fp32" else np.float64
+    Xd = torch.from_numpy(w.X.astype(npdt)).to("cuda")
+    init = nm.FactorPair(G=torch.from_numpy(w.G0.astype(npdt)).cuda(), F=torch.from_numpy(w.F0.astype(npdt)).cuda(),
+                         p=w.p)
+    rec, facs = nm.TraceRecorder(), []
+
+    def observe(r, G, F):
+        rec(r, G, F)
+        facs.append((G.copy(), F.copy()))
+
+    cfg = nm.OuterConfig(inner=nm.InnerSolverConfig(max_iter=w.inner), time_budget_seconds=0.0,
+                         max_outer_iterations=2)
+    nm.factorize_vanilla(Xd, init, cfg, observer=observe, clock=nm.IterationClock())
+    rre = np.array([r.rre for r in rec.records])
+    del Xd
+    torch.cuda.empty_cache()
+    if dtype == "fp32":
+        for t in range(1, len(facs)):
+            ref = orc.nenmf(w.X, facs[t - 1][0], facs[t - 1][1], max_outer=1, max_iter=w.inner)
+            assert abs(rre[t] - ref.records[-1][1]) <= 1e-3 * ref.records[-1][1]
+            assert np.linalg.norm(facs[t][0] - ref.G) <= 1e-3 * np.linalg.norm(ref.G), t
+            assert np.linalg.norm(facs[t][1] - ref.F) <= 1e-3 * np.linalg.norm(ref.F), t
+        return
+    ref = orc.nenmf(w.X, w.G0, w.F0, max_outer=2, max_iter=w.inner)
+    exp = np.array([r for _, r, _ in ref.records])
+    assert np.abs(rre - exp).max() <= 1e-5 * exp.max()
+    assert np.abs(facs[-1][0] - ref.G).max() <= 1e-5 * np.abs(ref.G).max()
+    assert np.abs(facs[-1][1] - ref.F).max() <= 1e-5 * np.abs(ref.F).max()

@@ -256,8 +256,9 @@ def test_vanilla_fp32_tensor_v_vs_oracle():
     """FP32 vanilla NeNMF, default (CUDA-core V) and tensor_v=True (V = A^T B
     from the BF16x3 tensor-core pass over the prepared X,
     nenmf_solve_nnls_prepared), against the fp64 oracle on the fp32-rounded
-    inputs: RRE trajectory within 1e-3; factors within 1e-3 (default) and
-    2e-3 (tensor_v, measured ~1.05e-3) in relative Frobenius norm."""
+    inputs: RRE trajectory and factors within 1e-3 (relative Frobenius) in
+    both forms (the tensor_v form was 1.05e-3 before the FP32 solver's
+    round-to-nearest accumulation)."""
     import nenmf_oracle as orc
 
     rng = np.random.default_rng(9)
@@ -269,7 +270,7 @@ def test_vanilla_fp32_tensor_v_vs_oracle():
     cfg = nm.OuterConfig(inner=nm.InnerSolverConfig(max_iter=60), time_budget_seconds=0.0, max_outer_iterations=8)
     ref = orc.nenmf(X, G0, F0, max_outer=8, max_iter=60)
     exp = np.array([r for _, r, _ in ref.records])
-    for tensor_v, ftol in ((False, 1e-3), (True, 2e-3)):
+    for tensor_v, ftol in ((False, 1e-3), (True, 1e-3)):
         rec = nm.TraceRecorder()
         out = nm.factorize_vanilla(X, nm.FactorPair(G=G0, F=F0, p=p), cfg, observer=rec, clock=nm.IterationClock(),
                                    dtype="fp32", tensor_v=tensor_v)
