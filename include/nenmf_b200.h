@@ -166,7 +166,7 @@ typedef struct nenmf_group {
   int ranks;        /* R, 2..8 */
   int rank0;        /* rank of this launch's first virtual rank */
   int nvr;          /* virtual ranks in this launch: 1 per GPU, or R to emulate the group */
-  int reserved;
+  int watchdog_s;   /* > 0: this solve's no-progress limit in seconds (else NENMF_WATCHDOG_S / 60 s) */
   int64_t col0[9];  /* virtual rank v owns columns [col0[v], col0[v+1]) of this launch's arrays; col0[nvr] = c */
   void* xch[8];     /* every rank's exchange buffer (nenmf_group_xch_bytes() each, zeroed once) */
   uint64_t epoch;   /* the same on every rank, unique per solve over the buffers' lifetime, 0 < epoch < 2^40 */

@@ -192,7 +192,7 @@ def workspace(nbytes: int):
 class GroupStruct(C.Structure):
     """nenmf_group (include/nenmf_b200.h): one solve split over R ranks."""
 
-    _fields_ = [("ranks", C.c_int), ("rank0", C.c_int), ("nvr", C.c_int), ("reserved", C.c_int),
+    _fields_ = [("ranks", C.c_int), ("rank0", C.c_int), ("nvr", C.c_int), ("watchdog_s", C.c_int),
                 ("col0", C.c_int64 * 9), ("xch", C.c_void_p * 8), ("epoch", C.c_uint64)]
 
 

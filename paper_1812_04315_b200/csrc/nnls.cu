@@ -349,6 +349,7 @@ int solve_nnls(Arena& ws, const T* At, int64_t r, int64_t p, const T* B, int64_t
       a.watchdog_ns = nn_watchdog_ns();
       a.grp.ranks = 1;
       if (grouped) {
+        if (grp->watchdog_s > 0) a.watchdog_ns = (unsigned long long)grp->watchdog_s * 1000000000ull;
         a.grp.ranks = grp->ranks;
         a.grp.rank0 = grp->rank0;
         a.grp.nvr = grp->nvr;

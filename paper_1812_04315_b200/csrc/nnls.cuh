@@ -7,7 +7,7 @@ namespace nenmf {
 struct GroupDev;
 // Host view of a rank group (C ABI nenmf_group, include/nenmf_b200.h).
 struct GroupHost {
-  int ranks, rank0, nvr, reserved;
+  int ranks, rank0, nvr, watchdog_s;
   int64_t col0[9];
   void* xch[8];
   unsigned long long epoch;

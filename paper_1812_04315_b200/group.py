@@ -87,6 +87,50 @@ class SolveGroup:
         self._opened = []
 
     # ---------------------------------------------------------------- solves
+    def self_test(self, comm) -> bool:
+        """Probe the exchange before a real run: a small group solve over the
+        ranks (5 s watchdog) against the same solve on one GPU.  True on every
+        rank only if every rank finished, took the same decisions and matches
+        its 1-GPU columns; the ranks agree through one all-reduce, so a broken
+        peer mapping degrades to replicated solves instead of hanging."""
+        import numpy as np
+
+        lib, torch = _lib.require_device()
+        ok = True
+        try:
+            rng = np.random.default_rng(1234)
+            r, p, c = 12, 6, 96 * self.ranks
+            At = _lib.to_device(rng.random((p, r)), "fp64")
+            B = _lib.to_device(rng.random((r, p)) @ rng.random((p, c)) + 0.05 * rng.random((r, c)), "fp64")
+            F0 = _lib.to_device(rng.random((p, c)), "fp64")
+            Pt = _lib.to_device(rng.standard_normal((r, c)), "fp64")
+            from . import _ops
+
+            F1 = torch.empty_like(F0)
+            P1 = torch.empty((p, r), dtype=F0.dtype, device="cuda")
+            st1 = _lib.new_status()
+            _ops.solve(At, B, F0, F1, trans_b=False, max_iter=60, grad_tol=1e-8, lipschitz_safety=1.0,
+                       status=st1, next_bt=Pt, next_out=P1)
+            cols = partition(c, self.ranks)
+            c0, c1 = cols[self.rank], cols[self.rank + 1]
+            loc = lambda t: t[:, c0:c1].contiguous()  # noqa: E731
+            F2 = torch.empty_like(loc(F0))
+            P2 = torch.empty((1, p, r), dtype=F0.dtype, device="cuda")
+            st2 = _lib.new_status()
+            g = self.struct([0, c1 - c0])
+            g.watchdog_s = 5
+            _ops.solve_group(At, loc(B), loc(F0), F2, max_iter=60, grad_tol=1e-8, lipschitz_safety=1.0,
+                             status=st2, group=g, next_bt=loc(Pt), next_out=P2)
+            s1, s2 = _lib.read_status(st1)[0], _lib.read_status(st2)[0]
+            ok = (int(s1["code"]) == 0 and int(s2["code"]) == 0 and s1["inner_iters"] == s2["inner_iters"] and
+                  bool(torch.allclose(F2, loc(F1), rtol=1e-9, atol=1e-12)))
+            part = P2[0].clone()
+            comm.all_reduce(part)
+            ok = ok and bool(torch.allclose(part, P1, rtol=1e-9, atol=1e-9))
+        except Exception:  # noqa: BLE001 - any failure disables the group path
+            ok = False
+        return not comm.any(not ok)
+
     def struct(self, col0) -> "_lib.GroupStruct":
         """nenmf_group for the next solve: ``col0`` is this launch's column
         partition (nvr + 1 offsets); the epoch advances identically on every

@@ -285,6 +285,9 @@ def _group_for(comm: Comm):
         uuids = [None] * comm.size
         comm.dist.all_gather_object(uuids, uuid, group=comm.group)
         g = SolveGroup.over(comm) if len(set(uuids)) == comm.size else None
+        if g is not None and not g.self_test(comm):
+            g.close()
+            g = None
         comm._solve_group = g
     return g
 
