@@ -148,6 +148,18 @@ int nenmf_solve_nnls_next(int dtype, const void* At, int64_t r, int64_t p,
 
 /* sigma_max(A)^2 by power iteration on the smaller Gram (matrix.py:158-174).
  * A (r x p) passed as At (p x r).  Result (double) -> *out (device). */
+/* ---- exact-SNR problem generator (synthetic.py:47-95), fused -----------
+ * G (n x p), F (p x m), N (n x m) fp64 on the device (the draws of
+ * generate_problem, bit-identical streams).  nenmf_generate_norms: out2[0] =
+ * ||G F||^2 (G F formed on the fly, not stored), out2[1] = ||N||^2, one read
+ * of N.  nenmf_generate_write: X = G F + scale N in dtype (N may be NULL for
+ * the noiseless case).  p <= 64. */
+size_t nenmf_generate_workspace_bytes(void);
+int nenmf_generate_norms(const double* G, const double* F, const double* N, int64_t n, int64_t m, int64_t p,
+                         double* out2, void* ws, size_t ws_bytes, void* stream);
+int nenmf_generate_write(int dtype, const double* G, const double* F, const double* N, int64_t n, int64_t m,
+                         int64_t p, double scale, void* X, void* stream);
+
 /* ---- rank groups ------------------------------------------
  * A compressed half-step whose columns are split over R ranks (X row-sharded
  * across GPUs: the G-half owns this rank's rows of G, the F-half a slice of

@@ -38,6 +38,9 @@ _SIGS = {
                                      _vp, _i32, _i32, _dbl, _vp, _i64, _vp, _vp, _vp, _sz, _vp]),
     "nenmf_solve_nnls_prepared_workspace_bytes": (_sz, [_i32, _i64, _i64, _i64]),
     "nenmf_group_xch_bytes": (_sz, []),
+    "nenmf_generate_workspace_bytes": (_sz, []),
+    "nenmf_generate_norms": (_i32, [_vp, _vp, _vp, _i64, _i64, _i64, _vp, _vp, _sz, _vp]),
+    "nenmf_generate_write": (_i32, [_i32, _vp, _vp, _vp, _i64, _i64, _i64, _dbl, _vp, _vp]),
     "nenmf_solve_nnls_group_check": (_i32, [_i32, _i64, _i64, _i64, _i64, _i32, _i32, _i32]),
     "nenmf_solve_nnls_group": (_i32, [_i32, _vp, _i64, _i64, _vp, _i64, _i64, _i32, _vp, _vp, _i32, _dbl, _dbl,
                                       _vp, _i32, _i32, _dbl, _vp, _i64, _vp, _vp, _vp, _vp, _sz, _vp]),

@@ -78,12 +78,16 @@ def generate_problem_device(n: int, m: int, p: int, snr_db: float, seed: int, *,
         Gh, Fh = open_uniform(rng, n, p), open_uniform(rng, p, m)
         G, F = torch.from_numpy(Gh).cuda(), torch.from_numpy(Fh).cuda()
         bitgen = rng.bit_generator
-    G = G.view(n, p)
-    F = F.view(p, m)
-    X = torch.matmul(G, F)  # plain library GEMM (cuBLAS DGEMM)
+    G = G.view(n, p).contiguous()
+    F = F.view(p, m).contiguous()
     tdt = _lib.torch_dtype(dtype)
+    X = torch.empty((n, m), dtype=tdt, device="cuda")
+    stream = _lib.stream_handle()
     if snr_db == math.inf:
-        return DeviceProblemInstance(X=X.to(tdt), G_true=G.to(tdt), F_true=F.to(tdt), snr_db_target=snr_db,
+        # G F straight into X (synthetic.py:62-66, noiseless)
+        _lib.check(lib.nenmf_generate_write(_lib.code_of(dtype), G.data_ptr(), F.data_ptr(), None, n, m, p, 0.0,
+                                            X.data_ptr(), stream), "generate_write")
+        return DeviceProblemInstance(X=X, G_true=G.to(tdt), F_true=F.to(tdt), snr_db_target=snr_db,
                                      snr_db_realized=math.inf, seed=seed)
     st = bitgen.state["state"]
     draws = normal_draws_device(int(st["state"]), int(st["inc"]), 1, n, m, "fp64")
@@ -91,12 +95,19 @@ def generate_problem_device(n: int, m: int, p: int, snr_db: float, seed: int, *,
         Nh = np.random.Generator(bitgen).standard_normal((n, m))
         noise = torch.from_numpy(Nh).cuda()
     else:
-        noise = draws[0].t()  # the first n*m draws, row-major n x m (stored transposed)
-    clean_norm = math.sqrt(_sumsq(X))
-    noise_norm = math.sqrt(_sumsq(noise.contiguous()))
+        noise = draws[0].t().contiguous()  # the first n*m draws, row-major n x m (stored transposed)
+    # the exact-SNR rescale (synthetic.py:77-81) in two fused passes: both
+    # norms in one read of the noise (G F formed on the fly), then X = G F + s N
+    ws = _lib.workspace(lib.nenmf_generate_workspace_bytes())
+    norms = _lib.zeros(2, torch.float64)
+    _lib.check(lib.nenmf_generate_norms(G.data_ptr(), F.data_ptr(), noise.data_ptr(), n, m, p, norms.data_ptr(),
+                                        ws.data_ptr(), ws.numel(), stream), "generate_norms")
+    c2, n2 = (float(v) for v in norms.cpu())
+    clean_norm, noise_norm = math.sqrt(c2), math.sqrt(n2)
     scale = clean_norm * 10.0 ** (-snr_db / 20.0) / noise_norm
-    noise = noise * scale
-    X = X + noise
-    realized = 10.0 * math.log10((clean_norm / math.sqrt(_sumsq(noise.contiguous()))) ** 2)
-    return DeviceProblemInstance(X=X.to(tdt), G_true=G.to(tdt), F_true=F.to(tdt), snr_db_target=float(snr_db),
+    _lib.check(lib.nenmf_generate_write(_lib.code_of(dtype), G.data_ptr(), F.data_ptr(), noise.data_ptr(), n, m, p,
+                                        scale, X.data_ptr(), stream), "generate_write")
+    # ||s N|| = s ||N|| up to rounding (the reference forms the scaled noise's norm)
+    realized = 10.0 * math.log10((clean_norm / (scale * noise_norm)) ** 2)
+    return DeviceProblemInstance(X=X, G_true=G.to(tdt), F_true=F.to(tdt), snr_db_target=float(snr_db),
                                  snr_db_realized=realized, seed=seed)
