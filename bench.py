@@ -555,9 +555,12 @@ def run_ours(args, rank, world, local_rank):
         del P32
         torch.cuda.empty_cache()
 
-    vanilla = None
+    vanilla = vanilla32 = None
     if not args.no_secondary:
         vanilla = run_vanilla(args, w, dtype, rank, world)
+        if dtype == "fp64":
+            vanilla32 = run_vanilla(args, workloads.make_workload(CFG, dtype="fp32"), "fp32", rank, world,
+                                    cpu_leg=False)
 
     cfg5 = None
     if not args.no_secondary:
@@ -590,7 +593,7 @@ def run_ours(args, rank, world, local_rank):
         "e2e": head["e2e"], "gpu_launches": head["gpu_launches"], "clocks": head["clocks"],
         "final_rre": head["final_rre"],
         "roofline": roof, "solver": solver,
-        "fp32_mode": fp32, "vanilla": vanilla, "cfg5_sharded": cfg5,
+        "fp32_mode": fp32, "vanilla": vanilla, "vanilla_fp32": vanilla32, "cfg5_sharded": cfg5,
         "cpu_baseline": cpu,
     }
     print(json.dumps(line), flush=True)
@@ -599,7 +602,7 @@ def run_ours(args, rank, world, local_rank):
 
 
 # ------------------------------------------------------ vanilla cfg2 block
-def run_vanilla(args, w, dtype, rank, world):
+def run_vanilla(args, w, dtype, rank, world, cpu_leg=True):
     """Vanilla NeNMF (factorize_vanilla, factorize.py:186-194) on BASELINE cfg 2
     (1 GPU as BASELINE.json states): 100 outer iterations, inner <= 500, on
     the full X; value = outer it/s.  FP32 forms V = A^T X with the tcgen05 pass
@@ -625,8 +628,10 @@ def run_vanilla(args, w, dtype, rank, world):
     ms = timer(run, k) / k
     out = {"metric": f"vanilla NeNMF outer iters/s (cfg2 n=m=1e4 p=20, {dtype}, 100 outer, inner<=500)",
            "value": OUTER / (ms / 1e3), "unit": UNIT, "ms_per_step": ms, "steps": k, "dtype": dtype,
-           "v_products": "tcgen05 BF16x3 pass over the prepared X" if dtype == "fp32" else "DMMA (FP64 tensor pipe)"}
-    if not args.no_cpu_baseline:
+           "v_products": "tcgen05 BF16x3 pass over the prepared X" if dtype == "fp32" else "DMMA (FP64 tensor pipe)",
+           "tie_break_residuals": ("tcgen05 pair pass over the prepared X (k_resid_bulk)" if dtype == "fp32"
+                                   else "DMMA (k_resid64)")}
+    if cpu_leg and not args.no_cpu_baseline:
         nenmf = _reference_package()
         if nenmf is not None:
             t0 = time.perf_counter()

@@ -244,6 +244,16 @@ int nenmf_residual_sumsq(int dtype, const void* X, int64_t n, int64_t m, int64_t
                          const void* Gt, const void* F, int64_t p, double* out,
                          void* ws, size_t ws_bytes, void* stream);
 
+/* nenmf_residual_sumsq reading X from its prepared copy Xp (FP32, p <= 32):
+ * one tensor-core pass (tcgen05, BF16x3 products, fp32 accumulators) per
+ * 128 x 128 tile computes G F and accumulates (x - (G F))^2 in fp64.  Falls
+ * back to the plain call on X when Xp is NULL or the shape has no prepared
+ * form (X may then not be NULL).  Workspace: *_prepared_workspace_bytes. */
+size_t nenmf_residual_sumsq_prepared_workspace_bytes(int dtype, int64_t n, int64_t m, int64_t p);
+int nenmf_residual_sumsq_prepared(int dtype, const void* X, const void* Xp, int64_t n, int64_t m,
+                                  int64_t ldx, const void* Gt, const void* F, int64_t p,
+                                  double* out, void* ws, size_t ws_bytes, void* stream);
+
 /* C (p x q) = A (p x K) B (q x K)^T, long K (factorize.py:110,113). */
 size_t nenmf_abt_workspace_bytes(int dtype, int64_t p, int64_t q, int64_t K);
 int nenmf_abt(int dtype, const void* A, int64_t p, const void* B, int64_t q, int64_t K,

@@ -63,6 +63,8 @@ _SIGS = {
     "nenmf_uniform_draws": (_i32, [C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, _i64, _vp, _vp, _vp]),
     "nenmf_residual_sumsq_workspace_bytes": (_sz, [_i32, _i64, _i64, _i64]),
     "nenmf_residual_sumsq": (_i32, [_i32, _vp, _i64, _i64, _i64, _vp, _vp, _i64, _vp, _vp, _sz, _vp]),
+    "nenmf_residual_sumsq_prepared_workspace_bytes": (_sz, [_i32, _i64, _i64, _i64]),
+    "nenmf_residual_sumsq_prepared": (_i32, [_i32, _vp, _vp, _i64, _i64, _i64, _vp, _vp, _i64, _vp, _vp, _sz, _vp]),
     "nenmf_abt_workspace_bytes": (_sz, [_i32, _i64, _i64, _i64]),
     "nenmf_abt": (_i32, [_i32, _vp, _i64, _vp, _i64, _i64, _vp, _vp, _sz, _vp]),
     "nenmf_dual_pass_workspace_bytes": (_sz, [_i32, _i64, _i64, _i64]),

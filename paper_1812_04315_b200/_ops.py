@@ -133,12 +133,20 @@ def sumsq(M, out, g=None) -> None:
     _lib.check(rc, "sumsq")
 
 
-def residual_sumsq(X, Gt, F, out) -> None:
-    """out[0] = ||X - Gt^T F||_F^2."""
+def residual_sumsq(X, Gt, F, out, Xp=None) -> None:
+    """out[0] = ||X - Gt^T F||_F^2; with ``Xp`` (prepare_x of X) the FP32
+    tensor-core pass over the prepared copy (nenmf_residual_sumsq_prepared)."""
     lib, _ = _lib.require_device()
     code = _lib.code_of(_dt(X))
     n, m = X.shape
     p = Gt.shape[0]
+    if Xp is not None:
+        ws = _lib.workspace(lib.nenmf_residual_sumsq_prepared_workspace_bytes(code, n, m, p))
+        rc = lib.nenmf_residual_sumsq_prepared(code, X.data_ptr(), Xp.data_ptr(), n, m, X.stride(0), Gt.data_ptr(),
+                                               F.data_ptr(), p, out.data_ptr(), ws.data_ptr(), ws.numel(),
+                                               _lib.stream_handle())
+        _lib.check(rc, "residual_sumsq_prepared")
+        return
     ws = _lib.workspace(lib.nenmf_residual_sumsq_workspace_bytes(code, n, m, p))
     rc = lib.nenmf_residual_sumsq(code, X.data_ptr(), n, m, X.stride(0), Gt.data_ptr(), F.data_ptr(), p,
                                   out.data_ptr(), ws.data_ptr(), ws.numel(), _lib.stream_handle())

@@ -3,6 +3,7 @@
 #include "common.cuh"
 #include "nnls.cuh"
 #include "nnls_common.cuh"
+#include <algorithm>
 #include <cstring>
 #include "rsi.cuh"
 #include "skinny.cuh"
@@ -323,6 +324,31 @@ int nenmf_residual_sumsq(int dtype, const void* X, int64_t n, int64_t m, int64_t
   if (rc != NENMF_OK) return rc;
   NENMF_CUDA_TRY(cudaMemcpyAsync(out, out2, sizeof(double), cudaMemcpyDeviceToDevice, S(stream)));
   return NENMF_OK;
+}
+
+size_t nenmf_residual_sumsq_prepared_workspace_bytes(int dtype, int64_t n, int64_t m, int64_t p) {
+  size_t b = nenmf_residual_sumsq_workspace_bytes(dtype, n, m, p);
+  if (dtype == NENMF_F32 && p >= 1 && p <= 32 && tc_pass_eligible(n, m, p)) {
+    Arena a(nullptr, 0);
+    const float* sent = reinterpret_cast<const float*>(16);
+    resid_tc_pre(a, reinterpret_cast<const uint8_t*>(16), n, m, sent, sent, p, nullptr, nullptr);
+    b = std::max(b, a.used + 256);
+  }
+  return b;
+}
+
+int nenmf_residual_sumsq_prepared(int dtype, const void* X, const void* Xp, int64_t n, int64_t m, int64_t ldx,
+                                  const void* Gt, const void* F, int64_t p, double* out, void* ws, size_t ws_bytes,
+                                  void* stream) {
+  if (ws == nullptr || out == nullptr) return NENMF_ERR_VALUE;
+  if (Xp != nullptr && dtype == NENMF_F32) {
+    Arena a(ws, ws_bytes);
+    const int rc = resid_tc_pre(a, static_cast<const uint8_t*>(Xp), n, m, static_cast<const float*>(Gt),
+                                static_cast<const float*>(F), p, out, S(stream));
+    if (rc != NENMF_ERR_UNSUPPORTED) return rc;
+  }
+  if (X == nullptr) return NENMF_ERR_UNSUPPORTED;
+  return nenmf_residual_sumsq(dtype, X, n, m, ldx, Gt, F, p, out, ws, ws_bytes, stream);
 }
 
 size_t nenmf_abt_workspace_bytes(int dtype, int64_t p, int64_t q, int64_t K) {

@@ -435,6 +435,185 @@ k_dual_bulk(const uint8_t* __restrict__ Xs, int64_t n, int64_t m, const uint8_t*
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
 }
 
+// ---------------------------------------------------------------------------
+// ||X - U^T V||^2 over the prepared X on the tensor cores (the RRE emit,
+// tracing.py:45-57, and the explicit-residual pair of the vanilla tie-break,
+// nnls.py:219-227).  Per 128 x 128 tile: P = U[:, rows]^T V[:, cols] by
+// tcgen05.mma (BF16x3, fp32 accumulator in TMEM, M = N = 128, K = kpad;
+// both operands MN-major: the split skinny tiles of k_split_skinny), then
+// the epilogue warps read their row of P from TMEM and of X (hi + lo) from
+// the same staged tile and accumulate (x - p)^2 in fp64.  NC = 2: a second
+// candidate that differs from the first in ONE operand (W replaces V when
+// w_is_v, else U) shares the X tile; its product goes to a second pair of
+// TMEM buffers.  The prepared X holds X to 16 significant bits and the
+// products carry BF16x3 error (~2^-17 relative); both enter the residual
+// norm at second order.
+//   warp 0: bulk-copy producer (X tile + U tile + V tile [+ W tile] per stage)
+//   warp 1: MMA issuer, TMEM owner (2 buffers x NC accumulators of 128 columns)
+//   warps 2-5: epilogue; a stage is free once the MMAs committed AND the
+//              epilogue read its X (mbarrier count 1 + 128)
+template <int KPAD, int NC>
+__global__ void __launch_bounds__(NWARPS * 32, 1)
+k_resid_bulk(const uint8_t* __restrict__ Xs, int64_t n, int64_t m, const uint8_t* __restrict__ U2,
+             const uint8_t* __restrict__ V2, const uint8_t* __restrict__ W2, int w_is_v, double* __restrict__ part,
+             const int* __restrict__ gate) {
+  constexpr int SK_SUB = 2 * KPAD * 128;
+  constexpr int SK_TILE = 2 * SK_SUB;
+  constexpr int STAGE = XTILE_BYTES + (1 + NC) * SK_TILE;  // X tile | U tile | V tile [| W tile]
+  constexpr uint32_t LO_OFF = KPAD * 128;
+  constexpr uint32_t TCOLS = NC == 1 ? 256 : 512;
+  // BF16 x BF16 -> F32, M = N = 128, A and B MN-major
+  constexpr uint32_t ID = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 15) | (1u << 16) | ((uint32_t)(TILE >> 3) << 17) |
+                          ((uint32_t)(TILE >> 4) << 24);
+  if (gate != nullptr && *gate == 0) return;  // uniform over the grid: nothing allocated yet
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  __shared__ __align__(8) uint64_t bar_full[NSTAGE], bar_empty[NSTAGE], bar_afull[2], bar_aempty[2];
+  __shared__ uint32_t tmem_base_sh;
+  __shared__ double red[33];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int n_ct = (int)((m + TILE - 1) / TILE);
+  const int64_t ntiles = (int64_t)((n + TILE - 1) / TILE) * n_ct;
+  if (tid == 0) {
+    for (int st = 0; st < NSTAGE; ++st) {
+      mbar_init(&bar_full[st], 1);
+      mbar_init(&bar_empty[st], 1 + 128);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&bar_afull[b], 1);
+      mbar_init(&bar_aempty[b], 128);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (wid == MMA_WARP) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_sh)),
+                 "n"(TCOLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  const uint32_t tmem = tmem_base_sh;
+  double acc[NC];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) acc[c] = 0.0;
+  if (wid == PROD_WARP) {
+    if (lane == 0) {
+      asm volatile("griddepcontrol.wait;" ::: "memory");  // the split operands are complete
+      const uint64_t pol_x = policy_evict_first(), pol_s = policy_evict_last();
+      int t = 0;
+      for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++t) {
+        const int rt = (int)(tile / n_ct), ct = (int)(tile % n_ct);
+        const int st = t % NSTAGE;
+        mbar_wait(&bar_empty[st], ((t / NSTAGE) & 1) ^ 1);
+        uint8_t* sp = smem + (size_t)st * STAGE;
+        mbar_expect_tx(&bar_full[st], (uint32_t)STAGE);
+        bulk_g2s(sp, Xs + ((int64_t)rt * n_ct + ct) * XTILE_BYTES, XTILE_BYTES, &bar_full[st], pol_x);
+        bulk_g2s(sp + XTILE_BYTES, U2 + (int64_t)rt * SK_TILE, SK_TILE, &bar_full[st], pol_s);
+        bulk_g2s(sp + XTILE_BYTES + SK_TILE, V2 + (int64_t)ct * SK_TILE, SK_TILE, &bar_full[st], pol_s);
+        if constexpr (NC == 2)
+          bulk_g2s(sp + XTILE_BYTES + 2 * SK_TILE, W2 + (int64_t)(w_is_v ? ct : rt) * SK_TILE, SK_TILE, &bar_full[st],
+                   pol_s);
+      }
+    }
+  } else if (wid == MMA_WARP) {
+    int t = 0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++t) {
+      const int st = t % NSTAGE, ab = t & 1;
+      if (lane == 0) {
+        mbar_wait(&bar_aempty[ab], ((t >> 1) & 1) ^ 1);
+        mbar_wait(&bar_full[st], (t / NSTAGE) & 1);
+      }
+      __syncwarp();
+      tc_fence_after();
+      if (lane == 0) {
+        const uint32_t sp = smem_u32(smem + (size_t)st * STAGE);
+        const uint32_t u2 = sp + XTILE_BYTES, v2 = u2 + SK_TILE, w2 = v2 + SK_TILE;
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+          const uint32_t a = (c == 1 && !w_is_v) ? w2 : u2, b = (c == 1 && w_is_v) ? w2 : v2;
+          const uint32_t d = tmem + (uint32_t)(2 * c + ab) * TILE;
+#pragma unroll
+          for (int kk = 0; kk < KPAD / 16; ++kk) {
+            const uint64_t ah = sdesc(a + kk * 2048, SK_SUB, 1024), al = sdesc(a + LO_OFF + kk * 2048, SK_SUB, 1024);
+            const uint64_t bh = sdesc(b + kk * 2048, SK_SUB, 1024), bl = sdesc(b + LO_OFF + kk * 2048, SK_SUB, 1024);
+            umma(d, ah, bh, ID, kk > 0 ? 1u : 0u);
+            umma(d, ah, bl, ID, 1u);
+            umma(d, al, bh, ID, 1u);
+          }
+        }
+        umma_commit(&bar_empty[st]);
+        umma_commit(&bar_afull[ab]);
+      }
+      __syncwarp();
+    }
+  } else if (wid >= EPI_WARP0 && wid < EPI_WARP0 + 4) {
+    const int quad = wid & 3;
+    const uint32_t lane_base = (uint32_t)(32 * quad) << 16;
+    const int r = 32 * quad + lane;  // this thread's row of the tile (TMEM lane)
+    int t = 0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++t) {
+      const int st = t % NSTAGE, ab = t & 1;
+      const int rt = (int)(tile / n_ct), ct = (int)(tile % n_ct);
+      mbar_wait(&bar_full[st], (t / NSTAGE) & 1);  // the X tile (already complete: the MMAs waited on it)
+      mbar_wait(&bar_afull[ab], (t >> 1) & 1);
+      tc_fence_after();
+      const uint8_t* sp = smem + (size_t)st * STAGE;
+      const bool row_ok = (int64_t)rt * TILE + r < n;
+      const int64_t cols = row_ok ? m - (int64_t)ct * TILE : 0;
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {  // 32 columns at a time, squares summed in fp32 then added in fp64
+        float pv[NC][32], sq[NC];
+#pragma unroll
+        for (int c = 0; c < NC; ++c) sq[c] = 0.f;
+#pragma unroll
+        for (int c = 0; c < NC; ++c) tmem_ld32(tmem + lane_base + (uint32_t)(2 * c + ab) * TILE + 32 * h, pv[c]);
+        // X (hi, lo) of this row, columns 32h..32h+31: sub h/2, 16-byte chunks 4(h%2)..4(h%2)+3
+        const uint8_t* rowp = sp + (h >> 1) * SUB_BYTES + r * 128;
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) {
+          const int chunk = 4 * (h & 1) + q4;
+          const int off = (chunk ^ (r & 7)) << 4;
+          const uint4 hv = *reinterpret_cast<const uint4*>(rowp + off);
+          const uint4 lv = *reinterpret_cast<const uint4*>(rowp + 2 * SUB_BYTES + off);
+          const uint32_t hw[4] = {hv.x, hv.y, hv.z, hv.w}, lw[4] = {lv.x, lv.y, lv.z, lv.w};
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const float2 hf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&hw[q]));
+            const float2 lf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&lw[q]));
+            const int col = 32 * h + 8 * q4 + 2 * q;
+            const float x0 = hf.x + lf.x, x1 = hf.y + lf.y;
+#pragma unroll
+            for (int c = 0; c < NC; ++c) {
+              const float d0 = col < cols ? x0 - pv[c][8 * q4 + 2 * q] : 0.f;
+              const float d1 = col + 1 < cols ? x1 - pv[c][8 * q4 + 2 * q + 1] : 0.f;
+              sq[c] = fmaf(d0, d0, sq[c]);
+              sq[c] = fmaf(d1, d1, sq[c]);
+            }
+          }
+        }
+#pragma unroll
+        for (int c = 0; c < NC; ++c) acc[c] += (double)sq[c];
+      }
+      tc_fence_before();
+      mbar_arrive(&bar_aempty[ab]);
+      mbar_arrive(&bar_empty[st]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (wid == MMA_WARP)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TCOLS) : "memory");
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    const double v = block_sum(acc[c], red);
+    if (tid == 0) part[NC * blockIdx.x + c] = v;
+  }
+}
+
 // fixed-order slab sums of both products in one launch: [0, cy) -> Y, [cy, cy + cz) -> Z
 __global__ void k_slabs(const float* __restrict__ py, int ny, int64_t cy, float* __restrict__ oy,
                         const float* __restrict__ pz, int nz, int64_t cz, float* __restrict__ oz) {
@@ -638,6 +817,82 @@ int dual_pass_tc(Arena& ws, const float* X, int64_t n, int64_t m, int64_t ldx, c
   if (ws.base != nullptr) NENMF_TRY(tc_presplit(X, n, m, ldx, Xs, s));
   NENMF_TRY(dual_pass_tc_pre(rest, Xs, n, m, At, Bt, k, Yt, Zt, s));
   ws = rest;
+  return NENMF_OK;
+}
+
+// ||X - U^T V||^2 over the prepared X (k_resid_bulk): out[0], and with a
+// second candidate out[1]: W replaces U (w_side 1) or V (w_side 2); X is
+// (n x m), U (k x n), V (k x m) fp32, contiguous.  `gate` (device int, may be
+// null): skip everything when zero (the tie-break's returned_best).
+// NENMF_ERR_UNSUPPORTED outside k <= 32 / the pass's shapes.
+__global__ void k_resid_final(const double* __restrict__ part, int nb, int nc, double* __restrict__ out,
+                              const int* __restrict__ gate) {
+  if (gate != nullptr && *gate == 0) return;
+  __shared__ double red[33];
+  for (int c = 0; c < nc; ++c) {
+    double a = 0.0;
+    for (int i = threadIdx.x; i < nb; i += blockDim.x) a += part[nc * i + c];
+    a = block_sum(a, red);
+    if (threadIdx.x == 0) out[c] = a;
+    __syncthreads();
+  }
+}
+
+int resid_tc_pre(Arena& ws, const uint8_t* Xs, int64_t n, int64_t m, const float* U, const float* V, int64_t k,
+                 double* out, cudaStream_t s, const float* W, int w_side, const int* gate) {
+  using namespace tc;
+  if (k < 1 || k > 32 || !tc_pass_eligible(n, m, k) || getenv("NENMF_RESID_NO_TC") != nullptr)
+    return NENMF_ERR_UNSUPPORTED;
+  const bool pair = w_side != 0;
+  const bool w_is_v = w_side == 2;
+  const int nc = pair ? 2 : 1;
+  const int kpad = k <= 16 ? 16 : 32;
+  const int n_rt = (int)cdiv(n, TILE), n_ct = (int)cdiv(m, TILE);
+  const int64_t sk_tile = (int64_t)2 * 2 * kpad * 128;
+  int sms = sm_count();
+  if (sms <= 0) sms = 148;
+  const unsigned grid = (unsigned)imin((int64_t)n_rt * n_ct, sms);
+  uint8_t* Us = ws.take<uint8_t>((size_t)n_rt * sk_tile);
+  uint8_t* Vs = ws.take<uint8_t>((size_t)n_ct * sk_tile);
+  uint8_t* Ws = pair ? ws.take<uint8_t>((size_t)(w_is_v ? n_ct : n_rt) * sk_tile) : nullptr;
+  double* part = ws.take<double>((size_t)grid * 2);
+  if (ws.base == nullptr) return NENMF_OK;
+  if (!ws.ok) return NENMF_ERR_WORKSPACE;
+  {
+    const int64_t ta = (int64_t)n_rt * 2 * 2 * kpad * 8, tb = (int64_t)n_ct * 2 * 2 * kpad * 8;
+    k_split_skinny<<<(unsigned)imin(cdiv(ta + tb, 256), 2368), 256, 0, s>>>(U, n, ta, Us, V, m, tb, Vs, (int)k,
+                                                                             kpad);
+    NENMF_LAUNCH_CHECK();
+    if (pair) {
+      const int64_t tw = w_is_v ? tb : ta;
+      k_split_skinny<<<(unsigned)imin(cdiv(tw, 256), 2368), 256, 0, s>>>(W, w_is_v ? m : n, tw, Ws, W, 0, 0, Ws,
+                                                                         (int)k, kpad);
+      NENMF_LAUNCH_CHECK();
+    }
+  }
+  const size_t smem = NSTAGE * (XTILE_BYTES + (1 + nc) * (size_t)sk_tile) + 1024;
+  cudaLaunchAttribute pdl[1];
+  pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  pdl[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(NWARPS * 32);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cfg.attrs = pdl;
+  cfg.numAttrs = 1;
+  const int wv = w_is_v ? 1 : 0;
+  auto go = [&](auto kern) -> int {
+    NENMF_CUDA_TRY(set_smem(kern, smem));
+    NENMF_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, Xs, n, m, (const uint8_t*)Us, (const uint8_t*)Vs,
+                                      (const uint8_t*)Ws, wv, part, gate));
+    return NENMF_OK;
+  };
+  if (kpad == 32) NENMF_TRY(pair ? go(k_resid_bulk<32, 2>) : go(k_resid_bulk<32, 1>));
+  else NENMF_TRY(pair ? go(k_resid_bulk<16, 2>) : go(k_resid_bulk<16, 1>));
+  NENMF_LAUNCH_CHECK();
+  k_resid_final<<<1, 256, 0, s>>>(part, (int)grid, nc, out, gate);
+  NENMF_LAUNCH_CHECK();
   return NENMF_OK;
 }
 

@@ -393,8 +393,24 @@ int solve_nnls(Arena& ws, const T* At, int64_t r, int64_t p, const T* B, int64_t
     }
   }
   if (fused) return (Pt != nullptr && !fused_next) ? abt<T>(ws, Fout, p, Pt, nup, c, Pout, s) : NENMF_OK;
-  // explicit residuals of best and start, only when an iterate improved (nnls.py:219-227)
-  NENMF_TRY(resid<T>(ws, At, p, r, B, c, ldb, trans, Fout, F0, Lbuf + 2, &st->returned_best, s));
+  // explicit residuals of best and start, only when an iterate improved (nnls.py:219-227);
+  // FP32 with a prepared X: both in one tensor-core pass (k_resid_bulk)
+  bool rdone = false;
+  if constexpr (sizeof(T) == 4) {
+    const int64_t nx = trans ? c : r, mx = trans ? r : c;
+    if (Xpre != nullptr && p <= 32 && tc_pass_eligible(nx, mx, p)) {
+      const float* A_f = reinterpret_cast<const float*>(At);
+      const float* F1 = reinterpret_cast<const float*>(Fout);
+      const float* F2 = reinterpret_cast<const float*>(F0);
+      const int rc = trans ? resid_tc_pre(ws, Xpre, nx, mx, F1, A_f, p, Lbuf + 2, s, F2, 1, &st->returned_best)
+                           : resid_tc_pre(ws, Xpre, nx, mx, A_f, F1, p, Lbuf + 2, s, F2, 2, &st->returned_best);
+      if (rc != NENMF_ERR_UNSUPPORTED) {
+        NENMF_TRY(rc);
+        rdone = true;
+      }
+    }
+  }
+  if (!rdone) NENMF_TRY(resid<T>(ws, At, p, r, B, c, ldb, trans, Fout, F0, Lbuf + 2, &st->returned_best, s));
   if (!dry) {
     k_decide<<<1, 1, 0, s>>>(Lbuf + 2, st);
     NENMF_LAUNCH_CHECK();

@@ -36,5 +36,9 @@ int tc_presplit(const float* X, int64_t n, int64_t m, int64_t ldx, uint8_t* Xs, 
                 int* nonzero = nullptr);
 int dual_pass_tc_pre(Arena& ws, const uint8_t* Xs, int64_t n, int64_t m, const float* At, const float* Bt,
                      int64_t k, float* Yt, float* Zt, cudaStream_t s);
+// ||X - U^T V||^2 over the prepared X on the tensor cores (U: k x n, V: k x m)
+// -> out[0]; with a second candidate -> out[1]: W replaces U (w_side 1) or V (w_side 2)
+int resid_tc_pre(Arena& ws, const uint8_t* Xs, int64_t n, int64_t m, const float* U, const float* V, int64_t k,
+                 double* out, cudaStream_t s, const float* W = nullptr, int w_side = 0, const int* gate = nullptr);
 
 }  // namespace nenmf

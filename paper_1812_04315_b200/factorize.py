@@ -144,7 +144,8 @@ class _DeviceLoop:
             L, Rt = sketch_on_device(self.sketch, self.dtype)
             self.L, self.Rt = L, Rt
             # the compressed preamble stays on the solver clock (factorize.py:130)
-            self.XL, self.XRt = compress_device(self.X, L, Rt, prepared=prepared_for(self.sketch, self.X))
+            self.Xp = prepared_for(self.sketch, self.X)  # also read by the emit's residual (objective)
+            self.XL, self.XRt = compress_device(self.X, L, Rt, prepared=self.Xp)
             nu = L.shape[0]
             self.FR = torch.empty((self.p, nu), dtype=self.X.dtype, device="cuda")
             self.fr_ready = False
@@ -211,8 +212,21 @@ class _DeviceLoop:
     def stop_vote(self, stop: bool) -> bool:
         return stop
 
+    def resid_xp(self):
+        """The prepared copy of this rank's X read by the emit's residual (FP32:
+        one tensor-core pass, k_resid_bulk): the solver's / sketch's copy when
+        there is one, else made once on first use; None for FP64."""
+        if self.dtype != "fp32":
+            return None
+        xp = getattr(self, "Xp", None)
+        if xp is None:
+            xp = getattr(self, "_resid_xp", None)
+            if xp is None:
+                xp = self._resid_xp = _ops.prepare_x(self.X, self.p)
+        return xp
+
     def objective(self) -> float:
-        _ops.residual_sumsq(self.X, self.Gt, self.F, self.scal[1:2])
+        _ops.residual_sumsq(self.X, self.Gt, self.F, self.scal[1:2], Xp=self.resid_xp())
         return math.sqrt(self.scal[1].item())
 
     def host_factors(self):
@@ -270,7 +284,7 @@ class _ShardedDeviceLoop(_DeviceLoop):
     def objective(self) -> float:
         Gl = self.Gt[:, self.row0:self.row0 + self.n_r].contiguous()
         _lib.zero_(self.scal[1:2])
-        _ops.residual_sumsq(self.X, Gl, self.F, self.scal[1:2])
+        _ops.residual_sumsq(self.X, Gl, self.F, self.scal[1:2], Xp=self.resid_xp())
         self.comm.all_reduce(self.scal[1:2])
         return math.sqrt(self.scal[1].item())
 
@@ -374,7 +388,7 @@ class _GroupDeviceLoop(_DeviceLoop):
 
     def objective(self) -> float:
         _lib.zero_(self.scal[1:2])
-        _ops.residual_sumsq(self.X, self.Gt, self.full_F(), self.scal[1:2])
+        _ops.residual_sumsq(self.X, self.Gt, self.full_F(), self.scal[1:2], Xp=self.resid_xp())
         if not self.emulated:
             self.comm.all_reduce(self.scal[1:2])
         return math.sqrt(self.scal[1].item())

@@ -121,7 +121,7 @@ def _worker(rank, world, port, X, Lfull, Rfull, G0, F0, outer, inner, out_dir):
     _lib.to_host = lambda t: t.detach().double().numpy()
     _ops.abt = lambda A, B, out: out.copy_(A @ B.T)
     _ops.sumsq = lambda M, out, g=None: out.add_(float((M.double() ** 2).sum()))
-    _ops.residual_sumsq = lambda X, Gt, F, out: out.add_(float(((X - Gt.T @ F) ** 2).sum()))
+    _ops.residual_sumsq = lambda X, Gt, F, out, Xp=None: out.add_(float(((X - Gt.T @ F) ** 2).sum()))
     _ops.solve_group = lambda *a, **k: _group_solve_numpy(dist, *a, **k)
     factorize._panel_t = lambda G, dtype: torch.from_numpy(np.ascontiguousarray(np.asarray(G).T))
 

@@ -25,4 +25,6 @@ ncu --set full --clock-control none --import-source on -k regex:k_dual_bulk -s 3
     -o gpurun_out/prof/full_k_dual_bulk python tools/sketch_launches.py fp32 > gpurun_out/prof/ncu_full4.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:k_nnls_mma -s 1 -c 1 \
     -o gpurun_out/prof/full_k_nnls_mma_f32 python tools/profile_solve.py fp32 2 > gpurun_out/prof/ncu_full5.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:k_resid_bulk -c 1 \
+    -o gpurun_out/prof/full_k_resid_bulk python tools/time_resid.py --reps 1 > gpurun_out/prof/ncu_full6.log 2>&1
 ls -la gpurun_out/prof
