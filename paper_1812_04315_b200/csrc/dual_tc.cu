@@ -83,6 +83,23 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t
   d |= (uint64_t)2 << 61;
   return d;
 }
+// The descriptor's address field holds (shared address >> 4) in 14 bits; shared
+// memory ends below 256 KB, so moving a descriptor by `bytes` is one 32-bit
+// add on its low word.  The MMA warp keeps every descriptor a warp-uniform
+// value (uniform registers, no per-MMA register-to-uniform transfers): the
+// whole warp computes them and one elected lane issues the instruction.
+__device__ __forceinline__ uint32_t sdesc_lo(uint32_t saddr, uint32_t lbo) {
+  return ((saddr >> 4) & 0x3FFFu) | (((lbo >> 4) & 0x3FFFu) << 16);
+}
+constexpr uint32_t SDESC_HI = ((1024u >> 4) & 0x3FFFu) | (1u << 14) | (2u << 29);  // SBO 1024, version 1, 128B swizzle
+__device__ __forceinline__ uint64_t sdesc_at(uint32_t lo, uint32_t bytes) {
+  return ((uint64_t)SDESC_HI << 32) | (uint64_t)(lo + (bytes >> 4));
+}
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred;
+  asm volatile("{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\tselp.u32 %0, 1, 0, p;\n\t}" : "=r"(pred));
+  return pred != 0;
+}
 // instruction descriptor: BF16 x BF16 -> F32, M = 128
 __host__ __device__ constexpr uint32_t idesc_bf16(int N, bool a_mn) {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((a_mn ? 1u : 0u) << 15) | ((uint32_t)(N >> 3) << 17) |
@@ -253,10 +270,13 @@ __global__ void k_split_skinny(const float* __restrict__ SA, int64_t lenA, int64
   }
 }
 
-template <int KPAD>
+// NST stages of [X tile | A tile]; NB buffers for the tile row's B tile.
+// dbg (development, tools/probe_dual.py): bit 0 skips the MMAs, bit 1 the X copies.
+template <int KPAD, int NST, int NB>
 __global__ void __launch_bounds__(NWARPS * 32, 1)
 k_dual_bulk(const uint8_t* __restrict__ Xs, int64_t n, int64_t m, const uint8_t* __restrict__ A2,
-            const uint8_t* __restrict__ B2, int k, Units U, float* __restrict__ Ypart, float* __restrict__ Zpart) {
+            const uint8_t* __restrict__ B2, int k, Units U, float* __restrict__ Ypart, float* __restrict__ Zpart,
+            int dbg) {
   constexpr int SK_SUB = 2 * KPAD * 128;             // skinny sub-tile bytes (hi + lo rows x 128 B)
   constexpr int SK_TILE = 2 * SK_SUB;                // one 128-wide K tile of a skinny operand
   constexpr int STAGE = XTILE_BYTES + SK_TILE;       // X tile | A tile (B: per tile row, below)
@@ -264,18 +284,19 @@ k_dual_bulk(const uint8_t* __restrict__ Xs, int64_t n, int64_t m, const uint8_t*
   constexpr uint32_t LO_OFF = KPAD * 128;            // lo rows of a skinny sub-tile
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
-  uint8_t* bbuf = smem + (size_t)NSTAGE * STAGE;  // [2][SK_TILE]: B tile of the current / next tile row
-  __shared__ __align__(8) uint64_t bar_full[NSTAGE], bar_empty[NSTAGE], bar_yfull[2], bar_yempty[2], bar_zfull,
-      bar_zempty, bar_bfull[2], bar_bempty[2];
+  uint8_t* bbuf = smem + (size_t)NST * STAGE;  // [NB][SK_TILE]: B tile of the current (/ next) tile row
+  __shared__ __align__(8) uint64_t bar_full[NST], bar_empty[NST], bar_yfull[2], bar_yempty[2], bar_zfull, bar_zempty,
+      bar_bfull[NB], bar_bempty[NB];
   __shared__ uint32_t tmem_base_sh;
 
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int wid = __shfl_sync(0xffffffffu, tid >> 5, 0);  // warp-uniform for the compiler
   if (tid == 0) {
-    for (int s = 0; s < NSTAGE; ++s) {
+    for (int s = 0; s < NST; ++s) {
       mbar_init(&bar_full[s], 1);
       mbar_init(&bar_empty[s], 1);
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < NB; ++b) {
       mbar_init(&bar_bfull[b], 1);
       mbar_init(&bar_bempty[b], 1);
     }
@@ -305,24 +326,30 @@ k_dual_bulk(const uint8_t* __restrict__ Xs, int64_t n, int64_t m, const uint8_t*
 
   if (wid == PROD_WARP) {
     // ------------------------------------------------------------ producer
-    if (lane == 0) {
-      asm volatile("griddepcontrol.wait;" ::: "memory");  // the split skinny operands are complete
-      const uint64_t pol_x = policy_evict_first(), pol_s = policy_evict_last();
-      int t = 0, row_count = 0;
-      for (int u = blockIdx.x; u < U.units; u += gridDim.x) {
-        int rt0, rt1, ct0, ct1, rc, cb;
-        unit_bounds(U, u, rt0, rt1, ct0, ct1, rc, cb);
-        for (int rt = rt0; rt < rt1; ++rt, ++row_count) {
-          const int rb = row_count & 1;
-          mbar_wait(&bar_bempty[rb], ((row_count >> 1) & 1) ^ 1);
+    // (the whole warp walks the unit; one elected lane issues the copies)
+    const bool leader = elect_one();
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // the split skinny operands are complete
+    const uint64_t pol_x = policy_evict_first(), pol_s = policy_evict_last();
+    const bool no_x = (dbg & 2) != 0;
+    int t = 0, row_count = 0;
+    for (int u = blockIdx.x; u < U.units; u += gridDim.x) {
+      int rt0, rt1, ct0, ct1, rc, cb;
+      unit_bounds(U, u, rt0, rt1, ct0, ct1, rc, cb);
+      for (int rt = rt0; rt < rt1; ++rt, ++row_count) {
+        const int rb = row_count % NB;
+        mbar_wait(&bar_bempty[rb], ((row_count / NB) & 1) ^ 1);
+        if (leader) {
           mbar_expect_tx(&bar_bfull[rb], (uint32_t)SK_TILE);
           bulk_g2s(bbuf + (size_t)rb * SK_TILE, B2 + (int64_t)rt * SK_TILE, SK_TILE, &bar_bfull[rb], pol_s);
-          for (int ct = ct0; ct < ct1; ++ct, ++t) {
-            const int s = t % NSTAGE;
-            mbar_wait(&bar_empty[s], ((t / NSTAGE) & 1) ^ 1);
-            uint8_t* st = smem + (size_t)s * STAGE;
-            mbar_expect_tx(&bar_full[s], (uint32_t)STAGE);
-            bulk_g2s(st, Xs + ((int64_t)rt * U.n_ct + ct) * XTILE_BYTES, XTILE_BYTES, &bar_full[s], pol_x);
+        }
+        for (int ct = ct0; ct < ct1; ++ct, ++t) {
+          const int s = t % NST;
+          mbar_wait(&bar_empty[s], ((t / NST) & 1) ^ 1);
+          uint8_t* st = smem + (size_t)s * STAGE;
+          if (leader) {
+            mbar_expect_tx(&bar_full[s], (uint32_t)(no_x ? SK_TILE : STAGE));
+            if (!no_x)
+              bulk_g2s(st, Xs + ((int64_t)rt * U.n_ct + ct) * XTILE_BYTES, XTILE_BYTES, &bar_full[s], pol_x);
             bulk_g2s(st + XTILE_BYTES, A2 + (int64_t)ct * SK_TILE, SK_TILE, &bar_full[s], pol_s);
           }
         }
@@ -330,58 +357,59 @@ k_dual_bulk(const uint8_t* __restrict__ Xs, int64_t n, int64_t m, const uint8_t*
     }
   } else if (wid == MMA_WARP) {
     // ------------------------------------------------------------ MMA issuer
+    const bool leader = elect_one();
+    const bool no_mma = (dbg & 1) != 0;
+    const uint32_t sbase = smem_u32(smem), bbase = smem_u32(bbuf);
     int t = 0, row_count = 0, unit_count = 0;
     for (int u = blockIdx.x; u < U.units; u += gridDim.x, ++unit_count) {
       int rt0, rt1, ct0, ct1, rc, cb;
       unit_bounds(U, u, rt0, rt1, ct0, ct1, rc, cb);
-      if (lane == 0) mbar_wait(&bar_zempty, (unit_count & 1) ^ 1);
+      mbar_wait(&bar_zempty, (unit_count & 1) ^ 1);
       for (int rt = rt0; rt < rt1; ++rt, ++row_count) {
-        const int yb = row_count & 1;
-        if (lane == 0) {
-          mbar_wait(&bar_yempty[yb], ((row_count >> 1) & 1) ^ 1);
-          mbar_wait(&bar_bfull[yb], (row_count >> 1) & 1);
-        }
+        const int yb = row_count & 1, rb = row_count % NB;
+        mbar_wait(&bar_yempty[yb], ((row_count >> 1) & 1) ^ 1);
+        mbar_wait(&bar_bfull[rb], (row_count / NB) & 1);
+        const uint32_t bk = sdesc_lo(bbase + (uint32_t)rb * SK_TILE, 16);  // B tile, K-major
+        const uint32_t dy = tmem + ycol0 + (uint32_t)yb * KPAD;
         for (int ct = ct0; ct < ct1; ++ct, ++t) {
-          const int s = t % NSTAGE;
-          if (lane == 0) mbar_wait(&bar_full[s], (t / NSTAGE) & 1);
-          __syncwarp();
+          const int s = t % NST;
+          mbar_wait(&bar_full[s], (t / NST) & 1);
           tc_fence_after();
-          if (lane == 0) {
-            const uint32_t st = smem_u32(smem + (size_t)s * STAGE);
-            const uint32_t xhi = st, xlo = st + 2 * SUB_BYTES, a2 = st + XTILE_BYTES;
-            const uint32_t b2 = smem_u32(bbuf + (size_t)yb * SK_TILE);
-            const uint32_t dy = tmem + ycol0 + (uint32_t)yb * KPAD;
-            const uint32_t dz = tmem + zcol0 + (uint32_t)(ct - ct0) * KPAD;
-            // Y: K = 128 columns of X = 2 sub-tiles x 4 chunks of 16
+          const uint32_t st = sbase + (uint32_t)s * STAGE;
+          const uint32_t xk = sdesc_lo(st, 16);                  // X hi, K-major (Y: K = columns)
+          const uint32_t xm = sdesc_lo(st, SUB_BYTES);           // X hi, MN-major (Z: K = rows)
+          const uint32_t ak = sdesc_lo(st + XTILE_BYTES, 16);    // A tile, K-major
+          const uint32_t dz = tmem + zcol0 + (uint32_t)(ct - ct0) * KPAD;
+          const uint32_t acc_y = ct > ct0 ? 1u : 0u, acc_z = rt > rt0 ? 1u : 0u;
+          if (leader) {
+            if (!no_mma) {
+              // Y: K = 128 columns of X = 2 sub-tiles x 4 chunks of 16
 #pragma unroll
-            for (int kk = 0; kk < 8; ++kk) {
-              const uint32_t sub = kk >> 2, koff = (kk & 3) * 32;
-              const uint64_t ah = sdesc(xhi + sub * SUB_BYTES + koff, 16, 1024);
-              const uint64_t al = sdesc(xlo + sub * SUB_BYTES + koff, 16, 1024);
-              const uint64_t bh = sdesc(a2 + sub * SK_SUB + koff, 16, 1024);
-              const uint64_t bl = sdesc(a2 + sub * SK_SUB + LO_OFF + koff, 16, 1024);
-              umma(dy, ah, bh, ID_Y, (ct > ct0 || kk > 0) ? 1u : 0u);
-              umma(dy, ah, bl, ID_Y, 1u);
-              umma(dy, al, bh, ID_Y, 1u);
-            }
-            // Z: K = 128 rows of X = 8 chunks of 16 rows; A is MN-major (LBO = next 64 columns)
+              for (int kk = 0; kk < 8; ++kk) {
+                const uint32_t xo = (kk >> 2) * SUB_BYTES + (kk & 3) * 32, so = (kk >> 2) * SK_SUB + (kk & 3) * 32;
+                const uint64_t ah = sdesc_at(xk, xo), al = sdesc_at(xk, 2 * SUB_BYTES + xo);
+                const uint64_t bh = sdesc_at(ak, so), bl = sdesc_at(ak, so + LO_OFF);
+                umma(dy, ah, bh, ID_Y, kk > 0 ? 1u : acc_y);
+                umma(dy, ah, bl, ID_Y, 1u);
+                umma(dy, al, bh, ID_Y, 1u);
+              }
+              // Z: K = 128 rows of X = 8 chunks of 16 rows; A is MN-major (LBO = next 64 columns)
 #pragma unroll
-            for (int kk = 0; kk < 8; ++kk) {
-              const uint64_t ah = sdesc(xhi + kk * 2048, SUB_BYTES, 1024);
-              const uint64_t al = sdesc(xlo + kk * 2048, SUB_BYTES, 1024);
-              const uint32_t bsub = b2 + (kk >> 2) * SK_SUB + (kk & 3) * 32;
-              const uint64_t bh = sdesc(bsub, 16, 1024);
-              const uint64_t bl = sdesc(bsub + LO_OFF, 16, 1024);
-              umma(dz, ah, bh, ID_Z, (rt > rt0 || kk > 0) ? 1u : 0u);
-              umma(dz, ah, bl, ID_Z, 1u);
-              umma(dz, al, bh, ID_Z, 1u);
+              for (int kk = 0; kk < 8; ++kk) {
+                const uint32_t so = (kk >> 2) * SK_SUB + (kk & 3) * 32;
+                const uint64_t ah = sdesc_at(xm, kk * 2048), al = sdesc_at(xm, 2 * SUB_BYTES + kk * 2048);
+                const uint64_t bh = sdesc_at(bk, so), bl = sdesc_at(bk, so + LO_OFF);
+                umma(dz, ah, bh, ID_Z, kk > 0 ? 1u : acc_z);
+                umma(dz, ah, bl, ID_Z, 1u);
+                umma(dz, al, bh, ID_Z, 1u);
+              }
             }
             umma_commit(&bar_empty[s]);
             if (ct == ct1 - 1) {
               umma_commit(&bar_yfull[yb]);
-              umma_commit(&bar_bempty[yb]);
+              umma_commit(&bar_bempty[rb]);
+              if (rt == rt1 - 1) umma_commit(&bar_zfull);
             }
-            if (ct == ct1 - 1 && rt == rt1 - 1) umma_commit(&bar_zfull);
           }
           __syncwarp();
         }
@@ -471,7 +499,8 @@ k_resid_bulk(const uint8_t* __restrict__ Xs, int64_t n, int64_t m, const uint8_t
   __shared__ __align__(8) uint64_t bar_full[NSTAGE], bar_empty[NSTAGE], bar_afull[2], bar_aempty[2];
   __shared__ uint32_t tmem_base_sh;
   __shared__ double red[33];
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int wid = __shfl_sync(0xffffffffu, tid >> 5, 0);  // warp-uniform for the compiler
   const int n_ct = (int)((m + TILE - 1) / TILE);
   const int64_t ntiles = (int64_t)((n + TILE - 1) / TILE) * n_ct;
   if (tid == 0) {
@@ -500,15 +529,16 @@ k_resid_bulk(const uint8_t* __restrict__ Xs, int64_t n, int64_t m, const uint8_t
 #pragma unroll
   for (int c = 0; c < NC; ++c) acc[c] = 0.0;
   if (wid == PROD_WARP) {
-    if (lane == 0) {
-      asm volatile("griddepcontrol.wait;" ::: "memory");  // the split operands are complete
-      const uint64_t pol_x = policy_evict_first(), pol_s = policy_evict_last();
-      int t = 0;
-      for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++t) {
-        const int rt = (int)(tile / n_ct), ct = (int)(tile % n_ct);
-        const int st = t % NSTAGE;
-        mbar_wait(&bar_empty[st], ((t / NSTAGE) & 1) ^ 1);
-        uint8_t* sp = smem + (size_t)st * STAGE;
+    const bool leader = elect_one();
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // the split operands are complete
+    const uint64_t pol_x = policy_evict_first(), pol_s = policy_evict_last();
+    int t = 0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++t) {
+      const int rt = (int)(tile / n_ct), ct = (int)(tile % n_ct);
+      const int st = t % NSTAGE;
+      mbar_wait(&bar_empty[st], ((t / NSTAGE) & 1) ^ 1);
+      uint8_t* sp = smem + (size_t)st * STAGE;
+      if (leader) {
         mbar_expect_tx(&bar_full[st], (uint32_t)STAGE);
         bulk_g2s(sp, Xs + ((int64_t)rt * n_ct + ct) * XTILE_BYTES, XTILE_BYTES, &bar_full[st], pol_x);
         bulk_g2s(sp + XTILE_BYTES, U2 + (int64_t)rt * SK_TILE, SK_TILE, &bar_full[st], pol_s);
@@ -519,26 +549,27 @@ k_resid_bulk(const uint8_t* __restrict__ Xs, int64_t n, int64_t m, const uint8_t
       }
     }
   } else if (wid == MMA_WARP) {
+    const bool leader = elect_one();
+    const uint32_t sbase = smem_u32(smem);
     int t = 0;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++t) {
       const int st = t % NSTAGE, ab = t & 1;
-      if (lane == 0) {
-        mbar_wait(&bar_aempty[ab], ((t >> 1) & 1) ^ 1);
-        mbar_wait(&bar_full[st], (t / NSTAGE) & 1);
-      }
-      __syncwarp();
+      mbar_wait(&bar_aempty[ab], ((t >> 1) & 1) ^ 1);
+      mbar_wait(&bar_full[st], (t / NSTAGE) & 1);
       tc_fence_after();
-      if (lane == 0) {
-        const uint32_t sp = smem_u32(smem + (size_t)st * STAGE);
-        const uint32_t u2 = sp + XTILE_BYTES, v2 = u2 + SK_TILE, w2 = v2 + SK_TILE;
+      const uint32_t sp = sbase + (uint32_t)st * STAGE;
+      // skinny tiles, MN-major (LBO = the next 64 of the long dimension)
+      const uint32_t u2 = sdesc_lo(sp + XTILE_BYTES, SK_SUB), v2 = sdesc_lo(sp + XTILE_BYTES + SK_TILE, SK_SUB),
+                     w2 = sdesc_lo(sp + XTILE_BYTES + 2 * SK_TILE, SK_SUB);
+      if (leader) {
 #pragma unroll
         for (int c = 0; c < NC; ++c) {
           const uint32_t a = (c == 1 && !w_is_v) ? w2 : u2, b = (c == 1 && w_is_v) ? w2 : v2;
           const uint32_t d = tmem + (uint32_t)(2 * c + ab) * TILE;
 #pragma unroll
           for (int kk = 0; kk < KPAD / 16; ++kk) {
-            const uint64_t ah = sdesc(a + kk * 2048, SK_SUB, 1024), al = sdesc(a + LO_OFF + kk * 2048, SK_SUB, 1024);
-            const uint64_t bh = sdesc(b + kk * 2048, SK_SUB, 1024), bl = sdesc(b + LO_OFF + kk * 2048, SK_SUB, 1024);
+            const uint64_t ah = sdesc_at(a, kk * 2048), al = sdesc_at(a, LO_OFF + kk * 2048);
+            const uint64_t bh = sdesc_at(b, kk * 2048), bl = sdesc_at(b, LO_OFF + kk * 2048);
             umma(d, ah, bh, ID, kk > 0 ? 1u : 0u);
             umma(d, ah, bl, ID, 1u);
             umma(d, al, bh, ID, 1u);
@@ -720,17 +751,18 @@ static int dual_pass_tc_chunk(Arena& ws, const uint8_t* Xs, int64_t n, int64_t m
                               int64_t k, float* Yt, float* Zt, cudaStream_t s);
 
 // One pass over a pre-split X (tc_presplit): Yt = At X^T (k x n), Zt = Bt X (k x m).
-// k > 32 (cfg3's p' = 60, cfg4's 40): the skinny operands are processed in
-// row blocks of 32 (short-major storage: a block is a contiguous slice), one
-// X stream per block.
+// k <= 64 reads X once (kpad 16 / 32 / 64: cfg3's p' = 60 and cfg4's 40 run the
+// 64-wide instance).  k > 64: the skinny operands are processed in row blocks
+// of 64 (short-major storage: a block is a contiguous slice), one X stream per block.
 int dual_pass_tc_pre(Arena& ws, const uint8_t* Xs, int64_t n, int64_t m, const float* At, const float* Bt,
                      int64_t k, float* Yt, float* Zt, cudaStream_t s) {
   if (At == nullptr || Bt == nullptr || !tc_pass_eligible(n, m, k)) return NENMF_ERR_UNSUPPORTED;
-  if (k <= 32) return dual_pass_tc_chunk(ws, Xs, n, m, At, Bt, k, Yt, Zt, s);
+  static const int64_t kblock = getenv("NENMF_DUAL_K32") != nullptr ? 32 : 64;
+  if (k <= kblock) return dual_pass_tc_chunk(ws, Xs, n, m, At, Bt, k, Yt, Zt, s);
   const bool dry = ws.base == nullptr;
   size_t need = 0;
-  for (int64_t k0 = 0; k0 < k; k0 += 32) {
-    const int64_t kc = imin(32, k - k0);
+  for (int64_t k0 = 0; k0 < k; k0 += kblock) {
+    const int64_t kc = imin(kblock, k - k0);
     Arena a = dry ? Arena(nullptr, 0) : ws;
     NENMF_TRY(dual_pass_tc_chunk(a, Xs, n, m, At + k0 * m, Bt + k0 * n, kc, Yt ? Yt + k0 * n : nullptr,
                                  Zt ? Zt + k0 * m : nullptr, s));
@@ -740,10 +772,23 @@ int dual_pass_tc_pre(Arena& ws, const uint8_t* Xs, int64_t n, int64_t m, const f
   return NENMF_OK;
 }
 
+// Shared-memory plan per kpad (227 KB per CTA): stages of [64 KB X tile | A tile] + B buffers.
+//   kpad 16: 3 x 72 KB + 1 x  8 KB;  kpad 32: 2 x 80 KB + 2 x 16 KB;  kpad 64: 2 x 96 KB + 1 x 32 KB
+template <int KPAD, int NST, int NB>
+static int launch_dual(const cudaLaunchConfig_t& base, const uint8_t* Xs, int64_t n, int64_t m, const uint8_t* A2,
+                       const uint8_t* B2, int k, const tc::Units& U, float* Yo, float* Zo, int dbg) {
+  cudaLaunchConfig_t cfg = base;
+  const size_t sk_tile = (size_t)2 * 2 * KPAD * 128;
+  cfg.dynamicSmemBytes = NST * (tc::XTILE_BYTES + sk_tile) + NB * sk_tile + 1024;
+  NENMF_CUDA_TRY(set_smem(tc::k_dual_bulk<KPAD, NST, NB>, cfg.dynamicSmemBytes));
+  NENMF_CUDA_TRY(cudaLaunchKernelEx(&cfg, tc::k_dual_bulk<KPAD, NST, NB>, Xs, n, m, A2, B2, k, U, Yo, Zo, dbg));
+  return NENMF_OK;
+}
+
 static int dual_pass_tc_chunk(Arena& ws, const uint8_t* Xs, int64_t n, int64_t m, const float* At, const float* Bt,
                               int64_t k, float* Yt, float* Zt, cudaStream_t s) {
   using namespace tc;
-  const int kpad = k <= 16 ? 16 : 32;
+  const int kpad = k <= 16 ? 16 : k <= 32 ? 32 : 64;
   const int ctmax = (512 - 2 * kpad) / kpad;
   int sms = sm_count();
   if (sms <= 0) sms = 148;
@@ -761,8 +806,6 @@ static int dual_pass_tc_chunk(Arena& ws, const uint8_t* Xs, int64_t n, int64_t m
                                                                              kpad);
     NENMF_LAUNCH_CHECK();
   }
-  const size_t stage = XTILE_BYTES + (size_t)sk_tile;
-  const size_t smem = NSTAGE * stage + 2 * (size_t)sk_tile + 1024;
   const unsigned grid = (unsigned)imin(U.units, sms);
   float* Yo = Ypart ? Ypart : Yt;
   float* Zo = Zpart ? Zpart : Zt;
@@ -775,19 +818,14 @@ static int dual_pass_tc_chunk(Arena& ws, const uint8_t* Xs, int64_t n, int64_t m
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(NWARPS * 32);
-  cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cfg.attrs = pdl;
   cfg.numAttrs = 1;
-  if (kpad == 32) {
-    NENMF_CUDA_TRY(set_smem(k_dual_bulk<32>, smem));
-    NENMF_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_dual_bulk<32>, Xs, n, m, (const uint8_t*)A2, (const uint8_t*)B2, (int)k,
-                                      U, Yo, Zo));
-  } else {
-    NENMF_CUDA_TRY(set_smem(k_dual_bulk<16>, smem));
-    NENMF_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_dual_bulk<16>, Xs, n, m, (const uint8_t*)A2, (const uint8_t*)B2, (int)k,
-                                      U, Yo, Zo));
-  }
+  const char* de = getenv("NENMF_DUAL_DBG");  // development: results invalid when set
+  const int dbg = de != nullptr ? atoi(de) : 0;
+  if (kpad == 64) NENMF_TRY((launch_dual<64, 2, 1>(cfg, Xs, n, m, A2, B2, (int)k, U, Yo, Zo, dbg)));
+  else if (kpad == 32) NENMF_TRY((launch_dual<32, 2, 2>(cfg, Xs, n, m, A2, B2, (int)k, U, Yo, Zo, dbg)));
+  else NENMF_TRY((launch_dual<16, 3, 1>(cfg, Xs, n, m, A2, B2, (int)k, U, Yo, Zo, dbg)));
   NENMF_LAUNCH_CHECK();
   if (timed) cudaEventRecord(ev1, s);
   if (Ypart || Zpart) {

@@ -51,7 +51,7 @@ int main() {
   uint8_t* flush; cudaMalloc(&flush, 256 << 20);
   cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
   int stages[] = {2, 3, 4, 6, 8};
-  int sizes[] = {16384, 32768, 65536, 98304};
+  int sizes[] = {16384, 32768, 65536, 81920, 98304};
   for (int order = 0; order < 2; ++order)
   for (int sz : sizes) for (int nst : stages) for (int pieces : {1, 4}) {
     if ((size_t)nst * sz > 220 * 1024) continue;
