@@ -146,6 +146,13 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// shared-space 16-byte load by 32-bit address (the tile base is rounded up through an integer cast,
+// which leaves plain dereferences as generic-address loads)
+__device__ __forceinline__ uint4 lds128(uint32_t a) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+  return v;
+}
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
 }
@@ -591,7 +598,7 @@ k_resid_bulk(const uint8_t* __restrict__ Xs, int64_t n, int64_t m, const uint8_t
       mbar_wait(&bar_full[st], (t / NSTAGE) & 1);  // the X tile (already complete: the MMAs waited on it)
       mbar_wait(&bar_afull[ab], (t >> 1) & 1);
       tc_fence_after();
-      const uint8_t* sp = smem + (size_t)st * STAGE;
+      const uint32_t sp = smem_u32(smem) + (uint32_t)st * STAGE;
       const bool row_ok = (int64_t)rt * TILE + r < n;
       const int64_t cols = row_ok ? m - (int64_t)ct * TILE : 0;
 #pragma unroll
@@ -602,13 +609,13 @@ k_resid_bulk(const uint8_t* __restrict__ Xs, int64_t n, int64_t m, const uint8_t
 #pragma unroll
         for (int c = 0; c < NC; ++c) tmem_ld32(tmem + lane_base + (uint32_t)(2 * c + ab) * TILE + 32 * h, pv[c]);
         // X (hi, lo) of this row, columns 32h..32h+31: sub h/2, 16-byte chunks 4(h%2)..4(h%2)+3
-        const uint8_t* rowp = sp + (h >> 1) * SUB_BYTES + r * 128;
+        const uint32_t rowp = sp + (h >> 1) * SUB_BYTES + r * 128;
 #pragma unroll
         for (int q4 = 0; q4 < 4; ++q4) {
           const int chunk = 4 * (h & 1) + q4;
           const int off = (chunk ^ (r & 7)) << 4;
-          const uint4 hv = *reinterpret_cast<const uint4*>(rowp + off);
-          const uint4 lv = *reinterpret_cast<const uint4*>(rowp + 2 * SUB_BYTES + off);
+          const uint4 hv = lds128(rowp + off);
+          const uint4 lv = lds128(rowp + 2 * SUB_BYTES + off);
           const uint32_t hw[4] = {hv.x, hv.y, hv.z, hv.w}, lw[4] = {lv.x, lv.y, lv.z, lv.w};
 #pragma unroll
           for (int q = 0; q < 4; ++q) {

@@ -137,9 +137,20 @@ k_nnls_mma(const __grid_constant__ MmaArgs<T> A) {
   if (st->code != 0) return;
 
   // element e of this thread: solver row / CTA-local column
+  // FP64 K permutation: the accumulator slot (8-row tile j, slot i = 2 tq + h) is both an output
+  // row of g and, one iteration later, a K index of the next product (k-step 2j + h covers the
+  // slots i = h, h + 2, h + 4, h + 6).  With p % 8 in 1..4 the last tile's real rows are kept in
+  // its even slots (solver row 8j + i / 2), so its odd slots -- one whole k-step -- are padding
+  // and that k-step's DMMAs are skipped (p = 20: 15 DMMAs per iteration instead of 18).
+  constexpr int PLAST = 8 * (NT - 1);
+  const bool kperm = S::EPT == 2 && p > PLAST && p - PLAST <= 4;
+  auto slot_row = [&](int j, int i) -> int {  // solver row of slot i of tile j
+    if (S::EPT == 4 || j < NT - 1 || !kperm) return 8 * j + i;
+    return PLAST + ((i & 1) ? 4 + (i >> 1) : (i >> 1));
+  };
   auto erow = [&](int e) -> int {
     if constexpr (S::EPT == 4) return 8 * (e >> 2) + 2 * tq + (e & 1);
-    else return 8 * (e >> 1) + 2 * tq + (e & 1);
+    else return slot_row(e >> 1, 2 * tq + (e & 1));
   };
   const int cblk = S::CB * wid;  // first CTA-local column of this warp
   auto ecol = [&](int e) -> int {
@@ -152,7 +163,7 @@ k_nnls_mma(const __grid_constant__ MmaArgs<T> A) {
   const int64_t ebase = (int64_t)(2 * tq) * c + j0 + cblk + gq;
   auto eoff = [&](int e) -> int64_t {
     if constexpr (S::EPT == 4) return (int64_t)(8 * (e >> 2) + (e & 1)) * c + ((e & 2) ? 8 : 0) + ebase;
-    else return (int64_t)(8 * (e >> 1) + (e & 1)) * c + ebase;
+    else return (int64_t)erow(e) * c + j0 + cblk + gq;
   };
   auto snref = [&](int s, int b, int e) -> T& { return snaps[(int64_t)(s * 4 + b) * pc + eoff(e)]; };
   // B(t, global column j) of the reference's V = A^T B (B may be a transposed view)
@@ -428,7 +439,7 @@ k_nnls_mma(const __grid_constant__ MmaArgs<T> A) {
 #pragma unroll
       for (int kk = 0; kk < 2 * NT; ++kk)
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt) bd[kk][nt] = (double)wval(8 * nt + gq, 8 * (kk >> 1) + 2 * tq + (kk & 1));
+        for (int nt = 0; nt < NT; ++nt) bd[kk][nt] = (double)wval(slot_row(nt, gq), slot_row(kk >> 1, 2 * tq + (kk & 1)));
     }
     // State per element (accumulator layout), with u = F - g / L:
     //   F_k = max(0, Y - grad_Y / L) = max(0, u_{k-1} + w_k (u_{k-1} - u_{k-2}))
@@ -513,9 +524,11 @@ k_nnls_mma(const __grid_constant__ MmaArgs<T> A) {
           cc[nt][1] = (double)nv[2 * nt + 1];
         }
 #pragma unroll
-        for (int kk = 0; kk < 2 * NT; ++kk)
+        for (int kk = 0; kk < 2 * NT; ++kk) {
+          if (kk == 2 * NT - 1 && kperm) continue;  // the padding k-step (warp-uniform)
 #pragma unroll
           for (int nt = 0; nt < NT; ++nt) mma_f64(cc[nt], (double)fe[kk], bd[kk][nt]);
+        }
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) {
           g[2 * nt] = (T)cc[nt][0];
@@ -525,17 +538,17 @@ k_nnls_mma(const __grid_constant__ MmaArgs<T> A) {
     };
 
     // per-iteration sums: ||PG||^2 and <F, g - V> (= 2 * partial objective)
-    auto post = [&](int j, T s0, T s1) {
-      // warp-level sums in the working precision, CTA and grid levels in double
+    // (FP32: ||PG||^2 in fp32 up to the warp level; the objective sum is carried
+    // in double from the element products on -- successive iterates' objectives
+    // differ by ~1e-9 relative on ill-conditioned problems and the reference's
+    // best-iterate rule, nnls.py:196-203, needs their order)
+    auto post = [&](int j, T s0, double s1) {
       double a0, a1;
       if constexpr (sizeof(T) == 4) {
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          s0 += __shfl_xor_sync(0xffffffffu, s0, o);
-          s1 += __shfl_xor_sync(0xffffffffu, s1, o);
-        }
+        for (int o = 16; o > 0; o >>= 1) s0 += __shfl_xor_sync(0xffffffffu, s0, o);
         a0 = s0;
-        a1 = s1;
+        a1 = warp_sum(s1);
       } else {
         a0 = warp_sum((double)s0);
         a1 = warp_sum((double)s1);
@@ -550,14 +563,15 @@ k_nnls_mma(const __grid_constant__ MmaArgs<T> A) {
     // the sums of TWO iterations (ja: a0, a1; jb: b0, b1) in one transposed
     // butterfly: 6 shuffles and a 5-level chain for 4 values instead of 20
     // and two 5-level chains; lanes 0 / 8 / 16 / 24 end with a0 / a1 / b0 / b1
-    auto post2 = [&](int ja, T a0, T a1, int jb, T b0, T b1) {
+    auto post2 = [&](int ja, T a0f, double a1, int jb, T b0f, double b1) {
+      const double a0 = (double)a0f, b0 = (double)b0f;
       const bool lo = lane < 16;
-      T k0 = lo ? a0 : b0, k1 = lo ? a1 : b1;
-      const T x0 = lo ? b0 : a0, x1 = lo ? b1 : a1;
+      double k0 = lo ? a0 : b0, k1 = lo ? a1 : b1;
+      const double x0 = lo ? b0 : a0, x1 = lo ? b1 : a1;
       k0 += __shfl_xor_sync(0xffffffffu, x0, 16);
       k1 += __shfl_xor_sync(0xffffffffu, x1, 16);
       const bool hi8 = (lane & 8) != 0;
-      T v = hi8 ? k1 : k0;
+      double v = hi8 ? k1 : k0;
       v += __shfl_xor_sync(0xffffffffu, hi8 ? k0 : k1, 8);
       v += __shfl_xor_sync(0xffffffffu, v, 4);
       v += __shfl_xor_sync(0xffffffffu, v, 2);
@@ -565,7 +579,7 @@ k_nnls_mma(const __grid_constant__ MmaArgs<T> A) {
       if ((lane & 7) == 0) {
         const int j = lo ? ja : jb;
         double* q = pp + ((size_t)((j + NW_PPD) % NW_PPD) * NW_MAXW + wid) * 3;
-        q[hi8 ? 1 : 0] = (double)v;
+        q[hi8 ? 1 : 0] = v;
         if (!hi8) q[2] = 0.0;
       }
     };
@@ -576,32 +590,42 @@ k_nnls_mma(const __grid_constant__ MmaArgs<T> A) {
       }
     };
     // F -> g -> (u, sums); u overwrites uo
-    auto finish = [&](const T (&fe)[NE], const T (&g)[NE], T (&uo)[NE], T& s0, T& s1) {
+    auto finish = [&](const T (&fe)[NE], const T (&g)[NE], T (&uo)[NE], T& s0, double& s1) {
       if constexpr (sizeof(T) == 4) {
         // packed fp32x2 arithmetic (FFMA2/FADD2 on sm_100): elements 2i, 2i+1
-        // are two solver rows of one column
-        float2 a0 = make_float2(0.f, 0.f), a1 = make_float2(0.f, 0.f);
+        // are two solver rows of one column; the objective products are added in double
+        float2 a0 = make_float2(0.f, 0.f);
+        double a1 = 0.0;
         const float2 rl = make_float2(rnegL, rnegL);
 #pragma unroll
-        for (int e = 0; e < NE; e += 2) {
-          const float2 f2 = make_float2(fe[e], fe[e + 1]), g2 = make_float2(g[e], g[e + 1]);
-          const float2 u2 = __ffma2_rn(g2, rl, f2);
-          uo[e] = u2.x;
-          uo[e + 1] = u2.y;
-          const float2 pg2 = make_float2(fe[e] > 0.f ? g[e] : min0_nan(g[e]), fe[e + 1] > 0.f ? g[e + 1] : min0_nan(g[e + 1]));
-          a0 = __ffma2_rn(pg2, pg2, a0);
-          a1 = __ffma2_rn(f2, __fadd2_rn(g2, make_float2(nv[e], nv[e + 1])), a1);
+        for (int e = 0; e < NE; e += 4) {
+          // four objective products summed in fp32 (their own rounding class), then added in double
+          float2 pr = make_float2(0.f, 0.f);
+#pragma unroll
+          for (int h = 0; h < 4; h += 2) {
+            const int i = e + h;
+            const float2 f2 = make_float2(fe[i], fe[i + 1]), g2 = make_float2(g[i], g[i + 1]);
+            const float2 u2 = __ffma2_rn(g2, rl, f2);
+            uo[i] = u2.x;
+            uo[i + 1] = u2.y;
+            const float2 pg2 =
+                make_float2(fe[i] > 0.f ? g[i] : min0_nan(g[i]), fe[i + 1] > 0.f ? g[i + 1] : min0_nan(g[i + 1]));
+            a0 = __ffma2_rn(pg2, pg2, a0);
+            pr = __ffma2_rn(f2, __fadd2_rn(g2, make_float2(nv[i], nv[i + 1])), pr);
+          }
+          a1 += (double)(pr.x + pr.y);
         }
         s0 = a0.x + a0.y;
-        s1 = a1.x + a1.y;
+        s1 = a1;
       } else {
-        s0 = s1 = T(0);
+        s0 = T(0);
+        s1 = 0.0;
 #pragma unroll
         for (int e = 0; e < NE; ++e) {
           uo[e] = fma_acc(g[e], rnegL, fe[e]);
           const T pgv = pg_entry_fast(fe[e], g[e]);
           s0 = fma_acc(pgv, pgv, s0);
-          s1 = fma_acc(fe[e], g[e] + nv[e], s1);
+          s1 = fma_acc((double)fe[e], (double)(g[e] + nv[e]), s1);
         }
       }
     };
@@ -630,7 +654,8 @@ k_nnls_mma(const __grid_constant__ MmaArgs<T> A) {
       fb[e] = fa[e];
       if (!fused) nv[e] = ok ? -A.V[eoff(e)] : T(0);
     }
-    T ps0, ps1;  // sums of the last iteration, posted during the next one
+    T ps0;  // sums of the last iteration, posted during the next one
+    double ps1;
     {
       T g[NE];
       grad(fa, g);
@@ -661,7 +686,8 @@ k_nnls_mma(const __grid_constant__ MmaArgs<T> A) {
     // the sums of iteration k-1 are reduced and posted while the MMAs run
     // iterations run in pairs (A: even k, B: odd k); B posts the sums of the
     // previous B (k - 2, in ps) and of A (k - 1, in pa) while its MMAs run
-    T pa0 = T(0), pa1 = T(0);
+    T pa0 = T(0);
+    double pa1 = 0.0;
     // momentum weights of the current pair (wA: k, wB: k + 1), fetched one
     // pair ahead so the shuffles are off the iteration's critical path
     T wA = T(0), wB = T(0);
@@ -840,7 +866,8 @@ k_nnls_mma(const __grid_constant__ MmaArgs<T> A) {
         for (int kk = wb * NW_WIN; kk <= bj; ++kk) {
           const T w = __shfl_sync(0xffffffffu, wrec, kk % NW_WIN);
           extrapolate(ua, ub, w, fa);
-          T g[NE], d0, d1;
+          T g[NE], d0;
+          double d1;
           grad(fa, g);
           finish(fa, g, ub, d0, d1);
 #pragma unroll

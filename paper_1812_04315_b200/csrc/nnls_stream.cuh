@@ -164,12 +164,13 @@ __global__ void __launch_bounds__(stream_threads<NT>(), 1) k_nnls_stream(const _
 #pragma unroll
         for (int r = 0; r < 4; ++r) g[4 * nt + r] = __fadd_rn(__fadd_rn(cc[nt][r], cl[nt][r]), nv[4 * nt + r]);
     };
-    auto post = [&](int j, float s0, float s1) {
+    // the objective sum s1 is carried in double from the element products on
+    // (nnls_mma.cuh: the best-iterate rule needs the order of objectives that
+    // differ by ~1e-9 relative)
+    auto post = [&](int j, float s0, double s1) {
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        s0 += __shfl_xor_sync(0xffffffffu, s0, o);
-        s1 += __shfl_xor_sync(0xffffffffu, s1, o);
-      }
+      for (int o = 16; o > 0; o >>= 1) s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+      s1 = warp_sum(s1);
       if (lane == 0) {
         double* q = pp + ((size_t)((j + NW_PPD) % NW_PPD) * SS<NT>::PPW + wid) * 3;
         q[0] = s0;
@@ -238,7 +239,7 @@ __global__ void __launch_bounds__(stream_threads<NT>(), 1) k_nnls_stream(const _
     // ring stage, or the resident copy); su_out: where u_k goes in shared
     // memory (resident), else u_k is written to U in HBM
     auto tcompute = [&](int tile, int k, float w, bool snap, int slot, bool save, const float* su1,
-                        const float* su2, const float* sv, float* su_out, float& s0, float& s1) {
+                        const float* su2, const float* sv, float* su_out, float& s0, double& s1) {
       const int64_t cb = j0 + (int64_t)tile * CB;
       float u1[NE], u2[NE], nv[NE], fe[NE], g[NE];
 #pragma unroll
@@ -272,6 +273,7 @@ __global__ void __launch_bounds__(stream_threads<NT>(), 1) k_nnls_stream(const _
       }
       grad(fe, nv, g);
       float* __restrict__ Uo = A.U + (int64_t)(k < 0 ? 1 : (k & 1)) * pc;  // u_{-1} -> slot 1
+      float pr4 = 0.f;
 #pragma unroll
       for (int e = 0; e < NE; ++e) {
         const bool ok = eok(cb, e);
@@ -285,12 +287,16 @@ __global__ void __launch_bounds__(stream_threads<NT>(), 1) k_nnls_stream(const _
         // entries): they add nothing to the sums
         const float pgv = fe[e] > 0.f ? g[e] : min0_nan(g[e]);
         s0 = fmaf(pgv, pgv, s0);
-        s1 = fmaf(fe[e], g[e] + nv[e], s1);
+        pr4 = fmaf(fe[e], g[e] + nv[e], pr4);  // four products in fp32, then added in double
+        if ((e & 3) == 3) {
+          s1 += (double)pr4;
+          pr4 = 0.f;
+        }
       }
     };
     // all of this warp's tiles for iteration k through the ring
     float* res = reinterpret_cast<float*>(smem_d + (size_t)NW_PPD * SS<NT>::PPW * 3);  // resident tiles
-    auto sweep = [&](int k, float w, bool snap, int slot, bool save, float& s0, float& s1) {
+    auto sweep = [&](int k, float w, bool snap, int slot, bool save, float& s0, double& s1) {
       __syncwarp();  // this warp's u stores of iteration k - 1 are visible to its reads
       const int nmine = wid < ntiles ? (ntiles - 1 - wid) / ncw + 1 : 0;
       if (resident) {
@@ -334,12 +340,17 @@ __global__ void __launch_bounds__(stream_threads<NT>(), 1) k_nnls_stream(const _
             for (int e = 0; e < NE; ++e) fe[e] = u1[e];  // F0
           }
           grad(fe, nv, g);
+          float pr4 = 0.f;
 #pragma unroll
           for (int e = 0; e < NE; ++e) {
             res[ob + erow(e) * SS_ROW + ecol(e) + so * SS_ARR_F] = fmaf(g[e], rnegL, fe[e]);
             const float pgv = fe[e] > 0.f ? g[e] : min0_nan(g[e]);
             s0 = fmaf(pgv, pgv, s0);
-            s1 = fmaf(fe[e], g[e] + nv[e], s1);
+            pr4 = fmaf(fe[e], g[e] + nv[e], pr4);  // four products in fp32, then added in double
+            if ((e & 3) == 3) {
+              s1 += (double)pr4;
+              pr4 = 0.f;
+            }
           }
         }
         return;
@@ -377,7 +388,8 @@ __global__ void __launch_bounds__(stream_threads<NT>(), 1) k_nnls_stream(const _
     }
     // start point (nnls.py:163-178)
     {
-      float s0 = 0.f, s1 = 0.f;
+      float s0 = 0.f;
+      double s1 = 0.0;
       sweep(-1, 0.f, false, 0, false, s0, s1);
       post(-1, s0, s1);
       post_flag(-1);
@@ -410,7 +422,8 @@ __global__ void __launch_bounds__(stream_threads<NT>(), 1) k_nnls_stream(const _
         break;
       }
       const float w = (float)__shfl_sync(0xffffffffu, wwin, k % NW_WIN);
-      float s0 = 0.f, s1 = 0.f;
+      float s0 = 0.f;
+      double s1 = 0.0;
       sweep(k, w, snap, slot, save, s0, s1);
       post(k, s0, s1);
       if ((k + 1) % NW_WIN == 0) post_flag(k);

@@ -1,4 +1,3 @@
-./tools/micro/bulk > gpurun_out/bulk_micro.log 2>&1
-cat gpurun_out/bulk_micro.log
-python tools/diag_cfg5_proxy.py 3 > gpurun_out/diag_cfg5.log 2>&1
-cat gpurun_out/diag_cfg5.log | tail -5
+NENMF_DUAL64=w NENMF_DUAL64_DBG=1 timeout 300 python tools/probe_dual64.py 10000 10000 30 2>&1 | tail -n 1
+NENMF_DUAL64=w timeout 300 python tools/probe_dual64.py 10000 10000 30 2>&1 | tail -n 1
+NENMF_DUAL64=w timeout 300 python tools/probe_dual64.py 10000 10000 8 2>&1 | tail -n 1

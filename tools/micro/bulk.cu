@@ -53,7 +53,8 @@ int main() {
   int stages[] = {2, 3, 4, 6, 8};
   int sizes[] = {16384, 32768, 65536, 81920, 98304};
   for (int order = 0; order < 2; ++order)
-  for (int sz : sizes) for (int nst : stages) for (int pieces : {1, 4}) {
+  for (int sz : sizes) for (int nst : stages) for (int pieces : {1, 4, 32, 128}) {
+    if (pieces > 4 && !(sz == 65536 && nst == 3)) continue;
     if ((size_t)nst * sz > 220 * 1024) continue;
     int grid = sms;
     int64_t per_cta = total / grid / sz * sz;
