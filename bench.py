@@ -433,7 +433,9 @@ def rsi_roofline(P, dtype):
     else:
         ms_prep = 0.0
         ms_op = timer(lambda: _ops.dual_pass(Xd, Rt, L, Yt, Zt), 10) / 10
-        kname = "k_xv64 + k_ux64 (RSI X-pass in FP64 on the DMMA tensor pipe)"
+        kname = ("k_dual64t (RSI X-pass in FP64: one TMA read of X feeds X*A and X^T*B on the DMMA tensor pipe)"
+                 if os.environ.get("NENMF_DUAL64", "")[:1] != "o" else
+                 "k_xv64 + k_ux64 (RSI X-pass in FP64 on the DMMA tensor pipe, two reads of X)")
         op = lambda: _ops.dual_pass(Xd, Rt, L, Yt, Zt)  # noqa: E731
     # the kernel(s) alone: CUDA events the library records around each X-pass
     # launch on its own stream

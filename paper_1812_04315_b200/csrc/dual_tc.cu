@@ -734,7 +734,7 @@ bool xpass_timing_begin(cudaEvent_t* e0, cudaEvent_t* e1) {
 }
 
 bool tc_pass_eligible(int64_t n, int64_t m, int64_t k) {
-  if (k < 1 || k > 128 || n < tc::TILE || m < tc::TILE) return false;
+  if (k < 1 || n < tc::TILE || m < tc::TILE) return false;
   return getenv("NENMF_NO_TC") == nullptr;
 }
 

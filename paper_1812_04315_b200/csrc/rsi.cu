@@ -151,6 +151,25 @@ template <typename T>
 int dual_pass(Arena& ws, const T* X, int64_t n, int64_t m, int64_t ldx, const T* At, const T* Bt, int64_t k,
               T* Yt, T* Zt, cudaStream_t s) {
   if (n < 1 || m < 1 || k < 1) return NENMF_ERR_DIM;
+  {
+    // wide sketches (any nu, compression.py:109-117): row blocks of the short-major skinny
+    // operands, one X stream per block (FP64: 32 rows, the DMMA pass; FP32: 128)
+    const int64_t kblk = sizeof(T) == 4 ? 128 : 32;
+    if (k > kblk) {
+      const bool dry = ws.base == nullptr;
+      size_t need = 0;
+      for (int64_t k0 = 0; k0 < k; k0 += kblk) {
+        const int64_t kc = imin(kblk, k - k0);
+        Arena a = dry ? Arena(nullptr, 0) : ws;
+        NENMF_TRY(dual_pass<T>(a, X, n, m, ldx, At != nullptr ? At + k0 * m : nullptr,
+                               Bt != nullptr ? Bt + k0 * n : nullptr, kc, Yt != nullptr ? Yt + k0 * n : nullptr,
+                               Zt != nullptr ? Zt + k0 * m : nullptr, s));
+        if (a.used - (dry ? 0 : ws.used) > need) need = a.used - (dry ? 0 : ws.used);
+      }
+      if (dry) ws.take<char>(need);
+      return NENMF_OK;
+    }
+  }
   if constexpr (sizeof(T) == 4) {
     // FP32 data: tcgen05 BF16x3 pass when the shape fits (dual_tc.cu)
     int rc = dual_pass_tc(ws, reinterpret_cast<const float*>(X), n, m, ldx, reinterpret_cast<const float*>(At),
@@ -436,9 +455,61 @@ int orthonormalize_tsqr(Arena& ws, T* Pt, int64_t rows, int64_t k, nenmf_device_
 }
 
 template <typename T>
+__global__ void k_sub_inplace(T* __restrict__ a, const T* __restrict__ b, int64_t count) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += stride) a[i] -= b[i];
+}
+
+// Panels wider than the 64 columns the one-launch factorizations hold (the
+// reference takes any nu <= min(n, m), compression.py:109-117): block
+// Gram-Schmidt over column blocks of 64.  Every block is projected against
+// the finished blocks (C = P_b Q_j^T, P_b -= C Q_j, block by block) and made
+// orthonormal by the rank-revealing CholeskyQR2; the sweep runs twice, so the
+// rounding of the first projection and the random completion directions of a
+// rank-deficient block are orthogonal to the earlier blocks as well.
+template <typename T>
+static int orthonormalize_blocked(Arena& ws, T* Pt, int64_t rows, int64_t k, nenmf_device_status* st,
+                                  cudaStream_t s) {
+  if (rows < 1 || k < 1 || k > rows) return NENMF_ERR_DIM;
+  constexpr int64_t KB = 64;
+  const bool dry = ws.base == nullptr;
+  T* C = ws.take<T>((size_t)KB * KB);
+  T* V = ws.take<T>((size_t)KB * rows);
+  if (!dry && !ws.ok) return NENMF_ERR_WORKSPACE;
+  size_t need = 0;
+  auto sub = [&](auto&& fn) -> int {  // a sub-step with its own view of the remaining scratch
+    Arena a = ws;
+    const int rc = fn(a);
+    if (a.used - ws.used > need) need = a.used - ws.used;
+    if (rc == NENMF_OK && !dry && !a.ok) return NENMF_ERR_WORKSPACE;
+    return rc;
+  };
+  for (int64_t k0 = 0; k0 < k; k0 += KB) {
+    const int64_t kb = imin(KB, k - k0);
+    T* Pb = dry ? nullptr : Pt + k0 * rows;
+    for (int sweep = 0; sweep < 2; ++sweep) {
+      for (int64_t j0 = 0; j0 < k0; j0 += KB) {
+        const T* Qj = dry ? nullptr : Pt + j0 * rows;
+        NENMF_TRY(sub([&](Arena& a) { return abt<T>(a, Pb, kb, Qj, KB, rows, C, s); }));
+        NENMF_TRY(sub([&](Arena& a) { return ab<T>(a, C, kb, KB, Qj, rows, rows, false, V, s); }));
+        if (!dry) {
+          k_sub_inplace<T><<<(unsigned)imin(cdiv(kb * rows, 256), 2368), 256, 0, s>>>(Pb, V, kb * rows);
+          NENMF_LAUNCH_CHECK();
+        }
+      }
+      if (sweep == 1 && k0 == 0) break;  // the first block has nothing to be projected against
+      NENMF_TRY(sub([&](Arena& a) { return orthonormalize_cholqr<T>(a, Pb, rows, kb, st, s); }));
+    }
+  }
+  if (dry) ws.take<char>(need);
+  return NENMF_OK;
+}
+
+template <typename T>
 int orthonormalize(Arena& ws, T* Pt, int64_t rows, int64_t k, nenmf_device_status* st, cudaStream_t s) {
   const char* e = getenv("NENMF_QR");
-  if ((e != nullptr && e[0] == 't') || k > 64) return orthonormalize_tsqr<T>(ws, Pt, rows, k, st, s);
+  if (k > 64) return orthonormalize_blocked<T>(ws, Pt, rows, k, st, s);
+  if (e != nullptr && e[0] == 't') return orthonormalize_tsqr<T>(ws, Pt, rows, k, st, s);
   return orthonormalize_cholqr<T>(ws, Pt, rows, k, st, s);
 }
 

@@ -321,3 +321,47 @@ def test_power_iteration_vs_golden(golden, dtype):
     with pytest.raises(nm.NumericalCollapseError) as exc:
         nm.power_iteration_pair(X, nu, q, seed, dtype=dtype)
     assert exc.value.iteration == step
+
+
+@pytest.mark.parametrize("dtype,nu", [("fp64", 100), ("fp64", 70), ("fp32", 100), ("fp32", 150)])
+def test_wide_sketch_beyond_64_columns(dtype, nu):
+    """The reference takes any nu <= min(n, m) (compression.py:109-117): sketches
+    wider than the 64 columns of the one-launch factorizations run the blocked
+    orthonormalisation and the chunked X-passes; subspace, compression and
+    the factorization against the oracle fed the same sketch."""
+    rng = np.random.default_rng(91)
+    n, m, p, q = 700, 600, 12, 2
+    X = rng.random((n, p)) @ rng.random((p, m)) + 0.02 * rng.random((n, m))
+    if dtype == "fp32":
+        X = X.astype(np.float32).astype(np.float64)
+    sk = nm.subspace_iteration_pair(X, nu, q, 92, dtype=dtype)
+    eye = np.eye(nu)
+    otol = 1e-10 if dtype == "fp64" else 2e-5
+    assert sk.L.shape == (nu, n) and sk.R.shape == (m, nu)
+    assert np.abs(sk.L @ sk.L.T - eye).max() <= otol
+    assert np.abs(sk.R.T @ sk.R - eye).max() <= otol
+    Lr, Rr = orc.rsi(X, nu, q, 92)
+    stol = 1e-6 if dtype == "fp64" else 1e-3
+    # full-rank noisy X: the whole nu-dimensional subspace is determined, but its trailing
+    # directions (noise singular values nearly equal) are ill-conditioned: compare what the
+    # sketch is for -- the dominant p directions and the captured energy
+    ul = np.linalg.svd(sk.L @ X, full_matrices=False)[0][:, :p]
+    ur = np.linalg.svd(Lr @ X, full_matrices=False)[0][:, :p]
+    assert sin_max_angle(sk.L.T @ ul, Lr.T @ ur) <= stol
+    vl = np.linalg.svd(X @ sk.R, full_matrices=False)[2][:p].T
+    vr = np.linalg.svd(X @ Rr, full_matrices=False)[2][:p].T
+    assert sin_max_angle(sk.R @ vl, Rr @ vr) <= stol
+    lg, rg = capture(X, nm.SketchPair(Lr, Rr, nu, nm.SUBSPACE_ITERATION, q, 92))
+    lm, rm = capture(X, sk)
+    assert abs(lm - lg) <= 1e-3 * lg and abs(rm - rg) <= 1e-3 * rg
+    # compression and three outer iterations with this sketch
+    init = nm.init_factors(n, m, p, seed=93)
+    rec = nm.TraceRecorder()
+    out = nm.factorize_compressed(X, sk, init, capped(3, inner=100), observer=rec, clock=nm.IterationClock(),
+                                  dtype=dtype)
+    ref = orc.nenmf(X, init.G, init.F, L=sk.L, R=sk.R, max_outer=3, max_iter=100)
+    got = np.array([r.rre for r in rec.records])
+    exp = np.array([r for _, r, _ in ref.records])
+    tol = FP64_TOL if dtype == "fp64" else 2e-3
+    assert np.abs(got - exp).max() <= tol * exp.max()
+    assert np.abs(out.F - ref.F).max() <= tol * np.abs(ref.F).max()

@@ -1,3 +1,3 @@
-NENMF_DUAL64=w NENMF_DUAL64_DBG=1 timeout 300 python tools/probe_dual64.py 10000 10000 30 2>&1 | tail -n 1
-NENMF_DUAL64=w timeout 300 python tools/probe_dual64.py 10000 10000 30 2>&1 | tail -n 1
-NENMF_DUAL64=w timeout 300 python tools/probe_dual64.py 10000 10000 8 2>&1 | tail -n 1
+python -m pytest tests/test_gpu_rsi_factorize.py -m gpu -q -k "wide" > gpurun_out/gputest_wide.log 2>&1; tail -n 30 gpurun_out/gputest_wide.log
+python tools/probe_solve.py fp64 0 2>&1 | grep dbg
+python tools/probe_solve.py fp32 0 2>&1 | grep dbg
