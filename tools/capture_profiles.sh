@@ -16,8 +16,8 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv \
 # the FP64 headline's kernels
 ncu --set full --clock-control none --import-source on -k regex:k_nnls_mma -s 1 -c 1 \
     -o gpurun_out/prof/full_k_nnls_mma_f64 python tools/profile_solve.py fp64 2 > gpurun_out/prof/ncu_full1.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:k_xv64 -s 3 -c 1 \
-    -o gpurun_out/prof/full_k_xv64 python tools/sketch_launches.py fp64 > gpurun_out/prof/ncu_full2.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:k_dual64t -s 3 -c 1 \
+    -o gpurun_out/prof/full_k_dual64t python tools/sketch_launches.py fp64 > gpurun_out/prof/ncu_full2.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:k_cholqr2 -s 3 -c 1 \
     -o gpurun_out/prof/full_k_cholqr2 python tools/sketch_launches.py fp64 > gpurun_out/prof/ncu_full3.log 2>&1
 # the FP32 mode's
