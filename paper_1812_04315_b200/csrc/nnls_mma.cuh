@@ -33,8 +33,20 @@ struct MmaShape<float> {
   static constexpr int CB = 16, EPT = 4;  // columns per warp, state elements per thread per n-tile
 };
 template <>
+// FP64, NN_F64_WIDE = 1 (compile-time experiment, off): a warp owns TWO 8-column DMMA m-tiles
+// (columns gq and gq + 8, the element layout of the fp32 accumulator) and the CTA 5 compute warps
+// instead of 9 at cfg2.  Measured slower (1.14 vs 0.88 us per inner iteration): the iteration is
+// bound by each warp's own dependent instruction stream, which nine warps hide better than the
+// two interleaved column groups of five.
+#ifndef NN_F64_WIDE
+#define NN_F64_WIDE 0
+#endif
 struct MmaShape<double> {
+#if NN_F64_WIDE
+  static constexpr int CB = 16, EPT = 4;
+#else
   static constexpr int CB = 8, EPT = 2;
+#endif
 };
 
 // 3xTF32 split: hi keeps the top 10 mantissa bits by truncation (exactly
@@ -59,6 +71,7 @@ __device__ __forceinline__ uint32_t tf32_lo(float x, uint32_t hi) {
 // address/bookkeeping registers); chosen so that ptxas reports no spills.
 template <typename T>
 __host__ __device__ constexpr int mma_threads(int nt) {
+  if (sizeof(T) == 8 && NN_F64_WIDE) return nt <= 1 ? 512 : 256;
   return sizeof(T) == 4 ? (nt <= 2 ? 512 : 256) : (nt <= 1 ? 512 : (nt == 2 ? 384 : (nt == 3 ? 320 : 256)));
 }
 
@@ -143,13 +156,13 @@ k_nnls_mma(const __grid_constant__ MmaArgs<T> A) {
   // its even slots (solver row 8j + i / 2), so its odd slots -- one whole k-step -- are padding
   // and that k-step's DMMAs are skipped (p = 20: 15 DMMAs per iteration instead of 18).
   constexpr int PLAST = 8 * (NT - 1);
-  const bool kperm = S::EPT == 2 && p > PLAST && p - PLAST <= 4;
+  const bool kperm = sizeof(T) == 8 && p > PLAST && p - PLAST <= 4;
   auto slot_row = [&](int j, int i) -> int {  // solver row of slot i of tile j
-    if (S::EPT == 4 || j < NT - 1 || !kperm) return 8 * j + i;
+    if (sizeof(T) == 4 || j < NT - 1 || !kperm) return 8 * j + i;
     return PLAST + ((i & 1) ? 4 + (i >> 1) : (i >> 1));
   };
   auto erow = [&](int e) -> int {
-    if constexpr (S::EPT == 4) return 8 * (e >> 2) + 2 * tq + (e & 1);
+    if constexpr (S::EPT == 4) return slot_row(e >> 2, 2 * tq + (e & 1));
     else return slot_row(e >> 1, 2 * tq + (e & 1));
   };
   const int cblk = S::CB * wid;  // first CTA-local column of this warp
@@ -162,8 +175,8 @@ k_nnls_mma(const __grid_constant__ MmaArgs<T> A) {
   const int64_t pc = (int64_t)p * c;
   const int64_t ebase = (int64_t)(2 * tq) * c + j0 + cblk + gq;
   auto eoff = [&](int e) -> int64_t {
-    if constexpr (S::EPT == 4) return (int64_t)(8 * (e >> 2) + (e & 1)) * c + ((e & 2) ? 8 : 0) + ebase;
-    else return (int64_t)erow(e) * c + j0 + cblk + gq;
+    if constexpr (sizeof(T) == 4) return (int64_t)(8 * (e >> 2) + (e & 1)) * c + ((e & 2) ? 8 : 0) + ebase;
+    else return (int64_t)erow(e) * c + j0 + ecol(e);
   };
   auto snref = [&](int s, int b, int e) -> T& { return snaps[(int64_t)(s * 4 + b) * pc + eoff(e)]; };
   // B(t, global column j) of the reference's V = A^T B (B may be a transposed view)
@@ -417,7 +430,7 @@ k_nnls_mma(const __grid_constant__ MmaArgs<T> A) {
     // bhi = TF32 hi (m16n8k8), blo = the residual W - W_hi (TF32 correction MMAs)
     uint32_t bhi[NT][NT][2], blo[NT][NT][2];
     double bd[2 * NT][NT];
-    if constexpr (S::EPT == 4) {
+    if constexpr (sizeof(T) == 4) {
 #pragma unroll
       for (int kt = 0; kt < NT; ++kt)
 #pragma unroll
@@ -447,7 +460,7 @@ k_nnls_mma(const __grid_constant__ MmaArgs<T> A) {
     T ua[NE], ub[NE], fa[NE], fb[NE];
     // g = W f - V in the accumulator layout (the MMA chain starts from -V)
     auto grad = [&](const T (&fe)[NE], T (&g)[NE]) {
-      if constexpr (S::EPT == 4) {
+      if constexpr (sizeof(T) == 4) {
         // accumulator element (col, row): c0 (gq, 2tq), c1 (gq, 2tq+1), c2 (gq+8, 2tq), c3 (gq+8, 2tq+1)
         uint32_t ahi[NT][4], alo[NT][4];
 #pragma unroll
@@ -516,6 +529,33 @@ k_nnls_mma(const __grid_constant__ MmaArgs<T> A) {
 #pragma unroll
           for (int r = 0; r < 4; ++r)
             g[4 * nt + r] = (T)__fadd_rn(__fadd_rn(cc[nt][r], cl[nt][r]), (float)nv[4 * nt + r]);
+      } else if constexpr (S::EPT == 4) {
+        // two m-tiles per warp (column halves hh: gq, gq + 8): element e = 4 nt + 2 hh + h is
+        // (row slot 2tq + h of tile nt, column half hh); k-step kk of half hh reads e = 4 (kk >> 1) + 2 hh + (kk & 1)
+        double cc[2][NT][2];
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh)
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) {
+            cc[hh][nt][0] = (double)nv[4 * nt + 2 * hh];
+            cc[hh][nt][1] = (double)nv[4 * nt + 2 * hh + 1];
+          }
+#pragma unroll
+        for (int kk = 0; kk < 2 * NT; ++kk) {
+          if (kk == 2 * NT - 1 && kperm) continue;  // the padding k-step (warp-uniform)
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh)
+              mma_f64(cc[hh][nt], (double)fe[4 * (kk >> 1) + 2 * hh + (kk & 1)], bd[kk][nt]);
+        }
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh)
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) {
+            g[4 * nt + 2 * hh] = (T)cc[hh][nt][0];
+            g[4 * nt + 2 * hh + 1] = (T)cc[hh][nt][1];
+          }
       } else {
         double cc[NT][2];
 #pragma unroll
