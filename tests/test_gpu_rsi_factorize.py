@@ -323,14 +323,19 @@ def test_power_iteration_vs_golden(golden, dtype):
     assert exc.value.iteration == step
 
 
-@pytest.mark.parametrize("dtype,nu", [("fp64", 100), ("fp64", 70), ("fp32", 100), ("fp32", 150)])
-def test_wide_sketch_beyond_64_columns(dtype, nu):
+@pytest.mark.parametrize("dtype,nu,shape", [("fp64", 100, (700, 600)), ("fp64", 70, (700, 600)),
+                                            ("fp32", 100, (700, 600)), ("fp32", 150, (700, 600)),
+                                            # 32 < nu <= 64: FP64 passes in row blocks of 32 (TMA + DMMA), FP32 the
+                                            # 64-wide tcgen05 instance; odd sizes take the unaligned fallbacks
+                                            ("fp64", 48, (900, 800)), ("fp64", 48, (901, 803)),
+                                            ("fp32", 48, (900, 800)), ("fp32", 60, (901, 803))])
+def test_wide_sketch_beyond_64_columns(dtype, nu, shape):
     """The reference takes any nu <= min(n, m) (compression.py:109-117): sketches
     wider than the 64 columns of the one-launch factorizations run the blocked
     orthonormalisation and the chunked X-passes; subspace, compression and
     the factorization against the oracle fed the same sketch."""
     rng = np.random.default_rng(91)
-    n, m, p, q = 700, 600, 12, 2
+    (n, m), p, q = shape, 12, 2
     X = rng.random((n, p)) @ rng.random((p, m)) + 0.02 * rng.random((n, m))
     if dtype == "fp32":
         X = X.astype(np.float32).astype(np.float64)
