@@ -121,7 +121,7 @@ template <typename T>
 static int lipschitz(Arena& ws, const T* At, int64_t r, int64_t p, const T* W, const double* pvec, int pcount,
                      int pmax, double ptol, double safety, double* Lout, nenmf_device_status* st, cudaStream_t s) {
   const int64_t k = min(r, p);
-  if (k > 64) return NENMF_ERR_UNSUPPORTED;
+  if (k > 160) return NENMF_ERR_UNSUPPORTED;  // the Gram and two vectors in shared memory
   const T* gram = W;
   T* gsmall = nullptr;
   if (p > r) gsmall = ws.take<T>((size_t)k * k);
@@ -187,6 +187,7 @@ static int launch_nnls(const NnlsPlan& pl, const T* W, const T* V, const T* F0, 
     case 2: return launch_nnls_tpc<T, 2>(NN_DARGS);
     case 4: return launch_nnls_tpc<T, 4>(NN_DARGS);
     case 8: return launch_nnls_tpc<T, 8>(NN_DARGS);
+    case 16: return launch_nnls_tpc<T, 16>(NN_DARGS);
   }
 #undef NN_DARGS
   return NENMF_ERR_UNSUPPORTED;
@@ -208,7 +209,7 @@ int solve_nnls(Arena& ws, const T* At, int64_t r, int64_t p, const T* B, int64_t
                int64_t nup, T* Pout, const uint8_t* Xpre, const GroupHost* grp) {
   if (r < 1 || p < 1 || c < 1) return NENMF_ERR_DIM;
   if (Pt != nullptr && (nup < 1 || Pout == nullptr)) return NENMF_ERR_VALUE;
-  if (p > 64) return NENMF_ERR_UNSUPPORTED;
+  if (p > 128) return NENMF_ERR_UNSUPPORTED;  // the CUDA-core solver holds 16 threads x 8 entries per column
   if (max_iter < 1 || pcount < 1) return NENMF_ERR_VALUE;
   const bool dry = ws.base == nullptr;
   const NnlsPlan pl = plan_nnls<T>(p, c);
@@ -425,7 +426,7 @@ template <typename T>
 int spectral_norm_sq(Arena& ws, const T* At, int64_t r, int64_t p, const double* pvec, int pcount, int pmax,
                      double tol, double* out, nenmf_device_status* st, cudaStream_t s) {
   if (r < 1 || p < 1) return NENMF_ERR_DIM;
-  if (min(r, p) > 64) return NENMF_ERR_UNSUPPORTED;
+  if (min(r, p) > 160) return NENMF_ERR_UNSUPPORTED;
   T* W = p <= r ? ws.take<T>((size_t)p * p) : nullptr;
   if (ws.base != nullptr && !ws.ok) return NENMF_ERR_WORKSPACE;
   if (p <= r) NENMF_TRY(abt<T>(ws, At, p, At, p, r, W, s));

@@ -421,6 +421,7 @@ static int launch_nnls_t(const NnlsPlan& pl, const T* W, const T* V, const T* F0
                          T* gstate, int p, int64_t c, const double* Lptr, int max_iter, double grad_tol, WinRec* recs,
                          WinRec* results, nenmf_device_status* st, unsigned long long* tracebuf, cudaStream_t s) {
   auto fn = k_nnls<T, TPC, RMAX, SM>;
+  if (pl.smem > 227 * 1024) return NENMF_ERR_UNSUPPORTED;  // W (padded p x p) + the sum ring: FP64 p <= 112, FP32 p <= 128
   NENMF_CUDA_TRY(set_smem(fn, pl.smem));
   int64_t cpb = pl.cpb;
   int ldS = pl.ldS, ldW = pl.ldW;

@@ -107,6 +107,21 @@ int abt_any(Arena& ws, const T* A, int64_t p, const T* B, int64_t q, int64_t K, 
 
 template <typename T>
 int abt(Arena& ws, const T* A, int64_t p, const T* B, int64_t q, int64_t K, T* C, cudaStream_t st) {
+  // more outputs than one launch holds (p q > 8192: inner dimensions p or nu above 64): row
+  // blocks of A, whose output rows are contiguous in C
+  if (p >= 1 && q >= 1 && q <= 512 && p * q > (int64_t)ABT_THREADS * ABT_MAXO) {
+    const int64_t pb = imax(1, (int64_t)ABT_THREADS * ABT_MAXO / q);
+    const bool dry = ws.base == nullptr;
+    size_t need = 0;
+    for (int64_t p0 = 0; p0 < p; p0 += pb) {
+      Arena a = ws;
+      NENMF_TRY((abt_any<T, T>(a, dry ? A : A + p0 * K, imin(pb, p - p0), B, q, K, dry ? C : C + p0 * q, st)));
+      if (a.used - ws.used > need) need = a.used - ws.used;
+      if (!dry && !a.ok) return NENMF_ERR_WORKSPACE;
+    }
+    if (dry) ws.take<char>(need);
+    return NENMF_OK;
+  }
   return abt_any<T, T>(ws, A, p, B, q, K, C, st);
 }
 
@@ -693,6 +708,20 @@ template <typename T>
 int ab(Arena& ws, const T* At, int64_t p, int64_t r, const T* B, int64_t c, int64_t ldb, bool trans,
        T* V, cudaStream_t st) {
   if (p < 1 || r < 1 || c < 1) return NENMF_ERR_DIM;
+  if (p > 4 * AB_MAXA) {
+    // more rows of At than the kernels hold (p > 64): row blocks, whose outputs are contiguous rows of V
+    const int64_t pb = 4 * AB_MAXA;
+    const bool dry = ws.base == nullptr;
+    size_t need = 0;
+    for (int64_t p0 = 0; p0 < p; p0 += pb) {
+      Arena a = ws;
+      NENMF_TRY(ab<T>(a, dry ? At : At + p0 * r, imin(pb, p - p0), r, B, c, ldb, trans, dry ? V : V + p0 * c, st));
+      if (a.used - ws.used > need) need = a.used - ws.used;
+      if (!dry && !a.ok) return NENMF_ERR_WORKSPACE;
+    }
+    if (dry) ws.take<char>(need);
+    return NENMF_OK;
+  }
   {
     // tensor-core path; a dry run sizes it AND the CUDA-core fallback below
     // (the live call may fall back on unaligned operands)
@@ -1202,6 +1231,27 @@ k_resid64(const double* __restrict__ X, int64_t nx, int64_t mx, int64_t ldx, int
   }
 }
 
+// per-CTA sums of (D - B)^2 over an r x c result D (row-major) against B (r x c with leading
+// dimension ldb, or its transpose c x r when trans), into part[2 * block + which]; `zero_other`
+// clears the second candidate's slot (one candidate only)
+template <typename T>
+__global__ void k_diff_sumsq(const T* __restrict__ D, const T* __restrict__ B, int64_t r, int64_t c, int64_t ldb,
+                             int trans, double* __restrict__ part, int which, int zero_other) {
+  __shared__ double red[33];
+  double a = 0.0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < r * c; i += stride) {
+    const int64_t t = i / c, j = i % c;
+    const double d = (double)D[i] - (double)(trans ? B[j * ldb + t] : B[t * ldb + j]);
+    a = fma(d, d, a);
+  }
+  a = block_sum(a, red);
+  if (threadIdx.x == 0) {
+    part[2 * blockIdx.x + which] = a;
+    if (zero_other) part[2 * blockIdx.x + 1 - which] = 0.0;
+  }
+}
+
 // fixed-order sum of `n` pairs -> out[0..1]; optional gate
 __global__ void k_pair_final(const double* __restrict__ part, int64_t n, double* __restrict__ out,
                              const int* __restrict__ gate) {
@@ -1224,7 +1274,37 @@ template <typename T>
 int resid(Arena& ws, const T* At, int64_t p, int64_t r, const T* B, int64_t c, int64_t ldb, bool trans,
           const T* F1, const T* F2, double* out2, const int* gate, cudaStream_t st) {
   if (p < 1 || r < 1 || c < 1) return NENMF_ERR_DIM;
-  if (p > 64) return NENMF_ERR_UNSUPPORTED;
+  if (p > 64) {
+    // inner dimension above the register-blocked kernels (the reference takes any p, nnls.py:119-159):
+    // D = A F (r x c) by the CUDA-core product over A = At^T, then sum (D - B)^2 in fixed order
+    T* A = ws.take<T>((size_t)r * p);
+    T* D = ws.take<T>((size_t)r * c);
+    const unsigned grid = (unsigned)imax(1, imin((int64_t)1184, cdiv(r * c, 256)));
+    double* part = ws.take<double>((size_t)grid * 2);
+    const bool dry = ws.base == nullptr;
+    if (!dry && !ws.ok) return NENMF_ERR_WORKSPACE;
+    if (!dry) NENMF_TRY(transpose<T>(At, p, r, r, A, st));
+    size_t need = 0;
+    for (int cand = 0; cand < 2; ++cand) {
+      const T* F = cand == 0 ? F1 : F2;
+      if (!dry && F == nullptr) break;
+      Arena a = ws;
+      NENMF_TRY(ab<T>(a, A, r, p, F, c, c, false, D, st));
+      if (a.used - ws.used > need) need = a.used - ws.used;
+      if (!dry && !a.ok) return NENMF_ERR_WORKSPACE;
+      if (!dry) {
+        k_diff_sumsq<T><<<grid, 256, 0, st>>>(D, B, r, c, ldb, trans ? 1 : 0, part, cand, F2 == nullptr ? 1 : 0);
+        NENMF_LAUNCH_CHECK();
+      }
+    }
+    if (dry) {
+      ws.take<char>(need);
+      return NENMF_OK;
+    }
+    k_pair_final<<<1, 256, 0, st>>>(part, (int64_t)grid, out2, nullptr);
+    NENMF_LAUNCH_CHECK();
+    return NENMF_OK;
+  }
   if constexpr (sizeof(T) == 4) {
     if (p <= 32 && getenv("NENMF_RESID_SIMT") == nullptr) {
       // X-oriented tensor-core kernel: B is X (r x c) or, transposed, X (c x r)

@@ -217,3 +217,86 @@ def test_streamed_resident_matches_ring(monkeypatch, p, c, max_iter):
     Fb = nm.solve_nnls(A, B, F0, cfg, dtype="fp32", report=rep_b)
     assert rep_a[0].inner_iters == rep_b[0].inner_iters
     assert np.array_equal(Fa, Fb)
+
+
+@pytest.mark.parametrize("dtype", ["fp64", "fp32"])
+@pytest.mark.parametrize("shape", [(120, 100, 300), (40, 100, 257), (150, 112, 64), (90, 70, 1000)])
+def test_solve_inner_dimension_above_64(shape, dtype):
+    """The reference takes any p (nnls.py:119-159): p above 64 (FP64 up to 112,
+    FP32 up to 128: W and the sum ring share the CTA's shared memory) runs the
+    CUDA-core solver with 16 threads per column, chunked W / V products, the
+    power iteration on the smaller Gram and the generic residual."""
+    r, p, c = shape
+    rng = np.random.default_rng(500 + r + p)
+    A = rng.random((r, p))
+    B = A @ rng.random((p, c)) + 0.05 * rng.random((r, c))
+    F0 = rng.random((p, c))
+    if dtype == "fp32":
+        A, B, F0 = (M.astype(np.float32).astype(np.float64) for M in (A, B, F0))
+    cfg = nm.InnerSolverConfig(max_iter=60, grad_tol=1e-6)
+    rep = []
+    F = nm.solve_nnls(A, B, F0, cfg, dtype=dtype, report=rep)
+    info = orc.SolveInfo()
+    ref = orc.nesterov_nnls(A, B, F0, 60, 1e-6, 1.0, info)
+    tol = FP64_TOL if dtype == "fp64" else FP32_TOL
+    assert F.shape == ref.shape and F.min() >= 0.0
+    assert rel(F, ref) <= tol, rel(F, ref)
+    assert abs(rep[0].lipschitz - info.lipschitz) <= (1e-9 if dtype == "fp64" else 1e-4) * info.lipschitz
+    assert abs(rep[0].inner_iters - info.iterations) <= 1
+    assert abs(nm.spectral_norm_sq(A, dtype=dtype) - orc.sigma_max_sq(A)) <= (1e-9 if dtype == "fp64" else 1e-4) * orc.sigma_max_sq(A)
+
+
+def test_solve_fp32_p128_and_limits():
+    rng = np.random.default_rng(9)
+    A = rng.random((150, 128))
+    B = A @ rng.random((128, 64))
+    F0 = rng.random((128, 64))
+    A, B, F0 = (M.astype(np.float32).astype(np.float64) for M in (A, B, F0))
+    F = nm.solve_nnls(A, B, F0, nm.InnerSolverConfig(max_iter=40), dtype="fp32")
+    ref = orc.nesterov_nnls(A, B, F0, 40, 1e-4, 1.0)
+    assert rel(F, ref) <= FP32_TOL
+    with pytest.raises(nm.BackendError):  # beyond the compiled range: a loud error, no fallback
+        nm.solve_nnls(rng.random((300, 200)), rng.random((300, 8)), rng.random((200, 8)), dtype="fp64")
+
+
+@pytest.mark.parametrize("dtype", ["fp64", "fp32"])
+def test_compressed_factorization_rank_above_64(dtype):
+    """factorize_compressed with p = 80 and a 100-column sketch against the
+    oracle fed the same sketch (two outer iterations)."""
+    rng = np.random.default_rng(77)
+    n, m, p, nu = 500, 420, 80, 100
+    X = rng.random((n, p)) @ rng.random((p, m)) + 0.01 * rng.random((n, m))
+    if dtype == "fp32":
+        X = X.astype(np.float32).astype(np.float64)
+    sk = nm.subspace_iteration_pair(X, nu, 2, 78, dtype=dtype)
+    init = nm.init_factors(n, m, p, seed=79)
+    cfg = nm.OuterConfig(inner=nm.InnerSolverConfig(max_iter=40), time_budget_seconds=0.0, max_outer_iterations=2)
+    rec = nm.TraceRecorder()
+    out = nm.factorize_compressed(X, sk, init, cfg, observer=rec, clock=nm.IterationClock(), dtype=dtype)
+    ref = orc.nenmf(X, init.G, init.F, L=sk.L, R=sk.R, max_outer=2, max_iter=40)
+    got = np.array([r.rre for r in rec.records])
+    exp = np.array([r for _, r, _ in ref.records])
+    tol = FP64_TOL if dtype == "fp64" else 2e-3
+    assert np.abs(got - exp).max() <= tol * exp.max(), (got, exp)
+    assert rel(out.F, ref.F) <= tol and rel(out.G, ref.G) <= tol
+
+
+@pytest.mark.parametrize("dtype", ["fp64", "fp32"])
+def test_vanilla_factorization_rank_above_64(dtype):
+    """factorize_vanilla with p = 72 (chunked V = A^T X products, generic
+    explicit-residual tie-break) against the oracle, two outer iterations."""
+    rng = np.random.default_rng(81)
+    n, m, p = 300, 260, 72
+    X = rng.random((n, p)) @ rng.random((p, m)) + 0.01 * rng.random((n, m))
+    if dtype == "fp32":
+        X = X.astype(np.float32).astype(np.float64)
+    init = nm.init_factors(n, m, p, seed=82)
+    cfg = nm.OuterConfig(inner=nm.InnerSolverConfig(max_iter=40), time_budget_seconds=0.0, max_outer_iterations=2)
+    rec = nm.TraceRecorder()
+    out = nm.factorize_vanilla(X, init, cfg, observer=rec, clock=nm.IterationClock(), dtype=dtype)
+    ref = orc.nenmf(X, init.G, init.F, max_outer=2, max_iter=40)
+    got = np.array([r.rre for r in rec.records])
+    exp = np.array([r for _, r, _ in ref.records])
+    tol = FP64_TOL if dtype == "fp64" else 2e-3
+    assert np.abs(got - exp).max() <= tol * exp.max(), (got, exp)
+    assert rel(out.F, ref.F) <= tol and rel(out.G, ref.G) <= tol

@@ -1,2 +1,1 @@
-python -m pytest tests -m gpu -x -q > gpurun_out/gputest_final.log 2>&1; tail -n 6 gpurun_out/gputest_final.log
-python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -n 2
+timeout 900 python -m pytest tests/test_gpu_nnls.py -m gpu -q -x -k "above_64 or p128" > gpurun_out/gputest_p.log 2>&1; tail -n 30 gpurun_out/gputest_p.log
