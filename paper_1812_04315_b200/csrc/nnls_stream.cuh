@@ -15,6 +15,11 @@
 #pragma once
 #include "nnls_mma.cuh"
 
+// objective products summed in fp32 in groups of NN_S1_GROUP (a power of two), then in double
+#ifndef NN_S1_GROUP
+#define NN_S1_GROUP 4
+#endif
+
 namespace nenmf {
 
 // 8 (NT <= 3) or 4 compute warps + the resolver.  When the CTA's columns fit
@@ -287,8 +292,8 @@ __global__ void __launch_bounds__(stream_threads<NT>(), 1) k_nnls_stream(const _
         // entries): they add nothing to the sums
         const float pgv = fe[e] > 0.f ? g[e] : min0_nan(g[e]);
         s0 = fmaf(pgv, pgv, s0);
-        pr4 = fmaf(fe[e], g[e] + nv[e], pr4);  // four products in fp32, then added in double
-        if ((e & 3) == 3) {
+        pr4 = fmaf(fe[e], g[e] + nv[e], pr4);  // NN_S1_GROUP products in fp32, then added in double
+        if ((e & (NN_S1_GROUP - 1)) == NN_S1_GROUP - 1 || e == NE - 1) {
           s1 += (double)pr4;
           pr4 = 0.f;
         }
@@ -346,8 +351,8 @@ __global__ void __launch_bounds__(stream_threads<NT>(), 1) k_nnls_stream(const _
             res[ob + erow(e) * SS_ROW + ecol(e) + so * SS_ARR_F] = fmaf(g[e], rnegL, fe[e]);
             const float pgv = fe[e] > 0.f ? g[e] : min0_nan(g[e]);
             s0 = fmaf(pgv, pgv, s0);
-            pr4 = fmaf(fe[e], g[e] + nv[e], pr4);  // four products in fp32, then added in double
-            if ((e & 3) == 3) {
+            pr4 = fmaf(fe[e], g[e] + nv[e], pr4);  // NN_S1_GROUP products in fp32, then added in double
+            if ((e & (NN_S1_GROUP - 1)) == NN_S1_GROUP - 1 || e == NE - 1) {
               s1 += (double)pr4;
               pr4 = 0.f;
             }
