@@ -1,8 +1,2 @@
-set -x
-python tools/probe_cfg.py 3 2 2>&1 | tail -n 2
-cp paper_1812_04315_b200/libnenmf_b200.so /tmp/lib_g4.so
-cp paper_1812_04315_b200/libnenmf_b200_g32.so.bak paper_1812_04315_b200/libnenmf_b200.so
-python tools/probe_cfg.py 3 2 2>&1 | tail -n 2
-python tools/probe_cfg.py 4 2 2>&1 | tail -n 2
-cp /tmp/lib_g4.so paper_1812_04315_b200/libnenmf_b200.so
-NENMF_NNLS_SIMT=1 python tools/probe_cfg.py 3 2 2>&1 | tail -n 2
+python bench.py --steps 5 --warmup 3 > gpurun_out/bench_final.json 2> gpurun_out/bench_final.err; tail -c 300 gpurun_out/bench_final.json
+python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; tail -c 400 gpurun_out/bench_ref.json
