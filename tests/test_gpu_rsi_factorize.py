@@ -370,3 +370,28 @@ def test_wide_sketch_beyond_64_columns(dtype, nu, shape):
     tol = FP64_TOL if dtype == "fp64" else 2e-3
     assert np.abs(got - exp).max() <= tol * exp.max()
     assert np.abs(out.F - ref.F).max() <= tol * np.abs(ref.F).max()
+
+
+@pytest.mark.parametrize("dtype", ["fp64", "fp32"])
+def test_wide_sketch_of_rank_deficient_matrix(dtype):
+    """nu = 100 on a noiseless rank-20 X: 80 of the sketch directions are the
+    random completion of rank-deficient blocks.  They must still be
+    orthonormal to the earlier blocks (the second sweep of the blocked
+    orthonormalisation), and the sketch must capture X (reference
+    test_compression.py: rank-deficient inputs)."""
+    rng = np.random.default_rng(310)
+    n, m, rank, nu = 640, 520, 20, 100
+    X = rng.random((n, rank)) @ rng.random((rank, m))
+    if dtype == "fp32":
+        X = X.astype(np.float32).astype(np.float64)
+    sk = nm.subspace_iteration_pair(X, nu, 2, 311, dtype=dtype)
+    eye = np.eye(nu)
+    otol = 1e-10 if dtype == "fp64" else 2e-5
+    assert np.abs(sk.L @ sk.L.T - eye).max() <= otol
+    assert np.abs(sk.R.T @ sk.R - eye).max() <= otol
+    left, right = capture(X, sk)
+    ctol = 1e-8 if dtype == "fp64" else 1e-4
+    assert left <= ctol and right <= ctol, (left, right)
+    Lr, Rr = orc.rsi(X, nu, 2, 311)
+    assert sin_max_angle(sk.L.T @ np.linalg.svd(sk.L @ X, full_matrices=False)[0][:, :rank],
+                         Lr.T @ np.linalg.svd(Lr @ X, full_matrices=False)[0][:, :rank]) <= (1e-6 if dtype == "fp64" else 1e-3)

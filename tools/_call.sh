@@ -1,2 +1,1 @@
-python bench.py --steps 5 --warmup 3 > gpurun_out/bench_final.json 2> gpurun_out/bench_final.err; tail -c 300 gpurun_out/bench_final.json
-python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; tail -c 400 gpurun_out/bench_ref.json
+timeout 600 python -m pytest tests/test_gpu_rsi_factorize.py -m gpu -q -x -k "rank_deficient" > gpurun_out/gputest_rd.log 2>&1; tail -n 30 gpurun_out/gputest_rd.log
