@@ -153,7 +153,7 @@ int nenmf_solve_nnls_next(int dtype, const void* At, int64_t r, int64_t p,
  * generate_problem, bit-identical streams).  nenmf_generate_norms: out2[0] =
  * ||G F||^2 (G F formed on the fly, not stored), out2[1] = ||N||^2, one read
  * of N.  nenmf_generate_write: X = G F + scale N in dtype (N may be NULL for
- * the noiseless case).  p <= 64. */
+ * the noiseless case). */
 size_t nenmf_generate_workspace_bytes(void);
 int nenmf_generate_norms(const double* G, const double* F, const double* N, int64_t n, int64_t m, int64_t p,
                          double* out2, void* ws, size_t ws_bytes, void* stream);

@@ -12,7 +12,7 @@
 namespace nenmf {
 
 constexpr int GEN_THREADS = 256;
-constexpr int GEN_PMAX = 64;
+constexpr int GEN_PMAX = 1 << 20;  // the kernels loop over p; no structural limit
 
 // one thread per (row, 4-column group); the CTA stages F's 4-column slabs
 __global__ void __launch_bounds__(GEN_THREADS)

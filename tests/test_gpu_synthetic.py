@@ -26,7 +26,8 @@ def _reference(n, m, p, snr_db, seed):
 
 
 @pytest.mark.parametrize("n,m,p,snr,seed", [(300, 200, 7, 20.0, 5), (1000, 1500, 15, 30.0, 9901),
-                                            (64, 4000, 3, 0.0, 2 ** 63 + 7), (250, 250, 10, math.inf, 1)])
+                                            (64, 4000, 3, 0.0, 2 ** 63 + 7), (250, 250, 10, math.inf, 1),
+                                            (400, 300, 100, 25.0, 77)])  # p above 64
 def test_device_generator_matches_reference(n, m, p, snr, seed):
     G, F, X, real = _reference(n, m, p, snr, seed)
     inst = generate_problem_device(n, m, p, snr, seed)
